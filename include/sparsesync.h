@@ -1,0 +1,201 @@
+/*
+ * sparsesync.h — C ABI of the B200-native SparseRL-Sync hot path
+ * (arxiv 2605.07330, "§3 Method").
+ *
+ * Implemented by paper_2605_07330_b200/libsparsesync.so (hand-written sm_100a
+ * CUDA). No torch types cross this boundary: pointers are plain host or device
+ * pointers, sizes are integers, every function returns an int status
+ * (SYNC_OK = 0, negative = error) and nothing throws.
+ *
+ * Conventions (apply to every call unless stated):
+ *  - "d_" pointers are DEVICE pointers owned by the caller; "h_" pointers are
+ *    host pointers owned by the caller. The library never allocates device
+ *    memory; the caller allocates the workspace whose size the *_workspace_size
+ *    calls return, and keeps it alive for the lifetime of the context.
+ *  - BF16 values travel as uint16_t raw bit patterns and are never converted,
+ *    so NaN payloads and signed zeros survive (C1, C9).
+ *  - Weight / snapshot / I / V pointers must be 16-byte aligned
+ *    (else SYNC_ERR_ALIGNMENT) — torch allocations are 256-byte aligned.
+ *  - Every call is asynchronous on `stream` unless documented as blocking.
+ *    Errors detected on the device (index range, capacity, corrupt stream,
+ *    CRC) are latched in a device status word and returned by sync_status().
+ *  - Indices are tensor-local row-major flat element indices, numel < 2^31
+ *    ("Indices are kept in int32 ... fits in 2^31 flattened elements").
+ *  - The wire format (records, chunks, buckets) is DESIGN.md §3, version 1.
+ */
+#ifndef SPARSESYNC_H
+#define SPARSESYNC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sync_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+/* ---- status codes -------------------------------------------------------- */
+#define SYNC_OK 0
+#define SYNC_ERR_ARG -1          /* bad argument (NULL, size out of range) */
+#define SYNC_ERR_ALIGNMENT -2    /* device pointer not 16-byte aligned */
+#define SYNC_ERR_DTYPE -3        /* dtype other than BF16 */
+#define SYNC_ERR_WORKSPACE -4    /* workspace too small */
+#define SYNC_ERR_CUDA -5         /* a CUDA runtime call failed */
+#define SYNC_ERR_INDEX_RANGE -6  /* an index >= numel (S:327 IndexOutOfRange); no OOB write happened */
+#define SYNC_ERR_CAPACITY -7     /* output capacity exceeded; no OOB write happened */
+#define SYNC_ERR_CORRUPT -8      /* malformed record / rANS end-state mismatch / unconsumed words */
+#define SYNC_ERR_BAD_MAGIC -9    /* bucket magic != "SRLB" */
+#define SYNC_ERR_VERSION -10     /* bucket version != 1 */
+#define SYNC_ERR_TRUNCATED -11   /* bucket shorter than its header says */
+#define SYNC_ERR_CRC -12         /* CRC-32 mismatch */
+
+/* ---- configuration ------------------------------------------------------- */
+#define SYNC_CODEC_RAW 0         /* u32 I + u16 V: the paper's measured raw path */
+#define SYNC_CODEC_COMPRESSED 1  /* DELTA16/ABS32 indices + byte-plane rANS values (§3.3) */
+#define SYNC_FLAG_CRC 1u         /* per-bucket CRC-32/IEEE */
+#define SYNC_CHUNK 16384u        /* values per chunk */
+
+/* Ordered tensor list = record order (model iteration order). Host memory. */
+typedef struct {
+  uint32_t n_tensors;
+  const uint64_t* numel;   /* [n_tensors], each < 2^31 (0 allowed) */
+} sync_manifest;
+
+typedef struct {
+  uint64_t bucket_limit;   /* L: max bytes per bucket incl. header (DESIGN C11); >= 64 */
+  uint64_t max_changed;    /* capacity of the caller's I/V arrays (elements) */
+  uint32_t codec;          /* SYNC_CODEC_* */
+  uint32_t flags;          /* SYNC_FLAG_* */
+} sync_config;
+
+/* Per-sync statistics, filled by sync_ctx_stats() (blocking). */
+typedef struct {
+  uint64_t nnz;            /* Σ changed elements (|I|) */
+  uint64_t n_records;      /* tensors with nnz > 0 */
+  uint64_t n_delta16;      /* records coded DELTA16 (b_i = 2) */
+  uint64_t n_abs32;        /* records coded ABS32 (b_i = 4) */
+  uint64_t n_chunks;       /* Σ ceil(nnz_t / SYNC_CHUNK) */
+  uint64_t n_chunks_rans;  /* hi chunks stored as rANS (rest RAW) */
+  uint64_t enc_bytes;      /* Σ record_bytes (compressed or raw records) */
+  uint64_t index_bytes;    /* Σ padded index-stream bytes */
+  uint64_t value_bytes;    /* Σ (record_bytes - 16 - index bytes): α numerator (DESIGN C5) */
+} sync_stats;
+
+/* Record view produced by sync_bucket_unpack (device memory, 32 B). */
+typedef struct {
+  uint32_t tensor_id;
+  uint32_t nnz;
+  uint32_t offset;         /* record offset from bucket start */
+  uint32_t record_bytes;
+  uint32_t first_chunk;    /* chunk index of the record's first chunk within the bucket */
+  uint8_t idx_mode, dtype, codec, reserved;
+  uint64_t out_offset;     /* Σ nnz of the preceding records in the bucket */
+} sync_record_view;
+
+typedef struct sync_ctx sync_ctx;   /* opaque host object */
+
+/* ---- context --------------------------------------------------------------
+ * sync_workspace_size: device bytes the context needs (tile look-back states,
+ * manifest tables, record/chunk plan, status word).
+ * sync_ctx_create: validates the manifest (numel < 2^31, dtype BF16 implied),
+ * uploads its tables into d_workspace on `stream`, and returns a host object.
+ * The same context serves a sender (extract/compress/pack/commit) and a
+ * receiver (unpack/decompress/apply) over the same manifest (the
+ * receiver needs only the manifest, not the Trainer's layout).            */
+int sync_workspace_size(const sync_manifest* m, const sync_config* c, size_t* bytes);
+int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c,
+                    void* d_workspace, size_t workspace_bytes, sync_stream_t stream);
+int sync_ctx_destroy(sync_ctx* ctx);
+
+/* ---- a1 extract: Alg. 1 l.6 + Alg. 2 l.5 -------------------
+ * Single tensor: I = ascending { i < n : old[i] != new_[i] bitwise },
+ * V[k] = new_[I[k]], *d_count = |I| (device u64). n < 2^31. If |I| > cap,
+ * only the first cap entries are written, *d_count is still the true count
+ * and the status word latches SYNC_ERR_CAPACITY. Needs its own small
+ * workspace (look-back tile states).                                       */
+int sync_extract_workspace_size(uint64_t n, size_t* bytes);
+int sync_extract(const uint16_t* d_old, const uint16_t* d_new, uint64_t n,
+                 uint32_t* d_I, uint16_t* d_V, uint64_t cap, uint64_t* d_count,
+                 void* d_workspace, size_t workspace_bytes, sync_stream_t stream);
+/* Reads and clears the status word of a single-tensor workspace (blocking). */
+int sync_extract_status(void* d_workspace, sync_stream_t stream);
+
+/* Whole manifest in one launch: d_old_ptrs/d_new_ptrs are DEVICE arrays of
+ * n_tensors device pointers. Records are contiguous in manifest order:
+ * tensor t's entries occupy [Σ_{u<t} counts[u], +counts[t]) of I and V, with
+ * tensor-local indices. d_counts: device u64[n_tensors]. Capacity =
+ * config.max_changed.                                                      */
+int sync_extract_batched(sync_ctx* ctx, const uint16_t* const* d_old_ptrs,
+                         const uint16_t* const* d_new_ptrs, uint32_t* d_I, uint16_t* d_V,
+                         uint64_t* d_counts, sync_stream_t stream);
+
+/* ---- a2-a4 plan + encode: §3.3 --------------------------------
+ * From the output of sync_extract_batched, build every record (DESIGN §3.1 or
+ * §3.2 per config.codec) back to back into d_enc (capacity enc_cap bytes;
+ * sync_enc_bound gives a safe capacity). Per-record sizes stay in the
+ * workspace for sync_bucket_pack. Deterministic bytes.                     */
+int sync_enc_bound(const sync_manifest* m, const sync_config* c, uint64_t* bytes);
+int sync_compress(sync_ctx* ctx, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,
+                  uint8_t* d_enc, uint64_t enc_cap, sync_stream_t stream);
+
+/* ---- a5 bucket pack (Fig. workflow, C11) ----------------
+ * BLOCKING: waits for the record sizes of the preceding sync_compress, runs
+ * the greedy bucketing on the host (the one host sync point of a sync),
+ * then launches the copy of every record into d_buckets plus the headers,
+ * directories and (flag) CRC-32. Bucket b starts at h_offsets[b] (256-aligned)
+ * and is h_sizes[b] bytes. *n_buckets = 0 when nothing changed.            */
+int sync_bucket_pack(sync_ctx* ctx, const uint8_t* d_enc, uint8_t* d_buckets, uint64_t buckets_cap,
+                     uint32_t* n_buckets, uint64_t* h_offsets, uint64_t* h_sizes, uint32_t max_buckets,
+                     sync_stream_t stream);
+/* Upper bound of the bucket buffer for the current plan (after sync_compress; blocking). */
+int sync_buckets_bound(sync_ctx* ctx, uint64_t* bytes, sync_stream_t stream);
+
+/* ---- a7 unpack / decompress (Alg. 3 l.5; "exact inverse") ---
+ * sync_bucket_unpack validates one bucket in device memory (magic, version,
+ * sizes, CRC when flagged) and writes one sync_record_view per record into
+ * d_views (device, max_views entries) and the record count into d_n_records
+ * (device u32). Failures latch BAD_MAGIC / VERSION / TRUNCATED / CRC / CORRUPT.
+ * sync_decompress decodes every record of the bucket into d_I / d_V at
+ * view.out_offset (tensor-local indices), d_cap entries of capacity.       */
+int sync_bucket_unpack(sync_ctx* ctx, const uint8_t* d_bucket, uint64_t bytes,
+                       sync_record_view* d_views, uint32_t max_views, uint32_t* d_n_records,
+                       sync_stream_t stream);
+int sync_decompress(sync_ctx* ctx, const uint8_t* d_bucket, uint64_t bytes, uint32_t* d_I, uint16_t* d_V,
+                    uint64_t d_cap, sync_stream_t stream);
+
+/* ---- a7+a8 fused decode + scatter-apply (Alg. 3 l.5-6) --
+ * Validates the bucket, decodes every chunk and scatters V into
+ * d_weight_ptrs[tensor_id] (DEVICE array of n_tensors device pointers) in
+ * place. Indices >= numel latch SYNC_ERR_INDEX_RANGE and are not written.  */
+int sync_decompress_apply(sync_ctx* ctx, const uint8_t* d_bucket, uint64_t bytes,
+                          uint16_t* const* d_weight_ptrs, sync_stream_t stream);
+
+/* ---- a8 scatter-apply / a9 snapshot commit (Alg. 3 l.6) -----
+ * d_W[d_I[k]] = d_V[k] for k < count (superset-safe, idempotent).
+ * Indices >= numel are skipped and latch SYNC_ERR_INDEX_RANGE into *d_status
+ * (device u32, OR-ed; may be NULL). sync_commit_snapshot is the same
+ * operation on the Trainer's snapshot; call it only after the transfer of
+ * this sync completed (DESIGN C13).                                        */
+int sync_apply(uint16_t* d_W, const uint32_t* d_I, const uint16_t* d_V, uint64_t count, uint64_t numel,
+               uint32_t* d_status, sync_stream_t stream);
+int sync_commit_snapshot(uint16_t* d_snapshot, const uint32_t* d_I, const uint16_t* d_V, uint64_t count,
+                         uint64_t numel, uint32_t* d_status, sync_stream_t stream);
+/* Batched commit over the manifest from the raw output of sync_extract_batched. */
+int sync_commit_snapshot_batched(sync_ctx* ctx, uint16_t* const* d_snapshot_ptrs, const uint32_t* d_I,
+                                 const uint16_t* d_V, const uint64_t* d_counts, sync_stream_t stream);
+
+/* ---- status ----------------------------------------------------------------
+ * sync_status: BLOCKING; synchronises `stream`, reads and clears the device
+ * status word, returns SYNC_OK or the first latched error.
+ * sync_ctx_stats: BLOCKING; statistics of the last sync_compress.          */
+int sync_status(sync_ctx* ctx, sync_stream_t stream);
+int sync_ctx_stats(sync_ctx* ctx, sync_stats* out, sync_stream_t stream);
+const char* sync_strerror(int status);
+/* Number of kernels the library launched since load (diagnostics). */
+uint64_t sync_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSESYNC_H */

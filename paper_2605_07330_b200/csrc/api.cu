@@ -1,0 +1,516 @@
+// api.cu — the C ABI of include/sparsesync.h: context, workspace layout,
+// argument checks and launch sequencing. All arithmetic of the method runs in
+// the kernels of extract.cu / plan.cu / encode.cu / pack.cu / decode.cu /
+// apply.cu; the host only sequences launches, plans bucket boundaries from the
+// record sizes (greedy, DESIGN C11) and reads back status words.
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace ss;
+
+namespace ss {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace ss
+
+namespace {
+
+constexpr u64 kAlign = 256;
+
+struct Layout {
+  u64 numel, tile_prefix, misc, tile_state, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
+  u64 chunk_hi, chunk_mode, chunk_hioff, totals, recs, bks, views, nviews, crc, total;
+};
+
+u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4; }
+
+Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n) {
+  Layout L{};
+  u64 o = 0;
+  auto take = [&](u64 bytes) {
+    u64 at = o;
+    o = pad_to(o + (bytes ? bytes : 8), kAlign);
+    return at;
+  };
+  L.numel = take(8ull * T);
+  L.tile_prefix = take(8ull * (T + 1));
+  L.misc = take(4 * 64);
+  L.tile_state = take(8ull * n_tiles);
+  L.rec_off = take(8ull * (T + 1));
+  L.chunk_off = take(8ull * (T + 1));
+  L.maxgap = take(4ull * T);
+  L.rec_mode = take(4ull * T);
+  L.rec_bytes = take(8ull * T);
+  L.enc_off = take(8ull * (T + 1));
+  L.chunk_hi = take(4ull * max_chunks);
+  L.chunk_mode = take(4ull * max_chunks);
+  L.chunk_hioff = take(8ull * (max_chunks + 1));
+  L.totals = take(8 * 16);
+  L.recs = take(sizeof(RecordDesc) * (u64)T);
+  L.bks = take(sizeof(BucketDesc) * (u64)(T + 1));
+  L.views = take(sizeof(sync_record_view) * (u64)T);
+  L.nviews = take(8);
+  L.crc = take(4ull * crc_n);
+  L.total = o;
+  return L;
+}
+
+struct Dims {
+  u32 T;
+  u64 n_tiles, max_chunks, max_record, crc_n;
+};
+
+int check_manifest(const sync_manifest* m, const sync_config* c, Dims* d) {
+  if (!m || !c || (m->n_tensors && !m->numel)) return SYNC_ERR_ARG;
+  if (c->codec > SYNC_CODEC_COMPRESSED || c->bucket_limit < 64) return SYNC_ERR_ARG;
+  d->T = m->n_tensors;
+  d->n_tiles = 0;
+  u64 maxn = 0;
+  for (u32 t = 0; t < m->n_tensors; ++t) {
+    if (m->numel[t] >= (1ull << 31)) return SYNC_ERR_ARG;
+    d->n_tiles += (m->numel[t] + kTile - 1) / kTile;
+    maxn = m->numel[t] > maxn ? m->numel[t] : maxn;
+  }
+  d->max_chunks = (c->max_changed + kChunk - 1) / kChunk + d->T + 1;
+  u64 rn = c->max_changed < maxn ? c->max_changed : maxn;
+  d->max_record = 6 * rn + 20 * ((rn + kChunk - 1) / kChunk) + 64;
+  u64 mb = c->bucket_limit > d->max_record + 64 ? c->bucket_limit : d->max_record + 64;
+  d->crc_n = crc_slots(mb);
+  return SYNC_OK;
+}
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+#define CK(x)                                   \
+  do {                                          \
+    if ((x) != cudaSuccess) return SYNC_ERR_CUDA; \
+  } while (0)
+
+}  // namespace
+
+struct sync_ctx {
+  Dims d;
+  sync_config cfg;
+  std::vector<u64> numel, tile_prefix;
+  u8* ws;
+  Layout L;
+  Plan plan;
+  u32* misc;  // [0] tile counter, [1] status, [2] crc bad flag
+  int sm_count;
+  int grid;   // grid-stride kernels: CTAs of 256 threads
+  const u64* plan_counts;
+  bool plan_valid;
+  std::vector<u64> h_rec_bytes, h_chunk_off, h_enc_off, h_totals;
+  std::vector<RecordDesc> h_recs;
+  std::vector<BucketDesc> h_bks;
+};
+
+extern "C" {
+
+int sync_workspace_size(const sync_manifest* m, const sync_config* c, size_t* bytes) {
+  Dims d;
+  int st = check_manifest(m, c, &d);
+  if (st) return st;
+  if (!bytes) return SYNC_ERR_ARG;
+  *bytes = make_layout(d.T, d.n_tiles, d.max_chunks, d.crc_n).total;
+  return SYNC_OK;
+}
+
+int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c, void* d_workspace,
+                    size_t workspace_bytes, sync_stream_t stream) {
+  if (!out) return SYNC_ERR_ARG;
+  *out = nullptr;
+  Dims d;
+  int st = check_manifest(m, c, &d);
+  if (st) return st;
+  Layout L = make_layout(d.T, d.n_tiles, d.max_chunks, d.crc_n);
+  if (!d_workspace || workspace_bytes < L.total) return SYNC_ERR_WORKSPACE;
+  if (!aligned16(d_workspace)) return SYNC_ERR_ALIGNMENT;
+  sync_ctx* x = new (std::nothrow) sync_ctx();
+  if (!x) return SYNC_ERR_ARG;
+  x->d = d;
+  x->cfg = *c;
+  x->ws = static_cast<u8*>(d_workspace);
+  x->L = L;
+  x->numel.assign(m->numel, m->numel + d.T);
+  x->tile_prefix.resize(d.T + 1);
+  u64 acc = 0;
+  for (u32 t = 0; t < d.T; ++t) {
+    x->tile_prefix[t] = acc;
+    acc += (x->numel[t] + kTile - 1) / kTile;
+  }
+  x->tile_prefix[d.T] = acc;
+  cudaStream_t s = (cudaStream_t)stream;
+  u8* w = x->ws;
+  if (d.T) {
+    if (cudaMemcpyAsync(w + L.numel, x->numel.data(), 8ull * d.T, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(w + L.tile_prefix, x->tile_prefix.data(), 8ull * (d.T + 1), cudaMemcpyHostToDevice, s) !=
+            cudaSuccess) {
+      delete x;
+      return SYNC_ERR_CUDA;
+    }
+  }
+  if (cudaMemsetAsync(w + L.misc, 0, 4 * 64, s) != cudaSuccess ||
+      cudaMemsetAsync(w + L.totals, 0, 8 * 16, s) != cudaSuccess) {
+    delete x;
+    return SYNC_ERR_CUDA;
+  }
+  x->misc = reinterpret_cast<u32*>(w + L.misc);
+  Plan& p = x->plan;
+  p.n_tensors = d.T;
+  p.cap = c->max_changed;
+  p.codec = c->codec;
+  p.max_chunks = d.max_chunks;
+  p.numel = reinterpret_cast<const u64*>(w + L.numel);
+  p.rec_off = reinterpret_cast<u64*>(w + L.rec_off);
+  p.chunk_off = reinterpret_cast<u64*>(w + L.chunk_off);
+  p.maxgap = reinterpret_cast<u32*>(w + L.maxgap);
+  p.rec_mode = reinterpret_cast<u32*>(w + L.rec_mode);
+  p.rec_bytes = reinterpret_cast<u64*>(w + L.rec_bytes);
+  p.enc_off = reinterpret_cast<u64*>(w + L.enc_off);
+  p.chunk_hi = reinterpret_cast<u32*>(w + L.chunk_hi);
+  p.chunk_mode = reinterpret_cast<u32*>(w + L.chunk_mode);
+  p.chunk_hioff = reinterpret_cast<u64*>(w + L.chunk_hioff);
+  p.totals = reinterpret_cast<u64*>(w + L.totals);
+  p.status = x->misc + 1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  x->sm_count = 148;
+  cudaDeviceGetAttribute(&x->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  x->grid = x->sm_count * 8;
+  x->plan_counts = nullptr;
+  x->plan_valid = false;
+  *out = x;
+  return SYNC_OK;
+}
+
+int sync_ctx_destroy(sync_ctx* ctx) {
+  delete ctx;
+  return SYNC_OK;
+}
+
+// ------------------------------------------------------------------------ extract
+int sync_extract_workspace_size(uint64_t n, size_t* bytes) {
+  if (!bytes || n >= (1ull << 31)) return SYNC_ERR_ARG;
+  *bytes = kAlign + 8 * ((n + kTile - 1) / kTile) + 8;
+  return SYNC_OK;
+}
+
+int sync_extract(const uint16_t* d_old, const uint16_t* d_new, uint64_t n, uint32_t* d_I, uint16_t* d_V,
+                 uint64_t cap, uint64_t* d_count, void* d_workspace, size_t workspace_bytes, sync_stream_t stream) {
+  size_t need;
+  if (sync_extract_workspace_size(n, &need)) return SYNC_ERR_ARG;
+  if (!d_count || !d_workspace || (n && (!d_old || !d_new))) return SYNC_ERR_ARG;
+  if (workspace_bytes < need) return SYNC_ERR_WORKSPACE;
+  if (!aligned16(d_workspace)) return SYNC_ERR_ALIGNMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  u8* w = static_cast<u8*>(d_workspace);
+  u32* misc = reinterpret_cast<u32*>(w);
+  u64 n_tiles = (n + kTile - 1) / kTile;
+  CK(cudaMemsetAsync(misc, 0, 4, s));  // tile counter (status is sticky until read)
+  CK(cudaMemsetAsync(d_count, 0, 8, s));
+  if (n_tiles) CK(cudaMemsetAsync(w + kAlign, 0, 8 * n_tiles, s));
+  launch_extract_single(d_old, d_new, n, d_I, d_V, cap, d_count, reinterpret_cast<u64*>(w + kAlign), misc, misc + 1,
+                        s);
+  CK(cudaGetLastError());
+  return SYNC_OK;
+}
+
+int sync_extract_status(void* d_workspace, sync_stream_t stream) {
+  if (!d_workspace) return SYNC_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  u32 v = 0;
+  u32* st = reinterpret_cast<u32*>(d_workspace) + 1;
+  CK(cudaStreamSynchronize(s));
+  CK(cudaMemcpy(&v, st, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemset(st, 0, 4));
+  return -(int)v;
+}
+
+int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const uint16_t* const* d_new_ptrs,
+                         uint32_t* d_I, uint16_t* d_V, uint64_t* d_counts, sync_stream_t stream) {
+  if (!x || (x->d.T && (!d_old_ptrs || !d_new_ptrs || !d_counts))) return SYNC_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  x->plan_valid = false;
+  if (x->d.T == 0) return SYNC_OK;
+  CK(cudaMemsetAsync(x->misc, 0, 4, s));
+  CK(cudaMemsetAsync(d_counts, 0, 8ull * x->d.T, s));
+  if (x->d.n_tiles) CK(cudaMemsetAsync(x->ws + x->L.tile_state, 0, 8 * x->d.n_tiles, s));
+  launch_extract_batched(d_old_ptrs, d_new_ptrs, reinterpret_cast<const u64*>(x->ws + x->L.tile_prefix),
+                         x->plan.numel, x->d.T, x->d.n_tiles, d_I, d_V, x->cfg.max_changed, d_counts,
+                         reinterpret_cast<u64*>(x->ws + x->L.tile_state), x->misc, x->misc + 1, s);
+  CK(cudaGetLastError());
+  return SYNC_OK;
+}
+
+// ------------------------------------------------------------------------ compress
+int sync_enc_bound(const sync_manifest* m, const sync_config* c, uint64_t* bytes) {
+  Dims d;
+  int st = check_manifest(m, c, &d);
+  if (st) return st;
+  if (!bytes) return SYNC_ERR_ARG;
+  *bytes = 6 * c->max_changed + 20 * d.max_chunks + 64ull * d.T + 64;
+  return SYNC_OK;
+}
+
+int sync_compress(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts, uint8_t* d_enc,
+                  uint64_t enc_cap, sync_stream_t stream) {
+  if (!x || (x->d.T && (!d_counts || !d_enc))) return SYNC_ERR_ARG;
+  if (!aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  x->plan.enc_cap = enc_cap;
+  launch_plan_scan(x->plan, d_counts, s);
+  if (x->cfg.codec == SYNC_CODEC_COMPRESSED) launch_chunk_stats(x->plan, d_I, d_V, d_counts, x->grid, s);
+  launch_plan_sizes(x->plan, d_counts, s);
+  launch_encode(x->plan, d_I, d_V, d_counts, d_enc, x->grid, s);
+  CK(cudaGetLastError());
+  x->plan_counts = d_counts;
+  x->plan_valid = true;
+  return SYNC_OK;
+}
+
+// ------------------------------------------------------------------------ pack
+static int read_plan(sync_ctx* x, cudaStream_t s) {
+  const u32 T = x->d.T;
+  x->h_rec_bytes.resize(T);
+  x->h_chunk_off.resize(T + 1);
+  x->h_enc_off.resize(T + 1);
+  x->h_totals.resize(16);
+  if (T) {
+    CK(cudaMemcpyAsync(x->h_rec_bytes.data(), x->plan.rec_bytes, 8ull * T, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(x->h_chunk_off.data(), x->plan.chunk_off, 8ull * (T + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(x->h_enc_off.data(), x->plan.enc_off, 8ull * (T + 1), cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaMemcpyAsync(x->h_totals.data(), x->plan.totals, 8 * 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return SYNC_OK;
+}
+
+int sync_buckets_bound(sync_ctx* x, uint64_t* bytes, sync_stream_t stream) {
+  if (!x || !bytes || !x->plan_valid) return SYNC_ERR_ARG;
+  int st = read_plan(x, (cudaStream_t)stream);
+  if (st) return st;
+  u64 nr = x->h_totals[kTotRecords];
+  *bytes = x->h_totals[kTotEnc] + 8 * nr + (nr + 1) * (32 + 16 + kBucketAlign);
+  return SYNC_OK;
+}
+
+int sync_bucket_pack(sync_ctx* x, const uint8_t* d_enc, uint8_t* d_buckets, uint64_t buckets_cap,
+                     uint32_t* n_buckets, uint64_t* h_offsets, uint64_t* h_sizes, uint32_t max_buckets,
+                     sync_stream_t stream) {
+  if (!x || !n_buckets || !x->plan_valid) return SYNC_ERR_ARG;
+  if (!aligned16(d_buckets) || !aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  *n_buckets = 0;
+  int st = read_plan(x, s);
+  if (st) return st;
+  if (x->h_totals[kTotOverflow]) return SYNC_ERR_CAPACITY;
+  const u32 T = x->d.T;
+  const u64 L = x->cfg.bucket_limit;
+  x->h_recs.clear();
+  x->h_bks.clear();
+  // greedy (DESIGN C11): size(bucket) = 32 + pad16(8 n) + Σ record_bytes
+  u64 base = 0;
+  BucketDesc cur{};
+  u64 cur_sum = 0;
+  auto close = [&]() {
+    if (cur.n_records == 0) return;
+    cur.bytes = 32 + pad_to(8ull * cur.n_records, 16) + cur_sum;
+    cur.base = pad_to(base, kBucketAlign);
+    base = cur.base + cur.bytes;
+    cur.seq = (u32)x->h_bks.size();
+    x->h_bks.push_back(cur);
+    cur = BucketDesc{};
+    cur_sum = 0;
+  };
+  for (u32 t = 0; t < T; ++t) {
+    const u64 rb = x->h_rec_bytes[t];
+    if (!rb) continue;
+    if (cur.n_records && 32 + pad_to(8ull * (cur.n_records + 1), 16) + cur_sum + rb > L) close();
+    if (cur.n_records == 0) cur.first_record = (u32)x->h_recs.size();
+    RecordDesc r{};
+    r.src = x->h_enc_off[t];
+    r.bytes = (u32)rb;
+    r.tensor = t;
+    r.first_chunk = cur.n_chunks;
+    r.dst = cur_sum;  // provisional: offset within the record area
+    x->h_recs.push_back(r);
+    cur.n_records++;
+    cur.n_chunks += (u32)(x->h_chunk_off[t + 1] - x->h_chunk_off[t]);
+    cur_sum += rb;
+  }
+  close();
+  const u32 nb = (u32)x->h_bks.size();
+  if (nb > max_buckets || base > buckets_cap) return SYNC_ERR_CAPACITY;
+  for (u32 b = 0; b < nb; ++b) {
+    const BucketDesc& bk = x->h_bks[b];
+    const u64 rec0 = 32 + pad_to(8ull * bk.n_records, 16);
+    for (u32 q = 0; q < bk.n_records; ++q) {
+      RecordDesc& r = x->h_recs[bk.first_record + q];
+      r.dir_offset = (u32)(rec0 + r.dst);
+      r.dst = bk.base + rec0 + r.dst;
+    }
+    if (h_offsets) h_offsets[b] = bk.base;
+    if (h_sizes) h_sizes[b] = bk.bytes;
+  }
+  *n_buckets = nb;
+  if (nb == 0) return SYNC_OK;
+  RecordDesc* d_recs = reinterpret_cast<RecordDesc*>(x->ws + x->L.recs);
+  BucketDesc* d_bks = reinterpret_cast<BucketDesc*>(x->ws + x->L.bks);
+  CK(cudaMemcpyAsync(d_recs, x->h_recs.data(), sizeof(RecordDesc) * x->h_recs.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_bks, x->h_bks.data(), sizeof(BucketDesc) * nb, cudaMemcpyHostToDevice, s));
+  launch_pack(d_enc, d_buckets, d_recs, (u32)x->h_recs.size(), d_bks, nb, x->h_totals[kTotEnc], x->cfg.flags,
+              x->grid, s);
+  if (x->cfg.flags & SYNC_FLAG_CRC) {
+    for (u32 b = 0; b < nb; ++b)
+      if (crc_slots(x->h_bks[b].bytes) > x->d.crc_n) return SYNC_ERR_CAPACITY;
+    crc_fill(d_buckets, x->h_bks.data(), nb, reinterpret_cast<u32*>(x->ws + x->L.crc), s);
+  }
+  CK(cudaGetLastError());
+  // the H2D copies read pageable host vectors: keep them valid until done
+  CK(cudaStreamSynchronize(s));
+  return SYNC_OK;
+}
+
+// ------------------------------------------------------------------------ receive
+static int maybe_crc_check(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, cudaStream_t s, const u32** bad) {
+  *bad = nullptr;
+  if (!(x->cfg.flags & SYNC_FLAG_CRC)) return SYNC_OK;
+  if (crc_slots(bytes) + 1 > x->d.crc_n) return SYNC_ERR_CAPACITY;
+  u32* scratch = reinterpret_cast<u32*>(x->ws + x->L.crc);
+  CK(cudaMemsetAsync(scratch, 0, 4, s));
+  launch_crc_check(d_bucket, bytes, scratch, x->plan.status, s);
+  *bad = scratch;
+  return SYNC_OK;
+}
+
+int sync_bucket_unpack(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, sync_record_view* d_views,
+                       uint32_t max_views, uint32_t* d_n_records, sync_stream_t stream) {
+  if (!x || !d_bucket || !d_views || !d_n_records) return SYNC_ERR_ARG;
+  if (!aligned16(d_bucket)) return SYNC_ERR_ALIGNMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const u32* bad;
+  int st = maybe_crc_check(x, d_bucket, bytes, s, &bad);
+  if (st) return st;
+  launch_unpack(d_bucket, bytes, x->d.T, x->plan.numel, d_views, max_views, d_n_records, x->plan.status, s);
+  CK(cudaGetLastError());
+  return SYNC_OK;
+}
+
+int sync_decompress(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, uint32_t* d_I, uint16_t* d_V,
+                    uint64_t d_cap, sync_stream_t stream) {
+  if (!x || !d_bucket) return SYNC_ERR_ARG;
+  if (!aligned16(d_bucket)) return SYNC_ERR_ALIGNMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const u32* bad;
+  int st = maybe_crc_check(x, d_bucket, bytes, s, &bad);
+  if (st) return st;
+  sync_record_view* views = reinterpret_cast<sync_record_view*>(x->ws + x->L.views);
+  u32* nv = reinterpret_cast<u32*>(x->ws + x->L.nviews);
+  launch_unpack(d_bucket, bytes, x->d.T, x->plan.numel, views, x->d.T, nv, x->plan.status, s);
+  launch_decode(d_bucket, bytes, x->d.T, x->plan.numel, nullptr, views, d_I, d_V, d_cap, x->plan.status, bad,
+                x->grid, s);
+  CK(cudaGetLastError());
+  return SYNC_OK;
+}
+
+int sync_decompress_apply(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, uint16_t* const* d_weight_ptrs,
+                          sync_stream_t stream) {
+  if (!x || !d_bucket || !d_weight_ptrs) return SYNC_ERR_ARG;
+  if (!aligned16(d_bucket)) return SYNC_ERR_ALIGNMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const u32* bad;
+  int st = maybe_crc_check(x, d_bucket, bytes, s, &bad);
+  if (st) return st;
+  launch_decode(d_bucket, bytes, x->d.T, x->plan.numel, d_weight_ptrs, nullptr, nullptr, nullptr, 0,
+                x->plan.status, bad, x->grid, s);
+  CK(cudaGetLastError());
+  return SYNC_OK;
+}
+
+// ------------------------------------------------------------------------ apply / commit
+int sync_apply(uint16_t* d_W, const uint32_t* d_I, const uint16_t* d_V, uint64_t count, uint64_t numel,
+               uint32_t* d_status, sync_stream_t stream) {
+  if (count && (!d_W || !d_I || !d_V)) return SYNC_ERR_ARG;
+  if (numel >= (1ull << 31)) return SYNC_ERR_ARG;
+  if (!aligned16(d_W) || !aligned16(d_I) || !aligned16(d_V)) return SYNC_ERR_ALIGNMENT;
+  launch_apply(d_W, d_I, d_V, count, numel, d_status, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return SYNC_OK;
+}
+
+int sync_commit_snapshot(uint16_t* d_snapshot, const uint32_t* d_I, const uint16_t* d_V, uint64_t count,
+                         uint64_t numel, uint32_t* d_status, sync_stream_t stream) {
+  return sync_apply(d_snapshot, d_I, d_V, count, numel, d_status, stream);
+}
+
+int sync_commit_snapshot_batched(sync_ctx* x, uint16_t* const* d_snapshot_ptrs, const uint32_t* d_I,
+                                 const uint16_t* d_V, const uint64_t* d_counts, sync_stream_t stream) {
+  if (!x || (x->d.T && (!d_snapshot_ptrs || !d_counts))) return SYNC_ERR_ARG;
+  if (x->d.T == 0) return SYNC_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(x->plan_valid && x->plan_counts == d_counts)) {
+    launch_plan_scan(x->plan, d_counts, s);
+    x->plan_valid = false;
+  }
+  launch_commit_batched(x->plan, d_snapshot_ptrs, d_I, d_V, x->grid, s);
+  CK(cudaGetLastError());
+  return SYNC_OK;
+}
+
+// ------------------------------------------------------------------------ status
+int sync_status(sync_ctx* x, sync_stream_t stream) {
+  if (!x) return SYNC_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  u32 v = 0;
+  CK(cudaStreamSynchronize(s));
+  CK(cudaMemcpy(&v, x->misc + 1, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemset(x->misc + 1, 0, 4));
+  return -(int)v;
+}
+
+int sync_ctx_stats(sync_ctx* x, sync_stats* out, sync_stream_t stream) {
+  if (!x || !out) return SYNC_ERR_ARG;
+  u64 t[16];
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  CK(cudaMemcpy(t, x->plan.totals, sizeof(t), cudaMemcpyDeviceToHost));
+  out->nnz = t[kTotNnz];
+  out->n_records = t[kTotRecords];
+  out->n_delta16 = t[kTotDelta16];
+  out->n_abs32 = t[kTotAbs32];
+  out->n_chunks = t[kTotChunks];
+  out->n_chunks_rans = t[kTotRansChunks];
+  out->enc_bytes = t[kTotEnc];
+  out->index_bytes = t[kTotIndexBytes];
+  out->value_bytes = t[kTotValueBytes];
+  return SYNC_OK;
+}
+
+const char* sync_strerror(int status) {
+  switch (status) {
+    case SYNC_OK: return "ok";
+    case SYNC_ERR_ARG: return "bad argument";
+    case SYNC_ERR_ALIGNMENT: return "device pointer not 16-byte aligned";
+    case SYNC_ERR_DTYPE: return "unsupported dtype (BF16 only)";
+    case SYNC_ERR_WORKSPACE: return "workspace too small";
+    case SYNC_ERR_CUDA: return "CUDA runtime error";
+    case SYNC_ERR_INDEX_RANGE: return "index out of range";
+    case SYNC_ERR_CAPACITY: return "output capacity exceeded";
+    case SYNC_ERR_CORRUPT: return "corrupt record or rANS stream";
+    case SYNC_ERR_BAD_MAGIC: return "bad bucket magic";
+    case SYNC_ERR_VERSION: return "unsupported bucket version";
+    case SYNC_ERR_TRUNCATED: return "truncated bucket";
+    case SYNC_ERR_CRC: return "CRC-32 mismatch";
+    default: return "unknown status";
+  }
+}
+
+uint64_t sync_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

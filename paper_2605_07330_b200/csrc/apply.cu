@@ -1,0 +1,68 @@
+// apply.cu — K5/K6 plain scatter (rows a8 + a9; Alg. 3 l.6; snapshot
+// commit after the transfer, P:300 / DESIGN C13).
+//
+// W[I[k]] <- V[k]. Scattered 2-byte stores: the cost is the partial-sector
+// read-modify-write of every touched 32-byte sector, not the I/V stream.
+// The batched commit walks the raw (I, V) of sync_extract_batched chunk by
+// chunk (one CTA per 16384 values, tensor found by a warp search over the
+// chunk offsets of the plan).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ss {
+
+__global__ void __launch_bounds__(256) k_apply(u16* W, const u32* I, const u16* V, u64 count, u64 numel,
+                                              u32* status) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += stride) {
+    u32 idx = I[k];
+    if (idx < numel) W[idx] = V[k];
+    else bad = true;
+  }
+  if (bad) latch(status, SYNC_ERR_INDEX_RANGE);
+}
+
+__global__ void __launch_bounds__(256) k_commit_batched(Plan p, u16* const* snaps, const u32* I, const u16* V) {
+  __shared__ u32 s_t;
+  const u64 n_chunks = p.totals[kTotChunks];
+  const u64* co = p.chunk_off;
+  for (u64 g = blockIdx.x; g < n_chunks; g += gridDim.x) {
+    if (threadIdx.x < 32) {
+      u32 t = warp_upper_search(p.n_tensors, g, [&](u32 i) { return co[i]; });
+      if (threadIdx.x == 0) s_t = t;
+    }
+    __syncthreads();
+    const u32 t = s_t;
+    const u64 nnz = p.rec_off[t + 1] - p.rec_off[t];
+    const u64 p0 = (g - co[t]) * kChunk;
+    const u64 nk = (nnz - p0) < kChunk ? (nnz - p0) : kChunk;
+    const u32* Ir = I + p.rec_off[t] + p0;
+    const u16* Vr = V + p.rec_off[t] + p0;
+    u16* S = snaps[t];
+    const u64 lim = p.numel[t];
+    bool bad = false;
+    for (u64 q = threadIdx.x; q < nk; q += blockDim.x) {
+      u32 idx = Ir[q];
+      if (idx < lim) S[idx] = Vr[q];
+      else bad = true;
+    }
+    if (bad) latch(p.status, SYNC_ERR_INDEX_RANGE);
+    __syncthreads();
+  }
+}
+
+void launch_apply(u16* W, const u32* I, const u16* V, u64 count, u64 numel, u32* status, cudaStream_t s) {
+  if (count == 0) return;
+  u64 blocks = (count + 255) / 256;
+  int grid = (int)(blocks < 148ull * 16 ? blocks : 148ull * 16);
+  k_apply<<<grid, 256, 0, s>>>(W, I, V, count, numel, status);
+  count_launch();
+}
+
+void launch_commit_batched(const Plan& p, u16* const* snaps, const u32* I, const u16* V, int grid, cudaStream_t s) {
+  k_commit_batched<<<grid, 256, 0, s>>>(p, snaps, I, V);
+  count_launch();
+}
+
+}  // namespace ss

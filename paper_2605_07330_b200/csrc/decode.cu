@@ -1,0 +1,371 @@
+// decode.cu — K5: bucket unpack, decompression and fused scatter-apply
+// (rows a7 + a8; Alg. 3 l.5-6; "exact inverse" and "fused kernel").
+//
+// One warp per chunk of the bucket (the record directory maps a global chunk
+// index to its record with a 32-ary warp search). For a rANS hi block the
+// warp builds the slot -> symbol table in shared memory, then decodes 32
+// symbols per step (lane j owns positions 32g + j); renormalisation words are
+// taken in lane order 31..0 with one ballot, exactly as DESIGN §3.3. The lo
+// byte and the DELTA16 delta of each position are plain coalesced loads; the
+// index is rebuilt with a warp inclusive scan from the chunk's base_idx, and
+// V = hi << 8 | lo is scattered straight into the weights (APPLY) or written
+// out as (I, V) (EMIT, the debug path). Every chunk checks the end states
+// (all lanes back at 2^16) and that every word was consumed.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ss {
+
+struct BucketHdr {
+  u32 n_records, n_chunks, flags;
+  u64 bytes;
+};
+
+__device__ __forceinline__ int read_bucket_header(const u8* bk, u64 avail, BucketHdr* h) {
+  if (avail < 32) return SYNC_ERR_TRUNCATED;
+  const u32* w = reinterpret_cast<const u32*>(bk);
+  if (w[0] != kMagic) return SYNC_ERR_BAD_MAGIC;
+  if ((w[1] & 0xFFFFu) != kVersion) return SYNC_ERR_VERSION;
+  h->flags = w[1] >> 16;
+  h->n_records = w[3];
+  h->n_chunks = w[4];
+  h->bytes = *reinterpret_cast<const u64*>(bk + 24);
+  if (h->bytes > avail || h->bytes < 32 + pad_to(8ull * h->n_records, 16)) return SYNC_ERR_TRUNCATED;
+  return SYNC_OK;
+}
+
+struct RecHdr {
+  u32 tid, nnz, rb, mode, dtype, codec;
+};
+
+__device__ __forceinline__ bool read_record(const u8* bk, const BucketHdr& h, u32 ro, u32 n_tensors,
+                                            const u64* numel, RecHdr* r) {
+  if ((ro & 15u) || (u64)ro + 16 > h.bytes) return false;
+  const u32* w = reinterpret_cast<const u32*>(bk + ro);
+  r->tid = w[0];
+  r->nnz = w[1];
+  r->rb = w[2];
+  r->mode = w[3] & 0xFFu;
+  r->dtype = (w[3] >> 8) & 0xFFu;
+  r->codec = (w[3] >> 16) & 0xFFu;
+  if (r->rb < 16 || (r->rb & 15u) || (u64)ro + r->rb > h.bytes) return false;
+  if (r->tid >= n_tensors || r->dtype != 1 || r->mode > 1 || r->codec > 1 || r->nnz == 0) return false;
+  if ((u64)r->nnz > numel[r->tid]) return false;
+  if (r->codec == SYNC_CODEC_RAW) return r->mode == 1 && 16 + 6ull * r->nnz <= r->rb;
+  const u64 nch = (r->nnz + kChunk - 1) / kChunk;
+  const u64 ib = (r->mode ? 4ull : 2ull) * r->nnz;
+  return 16 + pad_to(ib, 4) + pad_to(r->nnz, 4) + 16 * nch <= r->rb;
+}
+
+// ---------------------------------------------------------------------------- unpack
+__global__ void __launch_bounds__(1024) k_unpack(const u8* bk, u64 bytes, u32 n_tensors, const u64* numel,
+                                                 sync_record_view* views, u32 max_views, u32* n_out, u32* status) {
+  __shared__ u64 s_w[33];
+  __shared__ int s_err;
+  BucketHdr h;
+  int err = read_bucket_header(bk, bytes, &h);
+  if (err != SYNC_OK || h.n_records > max_views) {
+    if (threadIdx.x == 0) {
+      latch(status, err != SYNC_OK ? err : SYNC_ERR_CAPACITY);
+      *n_out = 0;
+    }
+    return;
+  }
+  if (threadIdx.x == 0) s_err = 0;
+  __syncthreads();
+  const u32* dir = reinterpret_cast<const u32*>(bk + 32);
+  u64 carry = 0;
+  u32 chunk_carry = 0;
+  for (u32 b = 0; b < h.n_records; b += blockDim.x) {
+    u32 q = b + threadIdx.x;
+    RecHdr r{};
+    u64 nnz = 0;
+    if (q < h.n_records) {
+      u32 ro = dir[2 * q];
+      if (!read_record(bk, h, ro, n_tensors, numel, &r)) {
+        s_err = 1;
+      } else {
+        nnz = r.nnz;
+        sync_record_view v;
+        v.tensor_id = r.tid;
+        v.nnz = r.nnz;
+        v.offset = ro;
+        v.record_bytes = r.rb;
+        v.first_chunk = dir[2 * q + 1];
+        v.idx_mode = (u8)r.mode;
+        v.dtype = (u8)r.dtype;
+        v.codec = (u8)r.codec;
+        v.reserved = 0;
+        v.out_offset = 0;
+        views[q] = v;
+      }
+    }
+    // inclusive/exclusive scan of nnz and chunk counts (block of 1024)
+    const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u64 packed = (nnz << 24) | ((nnz + kChunk - 1) / kChunk);  // chunks per record < 2^24
+    u64 inc = warp_incl_scan64(packed);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      u64 w = lane < (blockDim.x >> 5) ? s_w[lane] : 0;
+      u64 wi = warp_incl_scan64(w);
+      s_w[lane] = wi - w;
+      if (lane == 31) s_w[32] = wi;
+    }
+    __syncthreads();
+    u64 ex = s_w[warp] + inc - packed;
+    if (q < h.n_records) {
+      views[q].out_offset = carry + (ex >> 24);
+      if (views[q].first_chunk != chunk_carry + (u32)(ex & 0xFFFFFFull)) s_err = 1;
+    }
+    u64 tot = s_w[32];
+    carry += tot >> 24;
+    chunk_carry += (u32)(tot & 0xFFFFFFull);
+    __syncthreads();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_err || chunk_carry != h.n_chunks) {
+      latch(status, SYNC_ERR_CORRUPT);
+      *n_out = 0;
+    } else {
+      *n_out = h.n_records;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- decode
+struct DecodeModel {
+  u8 slot2sym[kM];
+  u16 freq[256];
+  u16 cum[256];
+};
+
+template <bool kApply>
+__global__ void __launch_bounds__(256) k_decode(const u8* bk, u64 bytes, u32 n_tensors, const u64* numel,
+                                               u16* const* weights, const sync_record_view* views, u32* I_out,
+                                               u16* V_out, u64 out_cap, u32* status, const u32* crc_bad) {
+  __shared__ DecodeModel s_dm[8];
+  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  DecodeModel& dm = s_dm[warp];
+  if (crc_bad && *crc_bad) return;
+  BucketHdr h;
+  int herr = read_bucket_header(bk, bytes, &h);
+  if (herr != SYNC_OK) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, herr);
+    return;
+  }
+  const u32* dir = reinterpret_cast<const u32*>(bk + 32);
+  const u64 nwarps = (u64)gridDim.x * (blockDim.x >> 5);
+  for (u64 g = (u64)blockIdx.x * (blockDim.x >> 5) + warp; g < h.n_chunks; g += nwarps) {
+    if (h.n_records == 0) break;
+    const u32 q = warp_upper_search(h.n_records, g, [&](u32 i) { return (u64)dir[2 * i + 1]; });
+    const u32 ro = dir[2 * q];
+    RecHdr r;
+    const u64 fc = dir[2 * q + 1];
+    bool ok = read_record(bk, h, ro, n_tensors, numel, &r);
+    const u64 nch = ok ? (r.nnz + kChunk - 1) / kChunk : 0;
+    const u64 k = g - fc;
+    if (!ok || k >= nch) {
+      if (lane == 0) latch(status, SYNC_ERR_CORRUPT);
+      continue;
+    }
+    const u8* rec = bk + ro;
+    const u64 nnz = r.nnz;
+    const u64 p0 = k * kChunk;
+    const u32 nk = (u32)((nnz - p0) < kChunk ? (nnz - p0) : kChunk);
+    const u64 lim = numel[r.tid];
+    u16* W = nullptr;
+    u32* Io = nullptr;
+    u16* Vo = nullptr;
+    if (kApply) {
+      W = weights[r.tid];
+    } else {
+      const u64 oo = views[q].out_offset + p0;
+      if (oo + nk > out_cap) {
+        if (lane == 0) latch(status, SYNC_ERR_CAPACITY);
+        continue;
+      }
+      Io = I_out + oo;
+      Vo = V_out + oo;
+    }
+    bool bad = false;
+
+    if (r.codec == SYNC_CODEC_RAW) {
+      const u32* Ir = reinterpret_cast<const u32*>(rec + 16) + p0;
+      const u16* Vr = reinterpret_cast<const u16*>(rec + 16 + 4 * nnz) + p0;
+      for (u32 qq = lane; qq < nk; qq += 32) {
+        u32 idx = Ir[qq];
+        u16 v = Vr[qq];
+        if (kApply) {
+          if (idx < lim) W[idx] = v;
+          else bad = true;
+        } else {
+          Io[qq] = idx;
+          Vo[qq] = v;
+        }
+      }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) latch(status, SYNC_ERR_INDEX_RANGE);
+      continue;
+    }
+
+    const u64 ib = (r.mode ? 4ull : 2ull) * nnz;
+    const u64 lo_off = 16 + pad_to(ib, 4);
+    const u64 dir_off = lo_off + pad_to(nnz, 4);
+    const u32* de = reinterpret_cast<const u32*>(rec + dir_off + 16 * k);
+    const u32 hi_off = de[0], hb = de[1], cm = de[2], base = de[3];
+    bool corrupt = ((u64)hi_off + hb > r.rb) || (hi_off & 3u) || cm > 1 || (cm == 0 && hb != nk);
+    const u8* blk = rec + hi_off;
+    const u8* lo = rec + lo_off + p0;
+    const u16* D = reinterpret_cast<const u16*>(rec + 16) + p0;
+    const u32* A = reinterpret_cast<const u32*>(rec + 16) + p0;
+
+    u32 x = kLow, nwords = 0;
+    const u16* words = nullptr;
+    if (!corrupt && cm == 1) {
+      if (hb < 136) {
+        corrupt = true;
+      } else {
+        const u32* bh = reinterpret_cast<const u32*>(blk);
+        x = bh[lane];
+        nwords = bh[32];
+        u32 nsym = bh[33] & 0xFFFFu;
+        if (nsym < 1 || nsym > 256 || 136ull + 4ull * nsym + 2ull * nwords != hb) {
+          corrupt = true;
+        } else {
+          // entries owned lane-contiguously: lane handles entries [8*lane, 8*lane+8)
+          u32 fsum = 0, e_s[8], e_f[8];
+          bool eok = true;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            u32 e = lane * 8 + j;
+            e_s[j] = 0;
+            e_f[j] = 0;
+            if (e < nsym) {
+              u32 ent = bh[34 + e];
+              e_s[j] = ent & 0xFFFFu;
+              e_f[j] = ent >> 16;
+              if (e_s[j] > 255 || e_f[j] == 0) eok = false;
+              fsum += e_f[j];
+            }
+          }
+          // ascending symbols: compare with the previous entry
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            u32 e = lane * 8 + j;
+            if (e < nsym && e > 0) {
+              u32 ps = (j > 0) ? e_s[j - 1] : 0xFFFFFFFFu;
+              if (j == 0) ps = bh[34 + e - 1] & 0xFFFFu;
+              if (e_s[j] <= ps) eok = false;
+            }
+          }
+          u32 incl = warp_incl_scan(fsum);
+          u32 total = __shfl_sync(0xffffffffu, incl, 31);
+          if (!__all_sync(0xffffffffu, eok) || total != kM) {
+            corrupt = true;
+          } else {
+            u32 c = incl - fsum;
+            for (u32 s = lane; s < 256; s += 32) dm.freq[s] = 0;
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (e_f[j]) {
+                dm.freq[e_s[j]] = (u16)e_f[j];
+                dm.cum[e_s[j]] = (u16)c;
+                c += e_f[j];
+              }
+            }
+            __syncwarp();
+            // fill slot -> symbol: entry by entry, lanes stride the entry's slot range
+            for (u32 e = 0; e < nsym; ++e) {
+              u32 ent = bh[34 + e];
+              u32 s = ent & 0xFFFFu;
+              u32 f = ent >> 16;
+              u32 c0 = dm.cum[s];
+              for (u32 sl = lane; sl < f; sl += 32) dm.slot2sym[c0 + sl] = (u8)s;
+            }
+            __syncwarp();
+            words = reinterpret_cast<const u16*>(blk + 136 + 4 * nsym);
+          }
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, corrupt)) {
+      if (lane == 0) latch(status, SYNC_ERR_CORRUPT);
+      continue;
+    }
+
+    const u32 G = (nk + 31) / 32;
+    u32 ptr = 0;
+    u32 carry = (r.mode == 0) ? base : 0u;
+    bool range_bad = false, word_bad = false;
+    for (u32 gs = 0; gs < G; ++gs) {
+      const u32 qq = gs * 32 + lane;
+      const bool act = qq < nk;
+      u32 lob = act ? lo[qq] : 0u;
+      u32 d = 0, idx = 0;
+      if (r.mode == 0) d = act ? D[qq] : 0u;
+      else idx = act ? A[qq] : 0u;
+      u32 s;
+      if (cm == 1) {
+        s = 0;
+        if (act) {
+          u32 slot = x & (kM - 1);
+          s = dm.slot2sym[slot];
+          x = (u32)dm.freq[s] * (x >> 12) + slot - dm.cum[s];
+        }
+        bool need = act && x < kLow;
+        u32 nm = __ballot_sync(0xffffffffu, need);
+        if (need) {
+          u32 pos = ptr + __popc(nm >> lane >> 1);
+          if (pos < nwords) x = (x << 16) | words[pos];
+          else word_bad = true;
+        }
+        ptr += __popc(nm);
+      } else {
+        s = act ? blk[qq] : 0u;
+      }
+      if (r.mode == 0) {
+        u32 sc = warp_incl_scan(d);
+        idx = carry + sc;
+        carry = __shfl_sync(0xffffffffu, idx, 31);
+      }
+      if (act) {
+        u16 v = (u16)((s << 8) | lob);
+        if (kApply) {
+          if (idx < lim) W[idx] = v;
+          else range_bad = true;
+        } else {
+          Io[qq] = idx;
+          Vo[qq] = v;
+          if (idx >= lim) range_bad = true;
+        }
+      }
+    }
+    if (cm == 1) {
+      bool endbad = word_bad || x != kLow || ptr != nwords;
+      if (__any_sync(0xffffffffu, endbad) && lane == 0) latch(status, SYNC_ERR_CORRUPT);
+    }
+    if (__any_sync(0xffffffffu, range_bad) && lane == 0) latch(status, SYNC_ERR_INDEX_RANGE);
+  }
+}
+
+void launch_unpack(const u8* bucket, u64 bytes, u32 n_tensors, const u64* numel, sync_record_view* views,
+                   u32 max_views, u32* n_records, u32* status, cudaStream_t s) {
+  k_unpack<<<1, 1024, 0, s>>>(bucket, bytes, n_tensors, numel, views, max_views, n_records, status);
+  count_launch();
+}
+
+void launch_decode(const u8* bucket, u64 bytes, u32 n_tensors, const u64* numel, u16* const* weights,
+                   const sync_record_view* views, u32* I_out, u16* V_out, u64 out_cap, u32* status,
+                   const u32* crc_bad, int grid, cudaStream_t s) {
+  if (weights)
+    k_decode<true><<<grid, 256, 0, s>>>(bucket, bytes, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0,
+                                        status, crc_bad);
+  else
+    k_decode<false><<<grid, 256, 0, s>>>(bucket, bytes, n_tensors, numel, nullptr, views, I_out, V_out, out_cap,
+                                         status, crc_bad);
+  count_launch();
+}
+
+}  // namespace ss

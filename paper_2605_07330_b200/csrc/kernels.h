@@ -1,0 +1,93 @@
+// kernels.h — host-side launchers of the sm_100a kernels (internal to libsparsesync).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sparsesync.h"
+
+namespace ss {
+
+void count_launch();
+
+// Device views of the workspace (all arrays live in the caller's workspace).
+struct Plan {
+  uint32_t n_tensors;
+  uint64_t cap;                  // I/V capacity
+  uint32_t codec;
+  uint64_t max_chunks;
+  uint64_t enc_cap;              // capacity of the caller's enc buffer (bytes)
+  const uint64_t* numel;         // [T]
+  uint64_t* rec_off;             // [T+1] value offset of tensor t in I/V
+  uint64_t* chunk_off;           // [T+1] first global chunk of tensor t
+  uint32_t* maxgap;              // [T]
+  uint32_t* rec_mode;            // [T] DELTA16 / ABS32
+  uint64_t* rec_bytes;           // [T]
+  uint64_t* enc_off;             // [T+1]
+  uint32_t* chunk_hi;            // [max_chunks] hi block bytes (unpadded)
+  uint32_t* chunk_mode;          // [max_chunks]
+  uint64_t* chunk_hioff;         // [max_chunks+1] exclusive prefix of pad4(chunk_hi)
+  uint64_t* totals;              // [16]
+  uint32_t* status;
+};
+
+enum TotalsIdx {
+  kTotNnz = 0, kTotChunks = 1, kTotRecords = 2, kTotEnc = 3, kTotDelta16 = 4, kTotAbs32 = 5,
+  kTotRansChunks = 6, kTotOverflow = 7, kTotIndexBytes = 8, kTotValueBytes = 9
+};
+
+void launch_extract_batched(const uint16_t* const* d_old, const uint16_t* const* d_new, const uint64_t* tile_prefix,
+                            const uint64_t* numel, uint32_t n_tensors, uint64_t n_tiles, uint32_t* I, uint16_t* V,
+                            uint64_t cap, uint64_t* counts, uint64_t* tile_state, uint32_t* tile_counter,
+                            uint32_t* status, cudaStream_t s);
+void launch_extract_single(const uint16_t* d_old, const uint16_t* d_new, uint64_t n, uint32_t* I, uint16_t* V,
+                           uint64_t cap, uint64_t* count, uint64_t* tile_state, uint32_t* tile_counter,
+                           uint32_t* status, cudaStream_t s);
+
+// plan.cu
+void launch_plan_scan(const Plan& p, const uint64_t* counts, cudaStream_t s);
+void launch_chunk_stats(const Plan& p, const uint32_t* I, const uint16_t* V, const uint64_t* counts, int grid,
+                        cudaStream_t s);
+void launch_plan_sizes(const Plan& p, const uint64_t* counts, cudaStream_t s);
+
+// encode.cu
+void launch_encode(const Plan& p, const uint32_t* I, const uint16_t* V, const uint64_t* counts, uint8_t* enc,
+                   int grid, cudaStream_t s);
+
+// pack.cu
+struct BucketDesc {              // host-computed bucket plan (uploaded)
+  uint64_t base;                 // byte offset of the bucket in the caller's buffer
+  uint64_t bytes;
+  uint32_t n_records;
+  uint32_t n_chunks;
+  uint32_t first_record;         // index into the record table
+  uint32_t seq;
+};
+struct RecordDesc {              // one per record, manifest order
+  uint64_t src;                  // offset in enc
+  uint64_t dst;                  // offset in the bucket buffer
+  uint32_t bytes;
+  uint32_t dir_offset;           // record offset from its bucket start
+  uint32_t first_chunk;          // within its bucket
+  uint32_t tensor;
+};
+void launch_pack(const uint8_t* enc, uint8_t* buckets, const RecordDesc* recs, uint32_t n_records,
+                 const BucketDesc* bks, uint32_t n_buckets, uint64_t enc_total, uint32_t flags, int grid,
+                 cudaStream_t s);
+void crc_fill(uint8_t* buckets, const BucketDesc* h_bks, uint32_t n_buckets, uint32_t* scratch, cudaStream_t s);
+
+// decode.cu
+void launch_crc_check(const uint8_t* bucket, uint64_t bytes, uint32_t* scratch, uint32_t* status, cudaStream_t s);
+void launch_unpack(const uint8_t* bucket, uint64_t bytes, uint32_t n_tensors, const uint64_t* numel,
+                   sync_record_view* views, uint32_t max_views, uint32_t* n_records, uint32_t* status,
+                   cudaStream_t s);
+void launch_decode(const uint8_t* bucket, uint64_t bytes, uint32_t n_tensors, const uint64_t* numel,
+                   uint16_t* const* weights, const sync_record_view* views, uint32_t* I_out, uint16_t* V_out,
+                   uint64_t out_cap, uint32_t* status, const uint32_t* crc_bad, int grid, cudaStream_t s);
+
+// apply.cu
+void launch_apply(uint16_t* W, const uint32_t* I, const uint16_t* V, uint64_t count, uint64_t numel,
+                  uint32_t* status, cudaStream_t s);
+void launch_commit_batched(const Plan& p, uint16_t* const* snaps, const uint32_t* I, const uint16_t* V, int grid,
+                           cudaStream_t s);
+
+}  // namespace ss

@@ -1,0 +1,195 @@
+// pack.cu — K4: bucket assembly (row a5) and CRC-32 (C11, C14).
+//
+// The greedy bucket plan is computed on the host from the record sizes (the
+// one host sync point of a sync; it yields the bucket sizes the transport
+// needs anyway). These kernels then write every byte of the buckets:
+//  * k_pack_meta : header (32 B) + record directory + directory padding
+//  * k_pack_copy : records, 16 B units, enc -> bucket position
+//  * k_crc_seg / k_crc_fin : parallel CRC-32/IEEE of [32, bytes) — per-segment
+//    raw CRCs combined with multiplications by x^(8n) mod P (the CRC is linear
+//    over GF(2)), then the init/xorout terms.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ss {
+
+constexpr u32 kPoly = 0xEDB88320u;  // reflected IEEE polynomial
+constexpr u32 kCrcSeg = 4096;       // bytes per segment (one CTA)
+constexpr int kCrcThreads = 128;    // 32 bytes per thread
+
+struct CrcTables {
+  u32 x2n[32];  // x^(2^k) mod P, reflected
+};
+
+// a * b mod P in the reflected representation (bit 31 = x^0); fixed 32 steps.
+__host__ __device__ __forceinline__ u32 multmodp(u32 a, u32 b) {
+  u32 r = 0;
+  for (int i = 0; i < 32; ++i) {
+    if (a & (0x80000000u >> i)) r ^= b;
+    b = (b & 1) ? (b >> 1) ^ kPoly : b >> 1;
+  }
+  return r;
+}
+
+// x^(8n) mod P
+__device__ __forceinline__ u32 x8n(const CrcTables& tb, u64 n) {
+  u32 r = 1u << 31;
+  int k = 3;
+  while (n) {
+    if (n & 1) r = multmodp(tb.x2n[k & 31], r);
+    n >>= 1;
+    ++k;
+  }
+  return r;
+}
+
+// Raw CRC (init 0, no xorout) of each right-aligned segment of data[0, len):
+// segment s covers [len - (S - s)*kCrcSeg, len - (S - 1 - s)*kCrcSeg); bytes
+// before 0 are virtual zeros (leading zeros leave an init-0 CRC unchanged).
+__global__ void __launch_bounds__(kCrcThreads) k_crc_seg(const u8* data, u64 len, u32* seg_crc, CrcTables tb) {
+  __shared__ u32 table[256];
+  __shared__ u32 s_c[kCrcThreads];
+  for (u32 i = threadIdx.x; i < 256; i += blockDim.x) {
+    u32 c = i;
+    for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (kPoly & (0u - (c & 1u)));
+    table[i] = c;
+  }
+  __syncthreads();
+  const u64 S = (len + kCrcSeg - 1) / kCrcSeg;
+  const u64 s = blockIdx.x;
+  const long long seg_start = (long long)len - (long long)(S - s) * kCrcSeg;
+  const long long start = seg_start + (long long)threadIdx.x * 32;
+  u32 c = 0;
+  for (int b = 0; b < 32; ++b) {
+    long long pos = start + b;
+    u32 byte = pos >= 0 ? data[pos] : 0u;
+    c = table[(c ^ byte) & 0xFFu] ^ (c >> 8);
+  }
+  // ordered combine of 32-byte pieces: crc(A||B) = crc(A) * x^(8|B|) ^ crc(B)
+  s_c[threadIdx.x] = c;
+  __syncthreads();
+  for (u32 w = 1; w < kCrcThreads; w <<= 1) {
+    u32 v = 0;
+    bool active = (threadIdx.x % (2 * w)) == 0;
+    if (active) v = multmodp(s_c[threadIdx.x], x8n(tb, (u64)32 * w)) ^ s_c[threadIdx.x + w];
+    __syncthreads();
+    if (active) s_c[threadIdx.x] = v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) seg_crc[s] = s_c[0];
+}
+
+// Combine segments and apply init/xorout; store into *out (or compare).
+__global__ void k_crc_fin(const u32* seg_crc, u64 len, CrcTables tb, u32* out, const u8* hdr_crc, u32* status,
+                          u32* bad) {
+  if (threadIdx.x != 0) return;
+  const u64 S = (len + kCrcSeg - 1) / kCrcSeg;
+  u32 raw = 0;
+  const u32 shift = x8n(tb, kCrcSeg);
+  for (u64 s = 0; s < S; ++s) raw = multmodp(raw, shift) ^ seg_crc[s];
+  u32 crc = raw ^ multmodp(0xFFFFFFFFu, x8n(tb, len)) ^ 0xFFFFFFFFu;
+  if (out) *out = crc;
+  if (hdr_crc) {
+    u32 want = (u32)hdr_crc[0] | ((u32)hdr_crc[1] << 8) | ((u32)hdr_crc[2] << 16) | ((u32)hdr_crc[3] << 24);
+    if (want != crc) {
+      latch(status, SYNC_ERR_CRC);
+      if (bad) *bad = 1;
+    }
+  }
+}
+
+static CrcTables host_crc_tables() {
+  CrcTables tb;
+  u32 p = 1u << 30;  // x^1
+  tb.x2n[0] = p;
+  for (int k = 1; k < 32; ++k) tb.x2n[k] = p = multmodp(p, p);
+  return tb;
+}
+
+// scratch: >= ceil(len / 4096) u32
+static void crc_bucket(const u8* bucket, u64 bytes, u32* scratch, u32* out, const u8* hdr_crc, u32* status,
+                       u32* bad, cudaStream_t s) {
+  static const CrcTables tb = host_crc_tables();
+  u64 len = bytes > 32 ? bytes - 32 : 0;
+  if (len == 0) {
+    k_crc_fin<<<1, 32, 0, s>>>(scratch, 0, tb, out, hdr_crc, status, bad);
+    count_launch();
+    return;
+  }
+  u64 S = (len + kCrcSeg - 1) / kCrcSeg;
+  k_crc_seg<<<(unsigned)S, kCrcThreads, 0, s>>>(bucket + 32, len, scratch, tb);
+  k_crc_fin<<<1, 32, 0, s>>>(scratch, len, tb, out, hdr_crc, status, bad);
+  count_launch();
+  count_launch();
+}
+
+__global__ void k_pack_meta(u8* buckets, const RecordDesc* recs, const BucketDesc* bks, u32 flags) {
+  const BucketDesc b = bks[blockIdx.x];
+  u8* bk = buckets + b.base;
+  if (threadIdx.x == 0) {
+    u32* h = reinterpret_cast<u32*>(bk);
+    h[0] = kMagic;
+    h[1] = kVersion | ((flags & SYNC_FLAG_CRC) << 16);
+    h[2] = b.seq;
+    h[3] = b.n_records;
+    h[4] = b.n_chunks;
+    h[5] = 0;  // CRC filled by k_crc_fin
+    *reinterpret_cast<u64*>(bk + 24) = b.bytes;
+  }
+  u32* dir = reinterpret_cast<u32*>(bk + 32);
+  for (u32 q = threadIdx.x; q < b.n_records; q += blockDim.x) {
+    const RecordDesc r = recs[b.first_record + q];
+    dir[2 * q] = r.dir_offset;
+    dir[2 * q + 1] = r.first_chunk;
+  }
+  u64 dir_end = 32 + 8ull * b.n_records, dir_pad = 32 + pad_to(8ull * b.n_records, 16);
+  for (u64 q = dir_end + threadIdx.x; q < dir_pad; q += blockDim.x) bk[q] = 0;
+}
+
+// 16-byte units of enc; each warp handles 32 consecutive units.
+__global__ void __launch_bounds__(256) k_pack_copy(const uint4* enc, u8* buckets, const RecordDesc* recs,
+                                                    u32 n_records, u64 n_units) {
+  const u32 lane = threadIdx.x & 31;
+  const u64 nwarps = (u64)gridDim.x * (blockDim.x >> 5);
+  for (u64 w = (u64)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * 32 < n_units; w += nwarps) {
+    const u64 u0 = w * 32;
+    const u64 u = u0 + lane;
+    u32 r = warp_upper_search(n_records, u0 * 16, [&](u32 i) { return recs[i].src; });
+    if (u < n_units) {
+      const u64 byte = u * 16;
+      while (r + 1 < n_records && recs[r + 1].src <= byte) ++r;
+      const RecordDesc& d = recs[r];
+      uint4 v = enc[u];
+      *reinterpret_cast<uint4*>(buckets + d.dst + (byte - d.src)) = v;
+    }
+  }
+}
+
+void launch_pack(const u8* enc, u8* buckets, const RecordDesc* recs, u32 n_records, const BucketDesc* bks,
+                 u32 n_buckets, u64 enc_total, u32 flags, int grid, cudaStream_t s) {
+  if (n_buckets == 0) return;
+  k_pack_meta<<<n_buckets, 256, 0, s>>>(buckets, recs, bks, flags);
+  count_launch();
+  u64 n_units = enc_total / 16;
+  if (n_units) {
+    u64 need = (n_units + 255) / 256;
+    int g = (int)(need < (u64)grid ? need : (u64)grid);
+    k_pack_copy<<<g, 256, 0, s>>>(reinterpret_cast<const uint4*>(enc), buckets, recs, n_records, n_units);
+    count_launch();
+  }
+}
+
+// Host-side bucket descriptors are also needed here (base, bytes): the caller passes a host copy.
+void crc_fill(u8* buckets, const BucketDesc* h_bks, u32 n_buckets, u32* scratch, cudaStream_t s) {
+  for (u32 b = 0; b < n_buckets; ++b) {
+    u8* bk = buckets + h_bks[b].base;
+    crc_bucket(bk, h_bks[b].bytes, scratch, reinterpret_cast<u32*>(bk + 20), nullptr, nullptr, nullptr, s);
+  }
+}
+
+void launch_crc_check(const u8* bucket, u64 bytes, u32* scratch, u32* status, cudaStream_t s) {
+  // scratch[0] = bad flag, scratch[1..] = segment CRCs
+  crc_bucket(bucket, bytes, scratch + 1, nullptr, bucket + 20, status, scratch, s);
+}
+
+}  // namespace ss

@@ -1,0 +1,228 @@
+// plan.cu — K2: record plan for the §3.3 encodings (rows a2 + sizing of a3/a4).
+//
+// From the per-tensor counts of K1:
+//  * k_plan_scan   (1 CTA)   value offsets, chunk offsets, totals (manifest order)
+//  * k_chunk_stats (grid)    per chunk: max index gap (-> DELTA16/ABS32, P:360,
+//                            DESIGN C4), hi-byte histogram, normalised rANS model
+//                            and an encode pass that only counts renormalisation
+//                            words -> exact hi block size and RAW/RANS decision
+//                            (never-expand)
+//  * k_plan_sizes  (1 CTA)   chunk hi-offset prefix, record sizes,
+//                            record byte offsets, statistics
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ss {
+
+constexpr int kScanThreads = 1024;
+
+// Block-wide exclusive scan of a u64 (1024 threads); returns the block total.
+__device__ __forceinline__ u64 block_excl_scan64(u64 v, u64* excl, u64* s_w) {
+  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u64 inc = warp_incl_scan64(v);
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    u64 w = s_w[lane];
+    u64 wi = warp_incl_scan64(w);
+    s_w[lane] = wi - w;
+    if (lane == 31) s_w[32] = wi;
+  }
+  __syncthreads();
+  *excl = s_w[warp] + inc - v;
+  u64 total = s_w[32];
+  __syncthreads();
+  return total;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_plan_scan(Plan p, const u64* counts) {
+  __shared__ u64 s_w[33];
+  __shared__ u64 s_w2[33];
+  u64 carry_nnz = 0, carry_ch = 0, carry_rec = 0;
+  const u32 T = p.n_tensors;
+  for (u32 b = 0; b < T; b += kScanThreads) {
+    u32 t = b + threadIdx.x;
+    u64 c = t < T ? counts[t] : 0;
+    u64 ch = (c + kChunk - 1) / kChunk;
+    u64 packed = (ch << 32) | (c ? 1u : 0u);   // chunks (< 2^32 total) | record flag
+    u64 e1, e2;
+    u64 tot1 = block_excl_scan64(c, &e1, s_w);
+    u64 tot2 = block_excl_scan64(packed, &e2, s_w2);
+    if (t < T) {
+      p.rec_off[t] = carry_nnz + e1;
+      p.chunk_off[t] = carry_ch + (e2 >> 32);
+      p.maxgap[t] = 0;
+    }
+    carry_nnz += tot1;
+    carry_ch += tot2 >> 32;
+    carry_rec += tot2 & 0xFFFFFFFFull;
+  }
+  if (threadIdx.x == 0) {
+    p.rec_off[T] = carry_nnz;
+    p.chunk_off[T] = carry_ch;
+    bool over = carry_nnz > p.cap || carry_ch > p.max_chunks;
+    if (over) latch(p.status, SYNC_ERR_CAPACITY);
+    for (int k = 0; k < 16; ++k) p.totals[k] = 0;
+    p.totals[kTotNnz] = carry_nnz;
+    p.totals[kTotChunks] = over ? 0 : carry_ch;
+    p.totals[kTotRecords] = carry_rec;
+    p.totals[kTotOverflow] = over ? 1 : 0;
+  }
+}
+
+// One warp per chunk: gap, histogram, model, counted rANS pass.
+__global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
+  __shared__ WarpModel s_model[8];
+  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpModel& m = s_model[warp];
+  const u64 n_chunks = p.totals[kTotChunks];
+  const u64 nwarps = (u64)gridDim.x * (blockDim.x >> 5);
+  const u64* co = p.chunk_off;
+  for (u64 g = (u64)blockIdx.x * (blockDim.x >> 5) + warp; g < n_chunks; g += nwarps) {
+    u32 t = warp_upper_search(p.n_tensors, g, [&](u32 i) { return co[i]; });
+    const u64 nnz = counts[t];
+    const u64 k = g - co[t];
+    const u64 p0 = k * kChunk;
+    const u32 nk = (u32)((nnz - p0) < kChunk ? (nnz - p0) : kChunk);
+    const u32* Ir = I + p.rec_off[t];
+    const u16* Vr = V + p.rec_off[t] + p0;
+
+    // max first difference (Δ_0 = I_0, prepended zero)
+    u32 gmax = 0;
+    for (u32 q = lane; q < nk; q += 32) {
+      u64 pp = p0 + q;
+      u32 prev = pp ? Ir[pp - 1] : 0u;
+      u32 d = Ir[pp] - prev;
+      gmax = d > gmax ? d : gmax;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      u32 v = __shfl_xor_sync(0xffffffffu, gmax, o);
+      gmax = v > gmax ? v : gmax;
+    }
+    if (lane == 0 && gmax) atomicMax(&p.maxgap[t], gmax);
+    if (p.codec != SYNC_CODEC_COMPRESSED) continue;
+
+    warp_histogram(m, nk, [&](u32 q) { return (u32)(Vr[q] >> 8); });
+    u32 nsym = warp_normalize(m, nk);
+
+    // counted encode pass: steps G-1..0, renorm if x >= f * 2^20
+    u32 x = kLow, nwords = 0;
+    const u32 G = (nk + 31) / 32;
+    for (int gg = (int)G - 1; gg >= 0; --gg) {
+      u32 q = (u32)gg * 32 + lane;
+      bool act = q < nk;
+      u32 s = act ? (u32)(Vr[q] >> 8) : 0u;
+      u32 f = m.freq[s];
+      bool emit = act && (x >> 20) >= f;
+      nwords += __popc(__ballot_sync(0xffffffffu, emit));
+      if (emit) x >>= 16;
+      if (act) {
+        u32 r;
+        u32 qq = div_by(x, f, m.rcp[s], &r);
+        x = qq * kM + r + m.cum[s];
+      }
+    }
+    u32 hb = 136u + 4u * nsym + 2u * nwords;
+    u32 mode = 1;
+    if (hb >= nk) { hb = nk; mode = 0; }
+    if (lane == 0) {
+      p.chunk_hi[g] = hb;
+      p.chunk_mode[g] = mode;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* counts) {
+  __shared__ u64 s_w[33];
+  __shared__ u64 s_w2[33];
+  const u32 T = p.n_tensors;
+  const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
+  const u64 n_chunks = p.totals[kTotChunks];
+  const bool over = p.totals[kTotOverflow] != 0;
+  // 1. exclusive prefix of padded hi block sizes over all chunks (+ RANS chunk count)
+  u64 carry = 0, rans = 0;
+  if (comp) {
+    for (u64 b = 0; b < n_chunks; b += kScanThreads) {
+      u64 g = b + threadIdx.x;
+      u64 v = g < n_chunks ? pad_to(p.chunk_hi[g], 4) : 0;
+      u64 r = g < n_chunks ? p.chunk_mode[g] : 0;
+      u64 e, e2;
+      u64 tot = block_excl_scan64(v, &e, s_w);
+      u64 tr = block_excl_scan64(r, &e2, s_w2);
+      if (g < n_chunks) p.chunk_hioff[g] = carry + e;
+      carry += tot;
+      rans += tr;
+    }
+    if (threadIdx.x == 0) p.chunk_hioff[n_chunks] = carry;
+    __syncthreads();
+  }
+  // 2. record sizes and offsets
+  u64 carry_enc = 0, n16 = 0, n32 = 0, ib_tot = 0, vb_tot = 0;
+  for (u32 b = 0; b < T; b += kScanThreads) {
+    u32 t = b + threadIdx.x;
+    u64 c = (t < T && !over) ? counts[t] : 0;
+    u64 bytes = 0, ib = 0;
+    u32 mode = 1;
+    if (c) {
+      if (comp) {
+        mode = p.maxgap[t] <= 32767u ? 0u : 1u;
+        ib = pad_to((mode ? 4 : 2) * c, 4);
+        u64 ch0 = p.chunk_off[t], ch1 = p.chunk_off[t + 1];
+        u64 hi = p.chunk_hioff[ch1] - p.chunk_hioff[ch0];
+        bytes = pad_to(16 + ib + pad_to(c, 4) + 16 * (ch1 - ch0) + hi, 16);
+      } else {
+        ib = 4 * c;
+        bytes = pad_to(16 + 6 * c, 16);
+      }
+    }
+    if (t < T) {
+      p.rec_mode[t] = mode;
+      p.rec_bytes[t] = bytes;
+    }
+    u64 e;
+    u64 tot = block_excl_scan64(bytes, &e, s_w);
+    if (t < T) p.enc_off[t] = carry_enc + e;
+    carry_enc += tot;
+    u64 flags = c ? (mode ? (1ull << 32) : 1ull) : 0ull;
+    u64 e2;
+    u64 tf = block_excl_scan64(flags, &e2, s_w2);
+    n16 += tf & 0xFFFFFFFFull;
+    n32 += tf >> 32;
+    u64 e3;
+    ib_tot += block_excl_scan64(ib, &e3, s_w);
+    u64 e4;
+    vb_tot += block_excl_scan64(c ? bytes - 16 - ib : 0, &e4, s_w2);
+  }
+  if (threadIdx.x == 0) {
+    p.enc_off[T] = carry_enc;
+    if (carry_enc > p.enc_cap) {
+      latch(p.status, SYNC_ERR_CAPACITY);
+      p.totals[kTotOverflow] = 1;
+      p.totals[kTotChunks] = 0;   // nothing gets encoded
+    }
+    p.totals[kTotEnc] = carry_enc;
+    p.totals[kTotDelta16] = comp ? n16 : 0;
+    p.totals[kTotAbs32] = comp ? n32 : n16 + n32;
+    p.totals[kTotRansChunks] = rans;
+    p.totals[kTotIndexBytes] = ib_tot;
+    p.totals[kTotValueBytes] = vb_tot;
+  }
+}
+
+void launch_plan_scan(const Plan& p, const u64* counts, cudaStream_t s) {
+  k_plan_scan<<<1, kScanThreads, 0, s>>>(p, counts);
+  count_launch();
+}
+
+void launch_chunk_stats(const Plan& p, const u32* I, const u16* V, const u64* counts, int grid, cudaStream_t s) {
+  k_chunk_stats<<<grid, 256, 0, s>>>(p, I, V, counts);
+  count_launch();
+}
+
+void launch_plan_sizes(const Plan& p, const u64* counts, cudaStream_t s) {
+  k_plan_sizes<<<1, kScanThreads, 0, s>>>(p, counts);
+  count_launch();
+}
+
+}  // namespace ss

@@ -1,0 +1,115 @@
+"""Sender / receiver objects over one manifest: buffers + the whole hot path.
+
+Sender (Trainer rank; Alg. 1 l.6 + Alg. 2):
+    extract (K1) -> compress (K2/K3) -> pack (K4) ... transfer ... -> commit (K6)
+Receiver (Rollout rank; Alg. 3):
+    per bucket: decompress + scatter-apply (K5)
+
+Every step is one or a few C-ABI calls into libsparsesync; this module only
+owns the torch buffers (grown on demand from the library's size reports).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import (SYNC_CODEC_COMPRESSED, SYNC_ERR_CAPACITY, SyncContext, SyncError, _bits, ptr_table)
+
+
+def _flat_bits(ts):
+    return [_bits(t).reshape(-1) for t in ts]
+
+
+class SparseSyncSender:
+    """Trainer side. `snapshot` = last-synced copy (W_prev), `current` = new weights W."""
+
+    def __init__(self, snapshot, current, bucket_limit: int = 256 << 20, max_changed: int | None = None,
+                 codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, expected_density: float = 0.02):
+        self.snapshot = _flat_bits(snapshot)
+        self.current = _flat_bits(current)
+        assert len(self.snapshot) == len(self.current)
+        for a, b in zip(self.snapshot, self.current):
+            if a.numel() != b.numel():
+                raise SyncError(-1, "snapshot/current shape mismatch")
+        self.device = self.current[0].device if self.current else torch.device("cuda")
+        numel = [t.numel() for t in self.current]
+        total = sum(numel)
+        cap = int(max_changed if max_changed is not None else min(total, int(total * expected_density) + 65536))
+        self.ctx = SyncContext(numel, bucket_limit=bucket_limit, max_changed=cap, codec=codec, crc=crc,
+                               device=self.device)
+        self.cap = cap
+        self.old_ptrs = ptr_table(self.snapshot, self.device)
+        self.new_ptrs = ptr_table(self.current, self.device)
+        self.I = torch.empty(max(cap, 1), dtype=torch.int32, device=self.device)
+        self.V = torch.empty(max(cap, 1), dtype=torch.int16, device=self.device)
+        self.counts = torch.zeros(max(len(numel), 1), dtype=torch.int64, device=self.device)
+        enc0 = min(self.ctx.enc_bound, int(3.6 * cap) + 64 * len(numel) + 4096)
+        self.enc = torch.empty(enc0, dtype=torch.uint8, device=self.device)
+        self.buckets = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self.bucket_list: list[tuple[int, int]] = []
+
+    # K1 + K2/K3
+    def extract_compress(self, stream=None):
+        self.ctx.sync_extract_batched(self.old_ptrs, self.new_ptrs, self.I, self.V, self.counts, stream)
+        self.ctx.sync_compress(self.I, self.V, self.counts, self.enc, stream)
+
+    # K4 (blocking: the greedy bucket plan needs the record sizes on the host)
+    def pack(self, stream=None):
+        try:
+            self.bucket_list = self._pack_once(stream)
+        except SyncError as e:
+            if e.code != SYNC_ERR_CAPACITY:
+                raise
+            st = self.ctx.sync_status(stream)      # clear the latched capacity error
+            stats = self.ctx.stats(stream)
+            if stats["nnz"] > self.cap:
+                raise SyncError(SYNC_ERR_CAPACITY, f"{stats['nnz']} changed > capacity {self.cap}") from e
+            self.enc = torch.empty(stats["enc_bytes"] + 4096, dtype=torch.uint8, device=self.device)
+            self.ctx.sync_compress(self.I, self.V, self.counts, self.enc, stream)
+            del st
+            self.bucket_list = self._pack_once(stream)
+        return self.bucket_list
+
+    def _pack_once(self, stream):
+        need = self.ctx.sync_buckets_bound(stream)
+        if self.buckets.numel() < need:
+            self.buckets = torch.empty(int(need * 1.05) + 4096, dtype=torch.uint8, device=self.device)
+        return self.ctx.sync_bucket_pack(self.enc, self.buckets, stream)
+
+    def bucket(self, b: int) -> torch.Tensor:
+        off, size = self.bucket_list[b]
+        return self.buckets[off:off + size]
+
+    # K6: after the transfer completed (DESIGN C13)
+    def commit(self, stream=None):
+        self.ctx.sync_commit_snapshot_batched(self.old_ptrs, self.I, self.V, self.counts, stream)
+
+    def sync(self, stream=None):
+        """extract + compress + pack; returns the bucket list. Call commit() once the buckets were delivered."""
+        self.extract_compress(stream)
+        return self.pack(stream)
+
+    def check(self, stream=None):
+        self.ctx.check("sender", stream)
+
+    def stats(self, stream=None) -> dict:
+        return self.ctx.stats(stream)
+
+
+class SparseSyncReceiver:
+    """Rollout side: holds the weights and applies buckets in place (bit-exact)."""
+
+    def __init__(self, weights, bucket_limit: int = 256 << 20, codec: int = SYNC_CODEC_COMPRESSED,
+                 crc: bool = False):
+        self.weights = _flat_bits(weights)
+        self.device = self.weights[0].device if self.weights else torch.device("cuda")
+        numel = [t.numel() for t in self.weights]
+        self.ctx = SyncContext(numel, bucket_limit=bucket_limit, max_changed=sum(numel), codec=codec, crc=crc,
+                               device=self.device)
+        self.weight_ptrs = ptr_table(self.weights, self.device)
+
+    def apply(self, bucket: torch.Tensor, nbytes: int | None = None, stream=None):
+        self.ctx.sync_decompress_apply(bucket, bucket.numel() if nbytes is None else nbytes, self.weight_ptrs,
+                                       stream)
+
+    def check(self, stream=None):
+        self.ctx.check("receiver", stream)

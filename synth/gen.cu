@@ -1,0 +1,99 @@
+// synth/gen.cu — GPU twin of synth/__init__.py's counter-based generator.
+// Input generation only (no arithmetic of the method): fills old/new bf16 bit
+// patterns exactly as the numpy recipe does, plus the bench's
+// synthetic "optimizer step" that flips the lowest mantissa bit of the
+// positions changed in the previous sync so every timed step syncs a fresh
+// update of the same density.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+typedef uint64_t u64;
+typedef uint32_t u32;
+typedef uint16_t u16;
+
+__device__ __forceinline__ u64 mix(u64 z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_fill_old(u16* out, u64 n, int norm, u64 key_val, const u16* table) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    out[i] = norm ? (u16)0x3F80 : table[mix(key_val ^ i) >> 48];
+}
+
+// mode 0 = U, 1 = R (row clustered), 2 = E (expert gate already folded into `active`)
+__global__ void k_fill_new(const u16* old, u16* nw, u64 n, int mode, int active, u64 key_mask, u64 thr,
+                           u64 key_pert, u64 key_row, u64 thr_row, u64 cols) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    bool m = active && (mix(key_mask ^ i) >> 32) < thr;
+    if (mode == 1) m = m && ((mix(key_row ^ (i / cols)) >> 32) < thr_row);
+    u16 o = old[i];
+    nw[i] = m ? (u16)(o ^ (u16)(1 + mix(key_pert ^ i) % 3)) : o;
+  }
+}
+
+// offsets[t] = exclusive prefix of counts (single CTA)
+__global__ void k_prefix(const u64* counts, u32 T, u64* offsets) {
+  if (threadIdx.x != 0) return;
+  u64 acc = 0;
+  for (u32 t = 0; t < T; ++t) {
+    offsets[t] = acc;
+    acc += counts[t];
+  }
+  offsets[T] = acc;
+}
+
+// Y[t][I[k]] ^= 1 for every extracted (tensor, index); 4096 entries per CTA.
+__global__ void k_toggle(u16* const* ys, const u32* I, const u64* offsets, u32 T) {
+  __shared__ u32 s_t;
+  const u64 total = offsets[T];
+  for (u64 b = (u64)blockIdx.x * 4096; b < total; b += (u64)gridDim.x * 4096) {
+    if (threadIdx.x == 0) {
+      u32 lo = 0, hi = T;  // largest t with offsets[t] <= b
+      while (hi - lo > 1) {
+        u32 mid = (lo + hi) / 2;
+        if (offsets[mid] <= b) lo = mid; else hi = mid;
+      }
+      s_t = lo;
+    }
+    __syncthreads();
+    u32 t = s_t;
+    for (u64 k = b + threadIdx.x; k < b + 4096 && k < total; k += blockDim.x) {
+      while (offsets[t + 1] <= k) ++t;
+      ys[t][I[k]] ^= (u16)1;
+    }
+    __syncthreads();
+  }
+}
+
+extern "C" {
+
+int synth_fill_old(void* out, u64 n, int norm, u64 key_val, const void* table, void* stream) {
+  if (!n) return 0;
+  u64 blocks = (n + 255) / 256;
+  int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
+  k_fill_old<<<grid, 256, 0, (cudaStream_t)stream>>>((u16*)out, n, norm, key_val, (const u16*)table);
+  return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+int synth_fill_new(const void* old, void* nw, u64 n, int mode, int active, u64 key_mask, u64 thr, u64 key_pert,
+                   u64 key_row, u64 thr_row, u64 cols, void* stream) {
+  if (!n) return 0;
+  u64 blocks = (n + 255) / 256;
+  int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
+  k_fill_new<<<grid, 256, 0, (cudaStream_t)stream>>>((const u16*)old, (u16*)nw, n, mode, active, key_mask, thr,
+                                                      key_pert, key_row, thr_row, cols ? cols : 1);
+  return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+int synth_toggle(void* const* ys, const void* I, const void* counts, u32 T, void* offsets_scratch, void* stream) {
+  if (!T) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_prefix<<<1, 32, 0, s>>>((const u64*)counts, T, (u64*)offsets_scratch);
+  k_toggle<<<148 * 8, 256, 0, s>>>((u16* const*)ys, (const u32*)I, (const u64*)offsets_scratch, T);
+  return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+}

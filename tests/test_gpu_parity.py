@@ -1,0 +1,277 @@
+"""GPU <-> oracle parity (run on a B200 with -m gpu). All calls go through the C ABI.
+
+Bar: bit-exact (integer / byte / index work; DESIGN C17 — exactly one correct byte
+string exists per input). Inputs: the shared seeded generator (synth), both its
+numpy twin (oracle side) and its CUDA twin (GPU side) — the two must agree too.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+ss = pytest.importorskip("paper_2605_07330_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2605_07330_b200 import build
+    build.build()
+    torch.cuda.set_device(0)
+
+
+DEV = "cuda:0"
+
+
+def to_dev(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(a.view(np.int16).copy()).to(DEV)
+
+
+def host16(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint16)
+
+
+# ----------------------------------------------------------------------------- a1 single tensor
+@pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 255, 8191, 8192, 8193, 65536 + 3, 1 << 20, 1_000_003])
+@pytest.mark.parametrize("rho", [0.0, 0.01, 0.3, 1.0])
+def test_extract_single_vs_oracle(n, rho):
+    rng = np.random.default_rng(n + int(rho * 1000))
+    old = rng.integers(0, 65536, n, dtype=np.uint16)
+    new = old.copy()
+    m = rng.random(n) < rho
+    new[m] ^= rng.integers(1, 65536, int(m.sum()), dtype=np.uint16)
+    I, V, cnt, ws = ss.sync_extract(to_dev(old), to_dev(new))
+    torch.cuda.synchronize()
+    assert ss.sync_extract_status(ws) == ss.SYNC_OK
+    Io, Vo = oracle.extract(old, new)
+    c = int(cnt.item())
+    assert c == Io.size
+    assert (I[:c].cpu().numpy().view(np.uint32) == Io).all()
+    assert (host16(V[:c]) == Vo).all()
+
+
+def test_extract_bf16_edge_cases():
+    old = np.array([0x0000, 0x7FC0, 0x7FC0, 0xFF80, 0x3F80] * 3000, np.uint16)
+    new = np.array([0x8000, 0x7FC0, 0x7FC1, 0xFF80, 0x3F81] * 3000, np.uint16)
+    I, V, cnt, ws = ss.sync_extract(to_dev(old), to_dev(new))
+    Io, Vo = oracle.extract(old, new)
+    c = int(cnt.item())
+    assert c == Io.size == 9000
+    assert (I[:c].cpu().numpy().view(np.uint32) == Io).all() and (host16(V[:c]) == Vo).all()
+
+
+def test_extract_capacity_reports_true_count():
+    n = 100_000
+    old = np.zeros(n, np.uint16)
+    new = old.copy()
+    new[::3] = 1
+    cap = 1000
+    I = torch.empty(cap, dtype=torch.int32, device=DEV)
+    V = torch.empty(cap, dtype=torch.int16, device=DEV)
+    I2, V2, cnt, ws = ss.sync_extract(to_dev(old), to_dev(new), I=I, V=V)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == len(range(0, n, 3))
+    assert ss.sync_extract_status(ws) == ss.SYNC_ERR_CAPACITY
+    assert (I.cpu().numpy() == np.arange(0, 3 * cap, 3)).all()   # first cap entries are exact
+
+
+def test_generator_twins_agree():
+    m = synth.Manifest("g", [synth.Tensor("a", (300, 1000)), synth.Tensor("n", (64,), synth.KIND_NORM),
+                             synth.Tensor("e", (96, 40), layer=3, expert=5)])
+    import synth.gpu as sg
+    for mask in [synth.MASK_U, synth.MASK_R, synth.MASK_E]:
+        _, old = sg.arena(m, DEV)
+        _, new = sg.arena(m, DEV)
+        sg.fill_old(old, m, seed=7, tid0=11)
+        sg.fill_new(old, new, m, seed=7, rho=0.05, mask=mask, tid0=11)
+        olds, news = synth.generate(m, seed=7, rho=0.05, mask=mask, tid0=11)
+        for a, b in zip(old, olds):
+            assert (host16(a) == b).all()
+        for a, b in zip(new, news):
+            assert (host16(a) == b).all()
+
+
+# ----------------------------------------------------------------------------- whole path
+def mixed_manifest():
+    T = [synth.Tensor("embed", (3000, 64)), synth.Tensor("norm", (64,), synth.KIND_NORM),
+         synth.Tensor("empty", (0,)), synth.Tensor("tiny", (8,)), synth.Tensor("odd", (1,)),
+         synth.Tensor("big", (70_000,)), synth.Tensor("q", (256, 512))]
+    T += [synth.Tensor(f"e{k}", (48, 64), layer=0, expert=k) for k in range(40)]
+    T += [synth.Tensor("tail", (8192 * 3 + 8,))]
+    return synth.Manifest("mixed", T)
+
+
+def run_path(olds, news, codec, limit, crc, max_changed=None):
+    """GPU sender on device copies; returns (sender, receiver weights after apply, bucket bytes list)."""
+    old_d = [to_dev(o) for o in olds]
+    new_d = [to_dev(n) for n in news]
+    rol_d = [to_dev(o) for o in olds]
+    snd = ss.SparseSyncSender(old_d, new_d, bucket_limit=limit, codec=codec, crc=crc, max_changed=max_changed)
+    rcv = ss.SparseSyncReceiver(rol_d, bucket_limit=limit, codec=codec, crc=crc)
+    bl = snd.sync()
+    got = [snd.bucket(b).cpu().numpy().tobytes() for b in range(len(bl))]
+    for b in range(len(bl)):
+        rcv.apply(snd.bucket(b))
+    snd.commit()
+    torch.cuda.synchronize()
+    snd.check()
+    rcv.check()
+    return snd, old_d, rol_d, got
+
+
+@pytest.mark.parametrize("codec", [ss.SYNC_CODEC_COMPRESSED, ss.SYNC_CODEC_RAW])
+@pytest.mark.parametrize("limit", [1024, 64 << 10, 1 << 30])
+@pytest.mark.parametrize("crc", [False, True])
+@pytest.mark.parametrize("rho,mask", [(0.01, synth.MASK_U), (0.2, synth.MASK_U), (0.02, synth.MASK_R)])
+def test_bucket_bytes_and_apply_bit_exact(codec, limit, crc, rho, mask):
+    m = mixed_manifest()
+    olds, news = synth.generate(m, seed=1, rho=rho, mask=mask)
+    ref = oracle.sync_pack(olds, news, codec=codec, limit=limit, crc=crc)
+    snd, old_d, rol_d, got = run_path(olds, news, codec, limit, crc)
+    assert len(got) == ref.n_buckets
+    for b in range(ref.n_buckets):
+        assert got[b] == ref.bucket(b), f"bucket {b} bytes differ"
+    for r, o, n in zip(rol_d, old_d, news):
+        assert (host16(r) == n).all()        # receiver bit-identical (G1)
+        assert (host16(o) == n).all()        # snapshot committed
+    st = snd.stats()
+    assert st["nnz"] == ref.stats["nnz"] and st["n_records"] == ref.stats["n_records"]
+
+
+def test_delta16_abs32_boundary():
+    # gap of exactly 32767 stays DELTA16, 32768 forces ABS32 (DESIGN C4)
+    n = 70_000
+    olds = [np.zeros(n, np.uint16), np.zeros(n, np.uint16), np.zeros(n, np.uint16)]
+    news = [o.copy() for o in olds]
+    news[0][[32767, 65534]] = 5
+    news[1][[32768]] = 5
+    news[2][[0, 32767 + 0, 32767 + 32768]] = 5
+    ref = oracle.sync_pack(olds, news, limit=1 << 20)
+    _, _, rol, got = run_path(olds, news, ss.SYNC_CODEC_COMPRESSED, 1 << 20, False)
+    assert got == [ref.bucket(b) for b in range(ref.n_buckets)]
+    assert ref.stats["delta16"] == 1 and ref.stats["abs32"] == 2
+
+
+def test_gpu_decoder_applies_oracle_buckets():
+    """Decoder checked independently of the GPU encoder: apply the oracle's bytes."""
+    m = mixed_manifest()
+    olds, news = synth.generate(m, seed=2, rho=0.05)
+    for codec in [ss.SYNC_CODEC_COMPRESSED, ss.SYNC_CODEC_RAW]:
+        ref = oracle.sync_pack(olds, news, codec=codec, limit=32 << 10, crc=True)
+        W = [to_dev(o) for o in olds]
+        rcv = ss.SparseSyncReceiver(W, crc=True, codec=codec)
+        for b in range(ref.n_buckets):
+            bk = torch.from_numpy(np.frombuffer(ref.bucket(b), np.uint8).copy()).to(DEV)
+            rcv.apply(bk)
+        torch.cuda.synchronize()
+        rcv.check()
+        for w, n in zip(W, news):
+            assert (host16(w) == n).all()
+
+
+def test_decompress_emits_extract():
+    m = mixed_manifest()
+    olds, news = synth.generate(m, seed=3, rho=0.1)
+    ref = oracle.sync_pack(olds, news, limit=1 << 30)
+    ctx = ss.SyncContext([t.numel for t in m.tensors], bucket_limit=1 << 30)
+    bk = torch.from_numpy(np.frombuffer(ref.bucket(0), np.uint8).copy()).to(DEV)
+    cap = sum(t.numel for t in m.tensors)
+    I = torch.empty(cap, dtype=torch.int32, device=DEV)
+    V = torch.empty(cap, dtype=torch.int16, device=DEV)
+    ctx.sync_decompress(bk, bk.numel(), I, V)
+    views = torch.zeros(32 * len(m.tensors), dtype=torch.uint8, device=DEV)
+    nrec = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ctx.sync_bucket_unpack(bk, bk.numel(), views, nrec)
+    torch.cuda.synchronize()
+    ctx.check()
+    st, recs = oracle.bucket_decode(ref.bucket(0), cap=cap)
+    assert st == oracle.OK and int(nrec.item()) == len(recs)
+    vv = views.cpu().numpy().view(np.uint32).reshape(-1, 8)
+    off = 0
+    Ih, Vh = I.cpu().numpy().view(np.uint32), host16(V)
+    for q, (tid, Io, Vo) in enumerate(recs):
+        assert vv[q, 0] == tid and vv[q, 1] == Io.size
+        assert (Ih[off:off + Io.size] == Io).all() and (Vh[off:off + Io.size] == Vo).all()
+        off += Io.size
+
+
+def test_apply_and_commit_vs_oracle():
+    rng = np.random.default_rng(5)
+    n = 200_000
+    W0 = rng.integers(0, 65536, n, dtype=np.uint16)
+    I = np.unique(rng.integers(0, n, 20_000)).astype(np.uint32)
+    V = rng.integers(0, 65536, I.size, dtype=np.uint16)
+    Wo = W0.copy()
+    assert oracle.apply(Wo, I, V) == oracle.OK
+    for fn in (ss.sync_apply, ss.sync_commit_snapshot):
+        Wd = to_dev(W0)
+        st = torch.zeros(1, dtype=torch.int32, device=DEV)
+        fn(Wd, torch.from_numpy(I.view(np.int32)).to(DEV), to_dev(V), status=st)
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0 and (host16(Wd) == Wo).all()
+    # out of range: skipped and latched
+    Wd = to_dev(W0)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    bad = np.array([1, n + 5, 3], np.uint32)
+    ss.sync_apply(Wd, torch.from_numpy(bad.view(np.int32)).to(DEV), to_dev(np.array([7, 8, 9], np.uint16)), status=st)
+    torch.cuda.synchronize()
+    assert -int(st.item()) == ss.SYNC_ERR_INDEX_RANGE
+    h = host16(Wd)
+    assert h[1] == 7 and h[3] == 9
+
+
+def rans_word_offset(bk: np.ndarray) -> int:
+    """Byte offset (in the bucket) of a middle rANS word of the first RANS chunk with >= 16 words."""
+    u32 = lambda o: int(bk[o:o + 4].view(np.uint32)[0])
+    nrec = u32(12)
+    for q in range(nrec):
+        ro = u32(32 + 8 * q)
+        nnz, mode = u32(ro + 4), int(bk[ro + 12])
+        ib = (4 if mode else 2) * nnz
+        dir_off = ro + 16 + (ib + 3) // 4 * 4 + (nnz + 3) // 4 * 4
+        for k in range((nnz + 16383) // 16384):
+            hi_off, hb, cm = u32(dir_off + 16 * k), u32(dir_off + 16 * k + 4), u32(dir_off + 16 * k + 8)
+            if cm == 1:
+                blk = ro + hi_off
+                nwords, nsym = u32(blk + 128), u32(blk + 132) & 0xFFFF
+                if nwords >= 16:
+                    return blk + 136 + 4 * nsym + 2 * (nwords // 2)
+    raise AssertionError("no rANS chunk with words")
+
+
+def test_corruption_is_detected():
+    m = mixed_manifest()
+    olds, news = synth.generate(m, seed=4, rho=0.05)
+    ref = oracle.sync_pack(olds, news, limit=1 << 30, crc=True)
+    good = np.frombuffer(ref.bucket(0), np.uint8).copy()
+    cases = []
+    b = good.copy(); b[len(b) // 2] ^= 1; cases.append((b, True, ss.SYNC_ERR_CRC))
+    b = good.copy(); b[0] ^= 1; cases.append((b, True, ss.SYNC_ERR_BAD_MAGIC))
+    b = good.copy(); b[4] = 2; cases.append((b, True, ss.SYNC_ERR_VERSION))
+    # without CRC: damage a rANS word deep inside the big record -> end-state check
+    ref2 = oracle.sync_pack(olds, news, limit=1 << 30, crc=False)
+    g2 = np.frombuffer(ref2.bucket(0), np.uint8).copy()
+    b = g2.copy(); b[rans_word_offset(g2) + 1] ^= 0x55; cases.append((b, False, ss.SYNC_ERR_CORRUPT))
+    for data, crc, want in cases:
+        W = [to_dev(o) for o in olds]
+        rcv = ss.SparseSyncReceiver(W, crc=crc)
+        rcv.apply(torch.from_numpy(data).to(DEV))
+        torch.cuda.synchronize()
+        assert rcv.ctx.sync_status() == want
+
+
+def test_config1_one_million_end_to_end():
+    """BASELINE config 1: one 2^20-element bf16 tensor, 99% sparsity, uniform mask."""
+    m = synth.single_manifest(1 << 20)
+    olds, news = synth.generate(m, seed=0, rho=0.01)
+    ref = oracle.sync_pack(olds, news, limit=256 << 20)
+    snd, old_d, rol_d, got = run_path(olds, news, ss.SYNC_CODEC_COMPRESSED, 256 << 20, False)
+    assert got == [ref.bucket(b) for b in range(ref.n_buckets)]
+    assert (host16(rol_d[0]) == news[0]).all()
+    x_comp = 2 * (1 << 20) / sum(len(g) for g in got)
+    assert 55 < x_comp < 65                      # ≈ 60x at ρ = 1% (Eq. 4, α ≈ 0.67)
