@@ -31,21 +31,25 @@ class SparseSyncSender:
             if a.numel() != b.numel():
                 raise SyncError(-1, "snapshot/current shape mismatch")
         self.device = self.current[0].device if self.current else torch.device("cuda")
-        numel = [t.numel() for t in self.current]
-        total = sum(numel)
+        self.numel = [t.numel() for t in self.current]
+        total = sum(self.numel)
         cap = int(max_changed if max_changed is not None else min(total, int(total * expected_density) + 65536))
-        self.ctx = SyncContext(numel, bucket_limit=bucket_limit, max_changed=cap, codec=codec, crc=crc,
-                               device=self.device)
-        self.cap = cap
+        self._cfg = dict(bucket_limit=bucket_limit, codec=codec, crc=crc)
         self.old_ptrs = ptr_table(self.snapshot, self.device)
         self.new_ptrs = ptr_table(self.current, self.device)
-        self.I = torch.empty(max(cap, 1), dtype=torch.int32, device=self.device)
-        self.V = torch.empty(max(cap, 1), dtype=torch.int16, device=self.device)
-        self.counts = torch.zeros(max(len(numel), 1), dtype=torch.int64, device=self.device)
-        enc0 = min(self.ctx.enc_bound, int(3.6 * cap) + 64 * len(numel) + 4096)
-        self.enc = torch.empty(enc0, dtype=torch.uint8, device=self.device)
+        self.counts = torch.zeros(max(len(self.numel), 1), dtype=torch.int64, device=self.device)
         self.buckets = torch.empty(0, dtype=torch.uint8, device=self.device)
         self.bucket_list: list[tuple[int, int]] = []
+        self._alloc(cap)
+
+    def _alloc(self, cap: int):
+        """(Re)size the changed-element capacity: context workspace, I/V and the encoded stream."""
+        self.ctx = SyncContext(self.numel, max_changed=cap, device=self.device, **self._cfg)
+        self.cap = cap
+        self.I = torch.empty(max(cap, 1), dtype=torch.int32, device=self.device)
+        self.V = torch.empty(max(cap, 1), dtype=torch.int16, device=self.device)
+        enc0 = min(self.ctx.enc_bound, int(3.6 * cap) + 64 * len(self.numel) + 4096)
+        self.enc = torch.empty(enc0, dtype=torch.uint8, device=self.device)
 
     # K1 + K2/K3
     def extract_compress(self, stream=None):
@@ -59,13 +63,15 @@ class SparseSyncSender:
         except SyncError as e:
             if e.code != SYNC_ERR_CAPACITY:
                 raise
-            st = self.ctx.sync_status(stream)      # clear the latched capacity error
+            self.ctx.sync_status(stream)           # clear the latched capacity error
             stats = self.ctx.stats(stream)
-            if stats["nnz"] > self.cap:
-                raise SyncError(SYNC_ERR_CAPACITY, f"{stats['nnz']} changed > capacity {self.cap}") from e
-            self.enc = torch.empty(stats["enc_bytes"] + 4096, dtype=torch.uint8, device=self.device)
-            self.ctx.sync_compress(self.I, self.V, self.counts, self.enc, stream)
-            del st
+            if stats["nnz"] > self.cap:            # more changes than I/V can hold: grow, extract again
+                self._alloc(min(sum(self.numel), int(stats["nnz"] * 1.1) + 65536))
+                self.extract_compress(stream)
+                stats = self.ctx.stats(stream)
+            if stats["enc_bytes"] > self.enc.numel():
+                self.enc = torch.empty(stats["enc_bytes"] + 4096, dtype=torch.uint8, device=self.device)
+                self.ctx.sync_compress(self.I, self.V, self.counts, self.enc, stream)
             self.bucket_list = self._pack_once(stream)
         return self.bucket_list
 
