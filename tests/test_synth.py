@@ -40,6 +40,16 @@ def test_mask_density_and_perturbation():
     assert 0.05 < r.any(axis=1).mean() < 0.15               # ~10% rows active
 
 
+def test_cpu_twin_matches_numpy_recipe():
+    import synth.cpu
+    m = synth.Manifest("g", [synth.Tensor("a", (300, 1000)), synth.Tensor("n", (64,), synth.KIND_NORM),
+                             synth.Tensor("e", (96, 40), layer=3, expert=5), synth.Tensor("z", (0,))])
+    for mask in [synth.MASK_U, synth.MASK_R, synth.MASK_E]:
+        a = synth.generate(m, seed=7, rho=0.05, mask=mask, tid0=11)
+        b = synth.cpu.generate(m, seed=7, rho=0.05, mask=mask, tid0=11)
+        assert all((x == y).all() for x, y in zip(a[0] + a[1], b[0] + b[1]))
+
+
 def test_shard_covers_manifest():
     m = synth.qwen3_manifest("qwen3-4b")
     parts = [synth.shard(m, r, 4) for r in range(4)]
