@@ -225,7 +225,7 @@ class Rank:
         return blist
 
 
-def chunked_digest(t: torch.Tensor, chunk: int = 1 << 27) -> tuple:
+def chunked_digest(t: torch.Tensor, chunk: int = 1 << 24) -> tuple:
     """Order-sensitive digest of an int16 tensor (verification only, outside the timed region)."""
     a = b = 0
     for s in range(0, t.numel(), chunk):

@@ -24,7 +24,7 @@ namespace {
 constexpr u64 kAlign = 256;
 
 struct Layout {
-  u64 numel, tile_prefix, misc, tile_state, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
+  u64 numel, tile_prefix, tile_tensor, misc, tile_state, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
   u64 chunk_hi, chunk_mode, chunk_hioff, totals, recs, bks, views, nviews, crc, total;
 };
 
@@ -40,6 +40,7 @@ Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n) {
   };
   L.numel = take(8ull * T);
   L.tile_prefix = take(8ull * (T + 1));
+  L.tile_tensor = take(4ull * n_tiles);
   L.misc = take(4 * 64);
   L.tile_state = take(8ull * n_tiles);
   L.rec_off = take(8ull * (T + 1));
@@ -98,6 +99,7 @@ struct sync_ctx {
   Dims d;
   sync_config cfg;
   std::vector<u64> numel, tile_prefix;
+  std::vector<u32> tile_tensor;
   u8* ws;
   Layout L;
   Plan plan;
@@ -146,12 +148,17 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
     acc += (x->numel[t] + kTile - 1) / kTile;
   }
   x->tile_prefix[d.T] = acc;
+  x->tile_tensor.resize(acc);
+  for (u32 t = 0; t < d.T; ++t)
+    for (u64 k = x->tile_prefix[t]; k < x->tile_prefix[t + 1]; ++k) x->tile_tensor[k] = t;
   cudaStream_t s = (cudaStream_t)stream;
   u8* w = x->ws;
   if (d.T) {
     if (cudaMemcpyAsync(w + L.numel, x->numel.data(), 8ull * d.T, cudaMemcpyHostToDevice, s) != cudaSuccess ||
         cudaMemcpyAsync(w + L.tile_prefix, x->tile_prefix.data(), 8ull * (d.T + 1), cudaMemcpyHostToDevice, s) !=
-            cudaSuccess) {
+            cudaSuccess ||
+        (acc && cudaMemcpyAsync(w + L.tile_tensor, x->tile_tensor.data(), 4ull * acc, cudaMemcpyHostToDevice, s) !=
+                    cudaSuccess)) {
       delete x;
       return SYNC_ERR_CUDA;
     }
@@ -243,7 +250,7 @@ int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const u
   CK(cudaMemsetAsync(d_counts, 0, 8ull * x->d.T, s));
   if (x->d.n_tiles) CK(cudaMemsetAsync(x->ws + x->L.tile_state, 0, 8 * x->d.n_tiles, s));
   launch_extract_batched(d_old_ptrs, d_new_ptrs, reinterpret_cast<const u64*>(x->ws + x->L.tile_prefix),
-                         x->plan.numel, x->d.T, x->d.n_tiles, d_I, d_V, x->cfg.max_changed, d_counts,
+                         reinterpret_cast<const u32*>(x->ws + x->L.tile_tensor), x->plan.numel, x->d.T, x->d.n_tiles, d_I, d_V, x->cfg.max_changed, d_counts,
                          reinterpret_cast<u64*>(x->ws + x->L.tile_state), x->misc, x->misc + 1, s);
   CK(cudaGetLastError());
   return SYNC_OK;

@@ -24,10 +24,14 @@ constexpr u32 kMagic = 0x424C5253u;         // "SRLB"
 constexpr u32 kVersion = 1;
 constexpr u64 kBucketAlign = 256;
 
-// Extract tiling: 256 threads x 4 x uint4 (8 bf16) = 8192 elements per tile.
+// Extract tiling: a sub-tile is 256 threads x 4 x uint4 (8 bf16) = 8192 elements
+// (one TMA stage: 16 KB of old + 16 KB of new); a tile (the look-back unit) is
+// kSubPerTile sub-tiles = 32768 elements (local indices fit 16 bits).
 constexpr int kXThreads = 256;
 constexpr int kXVec = 4;
-constexpr u64 kTile = (u64)kXThreads * kXVec * 8;
+constexpr u64 kSub = (u64)kXThreads * kXVec * 8;
+constexpr u32 kSubPerTile = 4;
+constexpr u64 kTile = kSub * kSubPerTile;
 
 // Look-back tile state: [63:62] flag, [61:0] value.
 constexpr u64 kFlagA = 1ull << 62;

@@ -4,26 +4,47 @@
 // records contiguous in manifest order (Alg. 1 l.6; Alg. 2 l.5, P:312;
 // sorted; bitwise compare, DESIGN C1).
 //
-// One pass over old+new (2S bytes — ~97% of the step's HBM traffic at 1%
-// density): each CTA takes the next 8192-element tile (dynamic tile id, so
-// look-back always waits on a running CTA), issues all eight 128-bit
-// streaming loads per thread up front, builds per-vector change masks, does a
-// block scan of the packed per-thread counts, and gets its global output
-// offset by decoupled look-back over the tile states. Tiles never straddle
-// tensors (the tile -> tensor map is a prefix over per-tensor tile counts).
+// One pass over old+new (2S bytes, ~97% of a sync's HBM traffic at 1%
+// density). Persistent, warp-specialised pipeline (DESIGN §6 K1):
+//   * scheduler + copier warps: the next tile (65536 elements, never straddling a
+//     tensor; static round-robin), maps it to its tensor (tile table)
+//     and streams its eight 8192-element sub-tiles
+//     (2 x 16 KB each) into shared-memory stages with TMA bulk copies
+//     (cp.async.bulk ... mbarrier::complete_tx), so loads stay in flight while
+//     the consumers work;
+//   * 8 consumer warps: per sub-tile, 8-bit change masks per 128-bit vector,
+//     release the stage, block scan, and append (local index, value) to a
+//     shared-memory staging list; at the end of the tile ONE decoupled
+//     look-back (warp 0) gives the tile's global offset and the staged list is
+//     written out coalesced. The look-back latency (an L2 round trip behind
+//     the streaming traffic) is paid once per 256 KB of input.
+//   * tiles denser than the staging list (> 12.5%) take a slow path: after
+//     the look-back the tile is re-read from global and written directly.
+// Every claimed tile belongs to a resident CTA and is processed in claim
+// order, so look-back always terminates.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ss {
 
+constexpr int kXConsumers = kXThreads;            // 256 consumer threads (8 warps)
+constexpr int kXBlock = kXConsumers + 96;         // + copier, scheduler and writer warps
+constexpr int kXQueue = 4;                        // tiles resolved ahead by the scheduler
+constexpr u32 kStageBytes = (u32)kSub * 2 * 2;    // old + new, 16 KB each
+constexpr u32 kStageCap = 4096;                   // staged changes per tile (12.5%), two buffers
+
 struct ExtractArgs {
   const u16* const* old_ptrs;  // batched: device arrays of tensor pointers
   const u16* const* new_ptrs;
-  const u16* old_single;       // single-tensor mode when old_ptrs == nullptr
+  const u16* old_single;       // single-tensor mode
   const u16* new_single;
   const u64* tile_prefix;      // [T+1]
+  const u32* tile_tensor;      // [n_tiles] tile -> tensor
   const u64* numel;            // [T]
   u64 numel_single;
+  u64 n_tiles;
   u32 n_tensors;
   u32* I;
   u16* V;
@@ -34,150 +55,499 @@ struct ExtractArgs {
   u32* status;
 };
 
+struct TileJob {              // scheduler -> copier
+  u64 tile;                    // ~0 = no more tiles
+  u64 base;
+  const u16* po;
+  const u16* pn;
+  u64 n;                       // tensor numel
+  u32 t;
+  u32 n_sub;
+};
+
+struct StagedTile {           // consumers -> writer, one per staging buffer
+  u64 tile;                    // ~0 = no more tiles
+  u64 tile_base;               // first element of the tile within its tensor
+  u64 tile_end;
+  const u16* po;
+  const u16* pn;
+  u32 t;
+  u32 count;
+  u32 overflow;
+  u32 pad;
+};
+
+struct SubInfo {
+  u64 tile;                    // ~0 = no more tiles
+  u64 base;                    // first element of the sub-tile within its tensor
+  const u16* po;
+  const u16* pn;
+  u32 t;
+  u32 n_valid;                 // elements of this sub-tile inside the tensor
+  u32 bulk;                    // elements delivered by the bulk copies (multiple of 8)
+  u16 sub;                     // sub-tile index within the tile
+  u16 n_sub;                   // sub-tiles in this tile
+};
+
+// ---------------------------------------------------------------- mbarrier / bulk-copy PTX
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  const u32 a = smem_u32(bar);
+  u32 done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar, u64 policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ u64 policy_evict_first() {
+  u64 p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kXConsumers) : "memory"); }
+
 // Full-warp decoupled look-back: returns the exclusive prefix of `tile`.
+// Each round reads a window of 32 x kLB predecessor states in one L2 round trip
+// (lane l covers distances 1 + l*kLB .. (l+1)*kLB): with ~one tile per CTA in
+// flight the nearest inclusive prefix is up to a grid's worth of tiles back.
+constexpr int kLB = 8;
+// Publication of the tile aggregate (consumers, as soon as the tile is counted).
+__device__ __forceinline__ void publish_aggregate(u64* state, u64 tile, u64 agg) {
+  st_relaxed(&state[tile], (tile == 0 ? kFlagP : kFlagA) | agg);
+}
+// Resolution of the exclusive prefix (writer warp); publishes the inclusive prefix.
 __device__ __forceinline__ u64 lookback(u64* state, u64 tile, u64 agg) {
   const u32 lane = lane_id();
-  if (tile == 0) {
-    if (lane == 0) st_relaxed(&state[0], kFlagP | agg);
-    return 0;
-  }
-  if (lane == 0) st_relaxed(&state[tile], kFlagA | agg);
+  if (tile == 0) return 0;
   u64 excl = 0;
   long long top = (long long)tile - 1;
   while (true) {
-    long long idx = top - (long long)lane;
-    u64 st = idx >= 0 ? ld_relaxed(&state[idx]) : kFlagP;
-    u32 flag = (u32)(st >> 62);
-    u32 pm = __ballot_sync(0xffffffffu, flag == 2);
-    u32 xm = __ballot_sync(0xffffffffu, flag == 0);
-    u32 upto = pm ? ((pm & (0u - pm)) << 1) - 1u : 0xffffffffu;  // lanes 0..first P
-    if (xm & upto) continue;                                        // a predecessor not ready yet
-    u64 v = ((upto >> lane) & 1u) ? (st & kValMask) : 0;
+    u64 st[kLB];
+#pragma unroll
+    for (int i = 0; i < kLB; ++i) {
+      long long idx = top - (long long)(lane * kLB + i);
+      st[i] = idx >= 0 ? ld_relaxed(&state[idx]) : kFlagP;
+    }
+    // per lane: first P (in distance order), X before it, sums
+    int pf = kLB;
+    bool x_before = false, x_any = false;
+    u64 sum_to_p = 0, sum_all = 0;
+#pragma unroll
+    for (int i = kLB - 1; i >= 0; --i) {  // reverse so pf ends as the smallest i with P
+      u32 flag = (u32)(st[i] >> 62);
+      if (flag == 2) pf = i;
+    }
+#pragma unroll
+    for (int i = 0; i < kLB; ++i) {
+      u32 flag = (u32)(st[i] >> 62);
+      u64 v = st[i] & kValMask;
+      if (flag == 0) {
+        x_any = true;
+        if (i < pf) x_before = true;
+      }
+      sum_all += v;
+      if (i <= pf) sum_to_p += v;
+    }
+    const u32 pm = __ballot_sync(0xffffffffu, pf < kLB);
+    const u32 fl = pm ? (u32)(__ffs(pm) - 1) : 32u;  // first lane holding a P
+    const bool mine_x = (lane < fl) ? x_any : (lane == fl ? x_before : false);
+    if (__any_sync(0xffffffffu, mine_x)) continue;     // a predecessor not ready yet
+    const u64 v = (lane < fl) ? sum_all : (lane == fl ? sum_to_p : 0);
     excl += warp_sum64(v);
     if (pm) break;
-    top -= 32;
+    top -= 32 * kLB;
   }
   if (lane == 0) st_relaxed(&state[tile], kFlagP | (excl + agg));
   return excl;
 }
 
-template <bool kSingle>
-__global__ void __launch_bounds__(kXThreads) k_extract(ExtractArgs a) {
-  __shared__ u64 s_tile;
-  __shared__ u32 s_t;
-  __shared__ u64 s_wsum[kXThreads / 32];
-  __shared__ u64 s_prefix;
-  __shared__ u64 s_total;
+__device__ __forceinline__ uint4 load8_direct(const u16* p, u64 e, u64 n) {
+  u16 h[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) h[k] = (e + k < n) ? p[e + k] : (u16)0;
+  return make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+}
+
+__device__ __forceinline__ u32 change_mask(const uint4& o, const uint4& n) {
+  u32 x0 = o.x ^ n.x, x1 = o.y ^ n.y, x2 = o.z ^ n.z, x3 = o.w ^ n.w;
+  return ((x0 & 0xFFFFu) ? 1u : 0u) | ((x0 >> 16) ? 2u : 0u) | ((x1 & 0xFFFFu) ? 4u : 0u) |
+         ((x1 >> 16) ? 8u : 0u) | ((x2 & 0xFFFFu) ? 16u : 0u) | ((x2 >> 16) ? 32u : 0u) |
+         ((x3 & 0xFFFFu) ? 64u : 0u) | ((x3 >> 16) ? 128u : 0u);
+}
+
+__device__ __forceinline__ u16 lane16(const uint4& v, int b) {
+  const u64 lo64 = v.x | ((u64)v.y << 32), hi64 = v.z | ((u64)v.w << 32);
+  return (u16)(((b < 4) ? lo64 : hi64) >> ((b & 3) * 16));
+}
+
+// Block (consumer) exclusive scan of packed per-vector counts. Returns this thread's
+// exclusive packed offsets; *total = block total (packed). Two consumer barriers.
+__device__ __forceinline__ u64 consumer_scan(u64 packed, u64* s_wsum, u64* total) {
+  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 incl = warp_incl_scan64(packed);
+  if (lane == 31) s_wsum[warp] = incl;
+  consumer_bar();
+  if (warp == 0) {
+    u64 w = lane < kXConsumers / 32 ? s_wsum[lane] : 0;
+    u64 wi = warp_incl_scan64(w);
+    if (lane < kXConsumers / 32) s_wsum[lane] = wi - w;
+    if (lane == kXConsumers / 32 - 1) s_wsum[8] = wi;
+  }
+  consumer_bar();
+  *total = s_wsum[8];
+  return s_wsum[warp] + incl - packed;
+}
+
+__device__ __forceinline__ u32 sum_fields(u64 p) {
+  return (u32)((p & 0xFFFF) + ((p >> 16) & 0xFFFF) + ((p >> 32) & 0xFFFF) + (p >> 48));
+}
+
+template <bool kSingle, int kStages>
+__global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
+  extern __shared__ __align__(128) u8 smem[];
+  u8* data = smem;
+  u32* staging = reinterpret_cast<u32*>(smem + kStages * kStageBytes);  // [2][kStageCap]
+  u64* full = reinterpret_cast<u64*>(staging + 2 * kStageCap);
+  u64* empty = full + kStages;
+  u64* qfull = empty + kStages;
+  u64* qempty = qfull + kXQueue;
+  u64* sfull = qempty + kXQueue;
+  u64* sempty = sfull + 2;
+  SubInfo* info = reinterpret_cast<SubInfo*>(sempty + 2);
+  TileJob* jobs = reinterpret_cast<TileJob*>(info + kStages);
+  StagedTile* meta = reinterpret_cast<StagedTile*>(jobs + kXQueue);
+  u64* s_wsum = reinterpret_cast<u64*>(meta + 2);  // [0..8] scan
   const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  if (warp == 0) {
-    u64 tile = 0;
-    if (lane == 0) tile = atomicAdd(a.tile_counter, 1u);
-    tile = __shfl_sync(0xffffffffu, tile, 0);
-    u32 t = 0;
-    if (!kSingle) {
-      const u64* tp = a.tile_prefix;
-      t = warp_upper_search(a.n_tensors, tile, [&](u32 i) { return tp[i]; });
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
     }
-    if (lane == 0) { s_tile = tile; s_t = t; }
+    for (int q = 0; q < kXQueue; ++q) {
+      mbar_init(&qfull[q], 1);
+      mbar_init(&qempty[q], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&sfull[q], 1);
+      mbar_init(&sempty[q], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const u64 tile = s_tile;
-  const u32 t = s_t;
-  const u64 n = kSingle ? a.numel_single : a.numel[t];
-  const u16* __restrict__ po = kSingle ? a.old_single : a.old_ptrs[t];
-  const u16* __restrict__ pn = kSingle ? a.new_single : a.new_ptrs[t];
-  const u64 base = (tile - (kSingle ? 0 : a.tile_prefix[t])) * kTile;
-  const bool aligned = ((((uintptr_t)po) | ((uintptr_t)pn)) & 15u) == 0;
 
-  uint4 vo[kXVec], vn[kXVec];
-#pragma unroll
-  for (int u = 0; u < kXVec; ++u) {
-    u64 e = base + ((u64)u * kXThreads + tid) * 8;
-    if (aligned && e + 8 <= n) {
-      vo[u] = ld_stream(po + e);
-      vn[u] = ld_stream(pn + e);
-    } else {
-      u16 ho[8], hn[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        bool in = e + k < n;
-        ho[k] = in ? po[e + k] : 0;
-        hn[k] = in ? pn[e + k] : 0;
-      }
-      vo[u] = make_uint4(ho[0] | (ho[1] << 16), ho[2] | (ho[3] << 16), ho[4] | (ho[5] << 16), ho[6] | (ho[7] << 16));
-      vn[u] = make_uint4(hn[0] | (hn[1] << 16), hn[2] | (hn[3] << 16), hn[4] | (hn[5] << 16), hn[6] | (hn[7] << 16));
-    }
-  }
-
-  // per-vector 8-bit change masks; packed counts (16 bits per vector slot)
-  u32 mask[kXVec];
-  u64 packed = 0;
-#pragma unroll
-  for (int u = 0; u < kXVec; ++u) {
-    u32 x0 = vo[u].x ^ vn[u].x, x1 = vo[u].y ^ vn[u].y, x2 = vo[u].z ^ vn[u].z, x3 = vo[u].w ^ vn[u].w;
-    u32 m = ((x0 & 0xFFFFu) ? 1u : 0u) | ((x0 >> 16) ? 2u : 0u) | ((x1 & 0xFFFFu) ? 4u : 0u) |
-            ((x1 >> 16) ? 8u : 0u) | ((x2 & 0xFFFFu) ? 16u : 0u) | ((x2 >> 16) ? 32u : 0u) |
-            ((x3 & 0xFFFFu) ? 64u : 0u) | ((x3 >> 16) ? 128u : 0u);
-    mask[u] = m;
-    packed |= (u64)__popc(m) << (16 * u);
-  }
-
-  // block exclusive scan of packed counts (each field <= 2048, no carries across fields)
-  u64 incl = warp_incl_scan64(packed);
-  if (lane == 31) s_wsum[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    u64 w = lane < kXThreads / 32 ? s_wsum[lane] : 0;
-    u64 wi = warp_incl_scan64(w);
-    if (lane < kXThreads / 32) s_wsum[lane] = wi - w;   // exclusive warp offsets
-    u64 total = __shfl_sync(0xffffffffu, wi, kXThreads / 32 - 1);
-    u64 agg = (total & 0xFFFF) + ((total >> 16) & 0xFFFF) + ((total >> 32) & 0xFFFF) + (total >> 48);
-    u64 pre = lookback(a.tile_state, tile, agg);
-    if (lane == 0) {
-      s_prefix = pre;
-      s_total = total;
-      if (agg) atomicAdd((unsigned long long*)&a.counts[t], (unsigned long long)agg);
-    }
-  }
-  __syncthreads();
-  const u64 total = s_total;
-  const u64 excl = s_wsum[warp] + incl - packed;
-  const u64 prefix = s_prefix;
-
-  u64 run = 0;  // Σ_{u' < u} total_u'
-#pragma unroll
-  for (int u = 0; u < kXVec; ++u) {
-    u32 m = mask[u];
-    if (m) {
-      u64 pos = prefix + run + ((excl >> (16 * u)) & 0xFFFF);
-      u64 e = base + ((u64)u * kXThreads + tid) * 8;
-      const u64 lo64 = vn[u].x | ((u64)vn[u].y << 32), hi64 = vn[u].z | ((u64)vn[u].w << 32);
-      while (m) {
-        int b = __ffs(m) - 1;
-        m &= m - 1;
-        if (pos < a.cap) {
-          a.I[pos] = (u32)(e + b);
-          a.V[pos] = (u16)(((b < 4) ? lo64 : hi64) >> ((b & 3) * 16));
-        } else {
-          latch(a.status, SYNC_ERR_CAPACITY);
+  if (warp == kXConsumers / 32 + 1) {
+    // ------------------------------------------------------------ scheduler warp
+    // Static assignment: CTA c owns tiles c, c+G, c+2G, ... (all CTAs resident,
+    // each processes its tiles in increasing order -> look-back terminates).
+    // Runs up to kXQueue tiles ahead of the copier: tile -> tensor table,
+    // then numel / pointers / tile prefix in one round of parallel loads.
+    for (u32 k = 0;; ++k) {
+      const u32 q = k % kXQueue;
+      if (k >= (u32)kXQueue) mbar_wait(&qempty[q], ((k / kXQueue) - 1) & 1);
+      const u64 tile = (u64)blockIdx.x + (u64)k * gridDim.x;
+      if (tile >= a.n_tiles) {
+        if (lane == 0) {
+          jobs[q].tile = ~0ull;
+          mbar_arrive(&qfull[q]);
         }
-        ++pos;
+        break;
       }
+      const u32 t = kSingle ? 0u : a.tile_tensor[tile];
+      u64 v = 0;
+      if (lane == 0) v = kSingle ? a.numel_single : a.numel[t];
+      if (lane == 1) v = (u64)(kSingle ? a.old_single : a.old_ptrs[t]);
+      if (lane == 2) v = (u64)(kSingle ? a.new_single : a.new_ptrs[t]);
+      if (lane == 3) v = kSingle ? 0ull : a.tile_prefix[t];
+      const u64 n = __shfl_sync(0xffffffffu, v, 0);
+      const u64 po = __shfl_sync(0xffffffffu, v, 1);
+      const u64 pn = __shfl_sync(0xffffffffu, v, 2);
+      const u64 tp = __shfl_sync(0xffffffffu, v, 3);
+      if (lane == 0) {
+        TileJob j;
+        j.tile = tile;
+        j.base = (tile - tp) * kTile;
+        j.po = reinterpret_cast<const u16*>(po);
+        j.pn = reinterpret_cast<const u16*>(pn);
+        j.n = n;
+        j.t = t;
+        const u64 rem = n - j.base;
+        const u64 nv = rem < kTile ? rem : kTile;
+        j.n_sub = (u32)((nv + kSub - 1) / kSub);
+        jobs[q] = j;
+        mbar_arrive(&qfull[q]);
+      }
+      __syncwarp();
     }
-    run += (total >> (16 * u)) & 0xFFFF;
+    return;
+  }
+
+  if (warp == kXConsumers / 32) {
+    // ------------------------------------------------------------ copier warp
+    const u64 pol = policy_evict_first();
+    u32 it = 0;
+    for (u32 k = 0;; ++k) {
+      const u32 q = k % kXQueue;
+      mbar_wait(&qfull[q], (k / kXQueue) & 1);
+      const TileJob j = jobs[q];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty[q]);
+      const bool done = j.tile == ~0ull;
+      const u32 n_sub = done ? 1u : j.n_sub;
+      const bool aligned = ((((uintptr_t)j.po) | ((uintptr_t)j.pn)) & 15u) == 0;
+      for (u32 sub = 0; sub < n_sub; ++sub, ++it) {
+        const u32 s = it % kStages;
+        if (it >= (u32)kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+        if (lane == 0) {
+          SubInfo si;
+          if (done) {
+            si.tile = ~0ull;
+            info[s] = si;
+            mbar_arrive(&full[s]);
+          } else {
+            const u64 sb = j.base + (u64)sub * kSub;
+            const u64 rem = j.n - sb;
+            const u32 n_valid = (u32)(rem < kSub ? rem : kSub);
+            const u32 bulk = aligned ? (n_valid & ~7u) : 0u;
+            si.tile = j.tile;
+            si.base = sb;
+            si.po = j.po;
+            si.pn = j.pn;
+            si.t = j.t;
+            si.n_valid = n_valid;
+            si.bulk = bulk;
+            si.sub = (u16)sub;
+            si.n_sub = (u16)n_sub;
+            info[s] = si;
+            u8* dst = data + (size_t)s * kStageBytes;
+            if (bulk) {
+              mbar_arrive_tx(&full[s], 4u * bulk);
+              bulk_g2s(dst, j.po + sb, 2u * bulk, &full[s], pol);
+              bulk_g2s(dst + kSub * 2, j.pn + sb, 2u * bulk, &full[s], pol);
+            } else {
+              mbar_arrive(&full[s]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (done) break;
+    }
+    return;
+  }
+
+  if (warp == kXConsumers / 32 + 2) {
+    // ------------------------------------------------------------ writer warp
+    // Per staged tile: look-back (the only wait on other CTAs), then the
+    // coalesced write of (I, V); the consumers are already counting the next tile.
+    for (u32 k = 0;; ++k) {
+      const u32 b = k & 1;
+      mbar_wait(&sfull[b], (k >> 1) & 1);
+      const StagedTile m = meta[b];
+      if (m.tile == ~0ull) break;
+      const u64 prefix = lookback(a.tile_state, m.tile, m.count);
+      if (lane == 0 && m.count) atomicAdd((unsigned long long*)&a.counts[m.t], (unsigned long long)m.count);
+      const u32* stg = staging + b * kStageCap;
+      if (!m.overflow) {
+        for (u32 q = lane; q < m.count; q += 32) {
+          const u32 e = stg[q];
+          const u64 pos = prefix + q;
+          if (pos < a.cap) {
+            a.I[pos] = (u32)(m.tile_base + (e & 0xFFFFu));
+            a.V[pos] = (u16)(e >> 16);
+          } else {
+            latch(a.status, SYNC_ERR_CAPACITY);
+          }
+        }
+      } else {
+        // slow path (tile denser than the staging list): re-read it from global
+        u64 run = prefix;
+        for (u64 e0 = m.tile_base; e0 < m.tile_end; e0 += 256) {
+          const u64 e = e0 + lane * 8;
+          const uint4 vo = load8_direct(m.po, e, m.tile_end);
+          const uint4 vd = load8_direct(m.pn, e, m.tile_end);
+          u32 mk = change_mask(vo, vd);
+          const u32 c = __popc(mk);
+          const u32 inc = warp_incl_scan(c);
+          u64 pos = run + inc - c;
+          while (mk) {
+            int bb = __ffs(mk) - 1;
+            mk &= mk - 1;
+            if (pos < a.cap) {
+              a.I[pos] = (u32)(e + bb);
+              a.V[pos] = lane16(vd, bb);
+            } else {
+              latch(a.status, SYNC_ERR_CAPACITY);
+            }
+            ++pos;
+          }
+          run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[b]);
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumer warps
+  u32 tile_cnt = 0, tseq = 0, b = 0;
+  bool overflow = false;
+  for (u32 it = 0;; ++it) {
+    const u32 s = it % kStages;
+    mbar_wait(&full[s], (it / kStages) & 1);
+    const SubInfo si = info[s];
+    if (si.tile == ~0ull) {
+      b = tseq & 1;
+      if (tseq >= 2) mbar_wait(&sempty[b], ((tseq >> 1) - 1) & 1);
+      if (tid == 0) {
+        meta[b].tile = ~0ull;
+        mbar_arrive(&sfull[b]);
+      }
+      break;
+    }
+    if (si.sub == 0) {
+      b = tseq & 1;
+      if (tseq >= 2) mbar_wait(&sempty[b], ((tseq >> 1) - 1) & 1);  // writer done with buffer b
+      tile_cnt = 0;
+      overflow = false;
+    }
+    const uint4* so = reinterpret_cast<const uint4*>(data + (size_t)s * kStageBytes);
+    const uint4* sn = reinterpret_cast<const uint4*>(data + (size_t)s * kStageBytes + kSub * 2);
+
+    uint4 vn[kXVec];
+    u32 mask[kXVec];
+    u64 packed = 0;
+#pragma unroll
+    for (int u = 0; u < kXVec; ++u) {
+      const u32 v = (u32)u * kXConsumers + tid;  // vector index within the sub-tile
+      uint4 vo;
+      if (v * 8 + 8 <= si.bulk) {
+        vo = so[v];
+        vn[u] = sn[v];
+      } else if (v * 8 < si.n_valid) {
+        vo = load8_direct(si.po, si.base + v * 8, si.base + si.n_valid);
+        vn[u] = load8_direct(si.pn, si.base + v * 8, si.base + si.n_valid);
+      } else {
+        vo = vn[u] = make_uint4(0, 0, 0, 0);
+      }
+      mask[u] = change_mask(vo, vn[u]);
+      packed |= (u64)__popc(mask[u]) << (16 * u);
+    }
+    u64 sub_total;
+    const u64 excl = consumer_scan(packed, s_wsum, &sub_total);  // first barrier: stage fully read
+    if (tid == 0) mbar_arrive(&empty[s]);                         // -> copier may refill it
+    const u32 st_total = sum_fields(sub_total);
+    if (!overflow && tile_cnt + st_total <= kStageCap) {
+      u32* stg = staging + b * kStageCap;
+      u32 run = tile_cnt;
+#pragma unroll
+      for (int u = 0; u < kXVec; ++u) {
+        u32 mk = mask[u];
+        u32 pos = run + (u32)((excl >> (16 * u)) & 0xFFFF);
+        const u32 local = (u32)si.sub * (u32)kSub + ((u32)u * kXConsumers + tid) * 8;
+        while (mk) {
+          int bb = __ffs(mk) - 1;
+          mk &= mk - 1;
+          stg[pos++] = (local + bb) | ((u32)lane16(vn[u], bb) << 16);
+        }
+        run += (u32)((sub_total >> (16 * u)) & 0xFFFF);
+      }
+    } else {
+      overflow = true;
+    }
+    tile_cnt += st_total;
+    if (si.sub + 1 < si.n_sub) continue;
+
+    // ---- end of tile: publish the aggregate now, hand the staged list to the writer
+    consumer_bar();                                     // all staging writes done
+    if (tid == 0) {
+      publish_aggregate(a.tile_state, si.tile, tile_cnt);
+      StagedTile m;
+      m.tile = si.tile;
+      m.tile_base = si.base - (u64)si.sub * kSub;
+      m.tile_end = si.base + si.n_valid;
+      m.po = si.po;
+      m.pn = si.pn;
+      m.t = si.t;
+      m.count = tile_cnt;
+      m.overflow = overflow ? 1u : 0u;
+      m.pad = 0;
+      meta[b] = m;
+      mbar_arrive(&sfull[b]);
+    }
+    ++tseq;
   }
 }
 
+template <int kStages>
+static size_t extract_smem() {
+  return (size_t)kStages * kStageBytes + 2 * kStageCap * 4 + 2 * (kStages + kXQueue + 2) * 8 +
+         kStages * sizeof(SubInfo) + kXQueue * sizeof(TileJob) + 2 * sizeof(StagedTile) + 16 * 8;
+}
+
+template <bool kSingle, int kStages>
+static void launch_k(const ExtractArgs& a, cudaStream_t s) {
+  static int grid_cap = 0;
+  const size_t sm = extract_smem<kStages>();
+  if (!grid_cap) {
+    cudaFuncSetAttribute(k_extract<kSingle, kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int dev = 0, n_sm = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_extract<kSingle, kStages>, kXBlock, sm);
+    grid_cap = n_sm * (per > 0 ? per : 1);
+  }
+  u64 grid = a.n_tiles < (u64)grid_cap ? a.n_tiles : (u64)grid_cap;
+  k_extract<kSingle, kStages><<<(unsigned)grid, kXBlock, sm, s>>>(a);
+  count_launch();
+}
+
+// Stage count: 2 (two CTAs per SM) unless SS_XSTAGES selects 3 or 4 (one CTA per SM).
+template <bool kSingle>
+static void launch(const ExtractArgs& a, cudaStream_t s) {
+  static int stages = 0;
+  if (!stages) {
+    const char* e = getenv("SS_XSTAGES");
+    stages = e ? atoi(e) : 2;
+  }
+  if (stages == 3) launch_k<kSingle, 3>(a, s);
+  else if (stages == 4) launch_k<kSingle, 4>(a, s);
+  else if (stages == 6) launch_k<kSingle, 6>(a, s);
+  else launch_k<kSingle, 2>(a, s);
+}
+
 void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, const u64* tile_prefix,
-                            const u64* numel, u32 n_tensors, u64 n_tiles, u32* I, u16* V, u64 cap,
+                            const u32* tile_tensor, const u64* numel, u32 n_tensors, u64 n_tiles, u32* I, u16* V, u64 cap,
                             u64* counts, u64* tile_state, u32* tile_counter, u32* status, cudaStream_t s) {
   if (n_tiles == 0) return;
   ExtractArgs a{};
   a.old_ptrs = d_old;
   a.new_ptrs = d_new;
   a.tile_prefix = tile_prefix;
+  a.tile_tensor = tile_tensor;
   a.numel = numel;
+  a.n_tiles = n_tiles;
   a.n_tensors = n_tensors;
   a.I = I;
   a.V = V;
@@ -186,8 +556,7 @@ void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, co
   a.tile_state = tile_state;
   a.tile_counter = tile_counter;
   a.status = status;
-  k_extract<false><<<(unsigned)n_tiles, kXThreads, 0, s>>>(a);
-  count_launch();
+  launch<false>(a, s);
 }
 
 void launch_extract_single(const u16* d_old, const u16* d_new, u64 n, u32* I, u16* V, u64 cap, u64* count,
@@ -198,6 +567,7 @@ void launch_extract_single(const u16* d_old, const u16* d_new, u64 n, u32* I, u1
   a.old_single = d_old;
   a.new_single = d_new;
   a.numel_single = n;
+  a.n_tiles = n_tiles;
   a.n_tensors = 1;
   a.I = I;
   a.V = V;
@@ -206,8 +576,7 @@ void launch_extract_single(const u16* d_old, const u16* d_new, u64 n, u32* I, u1
   a.tile_state = tile_state;
   a.tile_counter = tile_counter;
   a.status = status;
-  k_extract<true><<<(unsigned)n_tiles, kXThreads, 0, s>>>(a);
-  count_launch();
+  launch<true>(a, s);
 }
 
 }  // namespace ss
