@@ -24,7 +24,7 @@ namespace {
 constexpr u64 kAlign = 256;
 
 struct Layout {
-  u64 numel, tile_prefix, tile_tensor, misc, tile_state, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
+  u64 numel, tile_prefix, tile_tensor, misc, tile_state, stage_ring, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
   u64 chunk_hi, chunk_mode, chunk_hioff, totals, recs, bks, views, nviews, crc, total;
 };
 
@@ -43,6 +43,7 @@ Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n) {
   L.tile_tensor = take(4ull * n_tiles);
   L.misc = take(4 * 64);
   L.tile_state = take(8ull * n_tiles);
+  L.stage_ring = take(stage_ring_bytes(n_tiles));
   L.rec_off = take(8ull * (T + 1));
   L.chunk_off = take(8ull * (T + 1));
   L.maxgap = take(4ull * T);
@@ -205,7 +206,8 @@ int sync_ctx_destroy(sync_ctx* ctx) {
 // ------------------------------------------------------------------------ extract
 int sync_extract_workspace_size(uint64_t n, size_t* bytes) {
   if (!bytes || n >= (1ull << 31)) return SYNC_ERR_ARG;
-  *bytes = kAlign + 8 * ((n + kTile - 1) / kTile) + 8;
+  const u64 n_tiles = (n + kTile - 1) / kTile;
+  *bytes = kAlign + pad_to(8 * n_tiles + 8, kAlign) + stage_ring_bytes(n_tiles);
   return SYNC_OK;
 }
 
@@ -223,7 +225,8 @@ int sync_extract(const uint16_t* d_old, const uint16_t* d_new, uint64_t n, uint3
   CK(cudaMemsetAsync(misc, 0, 4, s));  // tile counter (status is sticky until read)
   CK(cudaMemsetAsync(d_count, 0, 8, s));
   if (n_tiles) CK(cudaMemsetAsync(w + kAlign, 0, 8 * n_tiles, s));
-  launch_extract_single(d_old, d_new, n, d_I, d_V, cap, d_count, reinterpret_cast<u64*>(w + kAlign), misc, misc + 1,
+  launch_extract_single(d_old, d_new, n, d_I, d_V, cap, d_count, reinterpret_cast<u64*>(w + kAlign),
+                        reinterpret_cast<u32*>(w + kAlign + pad_to(8 * n_tiles + 8, kAlign)), misc + 1,
                         s);
   CK(cudaGetLastError());
   return SYNC_OK;
@@ -251,7 +254,8 @@ int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const u
   if (x->d.n_tiles) CK(cudaMemsetAsync(x->ws + x->L.tile_state, 0, 8 * x->d.n_tiles, s));
   launch_extract_batched(d_old_ptrs, d_new_ptrs, reinterpret_cast<const u64*>(x->ws + x->L.tile_prefix),
                          reinterpret_cast<const u32*>(x->ws + x->L.tile_tensor), x->plan.numel, x->d.T, x->d.n_tiles, d_I, d_V, x->cfg.max_changed, d_counts,
-                         reinterpret_cast<u64*>(x->ws + x->L.tile_state), x->misc, x->misc + 1, s);
+                         reinterpret_cast<u64*>(x->ws + x->L.tile_state),
+                         reinterpret_cast<u32*>(x->ws + x->L.stage_ring), x->misc + 1, s);
   CK(cudaGetLastError());
   return SYNC_OK;
 }

@@ -32,6 +32,16 @@ constexpr int kXVec = 4;
 constexpr u64 kSub = (u64)kXThreads * kXVec * 8;
 constexpr u32 kSubPerTile = 4;
 constexpr u64 kTile = kSub * kSubPerTile;
+// Per-CTA staging ring (global memory, L2-resident) between the extract
+// consumers and its writer warp: kSlots tiles of up to kSlotCap changes.
+constexpr u32 kSlots = 4;
+constexpr u32 kSlotCap = 8192;
+constexpr u32 kMaxExtractCtas = 512;
+// bytes of the extract staging ring for a launch over n_tiles tiles
+__host__ __device__ inline u64 stage_ring_bytes(u64 n_tiles) {
+  const u64 ctas = n_tiles < kMaxExtractCtas ? n_tiles : kMaxExtractCtas;
+  return ctas * kSlots * kSlotCap * 4;
+}
 
 // Look-back tile state: [63:62] flag, [61:0] value.
 constexpr u64 kFlagA = 1ull << 62;

@@ -5,23 +5,27 @@
 // sorted; bitwise compare, DESIGN C1).
 //
 // One pass over old+new (2S bytes, ~97% of a sync's HBM traffic at 1%
-// density). Persistent, warp-specialised pipeline (DESIGN §6 K1):
-//   * scheduler + copier warps: the next tile (65536 elements, never straddling a
-//     tensor; static round-robin), maps it to its tensor (tile table)
-//     and streams its eight 8192-element sub-tiles
-//     (2 x 16 KB each) into shared-memory stages with TMA bulk copies
-//     (cp.async.bulk ... mbarrier::complete_tx), so loads stay in flight while
-//     the consumers work;
-//   * 8 consumer warps: per sub-tile, 8-bit change masks per 128-bit vector,
-//     release the stage, block scan, and append (local index, value) to a
-//     shared-memory staging list; at the end of the tile ONE decoupled
-//     look-back (warp 0) gives the tile's global offset and the staged list is
-//     written out coalesced. The look-back latency (an L2 round trip behind
-//     the streaming traffic) is paid once per 256 KB of input.
-//   * tiles denser than the staging list (> 12.5%) take a slow path: after
-//     the look-back the tile is re-read from global and written directly.
-// Every claimed tile belongs to a resident CTA and is processed in claim
-// order, so look-back always terminates.
+// density). Persistent, warp-specialised kernel (DESIGN §6 K1). A tile (the
+// look-back unit) is 32768 elements of one tensor, streamed as four 8192-
+// element sub-tiles (16 KB of old + 16 KB of new each):
+//   * scheduler warp: CTA c owns tiles c, c+G, c+2G, ...; resolves tile ->
+//     tensor / pointers a few tiles ahead (tile table + one round of loads);
+//   * copier warp: TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx)
+//     of each sub-tile into one of kStages shared-memory stages;
+//   * 8 consumer warps: per sub-tile, an 8-bit change mask per 128-bit vector,
+//     release the stage, block scan, append (local index | value << 16) to the
+//     tile's staging slot (a per-CTA ring of kSlots slots in global memory,
+//     L2-resident); at the end of the tile publish its aggregate at once;
+//   * writer warp: per tile, the global offset from its own previous tile's
+//     prefix plus the counts published in between (the only wait on other
+//     CTAs), then the coalesced write of (I, V).
+//     The ring gives the writer kSlots tiles of slack, so the look-back
+//     latency never stalls the stream.
+//   * tiles denser than a slot (> 25%) take a slow path: the writer re-reads
+//     the tile from global and writes directly.
+// All CTAs are resident and each counts its tiles in increasing order, so
+// every count a writer waits for is eventually published.
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -30,10 +34,9 @@
 namespace ss {
 
 constexpr int kXConsumers = kXThreads;            // 256 consumer threads (8 warps)
-constexpr int kXBlock = kXConsumers + 96;         // + copier, scheduler and writer warps
+constexpr int kXBlock = kXConsumers + 96;         // + copier, scheduler, writer warps
 constexpr int kXQueue = 4;                        // tiles resolved ahead by the scheduler
 constexpr u32 kStageBytes = (u32)kSub * 2 * 2;    // old + new, 16 KB each
-constexpr u32 kStageCap = 4096;                   // staged changes per tile (12.5%), two buffers
 
 struct ExtractArgs {
   const u16* const* old_ptrs;  // batched: device arrays of tensor pointers
@@ -51,11 +54,12 @@ struct ExtractArgs {
   u64 cap;
   u64* counts;                 // [T]
   u64* tile_state;             // [n_tiles]
-  u32* tile_counter;
+  u32* stage_ring;             // [grid][kSlots][kSlotCap]
   u32* status;
+  unsigned long long* prof;    // debug cycle counters (SS_XPROF=1), else null
 };
 
-struct TileJob {              // scheduler -> copier
+struct TileJob {               // scheduler -> copier
   u64 tile;                    // ~0 = no more tiles
   u64 base;
   const u16* po;
@@ -65,19 +69,7 @@ struct TileJob {              // scheduler -> copier
   u32 n_sub;
 };
 
-struct StagedTile {           // consumers -> writer, one per staging buffer
-  u64 tile;                    // ~0 = no more tiles
-  u64 tile_base;               // first element of the tile within its tensor
-  u64 tile_end;
-  const u16* po;
-  const u16* pn;
-  u32 t;
-  u32 count;
-  u32 overflow;
-  u32 pad;
-};
-
-struct SubInfo {
+struct SubInfo {               // copier -> consumers, one per stage
   u64 tile;                    // ~0 = no more tiles
   u64 base;                    // first element of the sub-tile within its tensor
   const u16* po;
@@ -87,6 +79,18 @@ struct SubInfo {
   u32 bulk;                    // elements delivered by the bulk copies (multiple of 8)
   u16 sub;                     // sub-tile index within the tile
   u16 n_sub;                   // sub-tiles in this tile
+};
+
+struct StagedTile {            // consumers -> writer, one per ring slot
+  u64 tile;                    // ~0 = no more tiles
+  u64 tile_base;               // first element of the tile within its tensor
+  u64 tile_end;
+  const u16* po;
+  const u16* pn;
+  u32 t;
+  u32 count;
+  u32 overflow;
+  u32 pad;
 };
 
 // ---------------------------------------------------------------- mbarrier / bulk-copy PTX
@@ -126,61 +130,53 @@ __device__ __forceinline__ u64 policy_evict_first() {
 }
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kXConsumers) : "memory"); }
 
-// Full-warp decoupled look-back: returns the exclusive prefix of `tile`.
-// Each round reads a window of 32 x kLB predecessor states in one L2 round trip
-// (lane l covers distances 1 + l*kLB .. (l+1)*kLB): with ~one tile per CTA in
-// flight the nearest inclusive prefix is up to a grid's worth of tiles back.
-constexpr int kLB = 8;
-// Publication of the tile aggregate (consumers, as soon as the tile is counted).
-__device__ __forceinline__ void publish_aggregate(u64* state, u64 tile, u64 agg) {
-  st_relaxed(&state[tile], (tile == 0 ? kFlagP : kFlagA) | agg);
-}
-// Resolution of the exclusive prefix (writer warp); publishes the inclusive prefix.
-__device__ __forceinline__ u64 lookback(u64* state, u64 tile, u64 agg) {
-  const u32 lane = lane_id();
-  if (tile == 0) return 0;
-  u64 excl = 0;
-  long long top = (long long)tile - 1;
-  while (true) {
-    u64 st[kLB];
-#pragma unroll
-    for (int i = 0; i < kLB; ++i) {
-      long long idx = top - (long long)(lane * kLB + i);
-      st[i] = idx >= 0 ? ld_relaxed(&state[idx]) : kFlagP;
-    }
-    // per lane: first P (in distance order), X before it, sums
-    int pf = kLB;
-    bool x_before = false, x_any = false;
-    u64 sum_to_p = 0, sum_all = 0;
-#pragma unroll
-    for (int i = kLB - 1; i >= 0; --i) {  // reverse so pf ends as the smallest i with P
-      u32 flag = (u32)(st[i] >> 62);
-      if (flag == 2) pf = i;
-    }
-#pragma unroll
-    for (int i = 0; i < kLB; ++i) {
-      u32 flag = (u32)(st[i] >> 62);
-      u64 v = st[i] & kValMask;
-      if (flag == 0) {
-        x_any = true;
-        if (i < pf) x_before = true;
-      }
-      sum_all += v;
-      if (i <= pf) sum_to_p += v;
-    }
-    const u32 pm = __ballot_sync(0xffffffffu, pf < kLB);
-    const u32 fl = pm ? (u32)(__ffs(pm) - 1) : 32u;  // first lane holding a P
-    const bool mine_x = (lane < fl) ? x_any : (lane == fl ? x_before : false);
-    if (__any_sync(0xffffffffu, mine_x)) continue;     // a predecessor not ready yet
-    const u64 v = (lane < fl) ? sum_all : (lane == fl ? sum_to_p : 0);
-    excl += warp_sum64(v);
-    if (pm) break;
-    top -= 32 * kLB;
-  }
-  if (lane == 0) st_relaxed(&state[tile], kFlagP | (excl + agg));
-  return excl;
+// ---------------------------------------------------------------- cross-CTA prefix
+// Tile states: bit 63 = published, [62:0] = the tile's change count. Consumers
+// publish a tile's count as soon as it is counted. With the static round-robin
+// assignment (tile j = c + k*G), the writer of CTA c already knows the inclusive
+// prefix of its own previous tile j-G, so
+//     excl(j) = incl(j-G) + sum_{i = j-G+1}^{j-1} count(i)
+// needs only the G-1 counts in between — published by consumers, never by other
+// writers, so no chain of look-backs forms. One L2 round trip reads the whole
+// window (32 lanes x kLB contiguous states); entries not yet published are
+// re-polled alone, with a short back-off.
+constexpr int kLB = 16;  // window 512 >= G - 1 for G <= 513 CTAs
+constexpr u64 kPublished = 1ull << 63;
+
+__device__ __forceinline__ void publish_count(u64* state, u64 tile, u64 cnt) {
+  st_relaxed(&state[tile], kPublished | cnt);
 }
 
+// Sum of the published counts of tiles [lo, hi) (full warp; waits until all are published).
+__device__ __forceinline__ u64 window_sum(u64* state, u64 lo, u64 hi) {
+  const u32 lane = lane_id();
+  u64 acc = 0;
+  for (u64 base = lo; base < hi; base += 32 * kLB) {
+    u32 pending = 0;
+    u64 part = 0;
+#pragma unroll
+    for (int i = 0; i < kLB; ++i)
+      if (base + lane * kLB + i < hi) pending |= 1u << i;
+    while (true) {
+#pragma unroll
+      for (int i = 0; i < kLB; ++i) {
+        if (pending & (1u << i)) {
+          const u64 v = ld_relaxed(&state[base + lane * kLB + i]);
+          if (v & kPublished) {
+            part += v & ~kPublished;
+            pending &= ~(1u << i);
+          }
+        }
+      }
+      if (!__any_sync(0xffffffffu, pending != 0)) break;
+      __nanosleep(128);
+    }
+    acc += warp_sum64(part);
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------- per-vector helpers
 __device__ __forceinline__ uint4 load8_direct(const u16* p, u64 e, u64 n) {
   u16 h[8];
 #pragma unroll
@@ -200,8 +196,9 @@ __device__ __forceinline__ u16 lane16(const uint4& v, int b) {
   return (u16)(((b < 4) ? lo64 : hi64) >> ((b & 3) * 16));
 }
 
-// Block (consumer) exclusive scan of packed per-vector counts. Returns this thread's
-// exclusive packed offsets; *total = block total (packed). Two consumer barriers.
+// Consumer-block exclusive scan of packed per-vector counts (four 16-bit fields,
+// each <= 2048: no carries). Returns this thread's exclusive offsets; *total =
+// block total. Two consumer barriers.
 __device__ __forceinline__ u64 consumer_scan(u64 packed, u64* s_wsum, u64* total) {
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const u64 incl = warp_incl_scan64(packed);
@@ -226,17 +223,17 @@ template <bool kSingle, int kStages>
 __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
   extern __shared__ __align__(128) u8 smem[];
   u8* data = smem;
-  u32* staging = reinterpret_cast<u32*>(smem + kStages * kStageBytes);  // [2][kStageCap]
-  u64* full = reinterpret_cast<u64*>(staging + 2 * kStageCap);
+  u64* full = reinterpret_cast<u64*>(smem + kStages * kStageBytes);
   u64* empty = full + kStages;
   u64* qfull = empty + kStages;
   u64* qempty = qfull + kXQueue;
   u64* sfull = qempty + kXQueue;
-  u64* sempty = sfull + 2;
-  SubInfo* info = reinterpret_cast<SubInfo*>(sempty + 2);
+  u64* sempty = sfull + kSlots;
+  SubInfo* info = reinterpret_cast<SubInfo*>(sempty + kSlots);
   TileJob* jobs = reinterpret_cast<TileJob*>(info + kStages);
   StagedTile* meta = reinterpret_cast<StagedTile*>(jobs + kXQueue);
-  u64* s_wsum = reinterpret_cast<u64*>(meta + 2);  // [0..8] scan
+  u64* s_wsum = reinterpret_cast<u64*>(meta + kSlots);  // [0..8] scan
+  u32* ring = a.stage_ring + (size_t)blockIdx.x * kSlots * kSlotCap;
   const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   if (tid == 0) {
@@ -248,7 +245,7 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
       mbar_init(&qfull[q], 1);
       mbar_init(&qempty[q], 1);
     }
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < (int)kSlots; ++q) {
       mbar_init(&sfull[q], 1);
       mbar_init(&sempty[q], 1);
     }
@@ -258,10 +255,6 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
 
   if (warp == kXConsumers / 32 + 1) {
     // ------------------------------------------------------------ scheduler warp
-    // Static assignment: CTA c owns tiles c, c+G, c+2G, ... (all CTAs resident,
-    // each processes its tiles in increasing order -> look-back terminates).
-    // Runs up to kXQueue tiles ahead of the copier: tile -> tensor table,
-    // then numel / pointers / tile prefix in one round of parallel loads.
     for (u32 k = 0;; ++k) {
       const u32 q = k % kXQueue;
       if (k >= (u32)kXQueue) mbar_wait(&qempty[q], ((k / kXQueue) - 1) & 1);
@@ -306,6 +299,7 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
     // ------------------------------------------------------------ copier warp
     const u64 pol = policy_evict_first();
     u32 it = 0;
+    long long p_copy = 0;
     for (u32 k = 0;; ++k) {
       const u32 q = k % kXQueue;
       mbar_wait(&qfull[q], (k / kXQueue) & 1);
@@ -317,7 +311,11 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
       const bool aligned = ((((uintptr_t)j.po) | ((uintptr_t)j.pn)) & 15u) == 0;
       for (u32 sub = 0; sub < n_sub; ++sub, ++it) {
         const u32 s = it % kStages;
-        if (it >= (u32)kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+        if (it >= (u32)kStages) {
+          const long long c0 = clock64();
+          mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+          p_copy += clock64() - c0;
+        }
         if (lane == 0) {
           SubInfo si;
           if (done) {
@@ -353,34 +351,54 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
       }
       if (done) break;
     }
+    if (a.prof && lane == 0) atomicAdd(&a.prof[2], (unsigned long long)p_copy);
     return;
   }
 
   if (warp == kXConsumers / 32 + 2) {
+    long long p_w = 0, p_lb = 0, p_wr = 0, n_t = 0;
+    u64 own_incl = 0;  // inclusive prefix of this CTA's previous tile
     // ------------------------------------------------------------ writer warp
-    // Per staged tile: look-back (the only wait on other CTAs), then the
-    // coalesced write of (I, V); the consumers are already counting the next tile.
     for (u32 k = 0;; ++k) {
-      const u32 b = k & 1;
-      mbar_wait(&sfull[b], (k >> 1) & 1);
+      const u32 b = k % kSlots;
+      long long c0 = clock64();
+      mbar_wait(&sfull[b], (k / kSlots) & 1);
+      long long c1 = clock64();
+      p_w += c1 - c0;
       const StagedTile m = meta[b];
       if (m.tile == ~0ull) break;
-      const u64 prefix = lookback(a.tile_state, m.tile, m.count);
+      const u64 G = gridDim.x;
+      const u64 prefix = (m.tile < G ? 0ull : own_incl) + window_sum(a.tile_state, m.tile < G ? 0ull : m.tile - G + 1, m.tile);
+      own_incl = prefix + m.count;
+      long long c2 = clock64();
+      p_lb += c2 - c1;
+      ++n_t;
       if (lane == 0 && m.count) atomicAdd((unsigned long long*)&a.counts[m.t], (unsigned long long)m.count);
-      const u32* stg = staging + b * kStageCap;
+      const u32* stg = ring + b * kSlotCap;
       if (!m.overflow) {
-        for (u32 q = lane; q < m.count; q += 32) {
-          const u32 e = stg[q];
-          const u64 pos = prefix + q;
-          if (pos < a.cap) {
-            a.I[pos] = (u32)(m.tile_base + (e & 0xFFFFu));
-            a.V[pos] = (u16)(e >> 16);
-          } else {
-            latch(a.status, SYNC_ERR_CAPACITY);
+        // 8 staged entries per lane in flight (the ring is L2-resident)
+        for (u32 q0 = 0; q0 < m.count; q0 += 256) {
+          u32 e[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const u32 q = q0 + i * 32 + lane;
+            e[i] = q < m.count ? stg[q] : 0u;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const u32 q = q0 + i * 32 + lane;
+            if (q >= m.count) break;
+            const u64 pos = prefix + q;
+            if (pos < a.cap) {
+              a.I[pos] = (u32)(m.tile_base + (e[i] & 0xFFFFu));
+              a.V[pos] = (u16)(e[i] >> 16);
+            } else {
+              latch(a.status, SYNC_ERR_CAPACITY);
+            }
           }
         }
       } else {
-        // slow path (tile denser than the staging list): re-read it from global
+        // slow path (tile denser than a slot): re-read it from global
         u64 run = prefix;
         for (u64 e0 = m.tile_base; e0 < m.tile_end; e0 += 256) {
           const u64 e = e0 + lane * 8;
@@ -405,7 +423,14 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
         }
       }
       __syncwarp();
+      p_wr += clock64() - c2;
       if (lane == 0) mbar_arrive(&sempty[b]);
+    }
+    if (a.prof && lane == 0) {
+      atomicAdd(&a.prof[3], (unsigned long long)p_w);
+      atomicAdd(&a.prof[4], (unsigned long long)p_lb);
+      atomicAdd(&a.prof[5], (unsigned long long)p_wr);
+      atomicAdd(&a.prof[8], (unsigned long long)n_t);
     }
     return;
   }
@@ -413,13 +438,18 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
   // -------------------------------------------------------------- consumer warps
   u32 tile_cnt = 0, tseq = 0, b = 0;
   bool overflow = false;
+  long long p_full = 0, p_se = 0, n_s = 0;
+  const long long c_start = clock64();
   for (u32 it = 0;; ++it) {
     const u32 s = it % kStages;
+    const long long c0 = clock64();
     mbar_wait(&full[s], (it / kStages) & 1);
+    p_full += clock64() - c0;
+    ++n_s;
     const SubInfo si = info[s];
     if (si.tile == ~0ull) {
-      b = tseq & 1;
-      if (tseq >= 2) mbar_wait(&sempty[b], ((tseq >> 1) - 1) & 1);
+      b = tseq % kSlots;
+      if (tseq >= kSlots) mbar_wait(&sempty[b], ((tseq / kSlots) - 1) & 1);
       if (tid == 0) {
         meta[b].tile = ~0ull;
         mbar_arrive(&sfull[b]);
@@ -427,8 +457,10 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
       break;
     }
     if (si.sub == 0) {
-      b = tseq & 1;
-      if (tseq >= 2) mbar_wait(&sempty[b], ((tseq >> 1) - 1) & 1);  // writer done with buffer b
+      b = tseq % kSlots;
+      const long long c1 = clock64();
+      if (tseq >= kSlots) mbar_wait(&sempty[b], ((tseq / kSlots) - 1) & 1);  // writer done with slot b
+      p_se += clock64() - c1;
       tile_cnt = 0;
       overflow = false;
     }
@@ -458,8 +490,8 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
     const u64 excl = consumer_scan(packed, s_wsum, &sub_total);  // first barrier: stage fully read
     if (tid == 0) mbar_arrive(&empty[s]);                         // -> copier may refill it
     const u32 st_total = sum_fields(sub_total);
-    if (!overflow && tile_cnt + st_total <= kStageCap) {
-      u32* stg = staging + b * kStageCap;
+    if (!overflow && tile_cnt + st_total <= kSlotCap) {
+      u32* stg = ring + b * kSlotCap;
       u32 run = tile_cnt;
 #pragma unroll
       for (int u = 0; u < kXVec; ++u) {
@@ -482,7 +514,7 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
     // ---- end of tile: publish the aggregate now, hand the staged list to the writer
     consumer_bar();                                     // all staging writes done
     if (tid == 0) {
-      publish_aggregate(a.tile_state, si.tile, tile_cnt);
+      publish_count(a.tile_state, si.tile, tile_cnt);
       StagedTile m;
       m.tile = si.tile;
       m.tile_base = si.base - (u64)si.sub * kSub;
@@ -498,12 +530,18 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
     }
     ++tseq;
   }
+  if (a.prof && tid == 0) {
+    atomicAdd(&a.prof[0], (unsigned long long)p_full);
+    atomicAdd(&a.prof[1], (unsigned long long)p_se);
+    atomicAdd(&a.prof[6], (unsigned long long)(clock64() - c_start));
+    atomicAdd(&a.prof[9], (unsigned long long)n_s);
+  }
 }
 
 template <int kStages>
 static size_t extract_smem() {
-  return (size_t)kStages * kStageBytes + 2 * kStageCap * 4 + 2 * (kStages + kXQueue + 2) * 8 +
-         kStages * sizeof(SubInfo) + kXQueue * sizeof(TileJob) + 2 * sizeof(StagedTile) + 16 * 8;
+  return (size_t)kStages * kStageBytes + 2 * (kStages + kXQueue + kSlots) * 8 + kStages * sizeof(SubInfo) +
+         kXQueue * sizeof(TileJob) + kSlots * sizeof(StagedTile) + 16 * 8;
 }
 
 template <bool kSingle, int kStages>
@@ -517,29 +555,49 @@ static void launch_k(const ExtractArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_extract<kSingle, kStages>, kXBlock, sm);
     grid_cap = n_sm * (per > 0 ? per : 1);
+    if (grid_cap > (int)kMaxExtractCtas) grid_cap = (int)kMaxExtractCtas;
   }
   u64 grid = a.n_tiles < (u64)grid_cap ? a.n_tiles : (u64)grid_cap;
-  k_extract<kSingle, kStages><<<(unsigned)grid, kXBlock, sm, s>>>(a);
+  static unsigned long long* prof = nullptr;
+  static int want_prof = -1;
+  if (want_prof < 0) want_prof = getenv("SS_XPROF") ? 1 : 0;
+  ExtractArgs b = a;
+  if (want_prof) {  // debug instrumentation only
+    if (!prof) cudaMalloc(&prof, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), s);
+    b.prof = prof;
+  }
+  k_extract<kSingle, kStages><<<(unsigned)grid, kXBlock, sm, s>>>(b);
   count_launch();
+  if (want_prof) {
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const double G = (double)grid;
+    fprintf(stderr,
+            "[xprof] grid %llu tiles/cta %.1f subs/cta %.1f | per CTA kcycles: consumer total %.1f wait_full %.1f "
+            "wait_slot %.1f | copier wait_empty %.1f | writer wait %.1f lookback %.1f write %.1f\n",
+            (unsigned long long)grid, h[8] / G, h[9] / G, h[6] / G / 1e3, h[0] / G / 1e3, h[1] / G / 1e3,
+            h[2] / G / 1e3, h[3] / G / 1e3, h[4] / G / 1e3, h[5] / G / 1e3);
+  }
 }
 
-// Stage count: 2 (two CTAs per SM) unless SS_XSTAGES selects 3 or 4 (one CTA per SM).
+// Stage count: 3 by default (two CTAs per SM); SS_XSTAGES=2|4 for experiments.
 template <bool kSingle>
 static void launch(const ExtractArgs& a, cudaStream_t s) {
   static int stages = 0;
   if (!stages) {
     const char* e = getenv("SS_XSTAGES");
-    stages = e ? atoi(e) : 2;
+    stages = e ? atoi(e) : 3;
   }
-  if (stages == 3) launch_k<kSingle, 3>(a, s);
+  if (stages == 2) launch_k<kSingle, 2>(a, s);
   else if (stages == 4) launch_k<kSingle, 4>(a, s);
-  else if (stages == 6) launch_k<kSingle, 6>(a, s);
-  else launch_k<kSingle, 2>(a, s);
+  else launch_k<kSingle, 3>(a, s);
 }
 
 void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, const u64* tile_prefix,
-                            const u32* tile_tensor, const u64* numel, u32 n_tensors, u64 n_tiles, u32* I, u16* V, u64 cap,
-                            u64* counts, u64* tile_state, u32* tile_counter, u32* status, cudaStream_t s) {
+                            const u32* tile_tensor, const u64* numel, u32 n_tensors, u64 n_tiles, u32* I, u16* V,
+                            u64 cap, u64* counts, u64* tile_state, u32* stage_ring, u32* status, cudaStream_t s) {
   if (n_tiles == 0) return;
   ExtractArgs a{};
   a.old_ptrs = d_old;
@@ -554,13 +612,13 @@ void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, co
   a.cap = cap;
   a.counts = counts;
   a.tile_state = tile_state;
-  a.tile_counter = tile_counter;
+  a.stage_ring = stage_ring;
   a.status = status;
   launch<false>(a, s);
 }
 
 void launch_extract_single(const u16* d_old, const u16* d_new, u64 n, u32* I, u16* V, u64 cap, u64* count,
-                           u64* tile_state, u32* tile_counter, u32* status, cudaStream_t s) {
+                           u64* tile_state, u32* stage_ring, u32* status, cudaStream_t s) {
   u64 n_tiles = (n + kTile - 1) / kTile;
   if (n_tiles == 0) return;
   ExtractArgs a{};
@@ -574,7 +632,7 @@ void launch_extract_single(const u16* d_old, const u16* d_new, u64 n, u32* I, u1
   a.cap = cap;
   a.counts = count;
   a.tile_state = tile_state;
-  a.tile_counter = tile_counter;
+  a.stage_ring = stage_ring;
   a.status = status;
   launch<true>(a, s);
 }

@@ -42,12 +42,22 @@ def main():
     sg.fill_new(X, Y, m, 0, rho)
     snd = ss.SparseSyncSender(X, Y, max_changed=int(m.total * rho * 1.1) + (1 << 20))
     S = 2 * m.total
-    tag = {"workload": wl, "rho": rho, "stages": os.environ.get("SS_XSTAGES", "2")}
-    t_ext = timeit(lambda: snd.ctx.sync_extract_batched(snd.old_ptrs, snd.new_ptrs, snd.I, snd.V, snd.counts), reps)
-    nnz = int(snd.counts.sum().item())
-    snd.check()
-    b = 2 * S + 6 * nnz
-    print(json.dumps({**tag, "stage": "extract", "ms": round(t_ext, 4), "GBps": round(b / t_ext / 1e6, 1)}))
+    tag = {"workload": wl, "rho": rho, "stages": os.environ.get("SS_XSTAGES", "3")}
+    # read-only and copy references over the same bytes (torch kernels)
+    xa = X[0].new_empty(0).set_(X[0].untyped_storage())  # whole arena
+    t_rd = timeit(lambda: xa.view(torch.int64).sum(), reps)
+    print(json.dumps({**tag, "stage": "ref_torch_sum_read", "ms": round(t_rd, 4),
+                      "GBps": round(2 * m.total / t_rd / 1e6, 1)}))
+    for trial in range(int(os.environ.get("XB_TRIALS", "3"))):
+        t_ext = timeit(lambda: snd.ctx.sync_extract_batched(snd.old_ptrs, snd.new_ptrs, snd.I, snd.V, snd.counts),
+                       reps)
+        nnz = int(snd.counts.sum().item())
+        snd.check()
+        b = 2 * S + 6 * nnz
+        print(json.dumps({**tag, "stage": "extract", "trial": trial, "ms": round(t_ext, 4),
+                          "GBps": round(b / t_ext / 1e6, 1)}))
+    if os.environ.get("XB_ONLY_EXTRACT"):
+        return
     t_cmp = timeit(lambda: snd.ctx.sync_compress(snd.I, snd.V, snd.counts, snd.enc), reps)
     st = snd.stats()
     print(json.dumps({**tag, "stage": "compress", "ms": round(t_cmp, 4), "nnz": nnz, "chunks": st["n_chunks"]}))
