@@ -34,8 +34,8 @@ constexpr u32 kSubPerTile = 4;
 constexpr u64 kTile = kSub * kSubPerTile;
 // Per-CTA staging ring (global memory, L2-resident) between the extract
 // consumers and its writer warp: kSlots tiles of up to kSlotCap changes.
-constexpr u32 kSlots = 4;
-constexpr u32 kSlotCap = 8192;
+constexpr u32 kSlots = 16;
+constexpr u32 kSlotCap = 4096;
 constexpr u32 kMaxExtractCtas = 512;
 // bytes of the extract staging ring for a launch over n_tiles tiles
 __host__ __device__ inline u64 stage_ring_bytes(u64 n_tiles) {

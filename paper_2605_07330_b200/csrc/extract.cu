@@ -13,15 +13,15 @@
 //   * copier warp: TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx)
 //     of each sub-tile into one of kStages shared-memory stages;
 //   * 8 consumer warps: per sub-tile, an 8-bit change mask per 128-bit vector,
-//     release the stage, block scan, append (local index | value << 16) to the
+//     one block scan, append (local index | value << 16) to the
 //     tile's staging slot (a per-CTA ring of kSlots slots in global memory,
 //     L2-resident); at the end of the tile publish its aggregate at once;
-//   * writer warp: per tile, the global offset from its own previous tile's
+//   * writer warps: per tile, the global offset from its own previous tile's
 //     prefix plus the counts published in between (the only wait on other
 //     CTAs), then the coalesced write of (I, V).
 //     The ring gives the writer kSlots tiles of slack, so the look-back
 //     latency never stalls the stream.
-//   * tiles denser than a slot (> 25%) take a slow path: the writer re-reads
+//   * tiles denser than a slot (> 12.5%) take a slow path: the writer re-reads
 //     the tile from global and writes directly.
 // All CTAs are resident and each counts its tiles in increasing order, so
 // every count a writer waits for is eventually published.
@@ -34,7 +34,8 @@
 namespace ss {
 
 constexpr int kXConsumers = kXThreads;            // 256 consumer threads (8 warps)
-constexpr int kXBlock = kXConsumers + 96;         // + copier, scheduler, writer warps
+constexpr int kWriters = 2;                       // writer warps
+constexpr int kXBlock = kXConsumers + 64 + 32 * kWriters;  // + copier, scheduler, writers
 constexpr int kXQueue = 4;                        // tiles resolved ahead by the scheduler
 constexpr u32 kStageBytes = (u32)kSub * 2 * 2;    // old + new, 16 KB each
 
@@ -196,29 +197,6 @@ __device__ __forceinline__ u16 lane16(const uint4& v, int b) {
   return (u16)(((b < 4) ? lo64 : hi64) >> ((b & 3) * 16));
 }
 
-// Consumer-block exclusive scan of packed per-vector counts (four 16-bit fields,
-// each <= 2048: no carries). Returns this thread's exclusive offsets; *total =
-// block total. Two consumer barriers.
-__device__ __forceinline__ u64 consumer_scan(u64 packed, u64* s_wsum, u64* total) {
-  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const u64 incl = warp_incl_scan64(packed);
-  if (lane == 31) s_wsum[warp] = incl;
-  consumer_bar();
-  if (warp == 0) {
-    u64 w = lane < kXConsumers / 32 ? s_wsum[lane] : 0;
-    u64 wi = warp_incl_scan64(w);
-    if (lane < kXConsumers / 32) s_wsum[lane] = wi - w;
-    if (lane == kXConsumers / 32 - 1) s_wsum[8] = wi;
-  }
-  consumer_bar();
-  *total = s_wsum[8];
-  return s_wsum[warp] + incl - packed;
-}
-
-__device__ __forceinline__ u32 sum_fields(u64 p) {
-  return (u32)((p & 0xFFFF) + ((p >> 16) & 0xFFFF) + ((p >> 32) & 0xFFFF) + (p >> 48));
-}
-
 template <bool kSingle, int kStages>
 __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
   extern __shared__ __align__(128) u8 smem[];
@@ -232,14 +210,18 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
   SubInfo* info = reinterpret_cast<SubInfo*>(sempty + kSlots);
   TileJob* jobs = reinterpret_cast<TileJob*>(info + kStages);
   StagedTile* meta = reinterpret_cast<StagedTile*>(jobs + kXQueue);
-  u64* s_wsum = reinterpret_cast<u64*>(meta + kSlots);  // [0..8] scan
+  u64* s_wsum = reinterpret_cast<u64*>(meta + kSlots);  // [0..7] scan (2 x 8 u32)
+  u64* s_incl = s_wsum + 8;                              // writer hand-off: inclusive prefix
+  u32* s_done = reinterpret_cast<u32*>(s_wsum + 9);      // tiles whose prefix is known
   u32* ring = a.stage_ring + (size_t)blockIdx.x * kSlots * kSlotCap;
   const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   if (tid == 0) {
+    *s_done = 0;
+    *s_incl = 0;
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kXConsumers / 32);
     }
     for (int q = 0; q < kXQueue; ++q) {
       mbar_init(&qfull[q], 1);
@@ -355,11 +337,16 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
     return;
   }
 
-  if (warp == kXConsumers / 32 + 2) {
+  if (warp >= kXConsumers / 32 + 2) {
+    // ------------------------------------------------------------ writer warps
+    // kWriters warps take the CTA's tiles round-robin. The expensive part — the
+    // window of G-1 published counts — runs concurrently in every writer; only
+    // the cheap inclusive-prefix hand-off between consecutive tiles is serial
+    // (through shared memory).
+    const u32 w = warp - (kXConsumers / 32 + 2);
     long long p_w = 0, p_lb = 0, p_wr = 0, n_t = 0;
-    u64 own_incl = 0;  // inclusive prefix of this CTA's previous tile
-    // ------------------------------------------------------------ writer warp
-    for (u32 k = 0;; ++k) {
+    const u64 G = gridDim.x;
+    for (u32 k = w;; k += kWriters) {
       const u32 b = k % kSlots;
       long long c0 = clock64();
       mbar_wait(&sfull[b], (k / kSlots) & 1);
@@ -367,33 +354,42 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
       p_w += c1 - c0;
       const StagedTile m = meta[b];
       if (m.tile == ~0ull) break;
-      const u64 G = gridDim.x;
-      const u64 prefix = (m.tile < G ? 0ull : own_incl) + window_sum(a.tile_state, m.tile < G ? 0ull : m.tile - G + 1, m.tile);
-      own_incl = prefix + m.count;
+      const u64 win = window_sum(a.tile_state, m.tile < G ? 0ull : m.tile - G + 1, m.tile);
+      // wait for the inclusive prefix of this CTA's previous tile (k - 1)
+      while (*(volatile u32*)s_done != k) __nanosleep(32);
+      const u64 prefix = (m.tile < G ? 0ull : *(volatile u64*)s_incl) + win;
+      __syncwarp();
+      if (lane == 0) {
+        *(volatile u64*)s_incl = prefix + m.count;
+        __threadfence_block();
+        *(volatile u32*)s_done = k + 1;
+      }
       long long c2 = clock64();
       p_lb += c2 - c1;
       ++n_t;
       if (lane == 0 && m.count) atomicAdd((unsigned long long*)&a.counts[m.t], (unsigned long long)m.count);
       const u32* stg = ring + b * kSlotCap;
       if (!m.overflow) {
-        // 8 staged entries per lane in flight (the ring is L2-resident)
-        for (u32 q0 = 0; q0 < m.count; q0 += 256) {
-          u32 e[8];
+        // 16 staged entries per lane in flight: 4 x 128-bit loads (the ring is L2-resident)
+        for (u32 q0 = 0; q0 < m.count; q0 += 512) {
+          uint4 e[4];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const u32 q = q0 + i * 32 + lane;
-            e[i] = q < m.count ? stg[q] : 0u;
-          }
+          for (int i = 0; i < 4; ++i) e[i] = *reinterpret_cast<const uint4*>(stg + q0 + i * 128 + 4 * lane);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const u32 q = q0 + i * 32 + lane;
-            if (q >= m.count) break;
-            const u64 pos = prefix + q;
-            if (pos < a.cap) {
-              a.I[pos] = (u32)(m.tile_base + (e[i] & 0xFFFFu));
-              a.V[pos] = (u16)(e[i] >> 16);
-            } else {
-              latch(a.status, SYNC_ERR_CAPACITY);
+          for (int i = 0; i < 4; ++i) {
+            const u32 ev[4] = {e[i].x, e[i].y, e[i].z, e[i].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const u32 q = q0 + i * 128 + 4 * lane + c;
+              if (q < m.count) {
+                const u64 pos = prefix + q;
+                if (pos < a.cap) {
+                  a.I[pos] = (u32)(m.tile_base + (ev[c] & 0xFFFFu));
+                  a.V[pos] = (u16)(ev[c] >> 16);
+                } else {
+                  latch(a.status, SYNC_ERR_CAPACITY);
+                }
+              }
             }
           }
         }
@@ -448,11 +444,13 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
     ++n_s;
     const SubInfo si = info[s];
     if (si.tile == ~0ull) {
-      b = tseq % kSlots;
-      if (tseq >= kSlots) mbar_wait(&sempty[b], ((tseq / kSlots) - 1) & 1);
-      if (tid == 0) {
-        meta[b].tile = ~0ull;
-        mbar_arrive(&sfull[b]);
+      for (u32 kk = tseq; kk < tseq + kWriters; ++kk) {  // one sentinel per writer warp
+        b = kk % kSlots;
+        if (kk >= kSlots) mbar_wait(&sempty[b], ((kk / kSlots) - 1) & 1);
+        if (tid == 0) {
+          meta[b].tile = ~0ull;
+          mbar_arrive(&sfull[b]);
+        }
       }
       break;
     }
@@ -466,48 +464,61 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
     }
     const uint4* so = reinterpret_cast<const uint4*>(data + (size_t)s * kStageBytes);
     const uint4* sn = reinterpret_cast<const uint4*>(data + (size_t)s * kStageBytes + kSub * 2);
+    const u16* sn16 = reinterpret_cast<const u16*>(data + (size_t)s * kStageBytes + kSub * 2);
 
-    uint4 vn[kXVec];
-    u32 mask[kXVec];
-    u64 packed = 0;
+    // Thread t owns the 4 consecutive vectors 4t..4t+3 (elements 32t..32t+31), so
+    // thread order == index order and one u32 scan places every change. Load u
+    // reads vector 4t + ((t/2 + u) & 3): the 8 threads of each LDS.128 phase hit
+    // 8 distinct 16-byte columns (conflict-free).
+    u32 masks = 0;  // bit 8j + b <-> element 32t + 8j + b
+    const u32 rot = (tid >> 1) & 3;
 #pragma unroll
     for (int u = 0; u < kXVec; ++u) {
-      const u32 v = (u32)u * kXConsumers + tid;  // vector index within the sub-tile
-      uint4 vo;
+      const u32 j = (rot + (u32)u) & 3;
+      const u32 v = 4 * tid + j;  // vector index within the sub-tile
+      uint4 vo, vd;
       if (v * 8 + 8 <= si.bulk) {
         vo = so[v];
-        vn[u] = sn[v];
+        vd = sn[v];
       } else if (v * 8 < si.n_valid) {
         vo = load8_direct(si.po, si.base + v * 8, si.base + si.n_valid);
-        vn[u] = load8_direct(si.pn, si.base + v * 8, si.base + si.n_valid);
+        vd = load8_direct(si.pn, si.base + v * 8, si.base + si.n_valid);
       } else {
-        vo = vn[u] = make_uint4(0, 0, 0, 0);
+        vo = vd = make_uint4(0, 0, 0, 0);
       }
-      mask[u] = change_mask(vo, vn[u]);
-      packed |= (u64)__popc(mask[u]) << (16 * u);
+      masks |= change_mask(vo, vd) << (8 * j);
     }
-    u64 sub_total;
-    const u64 excl = consumer_scan(packed, s_wsum, &sub_total);  // first barrier: stage fully read
-    if (tid == 0) mbar_arrive(&empty[s]);                         // -> copier may refill it
-    const u32 st_total = sum_fields(sub_total);
+    const u32 cnt = __popc(masks);
+    // block exclusive scan (one barrier; s_wsum double-buffered by sub-tile parity)
+    const u32 incl = warp_incl_scan(cnt);
+    u32* wsum = reinterpret_cast<u32*>(s_wsum) + (it & 1) * 8;
+    if (lane == 31) wsum[warp] = incl;
+    consumer_bar();
+    u32 wexcl = 0, st_total = 0;
+#pragma unroll
+    for (int w = 0; w < kXConsumers / 32; ++w) {
+      const u32 x = wsum[w];
+      wexcl += (w < (int)warp) ? x : 0u;
+      st_total += x;
+    }
     if (!overflow && tile_cnt + st_total <= kSlotCap) {
       u32* stg = ring + b * kSlotCap;
-      u32 run = tile_cnt;
-#pragma unroll
-      for (int u = 0; u < kXVec; ++u) {
-        u32 mk = mask[u];
-        u32 pos = run + (u32)((excl >> (16 * u)) & 0xFFFF);
-        const u32 local = (u32)si.sub * (u32)kSub + ((u32)u * kXConsumers + tid) * 8;
-        while (mk) {
-          int bb = __ffs(mk) - 1;
-          mk &= mk - 1;
-          stg[pos++] = (local + bb) | ((u32)lane16(vn[u], bb) << 16);
-        }
-        run += (u32)((sub_total >> (16 * u)) & 0xFFFF);
+      u32 pos = tile_cnt + wexcl + incl - cnt;
+      const u32 local = (u32)si.sub * (u32)kSub + 32 * tid;
+      u32 mk = masks;
+      while (mk) {
+        const int bb = __ffs(mk) - 1;
+        mk &= mk - 1;
+        u16 val;
+        if (32 * tid + bb + 1 <= si.bulk) val = sn16[32 * tid + bb];
+        else val = si.pn[si.base + 32 * tid + bb];
+        stg[pos++] = (local + bb) | ((u32)val << 16);
       }
     } else {
       overflow = true;
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // 8 warp arrivals release the stage to the copier
     tile_cnt += st_total;
     if (si.sub + 1 < si.n_sub) continue;
 
