@@ -220,7 +220,7 @@ class Rank:
         rec(4)
         snd.commit()
         rec(5)
-        self.sg.toggle(snd.new_ptrs, snd.I, snd.counts, len(self.m.tensors), self.toggle_scratch)
+        self.sg.toggle(snd.new_ptrs, snd.I, snd.V, snd.counts, len(self.m.tensors), self.toggle_scratch)
         rec(6)
         return blist
 

@@ -2,23 +2,41 @@
 // commit after the transfer, P:300 / DESIGN C13).
 //
 // W[I[k]] <- V[k]. Scattered 2-byte stores: the cost is the partial-sector
-// read-modify-write of every touched 32-byte sector, not the I/V stream.
+// read-modify-write of every touched 32-byte sector (ncu: one 32 B DRAM read +
+// one 32 B write per touched sector), not the I/V stream. Stores are fire-and-
+// forget, so throughput is set by how many (I, V) loads each thread keeps in
+// flight: every thread loads kU pairs before issuing its kU stores.
 // The batched commit walks the raw (I, V) of sync_extract_batched chunk by
-// chunk (one CTA per 16384 values, tensor found by a warp search over the
+// chunk (one CTA per 16384 values; tensor found by a warp search over the
 // chunk offsets of the plan).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ss {
 
+constexpr int kU = 8;  // (I, V) pairs in flight per thread
+
 __global__ void __launch_bounds__(256) k_apply(u16* W, const u32* I, const u16* V, u64 count, u64 numel,
                                               u32* status) {
-  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 stride = (u64)gridDim.x * blockDim.x * kU;
   bool bad = false;
-  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += stride) {
-    u32 idx = I[k];
-    if (idx < numel) W[idx] = V[k];
-    else bad = true;
+  for (u64 k0 = (u64)blockIdx.x * blockDim.x * kU + threadIdx.x; k0 < count; k0 += stride) {
+    u32 idx[kU];
+    u16 val[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const u64 k = k0 + (u64)u * blockDim.x;
+      idx[u] = k < count ? I[k] : 0xFFFFFFFFu;
+      val[u] = k < count ? V[k] : (u16)0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const u64 k = k0 + (u64)u * blockDim.x;
+      if (k < count) {
+        if (idx[u] < numel) W[idx[u]] = val[u];
+        else bad = true;
+      }
+    }
   }
   if (bad) latch(status, SYNC_ERR_INDEX_RANGE);
 }
@@ -36,16 +54,29 @@ __global__ void __launch_bounds__(256) k_commit_batched(Plan p, u16* const* snap
     const u32 t = s_t;
     const u64 nnz = p.rec_off[t + 1] - p.rec_off[t];
     const u64 p0 = (g - co[t]) * kChunk;
-    const u64 nk = (nnz - p0) < kChunk ? (nnz - p0) : kChunk;
+    const u32 nk = (u32)((nnz - p0) < kChunk ? (nnz - p0) : kChunk);
     const u32* Ir = I + p.rec_off[t] + p0;
     const u16* Vr = V + p.rec_off[t] + p0;
     u16* S = snaps[t];
     const u64 lim = p.numel[t];
     bool bad = false;
-    for (u64 q = threadIdx.x; q < nk; q += blockDim.x) {
-      u32 idx = Ir[q];
-      if (idx < lim) S[idx] = Vr[q];
-      else bad = true;
+    for (u32 q0 = threadIdx.x; q0 < nk; q0 += blockDim.x * kU) {
+      u32 idx[kU];
+      u16 val[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const u32 q = q0 + u * blockDim.x;
+        idx[u] = q < nk ? Ir[q] : 0xFFFFFFFFu;
+        val[u] = q < nk ? Vr[q] : (u16)0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const u32 q = q0 + u * blockDim.x;
+        if (q < nk) {
+          if (idx[u] < lim) S[idx[u]] = val[u];
+          else bad = true;
+        }
+      }
     }
     if (bad) latch(p.status, SYNC_ERR_INDEX_RANGE);
     __syncthreads();
@@ -54,8 +85,8 @@ __global__ void __launch_bounds__(256) k_commit_batched(Plan p, u16* const* snap
 
 void launch_apply(u16* W, const u32* I, const u16* V, u64 count, u64 numel, u32* status, cudaStream_t s) {
   if (count == 0) return;
-  u64 blocks = (count + 255) / 256;
-  int grid = (int)(blocks < 148ull * 16 ? blocks : 148ull * 16);
+  u64 blocks = (count + 256 * kU - 1) / (256 * kU);
+  int grid = (int)(blocks < 148ull * 8 ? blocks : 148ull * 8);
   k_apply<<<grid, 256, 0, s>>>(W, I, V, count, numel, status);
   count_launch();
 }

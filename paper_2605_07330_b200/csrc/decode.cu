@@ -299,46 +299,72 @@ __global__ void __launch_bounds__(256) k_decode(const u8* bk, u64 bytes, u32 n_t
     u32 ptr = 0;
     u32 carry = (r.mode == 0) ? base : 0u;
     bool range_bad = false, word_bad = false;
-    for (u32 gs = 0; gs < G; ++gs) {
-      const u32 qq = gs * 32 + lane;
-      const bool act = qq < nk;
-      u32 lob = act ? lo[qq] : 0u;
-      u32 d = 0, idx = 0;
-      if (r.mode == 0) d = act ? D[qq] : 0u;
-      else idx = act ? A[qq] : 0u;
-      u32 s;
-      if (cm == 1) {
-        s = 0;
-        if (act) {
-          u32 slot = x & (kM - 1);
-          s = dm.slot2sym[slot];
-          x = (u32)dm.freq[s] * (x >> 12) + slot - dm.cum[s];
-        }
-        bool need = act && x < kLow;
-        u32 nm = __ballot_sync(0xffffffffu, need);
-        if (need) {
-          u32 pos = ptr + __popc(nm >> lane >> 1);
-          if (pos < nwords) x = (x << 16) | words[pos];
-          else word_bad = true;
-        }
-        ptr += __popc(nm);
-      } else {
-        s = act ? blk[qq] : 0u;
+    // software pipeline: the lo bytes and the index words (DELTA16 delta or
+    // ABS32 index) of the next 8 steps are loaded while the current 8 decode
+    constexpr int kPF = 8;
+    u32 nlb[kPF], ndd[kPF];
+    auto load_block = [&](u32 g0, u32* lb_, u32* dd_) {
+#pragma unroll
+      for (int i = 0; i < kPF; ++i) {
+        const u32 qq = (g0 + i) * 32 + lane;
+        const bool act = qq < nk;
+        lb_[i] = act ? (u32)lo[qq] : 0u;
+        dd_[i] = act ? (r.mode == 0 ? (u32)D[qq] : A[qq]) : 0u;
       }
-      if (r.mode == 0) {
-        u32 sc = warp_incl_scan(d);
-        idx = carry + sc;
-        carry = __shfl_sync(0xffffffffu, idx, 31);
+    };
+    load_block(0, nlb, ndd);
+    for (u32 g0 = 0; g0 < G; g0 += kPF) {
+      u32 lb[kPF], dd[kPF];
+#pragma unroll
+      for (int i = 0; i < kPF; ++i) {
+        lb[i] = nlb[i];
+        dd[i] = ndd[i];
       }
-      if (act) {
-        u16 v = (u16)((s << 8) | lob);
-        if (kApply) {
-          if (idx < lim) W[idx] = v;
-          else range_bad = true;
+      if (g0 + kPF < G) load_block(g0 + kPF, nlb, ndd);
+      if (cm == 1 && lane < 8 && ptr + 64 * (lane + 1) < nwords)  // warm L1 with the next words
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(words + ptr + 64 * (lane + 1)));
+#pragma unroll
+      for (int i = 0; i < kPF; ++i) {
+        const u32 gs = g0 + i;
+        if (gs >= G) break;
+        const u32 qq = gs * 32 + lane;
+        const bool act = qq < nk;
+        u32 s;
+        if (cm == 1) {
+          s = 0;
+          if (act) {
+            const u32 slot = x & (kM - 1);
+            s = dm.slot2sym[slot];
+            x = (u32)dm.freq[s] * (x >> 12) + slot - dm.cum[s];
+          }
+          const bool need = act && x < kLow;
+          const u32 nm = __ballot_sync(0xffffffffu, need);
+          if (need) {
+            const u32 pos = ptr + __popc(nm >> lane >> 1);
+            if (pos < nwords) x = (x << 16) | words[pos];
+            else word_bad = true;
+          }
+          ptr += __popc(nm);
         } else {
-          Io[qq] = idx;
-          Vo[qq] = v;
-          if (idx >= lim) range_bad = true;
+          s = act ? blk[qq] : 0u;
+        }
+        u32 idx;
+        if (r.mode == 0) {
+          idx = carry + warp_incl_scan(dd[i]);
+          carry = __shfl_sync(0xffffffffu, idx, 31);
+        } else {
+          idx = dd[i];
+        }
+        if (act) {
+          const u16 v = (u16)((s << 8) | lb[i]);
+          if (kApply) {
+            if (idx < lim) W[idx] = v;
+            else range_bad = true;
+          } else {
+            Io[qq] = idx;
+            Vo[qq] = v;
+            if (idx >= lim) range_bad = true;
+          }
         }
       }
     }

@@ -34,19 +34,46 @@ __global__ void k_fill_new(const u16* old, u16* nw, u64 n, int mode, int active,
   }
 }
 
-// offsets[t] = exclusive prefix of counts (single CTA)
-__global__ void k_prefix(const u64* counts, u32 T, u64* offsets) {
-  if (threadIdx.x != 0) return;
-  u64 acc = 0;
-  for (u32 t = 0; t < T; ++t) {
-    offsets[t] = acc;
-    acc += counts[t];
+// offsets[t] = exclusive prefix of counts (single CTA of 1024 threads)
+__global__ void __launch_bounds__(1024) k_prefix(const u64* counts, u32 T, u64* offsets) {
+  __shared__ u64 s_w[32];
+  __shared__ u64 s_carry;
+  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (u32 b = 0; b < T; b += 1024) {
+    const u32 t = b + threadIdx.x;
+    const u64 c = t < T ? counts[t] : 0;
+    u64 v = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      u64 x = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= (u32)o) v += x;
+    }
+    if (lane == 31) s_w[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      u64 w = s_w[lane], wi = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        u64 x = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= (u32)o) wi += x;
+      }
+      s_w[lane] = wi - w;
+    }
+    __syncthreads();
+    const u64 carry = s_carry;
+    if (t < T) offsets[t] = carry + s_w[warp] + v - c;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = carry + s_w[31] + v;  // block inclusive total (last thread)
+    __syncthreads();
   }
-  offsets[T] = acc;
+  if (threadIdx.x == 0) offsets[T] = s_carry;
 }
 
-// Y[t][I[k]] ^= 1 for every extracted (tensor, index); 4096 entries per CTA.
-__global__ void k_toggle(u16* const* ys, const u32* I, const u64* offsets, u32 T) {
+// Y[t][I[k]] = V[k] ^ 1 for every extracted (tensor, index, value): V[k] is the
+// value Y had at extraction, so this flips its lowest bit without reading Y.
+// 4096 entries per CTA, 8 loads in flight per thread.
+__global__ void __launch_bounds__(256) k_toggle(u16* const* ys, const u32* I, const u16* V, const u64* offsets,
+                                               u32 T) {
   __shared__ u32 s_t;
   const u64 total = offsets[T];
   for (u64 b = (u64)blockIdx.x * 4096; b < total; b += (u64)gridDim.x * 4096) {
@@ -59,10 +86,25 @@ __global__ void k_toggle(u16* const* ys, const u32* I, const u64* offsets, u32 T
       s_t = lo;
     }
     __syncthreads();
+    const u64 end = b + 4096 < total ? b + 4096 : total;
     u32 t = s_t;
-    for (u64 k = b + threadIdx.x; k < b + 4096 && k < total; k += blockDim.x) {
-      while (offsets[t + 1] <= k) ++t;
-      ys[t][I[k]] ^= (u16)1;
+    for (u64 k0 = b + threadIdx.x; k0 < end; k0 += 256 * 8) {
+      u32 idx[8];
+      u16 val[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const u64 k = k0 + u * 256;
+        idx[u] = k < end ? I[k] : 0u;
+        val[u] = k < end ? V[k] : (u16)0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const u64 k = k0 + u * 256;
+        if (k < end) {
+          while (offsets[t + 1] <= k) ++t;
+          ys[t][idx[u]] = (u16)(val[u] ^ 1u);
+        }
+      }
     }
     __syncthreads();
   }
@@ -88,11 +130,12 @@ int synth_fill_new(const void* old, void* nw, u64 n, int mode, int active, u64 k
   return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
-int synth_toggle(void* const* ys, const void* I, const void* counts, u32 T, void* offsets_scratch, void* stream) {
+int synth_toggle(void* const* ys, const void* I, const void* V, const void* counts, u32 T, void* offsets_scratch,
+                 void* stream) {
   if (!T) return 0;
   cudaStream_t s = (cudaStream_t)stream;
-  k_prefix<<<1, 32, 0, s>>>((const u64*)counts, T, (u64*)offsets_scratch);
-  k_toggle<<<148 * 8, 256, 0, s>>>((u16* const*)ys, (const u32*)I, (const u64*)offsets_scratch, T);
+  k_prefix<<<1, 1024, 0, s>>>((const u64*)counts, T, (u64*)offsets_scratch);
+  k_toggle<<<148 * 8, 256, 0, s>>>((u16* const*)ys, (const u32*)I, (const u16*)V, (const u64*)offsets_scratch, T);
   return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 

@@ -33,7 +33,7 @@ def lib():
         P, u64, i32, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32
         L.synth_fill_old.argtypes = [P, u64, i32, u64, P, P]
         L.synth_fill_new.argtypes = [P, P, u64, i32, i32, u64, u64, u64, u64, u64, u64, P]
-        L.synth_toggle.argtypes = [P, P, P, u32, P, P]
+        L.synth_toggle.argtypes = [P, P, P, P, u32, P, P]
         for f in (L.synth_fill_old, L.synth_fill_new, L.synth_toggle):
             f.restype = i32
         _lib = L
@@ -91,8 +91,10 @@ def fill_new(old_views, new_views, manifest: Manifest, seed: int, rho: float, ma
         assert rc == 0
 
 
-def toggle(y_ptrs: torch.Tensor, I: torch.Tensor, counts: torch.Tensor, T: int, scratch: torch.Tensor):
-    """Bench 'optimizer step': Y[t][I] ^= 1 for the positions of the last sync (scratch: >= T+1 int64)."""
+def toggle(y_ptrs: torch.Tensor, I: torch.Tensor, V: torch.Tensor, counts: torch.Tensor, T: int, scratch: torch.Tensor):
+    """Bench 'optimizer step': Y[t][I] = V ^ 1 (V = Y[I] at extraction) for the positions of the last sync
+    (scratch: >= T+1 int64)."""
     rc = lib().synth_toggle(ctypes.c_void_p(y_ptrs.data_ptr()), ctypes.c_void_p(I.data_ptr()),
-                            ctypes.c_void_p(counts.data_ptr()), T, ctypes.c_void_p(scratch.data_ptr()), _s())
+                            ctypes.c_void_p(V.data_ptr()), ctypes.c_void_p(counts.data_ptr()), T,
+                            ctypes.c_void_p(scratch.data_ptr()), _s())
     assert rc == 0
