@@ -119,13 +119,17 @@ __device__ __forceinline__ u64 warp_sum64(u64 v) {
   return v;
 }
 
-// Exact floor(x / f) for 1 <= f <= 4096 from rcp = floor((2^32-1)/f): the
-// estimate is at most 2 below the quotient.
+// Exact floor(x / f) for 1 <= f <= 4096 and x < 2^32 from rcp = rcp_of(f):
+// floor(2^32 / f) for f >= 2 (so umulhi(x, rcp) > x/f - 1) and 2^32 - 1 for f = 1
+// (umulhi = x - 1): the estimate is at most one below the quotient.
+__host__ __device__ __forceinline__ u32 rcp_of(u32 f) { return f == 1 ? 0xFFFFFFFFu : (u32)((1ull << 32) / f); }
 __device__ __forceinline__ u32 div_by(u32 x, u32 f, u32 rcp, u32* rem) {
   u32 q = __umulhi(x, rcp);
   u32 r = x - q * f;
-  if (r >= f) { q++; r -= f; }
-  if (r >= f) { q++; r -= f; }
+  if (r >= f) {
+    q++;
+    r -= f;
+  }
   *rem = r;
   return q;
 }
@@ -136,6 +140,7 @@ struct WarpModel {
   u16 freq[256];
   u16 cum[256];
   u32 rcp[256];
+  u32 fc[256];   // freq | cum << 16 (one load per symbol in the encode loops)
 };
 
 // Histogram of hi bytes hi(p) for p < n into m.hist (warp-aggregated smem atomics).
@@ -166,7 +171,7 @@ __device__ __forceinline__ u32 warp_normalize(WarpModel& m, u32 n) {
     c[k] = m.hist[s];
     u32 v = 0;
     if (c[k]) {
-      v = (u32)(((u64)c[k] * kM) / n);
+      v = (c[k] * kM) / n;  // c <= 16384: fits 32 bits
       if (v < 1) v = 1;
       nsym++;
     }
@@ -236,7 +241,8 @@ __device__ __forceinline__ u32 warp_normalize(WarpModel& m, u32 n) {
     u32 s = lane * 8 + k;
     m.freq[s] = (u16)f[k];
     m.cum[s] = (u16)run;
-    m.rcp[s] = f[k] ? 0xFFFFFFFFu / f[k] : 0u;
+    m.rcp[s] = f[k] ? rcp_of(f[k]) : 0u;
+    m.fc[s] = f[k] | (run << 16);
     run += f[k];
   }
   __syncwarp();

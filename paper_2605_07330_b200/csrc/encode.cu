@@ -1,6 +1,6 @@
 // encode.cu — K3: record encoding (rows a3 + a4), DESIGN §3.1 / §3.2.
 //
-// One warp per chunk (16384 values). COMPRESSED: the chunk's slice of the
+// One CTA per chunk (16384 values). COMPRESSED: the chunk's slice of the
 // index stream (DELTA16 first differences with a prepended zero, or ABS32
 // absolutes), its slice of the raw lo plane, its directory entry and
 // its hi block — a static order-0 rANS over 32 interleaved lanes (lane j owns
@@ -10,36 +10,38 @@
 // record writes the header; the last chunk writes the section paddings.
 #include "common.cuh"
 #include "kernels.h"
+#include "chunk.cuh"
 
 namespace ss {
 
-__device__ __forceinline__ void zero_bytes(u8* p, u64 n, u32 lane) {
-  for (u64 q = lane; q < n; q += 32) p[q] = 0;
+__device__ __forceinline__ void zero_bytes(u8* p, u64 n) {
+  for (u64 q = threadIdx.x; q < n; q += blockDim.x) p[q] = 0;
 }
 
-__global__ void __launch_bounds__(256) k_encode(Plan p, const u32* I, const u16* V, const u64* counts, u8* enc) {
-  __shared__ WarpModel s_model[8];
-  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpModel& m = s_model[warp];
+// One CTA per chunk (16384 values). All threads write the chunk's slices of the
+// index stream and of the lo plane (packed 32-bit stores); for a RANS hi block
+// the hi bytes are staged in shared memory and warp 0 runs the encoder.
+__global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, const u16* V, const u64* counts,
+                                                     u8* enc) {
+  __shared__ ChunkSmem sm;
+  const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u64 n_chunks = p.totals[kTotChunks];
-  const u64 nwarps = (u64)gridDim.x * (blockDim.x >> 5);
-  const u64* co = p.chunk_off;
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
-  for (u64 g = (u64)blockIdx.x * (blockDim.x >> 5) + warp; g < n_chunks; g += nwarps) {
-    const u32 t = warp_upper_search(p.n_tensors, g, [&](u32 i) { return co[i]; });
-    const u64 nnz = counts[t];
-    const u64 n_ch = co[t + 1] - co[t];
-    const u64 k = g - co[t];
-    const u64 p0 = k * kChunk;
-    const u32 nk = (u32)((nnz - p0) < kChunk ? (nnz - p0) : kChunk);
+  for (u64 g = blockIdx.x; g < n_chunks; g += gridDim.x) {
+    __syncthreads();
+    const ChunkPos c = locate_chunk(p, counts, g, sm, I, V);
+    const u32 t = c.t;
+    const u64 nnz = c.nnz, k = c.k, p0 = c.p0;
+    const u32 nk = c.nk;
+    const u64 n_ch = p.chunk_off[t + 1] - p.chunk_off[t];
     const bool last = (k + 1 == n_ch);
-    const u32* Ir = I + p.rec_off[t];
-    const u16* Vr = V + p.rec_off[t];
+    const u32* Ir = c.Ir;
+    const u16* Vc = c.Vc;
     u8* rec = enc + p.enc_off[t];
     const u64 rb = p.rec_bytes[t];
     const u32 mode = p.rec_mode[t];
 
-    if (k == 0 && lane == 0) {
+    if (k == 0 && tid == 0) {
       u32* h = reinterpret_cast<u32*>(rec);
       h[0] = t;
       h[1] = (u32)nnz;
@@ -48,44 +50,60 @@ __global__ void __launch_bounds__(256) k_encode(Plan p, const u32* I, const u16*
     }
 
     if (!comp) {
-      u32* Io = reinterpret_cast<u32*>(rec + 16);
-      u16* Vo = reinterpret_cast<u16*>(rec + 16 + 4 * nnz);
-      for (u32 q = lane; q < nk; q += 32) {
-        Io[p0 + q] = Ir[p0 + q];
-        Vo[p0 + q] = Vr[p0 + q];
+      u32* Io = reinterpret_cast<u32*>(rec + 16) + p0;
+      u16* Vo = reinterpret_cast<u16*>(rec + 16 + 4 * nnz) + p0;
+      for (u32 q = tid; q < nk; q += kCThreads) {
+        Io[q] = Ir[p0 + q];
+        Vo[q] = Vc[q];
       }
-      if (last) zero_bytes(rec + 16 + 6 * nnz, rb - (16 + 6 * nnz), lane);
+      if (last) zero_bytes(rec + 16 + 6 * nnz, rb - (16 + 6 * nnz));
       continue;
     }
 
-    // index stream slice
+    // ---- index stream slice (pairs of positions per thread -> 32-bit stores for DELTA16)
     const u64 ib = (mode ? 4 : 2) * nnz;
     if (mode == 0) {
-      u16* D = reinterpret_cast<u16*>(rec + 16);
-      for (u32 q = lane; q < nk; q += 32) {
-        u64 pp = p0 + q;
-        u32 prev = pp ? Ir[pp - 1] : 0u;
-        D[pp] = (u16)(Ir[pp] - prev);
+      u16* D = reinterpret_cast<u16*>(rec + 16) + p0;
+      for (u32 q = 2 * tid; q < nk; q += 2 * kCThreads) {
+        const u64 pp = p0 + q;
+        const u32 a0 = Ir[pp], prev = pp ? Ir[pp - 1] : 0u;
+        const u32 d0 = a0 - prev;
+        if (q + 1 < nk) {
+          const u32 d1 = Ir[pp + 1] - a0;
+          *reinterpret_cast<u32*>(D + q) = (d0 & 0xFFFFu) | (d1 << 16);
+        } else {
+          D[q] = (u16)d0;
+        }
       }
     } else {
-      u32* A = reinterpret_cast<u32*>(rec + 16);
-      for (u32 q = lane; q < nk; q += 32) A[p0 + q] = Ir[p0 + q];
+      u32* A = reinterpret_cast<u32*>(rec + 16) + p0;
+      for (u32 q = tid; q < nk; q += kCThreads) A[q] = Ir[p0 + q];
     }
     const u64 lo_off = 16 + pad_to(ib, 4);
     const u64 dir_off = lo_off + pad_to(nnz, 4);
     const u64 hi_base = dir_off + 16 * n_ch;
     if (last) {
-      zero_bytes(rec + 16 + ib, pad_to(ib, 4) - ib, lane);
-      zero_bytes(rec + lo_off + nnz, pad_to(nnz, 4) - nnz, lane);
+      zero_bytes(rec + 16 + ib, pad_to(ib, 4) - ib);
+      zero_bytes(rec + lo_off + nnz, pad_to(nnz, 4) - nnz);
     }
-    // lo plane slice
-    for (u32 q = lane; q < nk; q += 32) rec[lo_off + p0 + q] = (u8)(Vr[p0 + q] & 0xFFu);
-
-    // directory entry + hi block
+    // ---- lo plane slice: 4 values per thread -> one 32-bit store
+    {
+      u8* L = rec + lo_off + p0;
+      for (u32 q = 4 * tid; q < nk; q += 4 * kCThreads) {
+        if (q + 4 <= nk) {
+          const u32 w = (u32)(Vc[q] & 0xFFu) | ((u32)(Vc[q + 1] & 0xFFu) << 8) | ((u32)(Vc[q + 2] & 0xFFu) << 16) |
+                        ((u32)(Vc[q + 3] & 0xFFu) << 24);
+          *reinterpret_cast<u32*>(L + q) = w;
+        } else {
+          for (u32 r = q; r < nk; ++r) L[r] = (u8)(Vc[r] & 0xFFu);
+        }
+      }
+    }
+    // ---- directory entry + hi block
     const u32 hb = p.chunk_hi[g];
     const u32 cm = p.chunk_mode[g];
-    const u64 hi_off = hi_base + (p.chunk_hioff[g] - p.chunk_hioff[co[t]]);
-    if (lane == 0) {
+    const u64 hi_off = hi_base + (p.chunk_hioff[g] - p.chunk_hioff[p.chunk_off[t]]);
+    if (tid == 0) {
       u32* d = reinterpret_cast<u32*>(rec + dir_off + 16 * k);
       d[0] = (u32)hi_off;
       d[1] = hb;
@@ -93,65 +111,74 @@ __global__ void __launch_bounds__(256) k_encode(Plan p, const u32* I, const u16*
       d[3] = (mode == 0 && k > 0) ? Ir[p0 - 1] : 0u;
     }
     u8* blk = rec + hi_off;
-    const u16* Vc = Vr + p0;
-    if (cm == 0) {
-      for (u32 q = lane; q < nk; q += 32) blk[q] = (u8)(Vc[q] >> 8);
-      zero_bytes(blk + nk, pad_to(nk, 4) - nk, lane);
-    } else {
-      warp_histogram(m, nk, [&](u32 q) { return (u32)(Vc[q] >> 8); });
-      const u32 nsym = warp_normalize(m, nk);
-      const u32 nwords = (hb - 136u - 4u * nsym) / 2u;
-      u16* words = reinterpret_cast<u16*>(blk + 136 + 4 * nsym);
-      u32 x = kLow, e = 0;
-      const u32 G = (nk + 31) / 32;
-      const u32 lt = (1u << lane) - 1u;
-      for (int gg = (int)G - 1; gg >= 0; --gg) {
-        u32 q = (u32)gg * 32 + lane;
-        bool act = q < nk;
-        u32 s = act ? (u32)(Vc[q] >> 8) : 0u;
-        u32 f = m.freq[s];
-        bool emit = act && (x >> 20) >= f;
-        u32 em = __ballot_sync(0xffffffffu, emit);
-        if (emit) {
-          words[nwords - 1u - (e + __popc(em & lt))] = (u16)(x & 0xFFFFu);
-          x >>= 16;
-        }
-        e += __popc(em);
-        if (act) {
-          u32 r;
-          u32 qq = div_by(x, f, m.rcp[s], &r);
-          x = qq * kM + r + m.cum[s];
-        }
-      }
-      u32* hdr = reinterpret_cast<u32*>(blk);
-      hdr[lane] = x;                                   // final states, lane order
-      if (lane == 0) {
-        hdr[32] = nwords;
-        hdr[33] = nsym;                                // u16 nsym | u16 0
-      }
-      // symbol entries ascending: lane owns symbols 8*lane .. 8*lane+7
-      u32 present = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) present += m.freq[lane * 8 + j] ? 1u : 0u;
-      u32 rank = warp_incl_scan(present) - present;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        u32 s = lane * 8 + j;
-        u32 f = m.freq[s];
-        if (f) hdr[34 + rank++] = s | (f << 16);
-      }
-      if (lane == 0 && (hb & 3u)) *reinterpret_cast<u16*>(blk + hb) = 0;
-    }
     if (last) {
-      const u64 hi_end = hi_base + (p.chunk_hioff[co[t + 1]] - p.chunk_hioff[co[t]]);
-      zero_bytes(rec + hi_end, rb - hi_end, lane);
+      const u64 hi_end = hi_base + (p.chunk_hioff[p.chunk_off[t + 1]] - p.chunk_hioff[p.chunk_off[t]]);
+      zero_bytes(rec + hi_end, rb - hi_end);
     }
+    if (cm == 0) {
+      for (u32 q = tid; q < nk; q += kCThreads) blk[q] = (u8)(Vc[q] >> 8);
+      zero_bytes(blk + nk, pad_to(nk, 4) - nk);
+      continue;
+    }
+    stage_chunk(sm, Ir, Vc, p0, nk, false);
+    if (warp != 0) continue;
+    WarpModel& m = sm.m;
+    const u32 nsym = warp_normalize(m, nk);
+    const u32 nwords = (hb - 136u - 4u * nsym) / 2u;
+    u16* words = reinterpret_cast<u16*>(blk + 136 + 4 * nsym);
+    u32 x = kLow, e = 0;
+    const u32 G = (nk + 31) / 32;
+    const u32 lt = (1u << lane) - 1u;
+    auto fetch = [&](int gg, u32& s_, u32& fc_, u32& rc_) {
+      const u32 q = (u32)gg * 32 + lane;
+      s_ = (gg >= 0 && q < nk) ? (u32)sm.hi[q] : 0x100u;
+      fc_ = s_ < 256 ? m.fc[s_] : 0u;
+      rc_ = s_ < 256 ? m.rcp[s_] : 0u;
+    };
+    u32 ns, nfc, nrc;
+    fetch((int)G - 1, ns, nfc, nrc);
+    for (int gg = (int)G - 1; gg >= 0; --gg) {
+      const u32 s = ns, fcs = nfc, rcp = nrc;
+      fetch(gg - 1, ns, nfc, nrc);
+      const bool act = s < 256;
+      const u32 f = fcs & 0xFFFFu;
+      const bool emit = act && (x >> 20) >= f;
+      const u32 em = __ballot_sync(0xffffffffu, emit);
+      if (emit) {
+        words[nwords - 1u - (e + __popc(em & lt))] = (u16)(x & 0xFFFFu);
+        x >>= 16;
+      }
+      e += __popc(em);
+      if (act) {
+        u32 r;
+        const u32 qq = div_by(x, f, rcp, &r);
+        x = qq * kM + r + (fcs >> 16);
+      }
+    }
+    u32* hdr = reinterpret_cast<u32*>(blk);
+    hdr[lane] = x;  // final states, lane order
+    if (lane == 0) {
+      hdr[32] = nwords;
+      hdr[33] = nsym;  // u16 nsym | u16 0
+    }
+    // symbol entries ascending: lane owns symbols 8*lane .. 8*lane+7
+    u32 present = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) present += m.freq[lane * 8 + j] ? 1u : 0u;
+    u32 rank = warp_incl_scan(present) - present;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const u32 s = lane * 8 + j;
+      const u32 f = m.freq[s];
+      if (f) hdr[34 + rank++] = s | (f << 16);
+    }
+    if (lane == 0 && (hb & 3u)) *reinterpret_cast<u16*>(blk + hb) = 0;
   }
 }
 
 void launch_encode(const Plan& p, const u32* I, const u16* V, const u64* counts, u8* enc, int grid,
                    cudaStream_t s) {
-  k_encode<<<grid, 256, 0, s>>>(p, I, V, counts, enc);
+  k_encode<<<grid, kCThreads, 0, s>>>(p, I, V, counts, enc);
   count_launch();
 }
 

@@ -28,6 +28,7 @@ struct Plan {
   uint64_t* chunk_hioff;         // [max_chunks+1] exclusive prefix of pad4(chunk_hi)
   uint64_t* totals;              // [16]
   uint32_t* status;
+  int prof;                      // debug instrumentation switch
 };
 
 enum TotalsIdx {

@@ -9,8 +9,12 @@
 //                            (never-expand)
 //  * k_plan_sizes  (1 CTA)   chunk hi-offset prefix, record sizes,
 //                            record byte offsets, statistics
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
+#include "chunk.cuh"
 
 namespace ss {
 
@@ -70,65 +74,69 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_scan(Plan p, const u64* c
   }
 }
 
-// One warp per chunk: gap, histogram, model, counted rANS pass.
-__global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
-  __shared__ WarpModel s_model[8];
+// One CTA per chunk: staged hi bytes + histogram + max gap (all threads), then
+// the model and a counted rANS pass from shared memory (warp 0).
+__device__ unsigned long long g_cprof[8];  // debug cycle counters (SS_CPROF=1)
+
+__global__ void __launch_bounds__(kCThreads) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
+  __shared__ ChunkSmem sm;
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpModel& m = s_model[warp];
   const u64 n_chunks = p.totals[kTotChunks];
-  const u64 nwarps = (u64)gridDim.x * (blockDim.x >> 5);
-  const u64* co = p.chunk_off;
-  for (u64 g = (u64)blockIdx.x * (blockDim.x >> 5) + warp; g < n_chunks; g += nwarps) {
-    u32 t = warp_upper_search(p.n_tensors, g, [&](u32 i) { return co[i]; });
-    const u64 nnz = counts[t];
-    const u64 k = g - co[t];
-    const u64 p0 = k * kChunk;
-    const u32 nk = (u32)((nnz - p0) < kChunk ? (nnz - p0) : kChunk);
-    const u32* Ir = I + p.rec_off[t];
-    const u16* Vr = V + p.rec_off[t] + p0;
-
-    // max first difference (Δ_0 = I_0, prepended zero)
-    u32 gmax = 0;
-    for (u32 q = lane; q < nk; q += 32) {
-      u64 pp = p0 + q;
-      u32 prev = pp ? Ir[pp - 1] : 0u;
-      u32 d = Ir[pp] - prev;
-      gmax = d > gmax ? d : gmax;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      u32 v = __shfl_xor_sync(0xffffffffu, gmax, o);
-      gmax = v > gmax ? v : gmax;
-    }
-    if (lane == 0 && gmax) atomicMax(&p.maxgap[t], gmax);
-    if (p.codec != SYNC_CODEC_COMPRESSED) continue;
-
-    warp_histogram(m, nk, [&](u32 q) { return (u32)(Vr[q] >> 8); });
-    u32 nsym = warp_normalize(m, nk);
-
+  for (u64 g = blockIdx.x; g < n_chunks; g += gridDim.x) {
+    __syncthreads();  // shared memory of the previous chunk is free
+    const long long t0 = clock64();
+    const ChunkPos c = locate_chunk(p, counts, g, sm, I, V);
+    const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
+    const long long t1 = clock64();
+    const u32 gmax = stage_chunk(sm, c.Ir, c.Vc, c.p0, c.nk, true);
+    const long long t2 = clock64();
+    if (threadIdx.x == 0 && gmax) atomicMax(&p.maxgap[c.t], gmax);
+    if (!comp || warp != 0) continue;
+    const u32 nsym = warp_normalize(sm.m, c.nk);
+    const long long t3 = clock64();
     // counted encode pass: steps G-1..0, renorm if x >= f * 2^20
     u32 x = kLow, nwords = 0;
-    const u32 G = (nk + 31) / 32;
+    const u32 G = (c.nk + 31) / 32;
+    // symbol + model of the next step are loaded one step ahead (independent of x)
+    auto fetch = [&](int gg, u32& s_, u32& fc_, u32& rc_) {
+      const u32 q = (u32)gg * 32 + lane;
+      s_ = (gg >= 0 && q < c.nk) ? (u32)sm.hi[q] : 0x100u;
+      fc_ = s_ < 256 ? sm.m.fc[s_] : 0u;
+      rc_ = s_ < 256 ? sm.m.rcp[s_] : 0u;
+    };
+    u32 ns, nfc, nrc;
+    fetch((int)G - 1, ns, nfc, nrc);
     for (int gg = (int)G - 1; gg >= 0; --gg) {
-      u32 q = (u32)gg * 32 + lane;
-      bool act = q < nk;
-      u32 s = act ? (u32)(Vr[q] >> 8) : 0u;
-      u32 f = m.freq[s];
-      bool emit = act && (x >> 20) >= f;
+      const u32 s = ns, fcs = nfc, rcp = nrc;
+      fetch(gg - 1, ns, nfc, nrc);
+      const bool act = s < 256;
+      const u32 f = fcs & 0xFFFFu;
+      const bool emit = act && (x >> 20) >= f;
       nwords += __popc(__ballot_sync(0xffffffffu, emit));
       if (emit) x >>= 16;
       if (act) {
         u32 r;
-        u32 qq = div_by(x, f, m.rcp[s], &r);
-        x = qq * kM + r + m.cum[s];
+        const u32 qq = div_by(x, f, rcp, &r);
+        x = qq * kM + r + (fcs >> 16);
       }
     }
     u32 hb = 136u + 4u * nsym + 2u * nwords;
     u32 mode = 1;
-    if (hb >= nk) { hb = nk; mode = 0; }
+    if (hb >= c.nk) {
+      hb = c.nk;
+      mode = 0;
+    }
     if (lane == 0) {
       p.chunk_hi[g] = hb;
       p.chunk_mode[g] = mode;
+      if (p.prof) {
+        const long long t4 = clock64();
+        atomicAdd(&g_cprof[0], (unsigned long long)(t1 - t0));
+        atomicAdd(&g_cprof[1], (unsigned long long)(t2 - t1));
+        atomicAdd(&g_cprof[2], (unsigned long long)(t3 - t2));
+        atomicAdd(&g_cprof[3], (unsigned long long)(t4 - t3));
+        atomicAdd(&g_cprof[4], 1ull);
+      }
     }
   }
 }
@@ -216,7 +224,23 @@ void launch_plan_scan(const Plan& p, const u64* counts, cudaStream_t s) {
 }
 
 void launch_chunk_stats(const Plan& p, const u32* I, const u16* V, const u64* counts, int grid, cudaStream_t s) {
-  k_chunk_stats<<<grid, 256, 0, s>>>(p, I, V, counts);
+  static int want = -1;
+  if (want < 0) want = getenv("SS_CPROF") ? 1 : 0;
+  Plan q = p;
+  q.prof = want;
+  if (want) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbolAsync(g_cprof, z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
+  }
+  k_chunk_stats<<<grid, kCThreads, 0, s>>>(q, I, V, counts);
+  if (want) {
+    unsigned long long h[8];
+    cudaMemcpyFromSymbolAsync(h, g_cprof, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const double n = h[4] ? (double)h[4] : 1.0;
+    fprintf(stderr, "[cprof] chunks %llu per-chunk cycles: locate %.0f stage %.0f normalize %.0f rans %.0f\n", h[4],
+            h[0] / n, h[1] / n, h[2] / n, h[3] / n);
+  }
   count_launch();
 }
 
