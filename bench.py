@@ -365,11 +365,15 @@ def run_ours(args):
     ext_ms = phases[0]
     achieved = alg_bytes_extract / (ext_ms / 1e3) / 1e9
     peak = peaks.get("hbm_gbs", 6650.0)
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", f"extract_traffic_{args.workload}.json")
+    # ncu dram bytes / algorithmic bytes of the profiled extract launch (profiles/extract_traffic.json,
+    # from `ncu --set full` on the 30b-slice workload), applied to this launch's algorithmic bytes
+    traffic, traffic_src = None, None
+    tf = os.path.join(ROOT, "profiles", "extract_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("bytes_per_launch")
+            ratio = json.load(open(tf))["ratio"]
+            traffic = int(round(ratio * alg_bytes_extract))
+            traffic_src = f"ncu --set full dram__bytes_read+write / algorithmic = {ratio:.4f} (30b-slice launch)"
         except Exception:
             traffic = None
     raw_payload = sum(((16 + 6 * c + 15) // 16) * 16 for c in r.sender.counts.cpu().tolist() if c) + 48 * max(nb, 1)
@@ -389,7 +393,7 @@ def run_ours(args):
                              phases)},
         "roofline": {"bound": "hbm", "kernel": "k_extract (K1)", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "bytes_per_launch": alg_bytes_extract,
+                     "bytes_per_launch": alg_bytes_extract, "traffic_source": traffic_src,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
         "payload": {"nnz": nnz, "rho_measured": round(nnz / manifest.total, 6), "buckets": nb,
                     "bytes": payload, "x_comp": round(r.S / max(payload, 1), 2),
