@@ -3,8 +3,12 @@
 
 One step = one whole sync of one synthetic policy update (every §8(a) row):
   K1 extract -> K2/K3 compress -> K4 pack -> (NCCL transfer) -> K5 decompress+apply
-  -> K6 snapshot commit, then the synthetic "optimizer" flips the changed bits
-  again so the next step syncs a fresh update of the same density.
+  -> K6 snapshot commit. Default --commit swap: the trainer double-buffers its
+  weights, the commit is a pointer swap and the two buffers hold the model
+  versions v0 / v1, so consecutive steps sync v0 -> v1 -> v0 ... (a genuine
+  1%-dense update every step, no generator work in the timed region).
+  --commit scatter: in-place snapshot scatter (K6), then a synthetic
+  "optimizer" flips the changed bits again (write-only scatter).
 Topology: every rank is a Trainer for its own model and the
 Rollout replica of rank r-1's model; buckets go r -> r+1 over NCCL (weak
 scaling; at N=1 the ring closes on itself and the buckets are decoded locally).
@@ -46,6 +50,8 @@ def parse():
     p.add_argument("--codec", choices=["compressed", "raw"], default="compressed")
     p.add_argument("--bucket-mb", type=float, default=256)
     p.add_argument("--crc", action="store_true")
+    p.add_argument("--commit", choices=["swap", "scatter"], default="swap",
+                   help="snapshot commit: pointer swap of double-buffered trainer weights, or in-place scatter")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-e2e", action="store_true")
@@ -183,8 +189,8 @@ class Rank:
         dev = d.dev
         self.seed = args.seed + 1000 * d.rank
         peer_seed = args.seed + 1000 * ((d.rank - 1) % d.world)
-        self.X, self.Xv = sg.arena(manifest, dev)
-        self.Y, self.Yv = sg.arena(manifest, dev)
+        self.X, self.Xv = sg.arena(manifest, dev)   # trainer snapshot (swaps with Y under --commit swap)
+        self.Y, self.Yv = sg.arena(manifest, dev)   # trainer current weights
         self.R, self.Rv = sg.arena(manifest, dev)
         sg.fill_old(self.Xv, manifest, self.seed)
         sg.fill_new(self.Xv, self.Yv, manifest, self.seed, args.rho, MASKS[args.mask])
@@ -218,9 +224,16 @@ class Rank:
         else:
             self.link.exchange(snd.buckets, blist, rcv.apply)
         rec(4)
-        snd.commit()
+        snd.commit(mode=self.args.commit)
+        if self.args.commit == "swap":
+            self.X, self.Y, self.Xv, self.Yv = self.Y, self.X, self.Yv, self.Xv
         rec(5)
-        self.sg.toggle(snd.new_ptrs, snd.I, snd.V, snd.counts, len(self.m.tensors), self.toggle_scratch)
+        if self.args.commit == "scatter":
+            # snapshot == current now: the synthetic "optimizer step" flips the changed bits again so the
+            # next sync has a fresh update of the same density (write-only scatter, input generation)
+            self.sg.toggle(snd.new_ptrs, snd.I, snd.V, snd.counts, len(self.m.tensors), self.toggle_scratch)
+        # under --commit swap the two trainer buffers hold the two model versions v0 / v1 and trade roles
+        # every step, so every step syncs a genuine update (v0 -> v1, then v1 -> v0) with no generator work
         rec(6)
         return blist
 
@@ -385,7 +398,7 @@ def run_ours(args):
                 f"{args.mask}-mask sparse perturbations, seeded",
         "config": {"workload": f"{manifest.name} bf16, {100 * (1 - args.rho):.1f}% sparsity, {args.mask} mask",
                    "elements_per_rank": manifest.total, "tensors": len(manifest.tensors),
-                   "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc,
+                   "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
                    "topology": "ring: rank r = Trainer of its model + Rollout replica of rank r-1 (N=1: loopback)",
                    "l2": "inputs (2x61 GB) larger than L2; no flush"},
         "ms_per_phase": {n: round(float(v), 4) for n, v in

@@ -86,7 +86,18 @@ class SparseSyncSender:
         return self.buckets[off:off + size]
 
     # K6: after the transfer completed (DESIGN C13)
-    def commit(self, stream=None):
+    def commit(self, stream=None, mode: str = "scatter"):
+        """Advance the snapshot to the synced weights.
+
+        mode "scatter": snapshot[I] <- V in place (sync_commit_snapshot_batched, row a9).
+        mode "swap": for a trainer that double-buffers its working copy, the current buffers become the
+        snapshot by exchanging the two pointer tables (no bytes move); the next CastAndCopy / optimizer
+        step then writes into the former snapshot buffers (W_prev is a per-step clone).
+        """
+        if mode == "swap":
+            self.snapshot, self.current = self.current, self.snapshot
+            self.old_ptrs, self.new_ptrs = self.new_ptrs, self.old_ptrs
+            return
         self.ctx.sync_commit_snapshot_batched(self.old_ptrs, self.I, self.V, self.counts, stream)
 
     def sync(self, stream=None):

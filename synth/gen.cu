@@ -88,19 +88,21 @@ __global__ void __launch_bounds__(256) k_toggle(u16* const* ys, const u32* I, co
     __syncthreads();
     const u64 end = b + 4096 < total ? b + 4096 : total;
     u32 t = s_t;
-    for (u64 k0 = b + threadIdx.x; k0 < end; k0 += 256 * 8) {
+    // each warp: 512 contiguous entries of the block, 8 in flight per lane
+    const u64 wb = b + (threadIdx.x >> 5) * 512, we = wb + 512 < end ? wb + 512 : end;
+    for (u64 k0 = wb + (threadIdx.x & 31); k0 < we; k0 += 32 * 8) {
       u32 idx[8];
       u16 val[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const u64 k = k0 + u * 256;
-        idx[u] = k < end ? I[k] : 0u;
-        val[u] = k < end ? V[k] : (u16)0;
+        const u64 k = k0 + u * 32;
+        idx[u] = k < we ? I[k] : 0u;
+        val[u] = k < we ? V[k] : (u16)0;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const u64 k = k0 + u * 256;
-        if (k < end) {
+        const u64 k = k0 + u * 32;
+        if (k < we) {
           while (offsets[t + 1] <= k) ++t;
           ys[t][idx[u]] = (u16)(val[u] ^ 1u);
         }
@@ -135,7 +137,7 @@ int synth_toggle(void* const* ys, const void* I, const void* V, const void* coun
   if (!T) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   k_prefix<<<1, 1024, 0, s>>>((const u64*)counts, T, (u64*)offsets_scratch);
-  k_toggle<<<148 * 8, 256, 0, s>>>((u16* const*)ys, (const u32*)I, (const u16*)V, (const u64*)offsets_scratch, T);
+  k_toggle<<<148 * 16, 256, 0, s>>>((u16* const*)ys, (const u32*)I, (const u16*)V, (const u64*)offsets_scratch, T);
   return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
