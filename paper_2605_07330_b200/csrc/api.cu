@@ -25,12 +25,12 @@ constexpr u64 kAlign = 256;
 
 struct Layout {
   u64 numel, tile_prefix, tile_tensor, misc, tile_state, stage_ring, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
-  u64 chunk_hi, chunk_mode, chunk_hioff, totals, recs, bks, views, nviews, crc, total;
+  u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, totals, recs, bks, views, nviews, crc, total;
 };
 
 u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4; }
 
-Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n) {
+Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_changed) {
   Layout L{};
   u64 o = 0;
   auto take = [&](u64 bytes) {
@@ -53,6 +53,8 @@ Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n) {
   L.chunk_hi = take(4ull * max_chunks);
   L.chunk_mode = take(4ull * max_chunks);
   L.chunk_hioff = take(8ull * (max_chunks + 1));
+  L.chunk_rhdr = take(4ull * kRhdrWords * max_chunks);
+  L.word_scratch = take(2ull * (max_changed / 2 + max_chunks + 2));
   L.totals = take(8 * 16);
   L.recs = take(sizeof(RecordDesc) * (u64)T);
   L.bks = take(sizeof(BucketDesc) * (u64)(T + 1));
@@ -80,8 +82,8 @@ int check_manifest(const sync_manifest* m, const sync_config* c, Dims* d) {
     maxn = m->numel[t] > maxn ? m->numel[t] : maxn;
   }
   d->max_chunks = (c->max_changed + kChunk - 1) / kChunk + d->T + 1;
-  u64 rn = c->max_changed < maxn ? c->max_changed : maxn;
-  d->max_record = 6 * rn + 20 * ((rn + kChunk - 1) / kChunk) + 64;
+  // largest possible record (one tensor fully changed): bounds a received bucket for the CRC scratch
+  d->max_record = 6 * maxn + 20 * ((maxn + kChunk - 1) / kChunk) + 64;
   u64 mb = c->bucket_limit > d->max_record + 64 ? c->bucket_limit : d->max_record + 64;
   d->crc_n = crc_slots(mb);
   return SYNC_OK;
@@ -121,7 +123,7 @@ int sync_workspace_size(const sync_manifest* m, const sync_config* c, size_t* by
   int st = check_manifest(m, c, &d);
   if (st) return st;
   if (!bytes) return SYNC_ERR_ARG;
-  *bytes = make_layout(d.T, d.n_tiles, d.max_chunks, d.crc_n).total;
+  *bytes = make_layout(d.T, d.n_tiles, d.max_chunks, d.crc_n, c->max_changed).total;
   return SYNC_OK;
 }
 
@@ -132,7 +134,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   Dims d;
   int st = check_manifest(m, c, &d);
   if (st) return st;
-  Layout L = make_layout(d.T, d.n_tiles, d.max_chunks, d.crc_n);
+  Layout L = make_layout(d.T, d.n_tiles, d.max_chunks, d.crc_n, c->max_changed);
   if (!d_workspace || workspace_bytes < L.total) return SYNC_ERR_WORKSPACE;
   if (!aligned16(d_workspace)) return SYNC_ERR_ALIGNMENT;
   sync_ctx* x = new (std::nothrow) sync_ctx();
@@ -185,6 +187,8 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   p.chunk_hi = reinterpret_cast<u32*>(w + L.chunk_hi);
   p.chunk_mode = reinterpret_cast<u32*>(w + L.chunk_mode);
   p.chunk_hioff = reinterpret_cast<u64*>(w + L.chunk_hioff);
+  p.chunk_rhdr = reinterpret_cast<u32*>(w + L.chunk_rhdr);
+  p.word_scratch = reinterpret_cast<u16*>(w + L.word_scratch);
   p.totals = reinterpret_cast<u64*>(w + L.totals);
   p.status = x->misc + 1;
   int dev = 0;

@@ -30,18 +30,23 @@ struct ChunkPos {
   const u16* Vc;                  // chunk's V
 };
 
+// Renormalisation words of chunk g (first value at global position vpos) live at
+// word_scratch[vpos / 2 + g ...]: a chunk keeping its rANS block has fewer than
+// n_k / 2 words, so consecutive chunks never overlap.
+__device__ __forceinline__ u64 chunk_words_base(u64 vpos, u64 g) { return vpos / 2 + g; }
+
 // Locate chunk g (warp 0 searches the chunk offsets) — all threads get the same.
-__device__ __forceinline__ ChunkPos locate_chunk(const Plan& p, const u64* counts, u64 g, ChunkSmem& sm,
+__device__ __forceinline__ ChunkPos locate_chunk(const Plan& p, const u64* counts, u64 g, u32& s_t,
                                                  const u32* I, const u16* V) {
   const u32 warp = threadIdx.x >> 5;
   if (warp == 0) {
     const u64* co = p.chunk_off;
     const u32 t = warp_upper_search(p.n_tensors, g, [&](u32 i) { return co[i]; });
-    if ((threadIdx.x & 31) == 0) sm.t = t;
+    if ((threadIdx.x & 31) == 0) s_t = t;
   }
   __syncthreads();
   ChunkPos c;
-  c.t = sm.t;
+  c.t = s_t;
   c.nnz = counts[c.t];
   c.k = g - p.chunk_off[c.t];
   c.p0 = c.k * kChunk;

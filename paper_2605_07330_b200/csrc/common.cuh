@@ -23,6 +23,8 @@ constexpr u32 kLow = 1u << 16;              // rANS lower bound
 constexpr u32 kMagic = 0x424C5253u;         // "SRLB"
 constexpr u32 kVersion = 1;
 constexpr u64 kBucketAlign = 256;
+// rANS block head kept by the stats pass: 32 lane states, nwords, nsym, <= 256 entries
+constexpr u32 kRhdrWords = 34 + 256;
 
 // Extract tiling: a sub-tile is 256 threads x 4 x uint4 (8 bf16) = 8192 elements
 // (one TMA stage: 16 KB of old + 16 KB of new); a tile (the look-back unit) is

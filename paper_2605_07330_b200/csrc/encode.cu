@@ -19,17 +19,17 @@ __device__ __forceinline__ void zero_bytes(u8* p, u64 n) {
 }
 
 // One CTA per chunk (16384 values). All threads write the chunk's slices of the
-// index stream and of the lo plane (packed 32-bit stores); for a RANS hi block
-// the hi bytes are staged in shared memory and warp 0 runs the encoder.
+// index stream and of the lo plane (packed 32-bit stores) and copy the chunk's
+// rANS block (states, model, words) that k_chunk_stats already produced.
 __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, const u16* V, const u64* counts,
                                                      u8* enc) {
-  __shared__ ChunkSmem sm;
-  const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ u32 s_t;
+  const u32 tid = threadIdx.x;
   const u64 n_chunks = p.totals[kTotChunks];
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
   for (u64 g = blockIdx.x; g < n_chunks; g += gridDim.x) {
     __syncthreads();
-    const ChunkPos c = locate_chunk(p, counts, g, sm, I, V);
+    const ChunkPos c = locate_chunk(p, counts, g, s_t, I, V);
     const u32 t = c.t;
     const u64 nnz = c.nnz, k = c.k, p0 = c.p0;
     const u32 nk = c.nk;
@@ -120,59 +120,17 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
       zero_bytes(blk + nk, pad_to(nk, 4) - nk);
       continue;
     }
-    stage_chunk(sm, Ir, Vc, p0, nk, false);
-    if (warp != 0) continue;
-    WarpModel& m = sm.m;
-    const u32 nsym = warp_normalize(m, nk);
-    const u32 nwords = (hb - 136u - 4u * nsym) / 2u;
-    u16* words = reinterpret_cast<u16*>(blk + 136 + 4 * nsym);
-    u32 x = kLow, e = 0;
-    const u32 G = (nk + 31) / 32;
-    const u32 lt = (1u << lane) - 1u;
-    auto fetch = [&](int gg, u32& s_, u32& fc_, u32& rc_) {
-      const u32 q = (u32)gg * 32 + lane;
-      s_ = (gg >= 0 && q < nk) ? (u32)sm.hi[q] : 0x100u;
-      fc_ = s_ < 256 ? m.fc[s_] : 0u;
-      rc_ = s_ < 256 ? m.rcp[s_] : 0u;
-    };
-    u32 ns, nfc, nrc;
-    fetch((int)G - 1, ns, nfc, nrc);
-    for (int gg = (int)G - 1; gg >= 0; --gg) {
-      const u32 s = ns, fcs = nfc, rcp = nrc;
-      fetch(gg - 1, ns, nfc, nrc);
-      const bool act = s < 256;
-      const u32 f = fcs & 0xFFFFu;
-      const bool emit = act && (x >> 20) >= f;
-      const u32 em = __ballot_sync(0xffffffffu, emit);
-      if (emit) {
-        words[nwords - 1u - (e + __popc(em & lt))] = (u16)(x & 0xFFFFu);
-        x >>= 16;
-      }
-      e += __popc(em);
-      if (act) {
-        u32 r;
-        const u32 qq = div_by(x, f, rcp, &r);
-        x = qq * kM + r + (fcs >> 16);
-      }
-    }
+    // RANS block: states, model and words were produced by k_chunk_stats; copy them in
+    // (words stored in reverse emission order)
+    const u32* rh = p.chunk_rhdr + g * kRhdrWords;
+    const u32 nsym = rh[33];
+    const u32 nwords = rh[32];
     u32* hdr = reinterpret_cast<u32*>(blk);
-    hdr[lane] = x;  // final states, lane order
-    if (lane == 0) {
-      hdr[32] = nwords;
-      hdr[33] = nsym;  // u16 nsym | u16 0
-    }
-    // symbol entries ascending: lane owns symbols 8*lane .. 8*lane+7
-    u32 present = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) present += m.freq[lane * 8 + j] ? 1u : 0u;
-    u32 rank = warp_incl_scan(present) - present;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const u32 s = lane * 8 + j;
-      const u32 f = m.freq[s];
-      if (f) hdr[34 + rank++] = s | (f << 16);
-    }
-    if (lane == 0 && (hb & 3u)) *reinterpret_cast<u16*>(blk + hb) = 0;
+    for (u32 i = tid; i < 34 + nsym; i += kCThreads) hdr[i] = rh[i];
+    const u16* ws = p.word_scratch + chunk_words_base(p.rec_off[t] + p0, g);
+    u16* words = reinterpret_cast<u16*>(blk + 136 + 4 * nsym);
+    for (u32 i = tid; i < nwords; i += kCThreads) words[i] = ws[nwords - 1 - i];
+    if (tid == 0 && (hb & 3u)) *reinterpret_cast<u16*>(blk + hb) = 0;
   }
 }
 

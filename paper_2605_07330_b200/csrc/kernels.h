@@ -26,6 +26,8 @@ struct Plan {
   uint32_t* chunk_hi;            // [max_chunks] hi block bytes (unpadded)
   uint32_t* chunk_mode;          // [max_chunks]
   uint64_t* chunk_hioff;         // [max_chunks+1] exclusive prefix of pad4(chunk_hi)
+  uint32_t* chunk_rhdr;          // [max_chunks][kRhdrWords] rANS block head from the stats pass
+  uint16_t* word_scratch;        // renormalisation words in emission order (see chunk_words_base)
   uint64_t* totals;              // [16]
   uint32_t* status;
   int prof;                      // debug instrumentation switch

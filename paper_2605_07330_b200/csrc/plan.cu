@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kCThreads) k_chunk_stats(Plan p, const u32* I,
   for (u64 g = blockIdx.x; g < n_chunks; g += gridDim.x) {
     __syncthreads();  // shared memory of the previous chunk is free
     const long long t0 = clock64();
-    const ChunkPos c = locate_chunk(p, counts, g, sm, I, V);
+    const ChunkPos c = locate_chunk(p, counts, g, sm.t, I, V);
     const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
     const long long t1 = clock64();
     const u32 gmax = stage_chunk(sm, c.Ir, c.Vc, c.p0, c.nk, true);
@@ -95,8 +95,14 @@ __global__ void __launch_bounds__(kCThreads) k_chunk_stats(Plan p, const u32* I,
     const u32 nsym = warp_normalize(sm.m, c.nk);
     const long long t3 = clock64();
     // counted encode pass: steps G-1..0, renorm if x >= f * 2^20
+    // encode pass: steps G-1..0, renorm if x >= f * 2^20. The words go to the
+    // chunk's scratch in emission order and the final states + model to chunk_rhdr, so the
+    // encode kernel only copies them into the record.
     u32 x = kLow, nwords = 0;
     const u32 G = (c.nk + 31) / 32;
+    const u32 lt = (1u << lane) - 1u;
+    const u32 wcap = c.nk / 2;
+    u16* ws = p.word_scratch + chunk_words_base(p.rec_off[c.t] + c.p0, g);
     // symbol + model of the next step are loaded one step ahead (independent of x)
     auto fetch = [&](int gg, u32& s_, u32& fc_, u32& rc_) {
       const u32 q = (u32)gg * 32 + lane;
@@ -112,12 +118,35 @@ __global__ void __launch_bounds__(kCThreads) k_chunk_stats(Plan p, const u32* I,
       const bool act = s < 256;
       const u32 f = fcs & 0xFFFFu;
       const bool emit = act && (x >> 20) >= f;
-      nwords += __popc(__ballot_sync(0xffffffffu, emit));
-      if (emit) x >>= 16;
+      const u32 em = __ballot_sync(0xffffffffu, emit);
+      if (emit) {
+        const u32 e = nwords + __popc(em & lt);
+        if (e < wcap) ws[e] = (u16)(x & 0xFFFFu);
+        x >>= 16;
+      }
+      nwords += __popc(em);
       if (act) {
         u32 r;
         const u32 qq = div_by(x, f, rcp, &r);
         x = qq * kM + r + (fcs >> 16);
+      }
+    }
+    u32* rh = p.chunk_rhdr + (u64)g * kRhdrWords;
+    rh[lane] = x;
+    if (lane == 0) {
+      rh[32] = nwords;
+      rh[33] = nsym;
+    }
+    {
+      u32 present = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) present += sm.m.freq[lane * 8 + j] ? 1u : 0u;
+      u32 rank = warp_incl_scan(present) - present;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const u32 s = lane * 8 + j;
+        const u32 f = sm.m.freq[s];
+        if (f) rh[34 + rank++] = s | (f << 16);
       }
     }
     u32 hb = 136u + 4u * nsym + 2u * nwords;

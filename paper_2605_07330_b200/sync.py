@@ -120,7 +120,8 @@ class SparseSyncReceiver:
         self.weights = _flat_bits(weights)
         self.device = self.weights[0].device if self.weights else torch.device("cuda")
         numel = [t.numel() for t in self.weights]
-        self.ctx = SyncContext(numel, bucket_limit=bucket_limit, max_changed=sum(numel), codec=codec, crc=crc,
+        # a receiver never extracts or encodes: no changed-element capacity needed
+        self.ctx = SyncContext(numel, bucket_limit=bucket_limit, max_changed=0, codec=codec, crc=crc,
                                device=self.device)
         self.weight_ptrs = ptr_table(self.weights, self.device)
 
