@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--codec", choices=["compressed", "raw"], default="compressed")
     p.add_argument("--bucket-mb", type=float, default=256)
     p.add_argument("--crc", action="store_true")
+    p.add_argument("--topology", choices=["ring", "pair"], default="ring",
+                   help="ring: every rank is Trainer of its model + Rollout of rank r-1's; pair: ranks < N/2 are "
+                        "Trainers, rank t + N/2 is the Rollout of Trainer t (the paper's space-sharing layout)")
     p.add_argument("--commit", choices=["swap", "scatter"], default="swap",
                    help="snapshot commit: pointer swap of double-buffered trainer weights, or in-place scatter")
     p.add_argument("--seed", type=int, default=0)
@@ -152,6 +155,19 @@ class Dist:
             dist.init_process_group("nccl", device_id=self.dev)
             self.ctrl = dist.new_group(backend="gloo")   # control plane (bucket manifests), cf. Ray in P:275
             self.dist = dist
+            # bring up the NCCL communicator and its P2P channels before the weight arenas take the HBM
+            dist.barrier(device_ids=[self.local])
+            x = torch.zeros(1 << 20, dtype=torch.uint8, device=self.dev)
+            y = torch.empty_like(x)
+            ops = [dist.P2POp(dist.isend, x, (self.rank + 1) % self.world),
+                   dist.P2POp(dist.irecv, y, (self.rank - 1) % self.world)]
+            if self.world % 2 == 0:   # also the pair partner used by --topology pair
+                half = self.world // 2
+                peer = (self.rank + half) % self.world
+                ops += [dist.P2POp(dist.isend, x, peer), dist.P2POp(dist.irecv, y, peer)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            torch.cuda.synchronize()
 
     def barrier(self):
         if self.world > 1:
@@ -179,7 +195,8 @@ class Dist:
 
 # ============================================================================= our arm
 class Rank:
-    """State of one rank: Trainer (X snapshot, Y current) for its own model, Rollout replica R of rank r-1."""
+    """State of one rank. ring: Trainer (X snapshot, Y current) of its own model + Rollout replica R of rank
+    r-1's model. pair: Trainer only (ranks < N/2) or Rollout only (rank t + N/2 replicates Trainer t)."""
 
     def __init__(self, args, d: Dist, manifest: synth.Manifest):
         import paper_2605_07330_b200 as ss
@@ -187,48 +204,80 @@ class Rank:
         from paper_2605_07330_b200 import transport
         self.ss, self.sg, self.d, self.args, self.m = ss, sg, d, args, manifest
         dev = d.dev
+        W = d.world
+        if args.topology == "pair" and W % 2:
+            raise SystemExit("--topology pair needs an even number of GPUs")
+        half = W // 2
+        self.is_trainer = args.topology == "ring" or d.rank < half
+        self.is_rollout = args.topology == "ring" or d.rank >= half
         self.seed = args.seed + 1000 * d.rank
-        peer_seed = args.seed + 1000 * ((d.rank - 1) % d.world)
-        self.X, self.Xv = sg.arena(manifest, dev)   # trainer snapshot (swaps with Y under --commit swap)
-        self.Y, self.Yv = sg.arena(manifest, dev)   # trainer current weights
-        self.R, self.Rv = sg.arena(manifest, dev)
-        sg.fill_old(self.Xv, manifest, self.seed)
-        sg.fill_new(self.Xv, self.Yv, manifest, self.seed, args.rho, MASKS[args.mask])
-        sg.fill_old(self.Rv, manifest, peer_seed)
-        torch.cuda.synchronize()
+        if args.topology == "ring":
+            peer_seed = args.seed + 1000 * ((d.rank - 1) % W)
+        else:
+            peer_seed = args.seed + 1000 * (d.rank - half)
         codec = ss.SYNC_CODEC_COMPRESSED if args.codec == "compressed" else ss.SYNC_CODEC_RAW
         limit = int(args.bucket_mb * (1 << 20))
         total = manifest.total
-        self.sender = ss.SparseSyncSender(self.Xv, self.Yv, bucket_limit=limit, codec=codec, crc=args.crc,
-                                          max_changed=min(total, int(total * args.rho * 1.08) + (1 << 20)))
-        self.receiver = ss.SparseSyncReceiver(self.Rv, bucket_limit=limit, codec=codec, crc=args.crc)
-        self.link = transport.RingLink(d.rank, d.world, dev, d.ctrl) if d.world > 1 else None
+        self.X = self.Y = self.R = None
+        self.sender = self.receiver = None
+        if self.is_trainer:
+            self.X, self.Xv = sg.arena(manifest, dev)   # trainer snapshot (swaps with Y under --commit swap)
+            self.Y, self.Yv = sg.arena(manifest, dev)   # trainer current weights
+            sg.fill_old(self.Xv, manifest, self.seed)
+            sg.fill_new(self.Xv, self.Yv, manifest, self.seed, args.rho, MASKS[args.mask])
+            self.sender = ss.SparseSyncSender(self.Xv, self.Yv, bucket_limit=limit, codec=codec, crc=args.crc,
+                                              max_changed=min(total, int(total * args.rho * 1.02) + (1 << 20)))
+        if self.is_rollout:
+            self.R, self.Rv = sg.arena(manifest, dev)
+            sg.fill_old(self.Rv, manifest, peer_seed)
+            self.receiver = ss.SparseSyncReceiver(self.Rv, bucket_limit=limit, codec=codec, crc=args.crc)
+        torch.cuda.synchronize()
+        self.link = None
+        if W > 1:
+            if args.topology == "ring":
+                # under --commit swap the sender's I array is dead between pack and the next extract:
+                # receive the peer's buckets into it (saves a payload-sized buffer at 30B / 183 GB of arenas)
+                rb = self.sender.I.view(torch.uint8) if args.commit == "swap" else None
+                self.link = transport.RingLink(d.rank, W, dev, d.ctrl, recv_buf=rb)
+            else:
+                t = d.rank if self.is_trainer else d.rank - half
+                self.link = transport.PairLink(d.rank, W, dev, trainer=t, rollout=t + half, ctrl=d.ctrl)
         self.toggle_scratch = torch.empty(len(manifest.tensors) + 1, dtype=torch.int64, device=dev)
-        self.S = 2 * total
-        self.ev = None
+        self.S = 2 * total if self.is_trainer else 0   # weights this rank syncs per step (as the sender)
 
     def step(self, ev=None):
         """One sync. ev: list of 7 CUDA events recorded between the phases (or None)."""
         snd, rcv = self.sender, self.receiver
         rec = (lambda i: ev[i].record()) if ev else (lambda i: None)
         rec(0)
-        snd.ctx.sync_extract_batched(snd.old_ptrs, snd.new_ptrs, snd.I, snd.V, snd.counts)
-        rec(1)
-        snd.ctx.sync_compress(snd.I, snd.V, snd.counts, snd.enc)
-        rec(2)
-        blist = snd.pack()
-        rec(3)
+        blist = []
+        if snd is not None:
+            snd.ctx.sync_extract_batched(snd.old_ptrs, snd.new_ptrs, snd.I, snd.V, snd.counts)
+            rec(1)
+            snd.ctx.sync_compress(snd.I, snd.V, snd.counts, snd.enc)
+            rec(2)
+            blist = snd.pack()
+            rec(3)
+        else:
+            rec(1)
+            rec(2)
+            rec(3)
         if self.link is None:
             for b in range(len(blist)):
                 rcv.apply(snd.bucket(b))
-        else:
+        elif isinstance(self.link, self.ss.transport.RingLink):
             self.link.exchange(snd.buckets, blist, rcv.apply)
+        elif snd is not None:
+            self.link.send(snd.buckets, blist)
+        else:
+            self.link.receive(rcv.apply)
         rec(4)
-        snd.commit(mode=self.args.commit)
-        if self.args.commit == "swap":
-            self.X, self.Y, self.Xv, self.Yv = self.Y, self.X, self.Yv, self.Xv
+        if snd is not None:
+            snd.commit(mode=self.args.commit)
+            if self.args.commit == "swap":
+                self.X, self.Y, self.Xv, self.Yv = self.Y, self.X, self.Yv, self.Xv
         rec(5)
-        if self.args.commit == "scatter":
+        if snd is not None and self.args.commit == "scatter":
             # snapshot == current now: the synthetic "optimizer step" flips the changed bits again so the
             # next sync has a fresh update of the same density (write-only scatter, input generation)
             self.sg.toggle(snd.new_ptrs, snd.I, snd.V, snd.counts, len(self.m.tensors), self.toggle_scratch)
@@ -321,11 +370,12 @@ def run_ours(args):
     for _ in range(args.warmup):
         r.step()
     torch.cuda.synchronize()
-    st = r.sender.ctx.sync_status()
-    assert st == 0, f"sender status {st}"
-    stats = r.sender.stats()
-    nb = len(r.sender.bucket_list)
-    payload = sum(s for _, s in r.sender.bucket_list)
+    if r.sender is not None:   # rank 0 is always a Trainer
+        st = r.sender.ctx.sync_status()
+        assert st == 0, f"sender status {st}"
+        stats = r.sender.stats()
+        nb = len(r.sender.bucket_list)
+        payload = sum(s for _, s in r.sender.bucket_list)
 
     # ---- timed region
     K = args.steps
@@ -342,7 +392,8 @@ def run_ours(args):
     t_end.record()
     d.barrier()
     clk = clocks.stop()
-    launches = ss.launch_count() - launches0 + 2 * K   # + the bench's own toggle kernels (2 per step)
+    launches = ss.launch_count() - launches0 + (2 * K if args.commit == "scatter" else 0)  # + toggle kernels
+    launches = int(d.sum(launches))
     ms_local = t_start.elapsed_time(t_end)
     ms = d.max(ms_local)
     phases = np.zeros(6)
@@ -350,21 +401,29 @@ def run_ours(args):
         for i in range(6):
             phases[i] += evs[k][i].elapsed_time(evs[k][i + 1])
     phases /= K
-    st_s = r.sender.ctx.sync_status()
-    st_r = r.receiver.ctx.sync_status()
+    if d.world > 1:  # per phase, the max over ranks (pair: extract on Trainers, apply on Rollouts)
+        g = [None] * d.world
+        d.dist.all_gather_object(g, phases.tolist(), group=d.ctrl)
+        phases = np.max(np.array(g), axis=0)
+    st_s = r.sender.ctx.sync_status() if r.sender is not None else 0
+    st_r = r.receiver.ctx.sync_status() if r.receiver is not None else 0
     assert st_s == 0 and st_r == 0, f"status sender {st_s} receiver {st_r}"
 
     # ---- verification: rollout replica == peer's committed snapshot (bit-exact)
     verify = None
     if not args.no_verify:
-        mine_x = chunked_digest(r.X)
-        mine_r = chunked_digest(r.R)
+        mine_x = chunked_digest(r.X) if r.X is not None else None
+        mine_r = chunked_digest(r.R) if r.R is not None else None
         if d.world == 1:
             verify = mine_x == mine_r
         else:
             g = [None] * d.world
             d.dist.all_gather_object(g, (mine_x, mine_r), group=d.ctrl)
-            verify = all(g[(i - 1) % d.world][0] == g[i][1] for i in range(d.world))
+            W, half = d.world, d.world // 2
+            if args.topology == "ring":
+                verify = all(g[(i - 1) % W][0] == g[i][1] for i in range(W))
+            else:
+                verify = all(g[t][0] == g[t + half][1] for t in range(half))
 
     # ---- e2e through the public API with host buffers (H2D of the new weights, D2H of the result)
     e2e = None
@@ -397,9 +456,12 @@ def run_ours(args):
         "data": "synthetic: random-init bf16 weights of the named architecture (N(0,0.02) quantile table), "
                 f"{args.mask}-mask sparse perturbations, seeded",
         "config": {"workload": f"{manifest.name} bf16, {100 * (1 - args.rho):.1f}% sparsity, {args.mask} mask",
+                   "topology_mode": args.topology,
                    "elements_per_rank": manifest.total, "tensors": len(manifest.tensors),
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
-                   "topology": "ring: rank r = Trainer of its model + Rollout replica of rank r-1 (N=1: loopback)",
+                   "topology": ("ring: rank r = Trainer of its model + Rollout replica of rank r-1 (N=1: loopback)"
+                                if args.topology == "ring" else
+                                "pair: ranks < N/2 Trainers, rank t+N/2 = Rollout of Trainer t (NCCL P2P)"),
                    "l2": "inputs (2x61 GB) larger than L2; no flush"},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
                          zip(["extract", "compress", "pack", "transfer_apply", "commit", "synthetic_update"],
@@ -429,26 +491,48 @@ def run_ours(args):
 def run_e2e(args, d: Dist, r: Rank):
     """Same metric through the public API with HOST buffers: per step the new weights arrive from pinned host
     memory (H2D inside the timed region) and the per-tensor change counts go back to the host (D2H)."""
+    hosts, counts_h = None, None
+    # host RAM guard: every Trainer rank needs n_host x S of pinned inputs; refuse rather than risk the OOM killer
+    n_need = (2 if args.commit == "swap" else 1) * r.S
     try:
-        host = torch.empty(r.Y.numel(), dtype=torch.int16, pin_memory=True)
-    except Exception as e:
-        return {"value": None, "unit": UNIT, "reason": f"cannot pin {2 * r.Y.numel() / 1e9:.0f} GB: {e}"}
-    host.copy_(r.Y)          # step inputs as a host array
-    counts_h = torch.empty_like(r.sender.counts, device="cpu").pin_memory()
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 0
+    n_trainers = d.world if args.topology == "ring" else d.world // 2
+    ok = int(d.sum(1.0 if (avail - 24e9) / max(1, n_trainers) > n_need or r.sender is None else 0.0)) == d.world
+    if not ok:
+        return {"value": None, "unit": UNIT,
+                "reason": f"host RAM ({avail / 1e9:.0f} GB available) cannot hold {n_trainers} x "
+                          f"{n_need / 1e9:.0f} GB of pinned host inputs"}
+    if r.sender is not None:
+        # the inputs of consecutive steps: under --commit swap the versions alternate (v1, v0, v1, ...),
+        # so keep both as host arrays; under --commit scatter the toggle regenerates them on the device
+        n_host = 2 if args.commit == "swap" else 1
+        try:
+            hosts = [torch.empty(r.Y.numel(), dtype=torch.int16, pin_memory=True) for _ in range(n_host)]
+        except Exception as e:
+            return {"value": None, "unit": UNIT, "reason": f"cannot pin {n_host * 2 * r.Y.numel() / 1e9:.0f} GB: {e}"}
+        hosts[0].copy_(r.Y)
+        if n_host == 2:
+            hosts[1].copy_(r.X)
+        counts_h = torch.empty_like(r.sender.counts, device="cpu").pin_memory()
     K = args.e2e_steps
     d.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
-    for _ in range(K):
-        r.Y.copy_(host, non_blocking=True)
+    for k in range(K):
+        if hosts is not None:
+            r.Y.copy_(hosts[k % len(hosts)], non_blocking=True)
         r.step()
-        counts_h.copy_(r.sender.counts, non_blocking=True)
+        if counts_h is not None:
+            counts_h.copy_(r.sender.counts, non_blocking=True)
     t1.record()
     d.barrier()
     ms = d.max(t0.elapsed_time(t1))
     total_S = d.sum(r.S)
-    del host
+    del hosts
     return {"value": round(total_S * K / (ms / 1e3) / 1e9, 3), "unit": UNIT,
             "h2d_bytes_per_step": int(r.S), "d2h_bytes_per_step": int(8 * r.sender.counts.numel()),
             "steps": K, "ms_per_step": round(ms / K, 3)}

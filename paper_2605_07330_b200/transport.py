@@ -42,11 +42,13 @@ def _manifest_exchange(blist, dst, src, ctrl):
 
 
 class _Link:
-    def __init__(self, rank: int, world: int, device, ctrl=None, group=None):
+    def __init__(self, rank: int, world: int, device, ctrl=None, group=None, recv_buf: torch.Tensor | None = None):
+        """recv_buf: optional uint8 device tensor to receive into (e.g. memory the caller no longer needs
+        during the transfer); a private buffer is allocated if it is absent or too small."""
         self.rank, self.world, self.device = rank, world, torch.device(device)
         self.ctrl = ctrl
         self.group = group
-        self.recv = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self.recv = recv_buf if recv_buf is not None else torch.empty(0, dtype=torch.uint8, device=self.device)
         self.last_in = []
 
     def _ensure(self, need: int):
@@ -88,8 +90,8 @@ class RingLink(_Link):
 class PairLink(_Link):
     """Trainer rank `trainer` -> Rollout rank `rollout` (1T->1R; replica fan-out is several pairs)."""
 
-    def __init__(self, rank, world, device, trainer: int, rollout: int, ctrl=None, group=None):
-        super().__init__(rank, world, device, ctrl, group)
+    def __init__(self, rank, world, device, trainer: int, rollout: int, ctrl=None, group=None, recv_buf=None):
+        super().__init__(rank, world, device, ctrl, group, recv_buf)
         self.trainer, self.rollout = trainer, rollout
 
     def send(self, send_buf, blist):
