@@ -281,9 +281,10 @@ int sync_compress(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const u
   cudaStream_t s = (cudaStream_t)stream;
   x->plan.enc_cap = enc_cap;
   launch_plan_scan(x->plan, d_counts, s);
-  if (x->cfg.codec == SYNC_CODEC_COMPRESSED) launch_chunk_stats(x->plan, d_I, d_V, d_counts, x->grid, s);
+  // CTA-per-chunk kernels of 128 threads: 2x the grid of the 256-thread kernels (~9 resident per SM)
+  if (x->cfg.codec == SYNC_CODEC_COMPRESSED) launch_chunk_stats(x->plan, d_I, d_V, d_counts, 2 * x->grid, s);
   launch_plan_sizes(x->plan, d_counts, s);
-  launch_encode(x->plan, d_I, d_V, d_counts, d_enc, x->grid, s);
+  launch_encode(x->plan, d_I, d_V, d_counts, d_enc, 2 * x->grid, s);
   CK(cudaGetLastError());
   x->plan_counts = d_counts;
   x->plan_valid = true;

@@ -60,44 +60,59 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
       continue;
     }
 
-    // ---- index stream slice (pairs of positions per thread -> 32-bit stores for DELTA16)
+    // ---- index stream + lo plane slices: groups of 4 positions per thread, kG groups in flight
+    //      (DELTA16: one 64-bit store of 4 deltas; ABS32: one 128-bit store; lo: one 32-bit store)
     const u64 ib = (mode ? 4 : 2) * nnz;
-    if (mode == 0) {
-      u16* D = reinterpret_cast<u16*>(rec + 16) + p0;
-      for (u32 q = 2 * tid; q < nk; q += 2 * kCThreads) {
-        const u64 pp = p0 + q;
-        const u32 a0 = Ir[pp], prev = pp ? Ir[pp - 1] : 0u;
-        const u32 d0 = a0 - prev;
-        if (q + 1 < nk) {
-          const u32 d1 = Ir[pp + 1] - a0;
-          *reinterpret_cast<u32*>(D + q) = (d0 & 0xFFFFu) | (d1 << 16);
-        } else {
-          D[q] = (u16)d0;
-        }
-      }
-    } else {
-      u32* A = reinterpret_cast<u32*>(rec + 16) + p0;
-      for (u32 q = tid; q < nk; q += kCThreads) A[q] = Ir[p0 + q];
-    }
     const u64 lo_off = 16 + pad_to(ib, 4);
     const u64 dir_off = lo_off + pad_to(nnz, 4);
     const u64 hi_base = dir_off + 16 * n_ch;
+    {
+      constexpr int kG = 4;
+      u8* L = rec + lo_off + p0;
+      for (u32 q0 = 4 * tid; q0 < nk; q0 += 4 * kCThreads * kG) {
+        u32 iv[kG][5];
+        u16 vv[kG][4];
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+          const u32 q = q0 + 4 * kCThreads * j;
+          const u64 pp = p0 + q;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            iv[j][e + 1] = (q + e < nk) ? Ir[pp + e] : 0u;
+            vv[j][e] = (q + e < nk) ? Vc[q + e] : (u16)0;
+          }
+          iv[j][0] = (q < nk && pp) ? Ir[pp - 1] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+          const u32 q = q0 + 4 * kCThreads * j;
+          if (q >= nk) continue;
+          if (q + 4 <= nk) {
+            if (mode == 0) {
+              const uint2 d = make_uint2((iv[j][1] - iv[j][0]) | ((iv[j][2] - iv[j][1]) << 16),
+                                         (iv[j][3] - iv[j][2]) | ((iv[j][4] - iv[j][3]) << 16));
+              *reinterpret_cast<uint2*>(reinterpret_cast<u16*>(rec + 16) + p0 + q) = d;
+            } else {
+              *reinterpret_cast<uint4*>(reinterpret_cast<u32*>(rec + 16) + p0 + q) =
+                  make_uint4(iv[j][1], iv[j][2], iv[j][3], iv[j][4]);
+            }
+            *reinterpret_cast<u32*>(L + q) = (u32)(vv[j][0] & 0xFFu) | ((u32)(vv[j][1] & 0xFFu) << 8) |
+                                             ((u32)(vv[j][2] & 0xFFu) << 16) | ((u32)(vv[j][3] & 0xFFu) << 24);
+          } else {
+            for (u32 e = 0; q + e < nk; ++e) {  // chunk tail: reload (keeps the arrays in registers)
+              const u64 pe = p0 + q + e;
+              const u32 cur = Ir[pe], prev = pe ? Ir[pe - 1] : 0u;
+              if (mode == 0) reinterpret_cast<u16*>(rec + 16)[pe] = (u16)(cur - prev);
+              else reinterpret_cast<u32*>(rec + 16)[pe] = cur;
+              L[q + e] = (u8)(Vc[q + e] & 0xFFu);
+            }
+          }
+        }
+      }
+    }
     if (last) {
       zero_bytes(rec + 16 + ib, pad_to(ib, 4) - ib);
       zero_bytes(rec + lo_off + nnz, pad_to(nnz, 4) - nnz);
-    }
-    // ---- lo plane slice: 4 values per thread -> one 32-bit store
-    {
-      u8* L = rec + lo_off + p0;
-      for (u32 q = 4 * tid; q < nk; q += 4 * kCThreads) {
-        if (q + 4 <= nk) {
-          const u32 w = (u32)(Vc[q] & 0xFFu) | ((u32)(Vc[q + 1] & 0xFFu) << 8) | ((u32)(Vc[q + 2] & 0xFFu) << 16) |
-                        ((u32)(Vc[q + 3] & 0xFFu) << 24);
-          *reinterpret_cast<u32*>(L + q) = w;
-        } else {
-          for (u32 r = q; r < nk; ++r) L[r] = (u8)(Vc[r] & 0xFFu);
-        }
-      }
     }
     // ---- directory entry + hi block
     const u32 hb = p.chunk_hi[g];

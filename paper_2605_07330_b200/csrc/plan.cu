@@ -4,9 +4,9 @@
 //  * k_plan_scan   (1 CTA)   value offsets, chunk offsets, totals (manifest order)
 //  * k_chunk_stats (grid)    per chunk: max index gap (-> DELTA16/ABS32, P:360,
 //                            DESIGN C4), hi-byte histogram, normalised rANS model
-//                            and an encode pass that only counts renormalisation
-//                            words -> exact hi block size and RAW/RANS decision
-//                            (never-expand)
+//                            and the rANS encode pass -> exact hi block size and
+//                            RAW/RANS decision (never-expand); words, states
+//                            and model kept in scratch for k_encode
 //  * k_plan_sizes  (1 CTA)   chunk hi-offset prefix, record sizes,
 //                            record byte offsets, statistics
 #include <cstdio>
@@ -74,64 +74,111 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_scan(Plan p, const u64* c
   }
 }
 
-// One CTA per chunk: staged hi bytes + histogram + max gap (all threads), then
-// the model and a counted rANS pass from shared memory (warp 0).
 __device__ unsigned long long g_cprof[8];  // debug cycle counters (SS_CPROF=1)
 
-__global__ void __launch_bounds__(kCThreads) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
-  __shared__ ChunkSmem sm;
+// One warp per chunk: the warp builds its chunk's histogram + max first difference (8
+// loads in flight per lane, per-warp shared histogram), normalises the model, then runs
+// the rANS encode pass reading V from L2 with the next 8 steps prefetched into registers
+// (words to the chunk's scratch in emission order; final states + model to chunk_rhdr).
+// No hi plane in shared memory: ~32 independent rANS chains per SM (a CTA-per-chunk
+// variant with the hi plane staged in shared memory measured 1.2-1.7x slower).
+constexpr int kWPF = 8;
+__global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
+  __shared__ WarpModel s_m[8];
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpModel& m = s_m[warp];
   const u64 n_chunks = p.totals[kTotChunks];
-  for (u64 g = blockIdx.x; g < n_chunks; g += gridDim.x) {
-    __syncthreads();  // shared memory of the previous chunk is free
+  const u64 nwarps = (u64)gridDim.x * 8;
+  const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
+  for (u64 g = (u64)blockIdx.x * 8 + warp; g < n_chunks; g += nwarps) {
     const long long t0 = clock64();
-    const ChunkPos c = locate_chunk(p, counts, g, sm.t, I, V);
-    const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
+    const u64* co = p.chunk_off;
+    const u32 t = warp_upper_search(p.n_tensors, g, [&](u32 i) { return co[i]; });
+    const u64 nnz = counts[t];
+    const u64 p0 = (g - co[t]) * kChunk;
+    const u32 nk = (u32)((nnz - p0) < kChunk ? (nnz - p0) : kChunk);
+    const u32* Ir = I + p.rec_off[t];
+    const u16* Vc = V + p.rec_off[t] + p0;
     const long long t1 = clock64();
-    const u32 gmax = stage_chunk(sm, c.Ir, c.Vc, c.p0, c.nk, true);
-    const long long t2 = clock64();
-    if (threadIdx.x == 0 && gmax) atomicMax(&p.maxgap[c.t], gmax);
-    if (!comp || warp != 0) continue;
-    const u32 nsym = warp_normalize(sm.m, c.nk);
-    const long long t3 = clock64();
-    // counted encode pass: steps G-1..0, renorm if x >= f * 2^20
-    // encode pass: steps G-1..0, renorm if x >= f * 2^20. The words go to the
-    // chunk's scratch in emission order and the final states + model to chunk_rhdr, so the
-    // encode kernel only copies them into the record.
-    u32 x = kLow, nwords = 0;
-    const u32 G = (c.nk + 31) / 32;
-    const u32 lt = (1u << lane) - 1u;
-    const u32 wcap = c.nk / 2;
-    u16* ws = p.word_scratch + chunk_words_base(p.rec_off[c.t] + c.p0, g);
-    // symbol + model of the next step are loaded one step ahead (independent of x)
-    auto fetch = [&](int gg, u32& s_, u32& fc_, u32& rc_) {
-      const u32 q = (u32)gg * 32 + lane;
-      s_ = (gg >= 0 && q < c.nk) ? (u32)sm.hi[q] : 0x100u;
-      fc_ = s_ < 256 ? sm.m.fc[s_] : 0u;
-      rc_ = s_ < 256 ? sm.m.rcp[s_] : 0u;
-    };
-    u32 ns, nfc, nrc;
-    fetch((int)G - 1, ns, nfc, nrc);
-    for (int gg = (int)G - 1; gg >= 0; --gg) {
-      const u32 s = ns, fcs = nfc, rcp = nrc;
-      fetch(gg - 1, ns, nfc, nrc);
-      const bool act = s < 256;
-      const u32 f = fcs & 0xFFFFu;
-      const bool emit = act && (x >> 20) >= f;
-      const u32 em = __ballot_sync(0xffffffffu, emit);
-      if (emit) {
-        const u32 e = nwords + __popc(em & lt);
-        if (e < wcap) ws[e] = (u16)(x & 0xFFFFu);
-        x >>= 16;
+    // ---- histogram + max first difference
+    for (u32 sym = lane; sym < 256; sym += 32) m.hist[sym] = 0;
+    __syncwarp();
+    u32 gmax = 0;
+    for (u32 b0 = 0; b0 < nk; b0 += 32 * kWPF) {
+      u32 hv[kWPF], cur[kWPF];
+#pragma unroll
+      for (int u = 0; u < kWPF; ++u) {
+        const u32 q = b0 + u * 32 + lane;
+        hv[u] = q < nk ? (u32)(Vc[q] >> 8) : 0x100u;
+        cur[u] = q < nk ? Ir[p0 + q] : 0u;
       }
-      nwords += __popc(em);
-      if (act) {
-        u32 r;
-        const u32 qq = div_by(x, f, rcp, &r);
-        x = qq * kM + r + (fcs >> 16);
+#pragma unroll
+      for (int u = 0; u < kWPF; ++u) {
+        const u32 q = b0 + u * 32 + lane;
+        if (hv[u] < 256) atomicAdd(&m.hist[hv[u]], 1u);
+        u32 prev = __shfl_up_sync(0xffffffffu, cur[u], 1);
+        if (lane == 0) prev = (p0 + q) ? Ir[p0 + q - 1] : 0u;
+        if (q < nk) {
+          const u32 d = cur[u] - prev;
+          gmax = d > gmax ? d : gmax;
+        }
       }
     }
-    u32* rh = p.chunk_rhdr + (u64)g * kRhdrWords;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u32 x = __shfl_xor_sync(0xffffffffu, gmax, o);
+      gmax = x > gmax ? x : gmax;
+    }
+    if (lane == 0 && gmax) atomicMax(&p.maxgap[t], gmax);
+    __syncwarp();
+    const long long t2 = clock64();
+    if (!comp) continue;
+    const u32 nsym = warp_normalize(m, nk);
+    const long long t3 = clock64();
+    // ---- counted rANS pass (words -> scratch in emission order; states/model -> chunk_rhdr)
+    u32 x = kLow, nwords = 0;
+    const u32 G = (nk + 31) / 32;
+    const u32 lt = (1u << lane) - 1u;
+    const u32 wcap = nk / 2;
+    u16* ws = p.word_scratch + chunk_words_base(p.rec_off[t] + p0, g);
+    u32 nxt[kWPF];
+    auto load_block = [&](int top, u32* dst) {  // steps top, top-1, ..., top-7
+#pragma unroll
+      for (int u = 0; u < kWPF; ++u) {
+        const int gg = top - u;
+        const u32 q = (u32)gg * 32 + lane;
+        dst[u] = (gg >= 0 && q < nk) ? (u32)(Vc[q] >> 8) : 0x100u;
+      }
+    };
+    load_block((int)G - 1, nxt);
+    for (int top = (int)G - 1; top >= 0; top -= kWPF) {
+      u32 cur[kWPF];
+#pragma unroll
+      for (int u = 0; u < kWPF; ++u) cur[u] = nxt[u];
+      if (top - kWPF >= 0) load_block(top - kWPF, nxt);
+#pragma unroll
+      for (int u = 0; u < kWPF; ++u) {
+        if (top - u < 0) break;
+        const u32 sym = cur[u];
+        const bool act = sym < 256;
+        const u32 fcs = act ? m.fc[sym] : 0u, rcp = act ? m.rcp[sym] : 0u;
+        const u32 f = fcs & 0xFFFFu;
+        const bool emit = act && (x >> 20) >= f;
+        const u32 em = __ballot_sync(0xffffffffu, emit);
+        if (emit) {
+          const u32 e = nwords + __popc(em & lt);
+          if (e < wcap) ws[e] = (u16)(x & 0xFFFFu);
+          x >>= 16;
+        }
+        nwords += __popc(em);
+        if (act) {
+          u32 r;
+          const u32 qq = div_by(x, f, rcp, &r);
+          x = qq * kM + r + (fcs >> 16);
+        }
+      }
+    }
+    u32* rh = p.chunk_rhdr + g * kRhdrWords;
     rh[lane] = x;
     if (lane == 0) {
       rh[32] = nwords;
@@ -140,19 +187,19 @@ __global__ void __launch_bounds__(kCThreads) k_chunk_stats(Plan p, const u32* I,
     {
       u32 present = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) present += sm.m.freq[lane * 8 + j] ? 1u : 0u;
+      for (int j = 0; j < 8; ++j) present += m.freq[lane * 8 + j] ? 1u : 0u;
       u32 rank = warp_incl_scan(present) - present;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const u32 s = lane * 8 + j;
-        const u32 f = sm.m.freq[s];
-        if (f) rh[34 + rank++] = s | (f << 16);
+        const u32 sym = lane * 8 + j;
+        const u32 f = m.freq[sym];
+        if (f) rh[34 + rank++] = sym | (f << 16);
       }
     }
     u32 hb = 136u + 4u * nsym + 2u * nwords;
     u32 mode = 1;
-    if (hb >= c.nk) {
-      hb = c.nk;
+    if (hb >= nk) {
+      hb = nk;
       mode = 0;
     }
     if (lane == 0) {
@@ -167,6 +214,7 @@ __global__ void __launch_bounds__(kCThreads) k_chunk_stats(Plan p, const u32* I,
         atomicAdd(&g_cprof[4], 1ull);
       }
     }
+    __syncwarp();
   }
 }
 
@@ -261,7 +309,7 @@ void launch_chunk_stats(const Plan& p, const u32* I, const u16* V, const u64* co
     unsigned long long z[8] = {0};
     cudaMemcpyToSymbolAsync(g_cprof, z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
   }
-  k_chunk_stats<<<grid, kCThreads, 0, s>>>(q, I, V, counts);
+  k_chunk_stats<<<grid, 256, 0, s>>>(q, I, V, counts);
   if (want) {
     unsigned long long h[8];
     cudaMemcpyFromSymbolAsync(h, g_cprof, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
