@@ -254,9 +254,8 @@ class Rank:
         if snd is not None:
             snd.ctx.sync_extract_batched(snd.old_ptrs, snd.new_ptrs, snd.I, snd.V, snd.counts)
             rec(1)
-            snd.ctx.sync_compress(snd.I, snd.V, snd.counts, snd.enc)
+            blist = snd.compress_pack()   # fused K2-K4 (blocking: host bucket plan)
             rec(2)
-            blist = snd.pack()
             rec(3)
         else:
             rec(1)
@@ -464,8 +463,8 @@ def run_ours(args):
                                 "pair: ranks < N/2 Trainers, rank t+N/2 = Rollout of Trainer t (NCCL P2P)"),
                    "l2": "inputs (2x61 GB) larger than L2; no flush"},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
-                         zip(["extract", "compress", "pack", "transfer_apply", "commit", "synthetic_update"],
-                             phases)},
+                         zip(["extract", "compress_pack", None, "transfer_apply", "commit", "synthetic_update"],
+                             phases) if n},
         "roofline": {"bound": "hbm", "kernel": "k_extract (K1)", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "bytes_per_launch": alg_bytes_extract, "traffic_source": traffic_src,

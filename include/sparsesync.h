@@ -151,6 +151,18 @@ int sync_bucket_pack(sync_ctx* ctx, const uint8_t* d_enc, uint8_t* d_buckets, ui
 /* Upper bound of the bucket buffer for the current plan (after sync_compress; blocking). */
 int sync_buckets_bound(sync_ctx* ctx, uint64_t* bytes, sync_stream_t stream);
 
+/* ---- a2-a5 fused: plan -> bucket plan -> encode in place -------------------
+ * BLOCKING. Same bytes as sync_compress + sync_bucket_pack, but every record
+ * is encoded straight into its bucket position (no staging stream, no copy):
+ * plan + per-chunk model on the device, greedy bucketing on the host from the
+ * record sizes, then the encode kernel writes into d_buckets and the bucket
+ * headers/directories (+ CRC) follow. If d_buckets is too small (or more than
+ * max_buckets are needed) it returns SYNC_ERR_CAPACITY and *h_need (if not
+ * NULL) holds the required buffer bytes; nothing is written.               */
+int sync_compress_pack(sync_ctx* ctx, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,
+                       uint8_t* d_buckets, uint64_t buckets_cap, uint32_t* n_buckets, uint64_t* h_offsets,
+                       uint64_t* h_sizes, uint32_t max_buckets, uint64_t* h_need, sync_stream_t stream);
+
 /* ---- a7 unpack / decompress (Alg. 3 l.5; "exact inverse") ---
  * sync_bucket_unpack validates one bucket in device memory (magic, version,
  * sizes, CRC when flagged) and writes one sync_record_view per record into

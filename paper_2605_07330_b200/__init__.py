@@ -42,7 +42,7 @@ SYNC_CHUNK = 16384
 EXPORTS = [
     "sync_workspace_size", "sync_ctx_create", "sync_ctx_destroy", "sync_extract_workspace_size", "sync_extract",
     "sync_extract_status", "sync_extract_batched", "sync_enc_bound", "sync_compress", "sync_bucket_pack",
-    "sync_buckets_bound", "sync_bucket_unpack", "sync_decompress", "sync_decompress_apply", "sync_apply",
+    "sync_buckets_bound", "sync_compress_pack", "sync_bucket_unpack", "sync_decompress", "sync_decompress_apply", "sync_apply",
     "sync_commit_snapshot", "sync_commit_snapshot_batched", "sync_status", "sync_ctx_stats", "sync_strerror",
     "sync_launch_count",
 ]
@@ -94,6 +94,7 @@ def lib() -> ctypes.CDLL:
             "sync_compress": [P, P, P, P, P, u64, P],
             "sync_bucket_pack": [P, P, P, u64, P, P, P, u32, P],
             "sync_buckets_bound": [P, P, P],
+            "sync_compress_pack": [P, P, P, P, P, u64, P, P, P, u32, P, P],
             "sync_bucket_unpack": [P, P, u64, P, u32, P, P],
             "sync_decompress": [P, P, u64, P, P, u64, P],
             "sync_decompress_apply": [P, P, u64, P, P],
@@ -268,6 +269,21 @@ class SyncContext:
         _ck(lib().sync_bucket_pack(self._h, _dev_ptr(enc), _dev_ptr(buckets), buckets.numel(), ctypes.byref(nb),
                                    self._h_off, self._h_size, self._max_buckets, _stream(stream)),
             "sync_bucket_pack")
+        return [(int(self._h_off[b]), int(self._h_size[b])) for b in range(nb.value)]
+
+    def sync_compress_pack(self, I: torch.Tensor, V: torch.Tensor, counts: torch.Tensor, buckets: torch.Tensor,
+                           stream=None):
+        """Blocking fused compress + pack. Returns ([(offset, size)], needed_bytes); raises SyncError
+        (SYNC_ERR_CAPACITY) with .need set when `buckets` is too small."""
+        nb = ctypes.c_uint32()
+        need = ctypes.c_uint64()
+        code = lib().sync_compress_pack(self._h, _ptr(I), _ptr(V), _dev_ptr(counts), _dev_ptr(buckets),
+                                        buckets.numel(), ctypes.byref(nb), self._h_off, self._h_size,
+                                        self._max_buckets, ctypes.byref(need), _stream(stream))
+        if code != SYNC_OK:
+            err = SyncError(code, "sync_compress_pack")
+            err.need = need.value
+            raise err
         return [(int(self._h_off[b]), int(self._h_size[b])) for b in range(nb.value)]
 
     def sync_commit_snapshot_batched(self, snap_ptrs: torch.Tensor, I: torch.Tensor, V: torch.Tensor,

@@ -25,7 +25,7 @@ constexpr u64 kAlign = 256;
 
 struct Layout {
   u64 numel, tile_prefix, tile_tensor, misc, tile_state, stage_ring, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
-  u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, totals, recs, bks, views, nviews, crc, total;
+  u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, rec_dst, totals, recs, bks, views, nviews, crc, total;
 };
 
 u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4; }
@@ -55,6 +55,7 @@ Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_change
   L.chunk_hioff = take(8ull * (max_chunks + 1));
   L.chunk_rhdr = take(4ull * kRhdrWords * max_chunks);
   L.word_scratch = take(2ull * (max_changed / 2 + max_chunks + 2));
+  L.rec_dst = take(8ull * T);
   L.totals = take(8 * 16);
   L.recs = take(sizeof(RecordDesc) * (u64)T);
   L.bks = take(sizeof(BucketDesc) * (u64)(T + 1));
@@ -111,7 +112,7 @@ struct sync_ctx {
   int grid;   // grid-stride kernels: CTAs of 256 threads
   const u64* plan_counts;
   bool plan_valid;
-  std::vector<u64> h_rec_bytes, h_chunk_off, h_enc_off, h_totals;
+  std::vector<u64> h_rec_bytes, h_chunk_off, h_enc_off, h_totals, h_rec_dst;
   std::vector<RecordDesc> h_recs;
   std::vector<BucketDesc> h_bks;
 };
@@ -184,6 +185,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   p.rec_mode = reinterpret_cast<u32*>(w + L.rec_mode);
   p.rec_bytes = reinterpret_cast<u64*>(w + L.rec_bytes);
   p.enc_off = reinterpret_cast<u64*>(w + L.enc_off);
+  p.rec_dst = p.enc_off;
   p.chunk_hi = reinterpret_cast<u32*>(w + L.chunk_hi);
   p.chunk_mode = reinterpret_cast<u32*>(w + L.chunk_mode);
   p.chunk_hioff = reinterpret_cast<u64*>(w + L.chunk_hioff);
@@ -317,21 +319,15 @@ int sync_buckets_bound(sync_ctx* x, uint64_t* bytes, sync_stream_t stream) {
   return SYNC_OK;
 }
 
-int sync_bucket_pack(sync_ctx* x, const uint8_t* d_enc, uint8_t* d_buckets, uint64_t buckets_cap,
-                     uint32_t* n_buckets, uint64_t* h_offsets, uint64_t* h_sizes, uint32_t max_buckets,
-                     sync_stream_t stream) {
-  if (!x || !n_buckets || !x->plan_valid) return SYNC_ERR_ARG;
-  if (!aligned16(d_buckets) || !aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
-  cudaStream_t s = (cudaStream_t)stream;
-  *n_buckets = 0;
-  int st = read_plan(x, s);
-  if (st) return st;
-  if (x->h_totals[kTotOverflow]) return SYNC_ERR_CAPACITY;
+// Greedy bucket plan (DESIGN C11) from the record sizes read back by read_plan():
+// fills x->h_recs / x->h_bks and the caller's offsets/sizes. Host-side bookkeeping only.
+static int plan_buckets(sync_ctx* x, uint64_t buckets_cap, uint32_t max_buckets, uint64_t* h_offsets,
+                        uint64_t* h_sizes, uint32_t* n_buckets, uint64_t* h_need) {
   const u32 T = x->d.T;
   const u64 L = x->cfg.bucket_limit;
   x->h_recs.clear();
   x->h_bks.clear();
-  // greedy (DESIGN C11): size(bucket) = 32 + pad16(8 n) + Σ record_bytes
+  // size(bucket) = 32 + pad16(8 n) + Σ record_bytes; a record never splits; an oversized record sits alone
   u64 base = 0;
   BucketDesc cur{};
   u64 cur_sum = 0;
@@ -363,6 +359,7 @@ int sync_bucket_pack(sync_ctx* x, const uint8_t* d_enc, uint8_t* d_buckets, uint
   }
   close();
   const u32 nb = (u32)x->h_bks.size();
+  if (h_need) *h_need = base;
   if (nb > max_buckets || base > buckets_cap) return SYNC_ERR_CAPACITY;
   for (u32 b = 0; b < nb; ++b) {
     const BucketDesc& bk = x->h_bks[b];
@@ -376,22 +373,73 @@ int sync_bucket_pack(sync_ctx* x, const uint8_t* d_enc, uint8_t* d_buckets, uint
     if (h_sizes) h_sizes[b] = bk.bytes;
   }
   *n_buckets = nb;
-  if (nb == 0) return SYNC_OK;
+  return SYNC_OK;
+}
+
+static int finish_buckets(sync_ctx* x, uint8_t* d_buckets, const uint8_t* d_enc, cudaStream_t s) {
+  const u32 nb = (u32)x->h_bks.size();
   RecordDesc* d_recs = reinterpret_cast<RecordDesc*>(x->ws + x->L.recs);
   BucketDesc* d_bks = reinterpret_cast<BucketDesc*>(x->ws + x->L.bks);
   CK(cudaMemcpyAsync(d_recs, x->h_recs.data(), sizeof(RecordDesc) * x->h_recs.size(), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(d_bks, x->h_bks.data(), sizeof(BucketDesc) * nb, cudaMemcpyHostToDevice, s));
-  launch_pack(d_enc, d_buckets, d_recs, (u32)x->h_recs.size(), d_bks, nb, x->h_totals[kTotEnc], x->cfg.flags,
-              x->grid, s);
+  launch_pack(d_enc, d_buckets, d_recs, (u32)x->h_recs.size(), d_bks, nb, d_enc ? x->h_totals[kTotEnc] : 0,
+              x->cfg.flags, x->grid, s);
   if (x->cfg.flags & SYNC_FLAG_CRC) {
     for (u32 b = 0; b < nb; ++b)
       if (crc_slots(x->h_bks[b].bytes) > x->d.crc_n) return SYNC_ERR_CAPACITY;
     crc_fill(d_buckets, x->h_bks.data(), nb, reinterpret_cast<u32*>(x->ws + x->L.crc), s);
   }
   CK(cudaGetLastError());
-  // the H2D copies read pageable host vectors: keep them valid until done
-  CK(cudaStreamSynchronize(s));
+  CK(cudaStreamSynchronize(s));  // the H2D copies read pageable host vectors: keep them valid until done
   return SYNC_OK;
+}
+
+int sync_bucket_pack(sync_ctx* x, const uint8_t* d_enc, uint8_t* d_buckets, uint64_t buckets_cap,
+                     uint32_t* n_buckets, uint64_t* h_offsets, uint64_t* h_sizes, uint32_t max_buckets,
+                     sync_stream_t stream) {
+  if (!x || !n_buckets || !x->plan_valid) return SYNC_ERR_ARG;
+  if (!aligned16(d_buckets) || !aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  *n_buckets = 0;
+  int st = read_plan(x, s);
+  if (st) return st;
+  if (x->h_totals[kTotOverflow]) return SYNC_ERR_CAPACITY;
+  st = plan_buckets(x, buckets_cap, max_buckets, h_offsets, h_sizes, n_buckets, nullptr);
+  if (st || *n_buckets == 0) return st;
+  return finish_buckets(x, d_buckets, d_enc, s);
+}
+
+int sync_compress_pack(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,
+                       uint8_t* d_buckets, uint64_t buckets_cap, uint32_t* n_buckets, uint64_t* h_offsets,
+                       uint64_t* h_sizes, uint32_t max_buckets, uint64_t* h_need, sync_stream_t stream) {
+  if (!x || !n_buckets || (x->d.T && !d_counts)) return SYNC_ERR_ARG;
+  if (!aligned16(d_buckets)) return SYNC_ERR_ALIGNMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  *n_buckets = 0;
+  if (h_need) *h_need = 0;
+  // plan (record sizes) exactly as sync_compress, without the encode
+  x->plan.enc_cap = ~0ull;
+  x->plan.rec_dst = x->plan.enc_off;
+  launch_plan_scan(x->plan, d_counts, s);
+  if (x->cfg.codec == SYNC_CODEC_COMPRESSED) launch_chunk_stats(x->plan, d_I, d_V, d_counts, 2 * x->grid, s);
+  launch_plan_sizes(x->plan, d_counts, s);
+  CK(cudaGetLastError());
+  x->plan_counts = d_counts;
+  x->plan_valid = true;
+  int st = read_plan(x, s);
+  if (st) return st;
+  if (x->h_totals[kTotOverflow]) return SYNC_ERR_CAPACITY;
+  st = plan_buckets(x, buckets_cap, max_buckets, h_offsets, h_sizes, n_buckets, h_need);
+  if (st || *n_buckets == 0) return st;
+  // each record is encoded straight into its bucket position (no staging copy)
+  x->h_rec_dst.assign(x->d.T, 0);
+  for (const RecordDesc& r : x->h_recs) x->h_rec_dst[r.tensor] = r.dst;
+  u64* d_dst = reinterpret_cast<u64*>(x->ws + x->L.rec_dst);
+  CK(cudaMemcpyAsync(d_dst, x->h_rec_dst.data(), 8ull * x->d.T, cudaMemcpyHostToDevice, s));
+  x->plan.rec_dst = d_dst;
+  launch_encode(x->plan, d_I, d_V, d_counts, d_buckets, 2 * x->grid, s);
+  x->plan.rec_dst = x->plan.enc_off;
+  return finish_buckets(x, d_buckets, nullptr, s);
 }
 
 // ------------------------------------------------------------------------ receive

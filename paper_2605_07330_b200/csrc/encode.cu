@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
     const bool last = (k + 1 == n_ch);
     const u32* Ir = c.Ir;
     const u16* Vc = c.Vc;
-    u8* rec = enc + p.enc_off[t];
+    u8* rec = enc + p.rec_dst[t];
     const u64 rb = p.rec_bytes[t];
     const u32 mode = p.rec_mode[t];
 

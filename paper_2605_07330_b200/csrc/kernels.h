@@ -23,6 +23,7 @@ struct Plan {
   uint32_t* rec_mode;            // [T] DELTA16 / ABS32
   uint64_t* rec_bytes;           // [T]
   uint64_t* enc_off;             // [T+1]
+  const uint64_t* rec_dst;       // [T] where k_encode writes record t (enc_off, or bucket positions)
   uint32_t* chunk_hi;            // [max_chunks] hi block bytes (unpadded)
   uint32_t* chunk_mode;          // [max_chunks]
   uint64_t* chunk_hioff;         // [max_chunks+1] exclusive prefix of pad4(chunk_hi)

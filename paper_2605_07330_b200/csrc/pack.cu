@@ -170,8 +170,8 @@ void launch_pack(const u8* enc, u8* buckets, const RecordDesc* recs, u32 n_recor
   if (n_buckets == 0) return;
   k_pack_meta<<<n_buckets, 256, 0, s>>>(buckets, recs, bks, flags);
   count_launch();
-  u64 n_units = enc_total / 16;
-  if (n_units) {
+  u64 n_units = enc_total / 16;  // 0 when the records were encoded in place (sync_compress_pack)
+  if (enc && n_units) {
     u64 need = (n_units + 255) / 256;
     int g = (int)(need < (u64)grid ? need : (u64)grid);
     k_pack_copy<<<g, 256, 0, s>>>(reinterpret_cast<const uint4*>(enc), buckets, recs, n_records, n_units);

@@ -48,11 +48,13 @@ class SparseSyncSender:
         self.cap = cap
         self.I = torch.empty(max(cap, 1), dtype=torch.int32, device=self.device)
         self.V = torch.empty(max(cap, 1), dtype=torch.int16, device=self.device)
-        enc0 = min(self.ctx.enc_bound, int(3.6 * cap) + 64 * len(self.numel) + 4096)
-        self.enc = torch.empty(enc0, dtype=torch.uint8, device=self.device)
+        self.enc = torch.empty(0, dtype=torch.uint8, device=self.device)  # only the unfused path uses it
 
-    # K1 + K2/K3
+    # K1 + K2/K3 (unfused path: contiguous encoded stream, then sync_bucket_pack copies it)
     def extract_compress(self, stream=None):
+        if self.enc.numel() == 0:
+            enc0 = min(self.ctx.enc_bound, int(3.6 * self.cap) + 64 * len(self.numel) + 4096)
+            self.enc = torch.empty(enc0, dtype=torch.uint8, device=self.device)
         self.ctx.sync_extract_batched(self.old_ptrs, self.new_ptrs, self.I, self.V, self.counts, stream)
         self.ctx.sync_compress(self.I, self.V, self.counts, self.enc, stream)
 
@@ -100,8 +102,32 @@ class SparseSyncSender:
             return
         self.ctx.sync_commit_snapshot_batched(self.old_ptrs, self.I, self.V, self.counts, stream)
 
-    def sync(self, stream=None):
+    def compress_pack(self, stream=None):
+        """Fused K2-K4 (sync_compress_pack): records encoded straight into their bucket positions."""
+        if self.buckets.numel() == 0:
+            self.buckets = torch.empty(int(3.5 * self.cap) + 64 * len(self.numel) + 4096, dtype=torch.uint8,
+                                       device=self.device)
+        for _ in range(3):
+            try:
+                self.bucket_list = self.ctx.sync_compress_pack(self.I, self.V, self.counts, self.buckets, stream)
+                return self.bucket_list
+            except SyncError as e:
+                if e.code != SYNC_ERR_CAPACITY:
+                    raise
+                self.ctx.sync_status(stream)  # clear the latched error
+                stats = self.ctx.stats(stream)
+                if stats["nnz"] > self.cap:   # more changes than I/V can hold: grow, extract again
+                    self._alloc(min(sum(self.numel), int(stats["nnz"] * 1.1) + 65536))
+                    self.ctx.sync_extract_batched(self.old_ptrs, self.new_ptrs, self.I, self.V, self.counts, stream)
+                elif getattr(e, "need", 0) > self.buckets.numel():
+                    self.buckets = torch.empty(int(e.need * 1.05) + 4096, dtype=torch.uint8, device=self.device)
+        raise SyncError(SYNC_ERR_CAPACITY, "sync_compress_pack: could not size the buffers")
+
+    def sync(self, stream=None, fused: bool = True):
         """extract + compress + pack; returns the bucket list. Call commit() once the buckets were delivered."""
+        if fused:
+            self.ctx.sync_extract_batched(self.old_ptrs, self.new_ptrs, self.I, self.V, self.counts, stream)
+            return self.compress_pack(stream)
         self.extract_compress(stream)
         return self.pack(stream)
 

@@ -106,14 +106,15 @@ def mixed_manifest():
     return synth.Manifest("mixed", T)
 
 
-def run_path(olds, news, codec, limit, crc, max_changed=None):
-    """GPU sender on device copies; returns (sender, receiver weights after apply, bucket bytes list)."""
+def run_path(olds, news, codec, limit, crc, max_changed=None, fused=True):
+    """GPU sender on device copies; returns (sender, receiver weights after apply, bucket bytes list).
+    fused: sync_compress_pack (records encoded in place) vs sync_compress + sync_bucket_pack."""
     old_d = [to_dev(o) for o in olds]
     new_d = [to_dev(n) for n in news]
     rol_d = [to_dev(o) for o in olds]
     snd = ss.SparseSyncSender(old_d, new_d, bucket_limit=limit, codec=codec, crc=crc, max_changed=max_changed)
     rcv = ss.SparseSyncReceiver(rol_d, bucket_limit=limit, codec=codec, crc=crc)
-    bl = snd.sync()
+    bl = snd.sync(fused=fused)
     got = [snd.bucket(b).cpu().numpy().tobytes() for b in range(len(bl))]
     for b in range(len(bl)):
         rcv.apply(snd.bucket(b))
@@ -128,11 +129,12 @@ def run_path(olds, news, codec, limit, crc, max_changed=None):
 @pytest.mark.parametrize("limit", [1024, 64 << 10, 1 << 30])
 @pytest.mark.parametrize("crc", [False, True])
 @pytest.mark.parametrize("rho,mask", [(0.01, synth.MASK_U), (0.2, synth.MASK_U), (0.02, synth.MASK_R)])
-def test_bucket_bytes_and_apply_bit_exact(codec, limit, crc, rho, mask):
+@pytest.mark.parametrize("fused", [True, False])
+def test_bucket_bytes_and_apply_bit_exact(codec, limit, crc, rho, mask, fused):
     m = mixed_manifest()
     olds, news = synth.generate(m, seed=1, rho=rho, mask=mask)
     ref = oracle.sync_pack(olds, news, codec=codec, limit=limit, crc=crc)
-    snd, old_d, rol_d, got = run_path(olds, news, codec, limit, crc)
+    snd, old_d, rol_d, got = run_path(olds, news, codec, limit, crc, fused=fused)
     assert len(got) == ref.n_buckets
     for b in range(ref.n_buckets):
         assert got[b] == ref.bucket(b), f"bucket {b} bytes differ"
