@@ -50,13 +50,17 @@ def parse():
     p.add_argument("--codec", choices=["compressed", "raw"], default="compressed")
     p.add_argument("--bucket-mb", type=float, default=256)
     p.add_argument("--crc", action="store_true")
-    p.add_argument("--topology", choices=["ring", "pair"], default="ring",
-                   help="ring: every rank is Trainer of its model + Rollout of rank r-1's; pair: ranks < N/2 are "
-                        "Trainers, rank t + N/2 is the Rollout of Trainer t (the paper's space-sharing layout)")
+    p.add_argument("--topology", choices=["ring", "pair", "fanout", "sharded"], default="ring",
+                   help="ring: every rank is Trainer of its model + Rollout of rank r-1's (weak scaling); "
+                        "pair: ranks < N/2 are Trainers of a whole model, rank t + N/2 its Rollout; "
+                        "fanout: N/2 Trainers each own a shard of ONE model, every Rollout holds the whole model "
+                        "and receives every Trainer's buckets (P:61); sharded: N/2 sharded Trainers, Rollout "
+                        "t + N/2 holds shard t (SURVEY 8(e) sharded Rollout)")
     p.add_argument("--commit", choices=["swap", "scatter"], default="swap",
                    help="snapshot commit: pointer swap of double-buffered trainer weights, or in-place scatter")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--latency-steps", type=int, default=5, help="barrier-separated syncs for per-update latency")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-elems", type=float, default=1.2e9)
@@ -161,10 +165,11 @@ class Dist:
             y = torch.empty_like(x)
             ops = [dist.P2POp(dist.isend, x, (self.rank + 1) % self.world),
                    dist.P2POp(dist.irecv, y, (self.rank - 1) % self.world)]
-            if self.world % 2 == 0:   # also the pair partner used by --topology pair
+            if self.world % 2 == 0:   # also every Trainer <-> Rollout pair of --topology pair/fanout/sharded
                 half = self.world // 2
-                peer = (self.rank + half) % self.world
-                ops += [dist.P2POp(dist.isend, x, peer), dist.P2POp(dist.irecv, y, peer)]
+                peers = range(half, self.world) if self.rank < half else range(half)
+                for peer in peers:
+                    ops += [dist.P2POp(dist.isend, x, peer), dist.P2POp(dist.irecv, y, peer)]
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
             torch.cuda.synchronize()
@@ -195,8 +200,12 @@ class Dist:
 
 # ============================================================================= our arm
 class Rank:
-    """State of one rank. ring: Trainer (X snapshot, Y current) of its own model + Rollout replica R of rank
-    r-1's model. pair: Trainer only (ranks < N/2) or Rollout only (rank t + N/2 replicates Trainer t)."""
+    """State of one rank.
+    ring:    Trainer (X snapshot, Y current) of its own model + Rollout replica R of rank r-1's model.
+    pair:    ranks < N/2 Trainers of a whole model; rank t + N/2 the Rollout of Trainer t.
+    fanout:  ranks < N/2 Trainers of shard t of ONE model; ranks >= N/2 Rollouts of the whole model,
+             applying every Trainer's buckets (one receiver per Trainer shard).
+    sharded: ranks < N/2 Trainers of shard t; rank t + N/2 the Rollout of shard t."""
 
     def __init__(self, args, d: Dist, manifest: synth.Manifest):
         import paper_2605_07330_b200 as ss
@@ -205,45 +214,72 @@ class Rank:
         self.ss, self.sg, self.d, self.args, self.m = ss, sg, d, args, manifest
         dev = d.dev
         W = d.world
-        if args.topology == "pair" and W % 2:
-            raise SystemExit("--topology pair needs an even number of GPUs")
+        topo = args.topology
+        if topo != "ring" and W % 2:
+            raise SystemExit(f"--topology {topo} needs an even number of GPUs")
         half = W // 2
-        self.is_trainer = args.topology == "ring" or d.rank < half
-        self.is_rollout = args.topology == "ring" or d.rank >= half
-        self.seed = args.seed + 1000 * d.rank
-        if args.topology == "ring":
-            peer_seed = args.seed + 1000 * ((d.rank - 1) % W)
-        else:
-            peer_seed = args.seed + 1000 * (d.rank - half)
+        self.is_trainer = topo == "ring" or d.rank < half
+        self.is_rollout = topo == "ring" or d.rank >= half
+        sharded_model = topo in ("fanout", "sharded")
+        self.shards = transport.shard_ranges(manifest.numel, half) if sharded_model else None
         codec = ss.SYNC_CODEC_COMPRESSED if args.codec == "compressed" else ss.SYNC_CODEC_RAW
         limit = int(args.bucket_mb * (1 << 20))
-        total = manifest.total
         self.X = self.Y = self.R = None
         self.sender = self.receiver = None
+        self.receivers = {}
         if self.is_trainer:
-            self.X, self.Xv = sg.arena(manifest, dev)   # trainer snapshot (swaps with Y under --commit swap)
-            self.Y, self.Yv = sg.arena(manifest, dev)   # trainer current weights
-            sg.fill_old(self.Xv, manifest, self.seed)
-            sg.fill_new(self.Xv, self.Yv, manifest, self.seed, args.rho, MASKS[args.mask])
+            if sharded_model:
+                lo, hi = self.shards[d.rank]
+                mt, tid0, self.seed = manifest.slice(lo, hi, f"{manifest.name}[shard {d.rank}/{half}]"), lo, args.seed
+            else:
+                mt, tid0, self.seed = manifest, 0, args.seed + 1000 * d.rank
+            self.mt = mt
+            total = mt.total
+            self.X, self.Xv = sg.arena(mt, dev)   # trainer snapshot (swaps with Y under --commit swap)
+            self.Y, self.Yv = sg.arena(mt, dev)   # trainer current weights
+            sg.fill_old(self.Xv, mt, self.seed, tid0=tid0)
+            sg.fill_new(self.Xv, self.Yv, mt, self.seed, args.rho, MASKS[args.mask], tid0=tid0)
             self.sender = ss.SparseSyncSender(self.Xv, self.Yv, bucket_limit=limit, codec=codec, crc=args.crc,
                                               max_changed=min(total, int(total * args.rho * 1.02) + (1 << 20)))
         if self.is_rollout:
-            self.R, self.Rv = sg.arena(manifest, dev)
-            sg.fill_old(self.Rv, manifest, peer_seed)
-            self.receiver = ss.SparseSyncReceiver(self.Rv, bucket_limit=limit, codec=codec, crc=args.crc)
+            if topo == "ring":
+                mr, tid0, rseed = manifest, 0, args.seed + 1000 * ((d.rank - 1) % W)
+            elif topo == "pair":
+                mr, tid0, rseed = manifest, 0, args.seed + 1000 * (d.rank - half)
+            elif topo == "fanout":
+                mr, tid0, rseed = manifest, 0, args.seed
+            else:
+                lo, hi = self.shards[d.rank - half]
+                mr, tid0, rseed = manifest.slice(lo, hi), lo, args.seed
+            self.mr = mr
+            self.R, self.Rv = sg.arena(mr, dev)
+            sg.fill_old(self.Rv, mr, rseed, tid0=tid0)
+            if topo == "fanout":   # one receiver per Trainer shard: its records carry shard-local tensor ids
+                for t, (lo, hi) in enumerate(self.shards):
+                    self.receivers[t] = ss.SparseSyncReceiver(self.Rv[lo:hi], bucket_limit=limit, codec=codec,
+                                                              crc=args.crc)
+            else:
+                self.receiver = ss.SparseSyncReceiver(self.Rv, bucket_limit=limit, codec=codec, crc=args.crc)
         torch.cuda.synchronize()
         self.link = None
         if W > 1:
-            if args.topology == "ring":
+            if topo == "ring":
                 # under --commit swap the sender's I array is dead between pack and the next extract:
                 # receive the peer's buckets into it (saves a payload-sized buffer at 30B / 183 GB of arenas)
                 rb = self.sender.I.view(torch.uint8) if args.commit == "swap" else None
                 self.link = transport.RingLink(d.rank, W, dev, d.ctrl, recv_buf=rb)
+            elif topo == "fanout":
+                self.link = transport.FanoutLink(d.rank, W, dev, trainers=list(range(half)),
+                                                 rollouts=list(range(half, W)), ctrl=d.ctrl)
             else:
                 t = d.rank if self.is_trainer else d.rank - half
                 self.link = transport.PairLink(d.rank, W, dev, trainer=t, rollout=t + half, ctrl=d.ctrl)
-        self.toggle_scratch = torch.empty(len(manifest.tensors) + 1, dtype=torch.int64, device=dev)
-        self.S = 2 * total if self.is_trainer else 0   # weights this rank syncs per step (as the sender)
+        ntens = len(self.mt.tensors) if self.is_trainer else 1
+        self.toggle_scratch = torch.empty(ntens + 1, dtype=torch.int64, device=dev)
+        self.S = 2 * self.mt.total if self.is_trainer else 0   # weights this rank syncs per step (as the sender)
+
+    def receivers_all(self):
+        return ([self.receiver] if self.receiver is not None else []) + list(self.receivers.values())
 
     def step(self, ev=None):
         """One sync. ev: list of 7 CUDA events recorded between the phases (or None)."""
@@ -254,6 +290,8 @@ class Rank:
         if snd is not None:
             snd.ctx.sync_extract_batched(snd.old_ptrs, snd.new_ptrs, snd.I, snd.V, snd.counts)
             rec(1)
+            if self.link is not None:
+                self.link.fence()         # the previous sync's sends have left the bucket buffer
             blist = snd.compress_pack()   # fused K2-K4 (blocking: host bucket plan)
             rec(2)
             rec(3)
@@ -261,15 +299,18 @@ class Rank:
             rec(1)
             rec(2)
             rec(3)
-        if self.link is None:
+        L, T = self.link, self.ss.transport
+        if L is None:
             for b in range(len(blist)):
                 rcv.apply(snd.bucket(b))
-        elif isinstance(self.link, self.ss.transport.RingLink):
-            self.link.exchange(snd.buckets, blist, rcv.apply)
+        elif isinstance(L, T.RingLink):
+            L.exchange(snd.buckets, blist, rcv.apply)
         elif snd is not None:
-            self.link.send(snd.buckets, blist)
+            L.send(snd.buckets, blist)
+        elif isinstance(L, T.FanoutLink):
+            L.receive({t: self.receivers[t].apply for t in self.receivers})
         else:
-            self.link.receive(rcv.apply)
+            L.receive(rcv.apply)
         rec(4)
         if snd is not None:
             snd.commit(mode=self.args.commit)
@@ -279,11 +320,23 @@ class Rank:
         if snd is not None and self.args.commit == "scatter":
             # snapshot == current now: the synthetic "optimizer step" flips the changed bits again so the
             # next sync has a fresh update of the same density (write-only scatter, input generation)
-            self.sg.toggle(snd.new_ptrs, snd.I, snd.V, snd.counts, len(self.m.tensors), self.toggle_scratch)
+            self.sg.toggle(snd.new_ptrs, snd.I, snd.V, snd.counts, len(self.mt.tensors), self.toggle_scratch)
         # under --commit swap the two trainer buffers hold the two model versions v0 / v1 and trade roles
         # every step, so every step syncs a genuine update (v0 -> v1, then v1 -> v0) with no generator work
         rec(6)
         return blist
+
+    def digests(self):
+        """(trainer snapshot digest, [rollout digests per shard or whole]) for the bit-exact check."""
+        mine_x = chunked_digest(self.X) if self.X is not None else None
+        mine_r = None
+        if self.R is not None:
+            if self.args.topology == "fanout":
+                offs = np.cumsum([0] + self.mr.numel)
+                mine_r = [chunked_digest(self.R[int(offs[lo]):int(offs[hi])]) for lo, hi in self.shards]
+            else:
+                mine_r = chunked_digest(self.R)
+        return mine_x, mine_r
 
 
 def chunked_digest(t: torch.Tensor, chunk: int = 1 << 24) -> tuple:
@@ -369,12 +422,16 @@ def run_ours(args):
     for _ in range(args.warmup):
         r.step()
     torch.cuda.synchronize()
+    nnz = payload = nb = raw_payload = vbytes = n16 = n32 = 0
     if r.sender is not None:   # rank 0 is always a Trainer
         st = r.sender.ctx.sync_status()
         assert st == 0, f"sender status {st}"
         stats = r.sender.stats()
         nb = len(r.sender.bucket_list)
         payload = sum(s for _, s in r.sender.bucket_list)
+        nnz, vbytes, n16, n32 = stats["nnz"], stats["value_bytes"], stats["n_delta16"], stats["n_abs32"]
+        raw_payload = sum(((16 + 6 * c + 15) // 16) * 16 for c in r.sender.counts.cpu().tolist() if c) + 48 * max(nb, 1)
+    local_alg_extract = 2 * r.S + 6 * nnz
 
     # ---- timed region
     K = args.steps
@@ -391,8 +448,8 @@ def run_ours(args):
     t_end.record()
     d.barrier()
     clk = clocks.stop()
-    launches = ss.launch_count() - launches0 + (2 * K if args.commit == "scatter" else 0)  # + toggle kernels
-    launches = int(d.sum(launches))
+    launches = ss.launch_count() - launches0 + (K if args.commit == "scatter" and r.sender is not None else 0)
+    launches = int(d.sum(launches))   # + the toggle kernels under --commit scatter
     ms_local = t_start.elapsed_time(t_end)
     ms = d.max(ms_local)
     phases = np.zeros(6)
@@ -400,27 +457,44 @@ def run_ours(args):
         for i in range(6):
             phases[i] += evs[k][i].elapsed_time(evs[k][i + 1])
     phases /= K
+    ext_ms_local = phases[0]
     if d.world > 1:  # per phase, the max over ranks (pair: extract on Trainers, apply on Rollouts)
         g = [None] * d.world
         d.dist.all_gather_object(g, phases.tolist(), group=d.ctrl)
         phases = np.max(np.array(g), axis=0)
     st_s = r.sender.ctx.sync_status() if r.sender is not None else 0
-    st_r = r.receiver.ctx.sync_status() if r.receiver is not None else 0
-    assert st_s == 0 and st_r == 0, f"status sender {st_s} receiver {st_r}"
+    st_r = [x.ctx.sync_status() for x in r.receivers_all()]
+    assert st_s == 0 and not any(st_r), f"status sender {st_s} receivers {st_r}"
 
-    # ---- verification: rollout replica == peer's committed snapshot (bit-exact)
+    # ---- per-update latency (SURVEY §8(d) timing protocol): barrier, then one sync; max over ranks of
+    #      (start -> this rank's last kernel of the sync: commit on a Trainer, apply on a Rollout)
+    lat = []
+    for _ in range(args.latency_steps):
+        d.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r.step()
+        e1.record()
+        torch.cuda.synchronize()
+        lat.append(d.max(e0.elapsed_time(e1)))
+    latency = ({"median_ms": round(float(np.median(lat)), 4), "best_ms": round(float(min(lat)), 4),
+                "syncs": len(lat), "what": "one sync after a barrier, max over ranks (extract start -> last "
+                                           "apply/commit)"} if lat else None)
+
+    # ---- verification: rollout replica == the Trainer's committed snapshot (bit-exact)
     verify = None
     if not args.no_verify:
-        mine_x = chunked_digest(r.X) if r.X is not None else None
-        mine_r = chunked_digest(r.R) if r.R is not None else None
+        mine = r.digests()
         if d.world == 1:
-            verify = mine_x == mine_r
+            verify = mine[0] == mine[1]
         else:
             g = [None] * d.world
-            d.dist.all_gather_object(g, (mine_x, mine_r), group=d.ctrl)
+            d.dist.all_gather_object(g, mine, group=d.ctrl)
             W, half = d.world, d.world // 2
             if args.topology == "ring":
                 verify = all(g[(i - 1) % W][0] == g[i][1] for i in range(W))
+            elif args.topology == "fanout":
+                verify = all(g[rr][1][t] == g[t][0] for rr in range(half, W) for t in range(half))
             else:
                 verify = all(g[t][0] == g[t + half][1] for t in range(half))
 
@@ -431,10 +505,9 @@ def run_ours(args):
 
     total_S = d.sum(r.S)
     value = total_S * K / (ms / 1e3) / 1e9
-    nnz = stats["nnz"]
-    alg_bytes_extract = 2 * r.S + 6 * nnz
-    ext_ms = phases[0]
-    achieved = alg_bytes_extract / (ext_ms / 1e3) / 1e9
+    nnz_t, payload_t, raw_t = d.sum(nnz), d.sum(payload), d.sum(raw_payload)
+    vbytes_t, n16_t, n32_t, nb_t = d.sum(vbytes), d.sum(n16), d.sum(n32), d.sum(nb)
+    achieved = local_alg_extract / (ext_ms_local / 1e3) / 1e9   # rank 0 (a Trainer), its own launch
     peak = peaks.get("hbm_gbs", 6650.0)
     # ncu dram bytes / algorithmic bytes of the profiled extract launch (profiles/extract_traffic.json,
     # from `ncu --set full` on the 30b-slice workload), applied to this launch's algorithmic bytes
@@ -443,39 +516,47 @@ def run_ours(args):
     if os.path.exists(tf):
         try:
             ratio = json.load(open(tf))["ratio"]
-            traffic = int(round(ratio * alg_bytes_extract))
+            traffic = int(round(ratio * local_alg_extract))
             traffic_src = f"ncu --set full dram__bytes_read+write / algorithmic = {ratio:.4f} (30b-slice launch)"
         except Exception:
             traffic = None
-    raw_payload = sum(((16 + 6 * c + 15) // 16) * 16 for c in r.sender.counts.cpu().tolist() if c) + 48 * max(nb, 1)
+    topo_txt = {
+        "ring": "ring: rank r = Trainer of its model + Rollout replica of rank r-1 (N=1: loopback)",
+        "pair": "pair: ranks < N/2 Trainers of a whole model, rank t+N/2 = Rollout of Trainer t (NCCL P2P)",
+        "fanout": "fanout: N/2 Trainers own element-balanced shards of one model; each of the N/2 Rollouts holds "
+                  "the whole model and applies every Trainer's buckets (NCCL P2P fan-out, P:61)",
+        "sharded": "sharded: N/2 Trainers own shards of one model; Rollout t+N/2 holds shard t (NCCL P2P)",
+    }[args.topology]
+    strong = args.topology in ("fanout", "sharded")
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": d.world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": round(ms / K, 4), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms / K, 4), "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "u16 (bf16 bit patterns; integer/bit work only)",
         "data": "synthetic: random-init bf16 weights of the named architecture (N(0,0.02) quantile table), "
                 f"{args.mask}-mask sparse perturbations, seeded",
         "config": {"workload": f"{manifest.name} bf16, {100 * (1 - args.rho):.1f}% sparsity, {args.mask} mask",
                    "topology_mode": args.topology,
-                   "elements_per_rank": manifest.total, "tensors": len(manifest.tensors),
+                   "elements_per_trainer_rank": r.S // 2, "model_elements": manifest.total,
+                   "tensors": len(manifest.tensors),
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
-                   "topology": ("ring: rank r = Trainer of its model + Rollout replica of rank r-1 (N=1: loopback)"
-                                if args.topology == "ring" else
-                                "pair: ranks < N/2 Trainers, rank t+N/2 = Rollout of Trainer t (NCCL P2P)"),
-                   "l2": "inputs (2x61 GB) larger than L2; no flush"},
+                   "topology": topo_txt,
+                   "l2": "inputs larger than L2 (2 x S per Trainer); no flush"},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
                          zip(["extract", "compress_pack", None, "transfer_apply", "commit", "synthetic_update"],
                              phases) if n},
         "roofline": {"bound": "hbm", "kernel": "k_extract (K1)", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "bytes_per_launch": alg_bytes_extract, "traffic_source": traffic_src,
+                     "bytes_per_launch": local_alg_extract, "traffic_source": traffic_src,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
-        "payload": {"nnz": nnz, "rho_measured": round(nnz / manifest.total, 6), "buckets": nb,
-                    "bytes": payload, "x_comp": round(r.S / max(payload, 1), 2),
-                    "x_raw_eq1": round(r.S / raw_payload, 2),
-                    "alpha": round(stats["value_bytes"] / max(2 * nnz, 1), 4),
-                    "delta16_records": stats["n_delta16"], "abs32_records": stats["n_abs32"],
+        "payload": {"nnz": int(nnz_t), "rho_measured": round(nnz_t / max(total_S / 2, 1), 6), "buckets": int(nb_t),
+                    "bytes": int(payload_t), "x_comp": round(total_S / max(payload_t, 1), 2),
+                    "x_raw_eq1": round(total_S / max(raw_t, 1), 2),
+                    "alpha": round(vbytes_t / max(2 * nnz_t, 1), 4),
+                    "delta16_records": int(n16_t), "abs32_records": int(n32_t),
                     "paper_context": "paper: 32-54x raw, ~60-101x compressed on H100 clusters (P:22, P:380)"},
         "clocks": clk, "gpu_launches": int(launches), "bit_exact_replica": verify, "e2e": e2e,
+        "latency_per_update": latency,
     }
     if parity is not None:
         out["parity_sampled"] = parity
@@ -498,7 +579,7 @@ def run_e2e(args, d: Dist, r: Rank):
         avail = psutil.virtual_memory().available
     except Exception:
         avail = 0
-    n_trainers = d.world if args.topology == "ring" else d.world // 2
+    n_trainers = d.world if args.topology == "ring" else d.world // 2   # pinned buffers live on one host
     ok = int(d.sum(1.0 if (avail - 24e9) / max(1, n_trainers) > n_need or r.sender is None else 0.0)) == d.world
     if not ok:
         return {"value": None, "unit": UNIT,
@@ -531,9 +612,10 @@ def run_e2e(args, d: Dist, r: Rank):
     d.barrier()
     ms = d.max(t0.elapsed_time(t1))
     total_S = d.sum(r.S)
+    d2h = d.sum(8 * r.sender.counts.numel() if r.sender is not None else 0)
     del hosts
     return {"value": round(total_S * K / (ms / 1e3) / 1e9, 3), "unit": UNIT,
-            "h2d_bytes_per_step": int(r.S), "d2h_bytes_per_step": int(8 * r.sender.counts.numel()),
+            "h2d_bytes_per_step": int(total_S), "d2h_bytes_per_step": int(d2h),
             "steps": K, "ms_per_step": round(ms / K, 3)}
 
 
