@@ -58,6 +58,11 @@ def parse():
                         "t + N/2 holds shard t (SURVEY 8(e) sharded Rollout)")
     p.add_argument("--commit", choices=["swap", "scatter"], default="swap",
                    help="snapshot commit: pointer swap of double-buffered trainer weights, or in-place scatter")
+    p.add_argument("--transport", choices=["nccl", "peer", "peer-direct"], default="peer",
+                   help="bucket data plane: NCCL P2P, NVLink peer memory pulled by the copy engines, or decoded "
+                        "in place from peer memory by the decode kernel")
+    p.add_argument("--groups", type=int, default=0,
+                   help="tensor groups per Trainer, pipelined through transfer/apply (0: 1 for ring, 4 otherwise)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--latency-steps", type=int, default=5, help="barrier-separated syncs for per-update latency")
@@ -205,12 +210,15 @@ class Rank:
     pair:    ranks < N/2 Trainers of a whole model; rank t + N/2 the Rollout of Trainer t.
     fanout:  ranks < N/2 Trainers of shard t of ONE model; ranks >= N/2 Rollouts of the whole model,
              applying every Trainer's buckets (one receiver per Trainer shard).
-    sharded: ranks < N/2 Trainers of shard t; rank t + N/2 the Rollout of shard t."""
+    sharded: ranks < N/2 Trainers of shard t; rank t + N/2 the Rollout of shard t.
+    Every Trainer's tensors are split into G groups (--groups): group g's buckets travel and are applied
+    while group g+1 is extracted (bucket pipelining)."""
 
     def __init__(self, args, d: Dist, manifest: synth.Manifest):
         import paper_2605_07330_b200 as ss
         import synth.gpu as sg
         from paper_2605_07330_b200 import transport
+        from paper_2605_07330_b200.sync import GroupedReceiver, GroupedSender
         self.ss, self.sg, self.d, self.args, self.m = ss, sg, d, args, manifest
         dev = d.dev
         W = d.world
@@ -218,15 +226,16 @@ class Rank:
         if topo != "ring" and W % 2:
             raise SystemExit(f"--topology {topo} needs an even number of GPUs")
         half = W // 2
+        self.G = args.groups if args.groups > 0 else (1 if topo == "ring" else 4)
         self.is_trainer = topo == "ring" or d.rank < half
         self.is_rollout = topo == "ring" or d.rank >= half
         sharded_model = topo in ("fanout", "sharded")
         self.shards = transport.shard_ranges(manifest.numel, half) if sharded_model else None
         codec = ss.SYNC_CODEC_COMPRESSED if args.codec == "compressed" else ss.SYNC_CODEC_RAW
-        limit = int(args.bucket_mb * (1 << 20))
+        kw = dict(bucket_limit=int(args.bucket_mb * (1 << 20)), codec=codec, crc=args.crc)
         self.X = self.Y = self.R = None
-        self.sender = self.receiver = None
-        self.receivers = {}
+        self.sender = None
+        self.receivers = {}    # source rank -> GroupedReceiver
         if self.is_trainer:
             if sharded_model:
                 lo, hi = self.shards[d.rank]
@@ -239,35 +248,42 @@ class Rank:
             self.Y, self.Yv = sg.arena(mt, dev)   # trainer current weights
             sg.fill_old(self.Xv, mt, self.seed, tid0=tid0)
             sg.fill_new(self.Xv, self.Yv, mt, self.seed, args.rho, MASKS[args.mask], tid0=tid0)
-            self.sender = ss.SparseSyncSender(self.Xv, self.Yv, bucket_limit=limit, codec=codec, crc=args.crc,
-                                              max_changed=min(total, int(total * args.rho * 1.02) + (1 << 20)))
+            self.sender = GroupedSender(self.Xv, self.Yv, groups=self.G,
+                                        max_changed=min(total, int(total * args.rho * 1.02) + (1 << 20)), **kw)
         if self.is_rollout:
             if topo == "ring":
+                srcs = {(d.rank - 1) % W: (0, len(manifest.tensors))}
                 mr, tid0, rseed = manifest, 0, args.seed + 1000 * ((d.rank - 1) % W)
             elif topo == "pair":
+                srcs = {d.rank - half: (0, len(manifest.tensors))}
                 mr, tid0, rseed = manifest, 0, args.seed + 1000 * (d.rank - half)
             elif topo == "fanout":
+                srcs = {t: self.shards[t] for t in range(half)}
                 mr, tid0, rseed = manifest, 0, args.seed
             else:
                 lo, hi = self.shards[d.rank - half]
+                srcs = {d.rank - half: (0, hi - lo)}
                 mr, tid0, rseed = manifest.slice(lo, hi), lo, args.seed
             self.mr = mr
             self.R, self.Rv = sg.arena(mr, dev)
             sg.fill_old(self.Rv, mr, rseed, tid0=tid0)
-            if topo == "fanout":   # one receiver per Trainer shard: its records carry shard-local tensor ids
-                for t, (lo, hi) in enumerate(self.shards):
-                    self.receivers[t] = ss.SparseSyncReceiver(self.Rv[lo:hi], bucket_limit=limit, codec=codec,
-                                                              crc=args.crc)
-            else:
-                self.receiver = ss.SparseSyncReceiver(self.Rv, bucket_limit=limit, codec=codec, crc=args.crc)
+            # one receiver per source Trainer (its records carry ids local to its shard and group)
+            for src, (lo, hi) in srcs.items():
+                self.receivers[src] = GroupedReceiver(self.Rv[lo:hi], groups=self.G, **kw)
         torch.cuda.synchronize()
         self.link = None
-        if W > 1:
+        if W > 1 and args.transport != "nccl":
             if topo == "ring":
-                # under --commit swap the sender's I array is dead between pack and the next extract:
-                # receive the peer's buckets into it (saves a payload-sized buffer at 30B / 183 GB of arenas)
-                rb = self.sender.I.view(torch.uint8) if args.commit == "swap" else None
-                self.link = transport.RingLink(d.rank, W, dev, d.ctrl, recv_buf=rb)
+                dsts, srcs = [(d.rank + 1) % W], [(d.rank - 1) % W]
+            elif topo == "fanout":
+                dsts, srcs = (list(range(half, W)), []) if self.is_trainer else ([], list(range(half)))
+            else:
+                dsts, srcs = ([d.rank + half], []) if self.is_trainer else ([], [d.rank - half])
+            self.link = transport.PeerLink(d.rank, W, dev, dsts, srcs, ctrl=d.ctrl,
+                                           mode="direct" if args.transport == "peer-direct" else "copy")
+        elif W > 1:
+            if topo == "ring":
+                self.link = transport.RingLink(d.rank, W, dev, d.ctrl)
             elif topo == "fanout":
                 self.link = transport.FanoutLink(d.rank, W, dev, trainers=list(range(half)),
                                                  rollouts=list(range(half, W)), ctrl=d.ctrl)
@@ -279,63 +295,85 @@ class Rank:
         self.S = 2 * self.mt.total if self.is_trainer else 0   # weights this rank syncs per step (as the sender)
 
     def receivers_all(self):
-        return ([self.receiver] if self.receiver is not None else []) + list(self.receivers.values())
+        return [p for g in self.receivers.values() for p in g.parts]
+
+    def n_events(self):
+        return 3 * self.G + 4
 
     def step(self, ev=None):
-        """One sync. ev: list of 7 CUDA events recorded between the phases (or None)."""
-        snd, rcv = self.sender, self.receiver
+        """One sync. ev: n_events() CUDA events: per group (extract start, extract end, compress end), then
+        transfer/apply end, commit end, update end, and a spare."""
+        snd = self.sender
         rec = (lambda i: ev[i].record()) if ev else (lambda i: None)
-        rec(0)
-        blist = []
+        L, T, a = self.link, self.ss.transport, self.args
+        G = self.G
+        ring = a.topology == "ring"
+        ring_swap = ring and a.commit == "swap"
+        for g in range(G):
+            rec(3 * g)
+            if snd is not None:
+                p = snd.parts[g]
+                p.ctx.sync_extract_batched(p.old_ptrs, p.new_ptrs, p.I, p.V, p.counts)
+                rec(3 * g + 1)
+                if L is not None:
+                    L.fence(g)            # the previous sync's sends of group g have left its bucket buffer
+                blist = p.compress_pack()  # fused K2-K4 (blocking: host bucket plan)
+                rec(3 * g + 2)
+                if L is None:             # N = 1: the ring closes on itself
+                    rcv = self.receivers[0].parts[g]
+                    for b in range(len(blist)):
+                        rcv.apply(p.bucket(b))
+                elif ring:
+                    # under --commit swap group g's I array is dead until the next extract of group g:
+                    # receive the peer's group-g buckets into it (saves payload-sized buffers at 183 GB of arenas)
+                    src = (self.d.rank - 1) % self.d.world
+                    L.exchange(p.buckets, blist, self.receivers[src].parts[g].apply, tag=g,
+                               recv_buf=p.I.view(torch.uint8) if ring_swap else None)
+                else:
+                    L.send(p.buckets, blist, tag=g)
+            else:
+                rec(3 * g + 1)
+                rec(3 * g + 2)
+                if isinstance(L, (T.FanoutLink, T.PeerLink)):
+                    L.receive({t: self.receivers[t].parts[g].apply for t in self.receivers}, tag=g)
+                else:
+                    src = next(iter(self.receivers))
+                    L.receive(self.receivers[src].parts[g].apply, tag=g)
+        rec(3 * G)
         if snd is not None:
-            snd.ctx.sync_extract_batched(snd.old_ptrs, snd.new_ptrs, snd.I, snd.V, snd.counts)
-            rec(1)
-            if self.link is not None:
-                self.link.fence()         # the previous sync's sends have left the bucket buffer
-            blist = snd.compress_pack()   # fused K2-K4 (blocking: host bucket plan)
-            rec(2)
-            rec(3)
-        else:
-            rec(1)
-            rec(2)
-            rec(3)
-        L, T = self.link, self.ss.transport
-        if L is None:
-            for b in range(len(blist)):
-                rcv.apply(snd.bucket(b))
-        elif isinstance(L, T.RingLink):
-            L.exchange(snd.buckets, blist, rcv.apply)
-        elif snd is not None:
-            L.send(snd.buckets, blist)
-        elif isinstance(L, T.FanoutLink):
-            L.receive({t: self.receivers[t].apply for t in self.receivers})
-        else:
-            L.receive(rcv.apply)
-        rec(4)
-        if snd is not None:
-            snd.commit(mode=self.args.commit)
-            if self.args.commit == "swap":
+            snd.commit(mode=a.commit)
+            if a.commit == "swap":
                 self.X, self.Y, self.Xv, self.Yv = self.Y, self.X, self.Yv, self.Xv
-        rec(5)
-        if snd is not None and self.args.commit == "scatter":
+        rec(3 * G + 1)
+        if snd is not None and a.commit == "scatter":
             # snapshot == current now: the synthetic "optimizer step" flips the changed bits again so the
             # next sync has a fresh update of the same density (write-only scatter, input generation)
-            self.sg.toggle(snd.new_ptrs, snd.I, snd.V, snd.counts, len(self.mt.tensors), self.toggle_scratch)
+            for p in snd.parts:
+                self.sg.toggle(p.new_ptrs, p.I, p.V, p.counts, len(p.numel), self.toggle_scratch)
         # under --commit swap the two trainer buffers hold the two model versions v0 / v1 and trade roles
         # every step, so every step syncs a genuine update (v0 -> v1, then v1 -> v0) with no generator work
-        rec(6)
-        return blist
+        rec(3 * G + 2)
+
+    def phase_ms(self, ev):
+        """extract, compress_pack (summed over groups), transfer_apply (the rest of the sync loop on this
+        rank's stream: waiting for and applying buckets), commit, synthetic_update."""
+        G = self.G
+        t = lambda i, j: ev[i].elapsed_time(ev[j])  # noqa: E731
+        ext = sum(t(3 * g, 3 * g + 1) for g in range(G))
+        cmp = sum(t(3 * g + 1, 3 * g + 2) for g in range(G))
+        return [ext, cmp, t(0, 3 * G) - ext - cmp, t(3 * G, 3 * G + 1), t(3 * G + 1, 3 * G + 2)]
 
     def digests(self):
-        """(trainer snapshot digest, [rollout digests per shard or whole]) for the bit-exact check."""
+        """(trainer snapshot digest, {source: rollout digest of that source's range}) for the bit-exact check."""
         mine_x = chunked_digest(self.X) if self.X is not None else None
         mine_r = None
         if self.R is not None:
-            if self.args.topology == "fanout":
-                offs = np.cumsum([0] + self.mr.numel)
-                mine_r = [chunked_digest(self.R[int(offs[lo]):int(offs[hi])]) for lo, hi in self.shards]
-            else:
-                mine_r = chunked_digest(self.R)
+            mine_r = {}
+            for src, gr in self.receivers.items():
+                w = gr.parts[0].weights[0]
+                lo = (w.data_ptr() - self.R.data_ptr()) // 2
+                n = sum(sum(x.numel() for x in p.weights) for p in gr.parts)
+                mine_r[src] = chunked_digest(self.R[lo:lo + n])
         return mine_x, mine_r
 
 
@@ -410,12 +448,14 @@ def run_ours(args):
         gen_ok = all(np.array_equal(r.Xv[k].cpu().numpy().view(np.uint16), cpu["olds"][k]) and
                      np.array_equal(r.Yv[k].cpu().numpy().view(np.uint16), cpu["news"][k])
                      for k in range(min(cpu["k"], 64)))
-        blist = r.sender.sync()
-        gpu_recs = parse_records([r.sender.bucket(b).cpu().numpy().tobytes() for b in range(len(blist))])
+        p0 = r.sender.parts[0]   # group 0 starts at tensor 0: its record ids are the oracle's
+        p0.sync()
+        gpu_recs = parse_records([p0.bucket(b).cpu().numpy().tobytes() for b in range(len(p0.bucket_list))])
         ora_recs = parse_records([cpu["pack"].bucket(b) for b in range(cpu["pack"].n_buckets)])
-        same = all(gpu_recs.get(t) == v for t, v in ora_recs.items())
-        parity = {"records_checked": len(ora_recs), "bit_exact": bool(same and gen_ok),
-                  "sample": f"records of the first {cpu['k']} tensors vs the oracle"}
+        n0 = r.sender.ranges[0][1]
+        same = all(gpu_recs.get(t) == v for t, v in ora_recs.items() if t < n0)
+        parity = {"records_checked": sum(1 for t in ora_recs if t < n0), "bit_exact": bool(same and gen_ok),
+                  "sample": f"records of the first {min(cpu['k'], n0)} tensors vs the oracle"}
         del cpu["olds"], cpu["news"]
 
     # ---- warmup (also sizes every buffer)
@@ -424,18 +464,20 @@ def run_ours(args):
     torch.cuda.synchronize()
     nnz = payload = nb = raw_payload = vbytes = n16 = n32 = 0
     if r.sender is not None:   # rank 0 is always a Trainer
-        st = r.sender.ctx.sync_status()
-        assert st == 0, f"sender status {st}"
+        st = [p.ctx.sync_status() for p in r.sender.parts]
+        assert not any(st), f"sender status {st}"
         stats = r.sender.stats()
-        nb = len(r.sender.bucket_list)
-        payload = sum(s for _, s in r.sender.bucket_list)
+        bl = [x for p in r.sender.parts for x in p.bucket_list]
+        nb = len(bl)
+        payload = sum(z for _, z in bl)
         nnz, vbytes, n16, n32 = stats["nnz"], stats["value_bytes"], stats["n_delta16"], stats["n_abs32"]
-        raw_payload = sum(((16 + 6 * c + 15) // 16) * 16 for c in r.sender.counts.cpu().tolist() if c) + 48 * max(nb, 1)
+        counts = [c for p in r.sender.parts for c in p.counts.cpu().tolist()]
+        raw_payload = sum(((16 + 6 * c + 15) // 16) * 16 for c in counts if c) + 48 * max(nb, 1)
     local_alg_extract = 2 * r.S + 6 * nnz
 
     # ---- timed region
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(K)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(r.n_events())] for _ in range(K)]
     launches0 = ss.launch_count()
     clocks = Clocks(d.local)
     clocks.start()
@@ -448,23 +490,19 @@ def run_ours(args):
     t_end.record()
     d.barrier()
     clk = clocks.stop()
-    launches = ss.launch_count() - launches0 + (K if args.commit == "scatter" and r.sender is not None else 0)
+    launches = ss.launch_count() - launches0 + (K * r.G if args.commit == "scatter" and r.sender is not None else 0)
     launches = int(d.sum(launches))   # + the toggle kernels under --commit scatter
     ms_local = t_start.elapsed_time(t_end)
     ms = d.max(ms_local)
-    phases = np.zeros(6)
-    for k in range(K):
-        for i in range(6):
-            phases[i] += evs[k][i].elapsed_time(evs[k][i + 1])
-    phases /= K
+    phases = np.mean([r.phase_ms(e) for e in evs], axis=0)
     ext_ms_local = phases[0]
     if d.world > 1:  # per phase, the max over ranks (pair: extract on Trainers, apply on Rollouts)
         g = [None] * d.world
         d.dist.all_gather_object(g, phases.tolist(), group=d.ctrl)
         phases = np.max(np.array(g), axis=0)
-    st_s = r.sender.ctx.sync_status() if r.sender is not None else 0
+    st_s = [p.ctx.sync_status() for p in r.sender.parts] if r.sender is not None else []
     st_r = [x.ctx.sync_status() for x in r.receivers_all()]
-    assert st_s == 0 and not any(st_r), f"status sender {st_s} receivers {st_r}"
+    assert not any(st_s) and not any(st_r), f"status senders {st_s} receivers {st_r}"
 
     # ---- per-update latency (SURVEY §8(d) timing protocol): barrier, then one sync; max over ranks of
     #      (start -> this rank's last kernel of the sync: commit on a Trainer, apply on a Rollout)
@@ -486,17 +524,16 @@ def run_ours(args):
     if not args.no_verify:
         mine = r.digests()
         if d.world == 1:
-            verify = mine[0] == mine[1]
+            verify = mine[0] == mine[1][0]
         else:
             g = [None] * d.world
             d.dist.all_gather_object(g, mine, group=d.ctrl)
             W, half = d.world, d.world // 2
-            if args.topology == "ring":
-                verify = all(g[(i - 1) % W][0] == g[i][1] for i in range(W))
-            elif args.topology == "fanout":
-                verify = all(g[rr][1][t] == g[t][0] for rr in range(half, W) for t in range(half))
-            else:
-                verify = all(g[t][0] == g[t + half][1] for t in range(half))
+            verify = True
+            for i in range(W):
+                for src, dig in (g[i][1] or {}).items():
+                    verify = verify and dig == g[src][0]
+            verify = verify and sum(len(x[1] or {}) for x in g) > 0
 
     # ---- e2e through the public API with host buffers (H2D of the new weights, D2H of the result)
     e2e = None
@@ -540,11 +577,10 @@ def run_ours(args):
                    "elements_per_trainer_rank": r.S // 2, "model_elements": manifest.total,
                    "tensors": len(manifest.tensors),
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
-                   "topology": topo_txt,
+                   "groups": r.G, "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
                    "l2": "inputs larger than L2 (2 x S per Trainer); no flush"},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
-                         zip(["extract", "compress_pack", None, "transfer_apply", "commit", "synthetic_update"],
-                             phases) if n},
+                         zip(["extract", "compress_pack", "transfer_apply", "commit", "synthetic_update"], phases)},
         "roofline": {"bound": "hbm", "kernel": "k_extract (K1)", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "bytes_per_launch": local_alg_extract, "traffic_source": traffic_src,
@@ -596,7 +632,7 @@ def run_e2e(args, d: Dist, r: Rank):
         hosts[0].copy_(r.Y)
         if n_host == 2:
             hosts[1].copy_(r.X)
-        counts_h = torch.empty_like(r.sender.counts, device="cpu").pin_memory()
+        counts_h = [torch.empty_like(p.counts, device="cpu").pin_memory() for p in r.sender.parts]
     K = args.e2e_steps
     d.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -607,12 +643,13 @@ def run_e2e(args, d: Dist, r: Rank):
             r.Y.copy_(hosts[k % len(hosts)], non_blocking=True)
         r.step()
         if counts_h is not None:
-            counts_h.copy_(r.sender.counts, non_blocking=True)
+            for h, p in zip(counts_h, r.sender.parts):
+                h.copy_(p.counts, non_blocking=True)
     t1.record()
     d.barrier()
     ms = d.max(t0.elapsed_time(t1))
     total_S = d.sum(r.S)
-    d2h = d.sum(8 * r.sender.counts.numel() if r.sender is not None else 0)
+    d2h = d.sum(sum(8 * p.counts.numel() for p in r.sender.parts) if r.sender is not None else 0)
     del hosts
     return {"value": round(total_S * K / (ms / 1e3) / 1e9, 3), "unit": UNIT,
             "h2d_bytes_per_step": int(total_S), "d2h_bytes_per_step": int(d2h),

@@ -46,6 +46,12 @@ EXPORTS = [
     "sync_commit_snapshot", "sync_commit_snapshot_batched", "sync_status", "sync_ctx_stats", "sync_strerror",
     "sync_launch_count",
 ]
+# NVLink peer-memory plumbing (include/sparsesync_peer.h)
+PEER_EXPORTS = [
+    "sync_peer_mem_export", "sync_peer_mem_open", "sync_peer_mem_close", "sync_peer_event_create",
+    "sync_peer_event_open", "sync_peer_event_record", "sync_peer_stream_wait", "sync_peer_event_destroy",
+    "sync_peer_copy",
+]
 
 
 class SyncError(RuntimeError):
@@ -103,6 +109,15 @@ def lib() -> ctypes.CDLL:
             "sync_commit_snapshot_batched": [P, P, P, P, P, P],
             "sync_status": [P, P],
             "sync_ctx_stats": [P, P, P],
+            "sync_peer_mem_export": [P, P, P, P],
+            "sync_peer_mem_open": [P, P],
+            "sync_peer_mem_close": [P],
+            "sync_peer_event_create": [P, P],
+            "sync_peer_event_open": [P, P],
+            "sync_peer_event_record": [P, P],
+            "sync_peer_stream_wait": [P, P],
+            "sync_peer_event_destroy": [P],
+            "sync_peer_copy": [P, P, u64, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -305,6 +320,11 @@ class SyncContext:
     def sync_decompress_apply(self, bucket: torch.Tensor, nbytes: int, weight_ptrs: torch.Tensor, stream=None):
         _ck(lib().sync_decompress_apply(self._h, _dev_ptr(bucket), nbytes, _dev_ptr(weight_ptrs), _stream(stream)),
             "sync_decompress_apply")
+
+    def sync_decompress_apply_ptr(self, bucket_ptr: int, nbytes: int, weight_ptrs: torch.Tensor, stream=None):
+        """Same, for a raw device address (e.g. a bucket inside a peer GPU's mapped buffer)."""
+        _ck(lib().sync_decompress_apply(self._h, ctypes.c_void_p(bucket_ptr), nbytes, _dev_ptr(weight_ptrs),
+                                        _stream(stream)), "sync_decompress_apply")
 
     # -- status ---------------------------------------------------------------
     def sync_status(self, stream=None) -> int:

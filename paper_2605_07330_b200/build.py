@@ -19,9 +19,9 @@ def _sources():
 
 
 def _deps():
-    inc = os.path.join(os.path.dirname(HERE), "include", "sparsesync.h")
+    inc = os.path.join(os.path.dirname(HERE), "include")
     hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    return hdrs + [inc]
+    return hdrs + [os.path.join(inc, f) for f in os.listdir(inc) if f.endswith(".h")]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -151,9 +151,59 @@ class SparseSyncReceiver:
                                device=self.device)
         self.weight_ptrs = ptr_table(self.weights, self.device)
 
-    def apply(self, bucket: torch.Tensor, nbytes: int | None = None, stream=None):
+    def apply(self, bucket, nbytes: int | None = None, stream=None):
+        """bucket: a uint8 device tensor, or (device address, nbytes) — e.g. a bucket read in place from a
+        peer GPU's mapped buffer (transport.PeerLink mode "direct")."""
+        if isinstance(bucket, tuple):
+            self.ctx.sync_decompress_apply_ptr(bucket[0], bucket[1], self.weight_ptrs, stream)
+            return
         self.ctx.sync_decompress_apply(bucket, bucket.numel() if nbytes is None else nbytes, self.weight_ptrs,
                                        stream)
 
     def check(self, stream=None):
         self.ctx.check("receiver", stream)
+
+
+class GroupedSender:
+    """A Trainer's tensors split into G contiguous groups (transport.shard_ranges), each a SparseSyncSender with
+    its own context and buffers, so group g's buckets can be on the wire and applied while group g+1 is still
+    being extracted (bucket pipelining, P:61 / P:275). Records carry group-local tensor ids; the receiving
+    side uses a GroupedReceiver built from the same tensor list and G."""
+
+    def __init__(self, snapshot, current, groups: int = 1, max_changed: int | None = None,
+                 expected_density: float = 0.02, **kw):
+        from .transport import shard_ranges
+        snap, cur = list(snapshot), list(current)
+        numel = [t.numel() for t in cur]
+        self.ranges = shard_ranges(numel, max(1, min(groups, len(numel))))
+        total = max(sum(numel), 1)
+        self.parts = []
+        for lo, hi in self.ranges:
+            n = sum(numel[lo:hi])
+            cap = None if max_changed is None else min(n, int(max_changed * n / total) + (1 << 16))
+            self.parts.append(SparseSyncSender(snap[lo:hi], cur[lo:hi], max_changed=cap,
+                                               expected_density=expected_density, **kw))
+
+    def commit(self, stream=None, mode: str = "scatter"):
+        for p in self.parts:
+            p.commit(stream, mode)
+
+    def stats(self, stream=None) -> dict:
+        out = {}
+        for p in self.parts:
+            for k, v in p.stats(stream).items():
+                out[k] = out.get(k, 0) + v
+        return out
+
+    def bucket_lists(self):
+        return [p.bucket_list for p in self.parts]
+
+
+class GroupedReceiver:
+    """Receiving side of a GroupedSender: one SparseSyncReceiver per group of the same tensor list."""
+
+    def __init__(self, weights, groups: int = 1, **kw):
+        from .transport import shard_ranges
+        w = list(weights)
+        self.ranges = shard_ranges([t.numel() for t in w], max(1, min(groups, len(w))))
+        self.parts = [SparseSyncReceiver(w[lo:hi], **kw) for lo, hi in self.ranges]

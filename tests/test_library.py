@@ -10,11 +10,12 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "sparsesync.h")
+PEER_HEADER = os.path.join(ROOT, "include", "sparsesync_peer.h")
 PKG = os.path.join(ROOT, "paper_2605_07330_b200")
 
 
-def declared():
-    src = open(HEADER).read()
+def declared(path=HEADER):
+    src = open(path).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(sync_[a-z0-9_]+)\s*\(", src)))
 
@@ -39,6 +40,14 @@ def test_library_exports_every_declared_symbol(lib):
     assert not missing, missing
     import paper_2605_07330_b200 as ss
     assert sorted(ss.EXPORTS) == declared()
+
+
+def test_library_exports_peer_plumbing(lib):
+    """include/sparsesync_peer.h (NVLink peer-memory transfer plumbing) is exported too."""
+    import paper_2605_07330_b200 as ss
+    names = declared(PEER_HEADER)
+    assert names and not [n for n in names if not hasattr(lib, n)]
+    assert sorted(ss.PEER_EXPORTS) == names
 
 
 def test_library_is_sm100a_sass(lib):
