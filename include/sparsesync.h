@@ -106,6 +106,8 @@ typedef struct sync_ctx sync_ctx;   /* opaque host object */
 int sync_workspace_size(const sync_manifest* m, const sync_config* c, size_t* bytes);
 int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c,
                     void* d_workspace, size_t workspace_bytes, sync_stream_t stream);
+/* sync_ctx_destroy waits for the device first (enqueued copies may still read the context's pinned host
+ * tables), then frees the host object; the workspace stays the caller's.  */
 int sync_ctx_destroy(sync_ctx* ctx);
 
 /* ---- a1 extract: Alg. 1 l.6 + Alg. 2 l.5 -------------------
@@ -140,11 +142,12 @@ int sync_compress(sync_ctx* ctx, const uint32_t* d_I, const uint16_t* d_V, const
                   uint8_t* d_enc, uint64_t enc_cap, sync_stream_t stream);
 
 /* ---- a5 bucket pack (Fig. workflow, C11) ----------------
- * BLOCKING: waits for the record sizes of the preceding sync_compress, runs
- * the greedy bucketing on the host (the one host sync point of a sync),
- * then launches the copy of every record into d_buckets plus the headers,
- * directories and (flag) CRC-32. Bucket b starts at h_offsets[b] (256-aligned)
- * and is h_sizes[b] bytes. *n_buckets = 0 when nothing changed.            */
+ * BLOCKING until the record sizes of the preceding sync_compress are known:
+ * runs the greedy bucketing on the host (the one host sync point of a sync),
+ * then enqueues on `stream` the copy of every record into d_buckets plus the
+ * headers, directories and (flag) CRC-32, and returns (the bucket bytes are
+ * ready when `stream` reaches that point). Bucket b starts at h_offsets[b]
+ * (256-aligned) and is h_sizes[b] bytes. *n_buckets = 0 when nothing changed. */
 int sync_bucket_pack(sync_ctx* ctx, const uint8_t* d_enc, uint8_t* d_buckets, uint64_t buckets_cap,
                      uint32_t* n_buckets, uint64_t* h_offsets, uint64_t* h_sizes, uint32_t max_buckets,
                      sync_stream_t stream);
@@ -152,11 +155,12 @@ int sync_bucket_pack(sync_ctx* ctx, const uint8_t* d_enc, uint8_t* d_buckets, ui
 int sync_buckets_bound(sync_ctx* ctx, uint64_t* bytes, sync_stream_t stream);
 
 /* ---- a2-a5 fused: plan -> bucket plan -> encode in place -------------------
- * BLOCKING. Same bytes as sync_compress + sync_bucket_pack, but every record
- * is encoded straight into its bucket position (no staging stream, no copy):
- * plan + per-chunk model on the device, greedy bucketing on the host from the
- * record sizes, then the encode kernel writes into d_buckets and the bucket
- * headers/directories (+ CRC) follow. If d_buckets is too small (or more than
+ * BLOCKING until the record sizes are known. Same bytes as sync_compress +
+ * sync_bucket_pack, but every record is encoded straight into its bucket
+ * position (no staging stream, no copy): plan + per-chunk model on the device,
+ * greedy bucketing on the host from the record sizes (h_offsets / h_sizes are
+ * final on return), then the encode kernel and the bucket headers/directories
+ * (+ CRC) are enqueued on `stream`. If d_buckets is too small (or more than
  * max_buckets are needed) it returns SYNC_ERR_CAPACITY and *h_need (if not
  * NULL) holds the required buffer bytes; nothing is written.               */
 int sync_compress_pack(sync_ctx* ctx, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,

@@ -99,6 +99,28 @@ inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 }  // namespace
 
+// Page-locked host memory for the per-sync host<->device tables: the copies are truly asynchronous, and the
+// next call's read_plan() synchronises the stream before the host touches them again.
+template <class T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <class U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <class U>
+  bool operator==(const PinnedAlloc<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+template <class T>
+using pvec = std::vector<T, PinnedAlloc<T>>;
+
 struct sync_ctx {
   Dims d;
   sync_config cfg;
@@ -112,9 +134,9 @@ struct sync_ctx {
   int grid;   // grid-stride kernels: CTAs of 256 threads
   const u64* plan_counts;
   bool plan_valid;
-  std::vector<u64> h_rec_bytes, h_chunk_off, h_enc_off, h_totals, h_rec_dst;
-  std::vector<RecordDesc> h_recs;
-  std::vector<BucketDesc> h_bks;
+  pvec<u64> h_rec_bytes, h_chunk_off, h_enc_off, h_totals, h_rec_dst;
+  pvec<RecordDesc> h_recs;
+  pvec<BucketDesc> h_bks;
 };
 
 extern "C" {
@@ -173,6 +195,18 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
     return SYNC_ERR_CUDA;
   }
   x->misc = reinterpret_cast<u32*>(w + L.misc);
+  try {   // pinned host tables, sized once
+    x->h_rec_bytes.reserve(d.T);
+    x->h_chunk_off.reserve(d.T + 1);
+    x->h_enc_off.reserve(d.T + 1);
+    x->h_totals.reserve(16);
+    x->h_rec_dst.reserve(d.T);
+    x->h_recs.reserve(d.T);
+    x->h_bks.reserve(d.T + 1);
+  } catch (...) {
+    delete x;
+    return SYNC_ERR_CUDA;
+  }
   Plan& p = x->plan;
   p.n_tensors = d.T;
   p.cap = c->max_changed;
@@ -205,6 +239,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
 }
 
 int sync_ctx_destroy(sync_ctx* ctx) {
+  if (ctx) cudaDeviceSynchronize();   // in-flight copies may still read the ctx's pinned host tables
   delete ctx;
   return SYNC_OK;
 }
@@ -390,7 +425,7 @@ static int finish_buckets(sync_ctx* x, uint8_t* d_buckets, const uint8_t* d_enc,
     crc_fill(d_buckets, x->h_bks.data(), nb, reinterpret_cast<u32*>(x->ws + x->L.crc), s);
   }
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(s));  // the H2D copies read pageable host vectors: keep them valid until done
+  // no host wait: the H2D sources are pinned ctx tables, rewritten only after the next read_plan() sync
   return SYNC_OK;
 }
 

@@ -141,8 +141,10 @@ struct WarpModel {
   u32 hist[256];
   u16 freq[256];
   u16 cum[256];
-  u32 rcp[256];
-  u32 fc[256];   // freq | cum << 16 (one load per symbol in the encode loops)
+  // per symbol {freq | cum << 16, rcp_of(freq)}: one 64-bit load per step in the encode loop; entry 256 is a
+  // no-op symbol (freq 4096, cum 0) for the padding positions past a chunk's end: it never emits and
+  // x + q * (4096 - 4096) + 0 leaves the state unchanged
+  uint2 fr[257];
 };
 
 // Histogram of hi bytes hi(p) for p < n into m.hist (warp-aggregated smem atomics).
@@ -243,10 +245,10 @@ __device__ __forceinline__ u32 warp_normalize(WarpModel& m, u32 n) {
     u32 s = lane * 8 + k;
     m.freq[s] = (u16)f[k];
     m.cum[s] = (u16)run;
-    m.rcp[s] = f[k] ? rcp_of(f[k]) : 0u;
-    m.fc[s] = f[k] | (run << 16);
+    m.fr[s] = make_uint2(f[k] | (run << 16), f[k] ? rcp_of(f[k]) : 0u);
     run += f[k];
   }
+  if (lane == 0) m.fr[256] = make_uint2((u32)kM, rcp_of((u32)kM));
   __syncwarp();
   return nsym;
 }

@@ -144,7 +144,22 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
     for (u32 i = tid; i < 34 + nsym; i += kCThreads) hdr[i] = rh[i];
     const u16* ws = p.word_scratch + chunk_words_base(p.rec_off[t] + p0, g);
     u16* words = reinterpret_cast<u16*>(blk + 136 + 4 * nsym);
-    for (u32 i = tid; i < nwords; i += kCThreads) words[i] = ws[nwords - 1 - i];
+    {
+      constexpr int kW = 8;   // 8 loads in flight per thread (the copy is latency-bound otherwise)
+      for (u32 i0 = tid; i0 < nwords; i0 += kCThreads * kW) {
+        u16 w[kW];
+#pragma unroll
+        for (int j = 0; j < kW; ++j) {
+          const u32 i = i0 + j * kCThreads;
+          w[j] = i < nwords ? ws[nwords - 1 - i] : (u16)0;
+        }
+#pragma unroll
+        for (int j = 0; j < kW; ++j) {
+          const u32 i = i0 + j * kCThreads;
+          if (i < nwords) words[i] = w[j];
+        }
+      }
+    }
     if (tid == 0 && (hb & 3u)) *reinterpret_cast<u16*>(blk + hb) = 0;
   }
 }

@@ -39,23 +39,38 @@ __device__ __forceinline__ u64 block_excl_scan64(u64 v, u64* excl, u64* s_w) {
   return total;
 }
 
+constexpr int kPerScan = 8;   // tensors per thread per round (one block scan pair per 8192 tensors)
 __global__ void __launch_bounds__(kScanThreads) k_plan_scan(Plan p, const u64* counts) {
   __shared__ u64 s_w[33];
   __shared__ u64 s_w2[33];
   u64 carry_nnz = 0, carry_ch = 0, carry_rec = 0;
   const u32 T = p.n_tensors;
-  for (u32 b = 0; b < T; b += kScanThreads) {
-    u32 t = b + threadIdx.x;
-    u64 c = t < T ? counts[t] : 0;
-    u64 ch = (c + kChunk - 1) / kChunk;
-    u64 packed = (ch << 32) | (c ? 1u : 0u);   // chunks (< 2^32 total) | record flag
+  constexpr u32 kRound = kScanThreads * kPerScan;
+  for (u32 b = 0; b < T; b += kRound) {
+    const u32 t0 = b + threadIdx.x * kPerScan;
+    u64 c[kPerScan];
+    u64 s1 = 0, s2 = 0;
+#pragma unroll
+    for (int k = 0; k < kPerScan; ++k) {
+      const u32 t = t0 + k;
+      c[k] = t < T ? counts[t] : 0;
+      s1 += c[k];
+      s2 += (((c[k] + kChunk - 1) / kChunk) << 32) | (c[k] ? 1u : 0u);   // chunks (< 2^32 total) | record flag
+    }
     u64 e1, e2;
-    u64 tot1 = block_excl_scan64(c, &e1, s_w);
-    u64 tot2 = block_excl_scan64(packed, &e2, s_w2);
-    if (t < T) {
-      p.rec_off[t] = carry_nnz + e1;
-      p.chunk_off[t] = carry_ch + (e2 >> 32);
-      p.maxgap[t] = 0;
+    const u64 tot1 = block_excl_scan64(s1, &e1, s_w);
+    const u64 tot2 = block_excl_scan64(s2, &e2, s_w2);
+    u64 r1 = carry_nnz + e1, r2 = carry_ch + (e2 >> 32);
+#pragma unroll
+    for (int k = 0; k < kPerScan; ++k) {
+      const u32 t = t0 + k;
+      if (t < T) {
+        p.rec_off[t] = r1;
+        p.chunk_off[t] = r2;
+        p.maxgap[t] = 0;
+      }
+      r1 += c[k];
+      r2 += (c[k] + kChunk - 1) / kChunk;
     }
     carry_nnz += tot1;
     carry_ch += tot2 >> 32;
@@ -97,31 +112,42 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
     const u64 nnz = counts[t];
     const u64 p0 = (g - co[t]) * kChunk;
     const u32 nk = (u32)((nnz - p0) < kChunk ? (nnz - p0) : kChunk);
-    const u32* Ir = I + p.rec_off[t];
+    const u32* Ic = I + p.rec_off[t] + p0;
     const u16* Vc = V + p.rec_off[t] + p0;
     const long long t1 = clock64();
-    // ---- histogram + max first difference
+    // ---- histogram + max first difference; the next block's loads are issued before the current
+    //      block is consumed, and the element before each 32-group comes from the previous group
     for (u32 sym = lane; sym < 256; sym += 32) m.hist[sym] = 0;
     __syncwarp();
     u32 gmax = 0;
-    for (u32 b0 = 0; b0 < nk; b0 += 32 * kWPF) {
-      u32 hv[kWPF], cur[kWPF];
+    u32 carry = (lane == 0 && p0) ? Ic[-1] : 0u;   // I of the element before the chunk (Δ_0 = I_0 if none)
+    carry = __shfl_sync(0xffffffffu, carry, 0);
+    u32 hv[kWPF], cur[kWPF], hn[kWPF], cn[kWPF];
+    auto load = [&](u32 b0, u32* h, u32* c) {
 #pragma unroll
       for (int u = 0; u < kWPF; ++u) {
         const u32 q = b0 + u * 32 + lane;
-        hv[u] = q < nk ? (u32)(Vc[q] >> 8) : 0x100u;
-        cur[u] = q < nk ? Ir[p0 + q] : 0u;
+        h[u] = q < nk ? (u32)(Vc[q] >> 8) : 0x100u;
+        c[u] = q < nk ? Ic[q] : 0u;
       }
+    };
+    load(0, hn, cn);
+    for (u32 b0 = 0; b0 < nk; b0 += 32 * kWPF) {
+#pragma unroll
+      for (int u = 0; u < kWPF; ++u) {
+        hv[u] = hn[u];
+        cur[u] = cn[u];
+      }
+      if (b0 + 32 * kWPF < nk) load(b0 + 32 * kWPF, hn, cn);
 #pragma unroll
       for (int u = 0; u < kWPF; ++u) {
         const u32 q = b0 + u * 32 + lane;
         if (hv[u] < 256) atomicAdd(&m.hist[hv[u]], 1u);
         u32 prev = __shfl_up_sync(0xffffffffu, cur[u], 1);
-        if (lane == 0) prev = (p0 + q) ? Ir[p0 + q - 1] : 0u;
-        if (q < nk) {
-          const u32 d = cur[u] - prev;
-          gmax = d > gmax ? d : gmax;
-        }
+        if (lane == 0) prev = carry;
+        carry = __shfl_sync(0xffffffffu, cur[u], 31);
+        const u32 d = q < nk ? cur[u] - prev : 0u;
+        gmax = d > gmax ? d : gmax;
       }
     }
 #pragma unroll
@@ -135,12 +161,16 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
     if (!comp) continue;
     const u32 nsym = warp_normalize(m, nk);
     const long long t3 = clock64();
-    // ---- counted rANS pass (words -> scratch in emission order; states/model -> chunk_rhdr)
+    // ---- counted rANS pass (words -> scratch in emission order; states/model -> chunk_rhdr).
+    //      Branch-free steps: positions past the chunk end use the no-op symbol 256; the state update is
+    //      x' = x + q * (M - f) + cum with q = floor(x / f) (= floor(x/f) * M + x mod f + cum).
     u32 x = kLow, nwords = 0;
     const u32 G = (nk + 31) / 32;
     const u32 lt = (1u << lane) - 1u;
     const u32 wcap = nk / 2;
     u16* ws = p.word_scratch + chunk_words_base(p.rec_off[t] + p0, g);
+    asm volatile("" : "+l"(ws));   // keep the 64-bit base in registers (no per-step rematerialisation)
+    const uint2* const fr = m.fr;
     u32 nxt[kWPF];
     auto load_block = [&](int top, u32* dst) {  // steps top, top-1, ..., top-7
 #pragma unroll
@@ -152,30 +182,23 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
     };
     load_block((int)G - 1, nxt);
     for (int top = (int)G - 1; top >= 0; top -= kWPF) {
-      u32 cur[kWPF];
+      u32 cs[kWPF];
 #pragma unroll
-      for (int u = 0; u < kWPF; ++u) cur[u] = nxt[u];
+      for (int u = 0; u < kWPF; ++u) cs[u] = nxt[u];
       if (top - kWPF >= 0) load_block(top - kWPF, nxt);
 #pragma unroll
       for (int u = 0; u < kWPF; ++u) {
-        if (top - u < 0) break;
-        const u32 sym = cur[u];
-        const bool act = sym < 256;
-        const u32 fcs = act ? m.fc[sym] : 0u, rcp = act ? m.rcp[sym] : 0u;
-        const u32 f = fcs & 0xFFFFu;
-        const bool emit = act && (x >> 20) >= f;
+        const uint2 e2 = fr[cs[u]];
+        const u32 f = e2.x & 0xFFFFu;
+        const bool emit = (x >> 20) >= f;
         const u32 em = __ballot_sync(0xffffffffu, emit);
-        if (emit) {
-          const u32 e = nwords + __popc(em & lt);
-          if (e < wcap) ws[e] = (u16)(x & 0xFFFFu);
-          x >>= 16;
-        }
+        const u32 e = nwords + __popc(em & lt);
+        if (emit && e < wcap) ws[e] = (u16)(x & 0xFFFFu);
+        x = emit ? (x >> 16) : x;
         nwords += __popc(em);
-        if (act) {
-          u32 r;
-          const u32 qq = div_by(x, f, rcp, &r);
-          x = qq * kM + r + (fcs >> 16);
-        }
+        u32 q = __umulhi(x, e2.y);
+        q += (x - q * f) >= f ? 1u : 0u;
+        x = x + q * ((u32)kM - f) + (e2.x >> 16);
       }
     }
     u32* rh = p.chunk_rhdr + g * kRhdrWords;
@@ -218,6 +241,23 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
   }
 }
 
+// Block-wide sum of a u64 (1024 threads); every thread gets the total.
+__device__ __forceinline__ u64 block_sum64(u64 v, u64* s_w) {
+  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) s_w[warp] = v;
+  __syncthreads();
+  u64 t = s_w[lane];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __syncthreads();
+  return t;
+}
+
+// Single CTA; every thread owns kPer consecutive items per round, so a round covers 8192 chunks or tensors
+// with one block scan (30B: 3 rounds over the chunks, 3 over the tensors).
+constexpr int kPer = 8;
 __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* counts) {
   __shared__ u64 s_w[33];
   __shared__ u64 s_w2[33];
@@ -225,60 +265,86 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
   const u64 n_chunks = p.totals[kTotChunks];
   const bool over = p.totals[kTotOverflow] != 0;
+  constexpr u64 kRound = (u64)kScanThreads * kPer;
   // 1. exclusive prefix of padded hi block sizes over all chunks (+ RANS chunk count)
-  u64 carry = 0, rans = 0;
+  u64 carry = 0, rans_local = 0;
   if (comp) {
-    for (u64 b = 0; b < n_chunks; b += kScanThreads) {
-      u64 g = b + threadIdx.x;
-      u64 v = g < n_chunks ? pad_to(p.chunk_hi[g], 4) : 0;
-      u64 r = g < n_chunks ? p.chunk_mode[g] : 0;
-      u64 e, e2;
-      u64 tot = block_excl_scan64(v, &e, s_w);
-      u64 tr = block_excl_scan64(r, &e2, s_w2);
-      if (g < n_chunks) p.chunk_hioff[g] = carry + e;
+    for (u64 b = 0; b < n_chunks; b += kRound) {
+      const u64 g0 = b + (u64)threadIdx.x * kPer;
+      u64 v[kPer];
+      u64 sum = 0;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const u64 g = g0 + k;
+        v[k] = g < n_chunks ? pad_to(p.chunk_hi[g], 4) : 0;
+        rans_local += g < n_chunks ? p.chunk_mode[g] : 0;
+        sum += v[k];
+      }
+      u64 e;
+      const u64 tot = block_excl_scan64(sum, &e, s_w);
+      u64 run = carry + e;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const u64 g = g0 + k;
+        if (g < n_chunks) p.chunk_hioff[g] = run;
+        run += v[k];
+      }
       carry += tot;
-      rans += tr;
     }
     if (threadIdx.x == 0) p.chunk_hioff[n_chunks] = carry;
     __syncthreads();
   }
+  const u64 rans = block_sum64(rans_local, s_w2);
   // 2. record sizes and offsets
   u64 carry_enc = 0, n16 = 0, n32 = 0, ib_tot = 0, vb_tot = 0;
-  for (u32 b = 0; b < T; b += kScanThreads) {
-    u32 t = b + threadIdx.x;
-    u64 c = (t < T && !over) ? counts[t] : 0;
-    u64 bytes = 0, ib = 0;
-    u32 mode = 1;
-    if (c) {
-      if (comp) {
-        mode = p.maxgap[t] <= 32767u ? 0u : 1u;
-        ib = pad_to((mode ? 4 : 2) * c, 4);
-        u64 ch0 = p.chunk_off[t], ch1 = p.chunk_off[t + 1];
-        u64 hi = p.chunk_hioff[ch1] - p.chunk_hioff[ch0];
-        bytes = pad_to(16 + ib + pad_to(c, 4) + 16 * (ch1 - ch0) + hi, 16);
-      } else {
-        ib = 4 * c;
-        bytes = pad_to(16 + 6 * c, 16);
+  for (u32 b = 0; b < T; b += (u32)kRound) {
+    const u32 t0 = b + threadIdx.x * kPer;
+    u64 bytes[kPer];
+    u64 sum = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const u32 t = t0 + k;
+      const u64 c = (t < T && !over) ? counts[t] : 0;
+      u64 by = 0, ib = 0;
+      u32 mode = 1;
+      if (c) {
+        if (comp) {
+          mode = p.maxgap[t] <= 32767u ? 0u : 1u;
+          ib = pad_to((mode ? 4 : 2) * c, 4);
+          const u64 ch0 = p.chunk_off[t], ch1 = p.chunk_off[t + 1];
+          const u64 hi = p.chunk_hioff[ch1] - p.chunk_hioff[ch0];
+          by = pad_to(16 + ib + pad_to(c, 4) + 16 * (ch1 - ch0) + hi, 16);
+        } else {
+          ib = 4 * c;
+          by = pad_to(16 + 6 * c, 16);
+        }
+        if (mode) n32++;
+        else n16++;
+        ib_tot += ib;
+        vb_tot += by - 16 - ib;
       }
-    }
-    if (t < T) {
-      p.rec_mode[t] = mode;
-      p.rec_bytes[t] = bytes;
+      if (t < T) {
+        p.rec_mode[t] = mode;
+        p.rec_bytes[t] = by;
+      }
+      bytes[k] = by;
+      sum += by;
     }
     u64 e;
-    u64 tot = block_excl_scan64(bytes, &e, s_w);
-    if (t < T) p.enc_off[t] = carry_enc + e;
+    const u64 tot = block_excl_scan64(sum, &e, s_w);
+    u64 run = carry_enc + e;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const u32 t = t0 + k;
+      if (t < T) p.enc_off[t] = run;
+      run += bytes[k];
+    }
     carry_enc += tot;
-    u64 flags = c ? (mode ? (1ull << 32) : 1ull) : 0ull;
-    u64 e2;
-    u64 tf = block_excl_scan64(flags, &e2, s_w2);
-    n16 += tf & 0xFFFFFFFFull;
-    n32 += tf >> 32;
-    u64 e3;
-    ib_tot += block_excl_scan64(ib, &e3, s_w);
-    u64 e4;
-    vb_tot += block_excl_scan64(c ? bytes - 16 - ib : 0, &e4, s_w2);
   }
+  n16 = block_sum64(n16, s_w);
+  n32 = block_sum64(n32, s_w2);
+  ib_tot = block_sum64(ib_tot, s_w);
+  vb_tot = block_sum64(vb_tot, s_w2);
   if (threadIdx.x == 0) {
     p.enc_off[T] = carry_enc;
     if (carry_enc > p.enc_cap) {
