@@ -61,6 +61,10 @@ def parse():
     p.add_argument("--transport", choices=["nccl", "peer", "peer-direct"], default="peer",
                    help="bucket data plane: NCCL P2P, NVLink peer memory pulled by the copy engines, or decoded "
                         "in place from peer memory by the decode kernel")
+    p.add_argument("--replica", choices=["separate", "snapshot"], default="separate",
+                   help="N=1 only. separate: a third arena is the Rollout replica; snapshot: the decode+apply "
+                        "writes into the Trainer's snapshot (it IS the commit, SURVEY config 1 loopback) and a "
+                        "write-only toggle of the changed bits makes the next update (2 arenas: fits 30B at 10%%)")
     p.add_argument("--groups", type=int, default=0,
                    help="tensor groups per Trainer, pipelined through transfer/apply (0: 1 for ring, 4 otherwise)")
     p.add_argument("--seed", type=int, default=0)
@@ -250,7 +254,14 @@ class Rank:
             sg.fill_new(self.Xv, self.Yv, mt, self.seed, args.rho, MASKS[args.mask], tid0=tid0)
             self.sender = GroupedSender(self.Xv, self.Yv, groups=self.G,
                                         max_changed=min(total, int(total * args.rho * 1.02) + (1 << 20)), **kw)
-        if self.is_rollout:
+        self.loop_snapshot = args.replica == "snapshot"
+        if self.loop_snapshot and (W != 1 or topo != "ring"):
+            raise SystemExit("--replica snapshot is the N=1 loopback layout")
+        if self.loop_snapshot:
+            # the replica is the snapshot itself: decode+apply = commit; a toggle regenerates the update
+            self.mr = self.mt
+            self.receivers[0] = GroupedReceiver(self.Xv, groups=self.G, **kw)
+        elif self.is_rollout:
             if topo == "ring":
                 srcs = {(d.rank - 1) % W: (0, len(manifest.tensors))}
                 mr, tid0, rseed = manifest, 0, args.seed + 1000 * ((d.rank - 1) % W)
@@ -300,9 +311,10 @@ class Rank:
     def n_events(self):
         return 3 * self.G + 4
 
-    def step(self, ev=None):
+    def step(self, ev=None, toggle: bool = True):
         """One sync. ev: n_events() CUDA events: per group (extract start, extract end, compress end), then
-        transfer/apply end, commit end, update end, and a spare."""
+        transfer/apply end, commit end, update end, and a spare. toggle=False skips the synthetic update
+        (the final verification sync)."""
         snd = self.sender
         rec = (lambda i: ev[i].record()) if ev else (lambda i: None)
         L, T, a = self.link, self.ss.transport, self.args
@@ -340,12 +352,14 @@ class Rank:
                     src = next(iter(self.receivers))
                     L.receive(self.receivers[src].parts[g].apply, tag=g)
         rec(3 * G)
-        if snd is not None:
+        if self.loop_snapshot:
+            pass                        # the decode+apply above wrote the snapshot: committed
+        elif snd is not None:
             snd.commit(mode=a.commit)
             if a.commit == "swap":
                 self.X, self.Y, self.Xv, self.Yv = self.Y, self.X, self.Yv, self.Xv
         rec(3 * G + 1)
-        if snd is not None and a.commit == "scatter":
+        if snd is not None and (a.commit == "scatter" or self.loop_snapshot) and toggle:
             # snapshot == current now: the synthetic "optimizer step" flips the changed bits again so the
             # next sync has a fresh update of the same density (write-only scatter, input generation)
             for p in snd.parts:
@@ -365,6 +379,10 @@ class Rank:
 
     def digests(self):
         """(trainer snapshot digest, {source: rollout digest of that source's range}) for the bit-exact check."""
+        if self.loop_snapshot:   # the replica is the snapshot: after a sync without toggle it must equal Y
+            self.step(toggle=False)
+            torch.cuda.synchronize()
+            return chunked_digest(self.Y), {0: chunked_digest(self.X)}
         mine_x = chunked_digest(self.X) if self.X is not None else None
         mine_r = None
         if self.R is not None:
@@ -490,7 +508,8 @@ def run_ours(args):
     t_end.record()
     d.barrier()
     clk = clocks.stop()
-    launches = ss.launch_count() - launches0 + (K * r.G if args.commit == "scatter" and r.sender is not None else 0)
+    launches = ss.launch_count() - launches0 + (K * r.G if (args.commit == "scatter" or r.loop_snapshot)
+                                                and r.sender is not None else 0)
     launches = int(d.sum(launches))   # + the toggle kernels under --commit scatter
     ms_local = t_start.elapsed_time(t_end)
     ms = d.max(ms_local)
@@ -577,7 +596,7 @@ def run_ours(args):
                    "elements_per_trainer_rank": r.S // 2, "model_elements": manifest.total,
                    "tensors": len(manifest.tensors),
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
-                   "groups": r.G, "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
+                   "groups": r.G, "replica": args.replica, "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
                    "l2": "inputs larger than L2 (2 x S per Trainer); no flush"},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
                          zip(["extract", "compress_pack", "transfer_apply", "commit", "synthetic_update"], phases)},

@@ -34,8 +34,7 @@
 namespace ss {
 
 constexpr int kXConsumers = kXThreads;            // 256 consumer threads (8 warps)
-constexpr int kWriters = 2;                       // writer warps
-constexpr int kXBlock = kXConsumers + 64 + 32 * kWriters;  // + copier, scheduler, writers
+constexpr int xblock(int writers) { return kXConsumers + 64 + 32 * writers; }  // + copier, scheduler, writers
 constexpr int kXQueue = 4;                        // tiles resolved ahead by the scheduler
 constexpr u32 kStageBytes = (u32)kSub * 2 * 2;    // old + new, 16 KB each
 
@@ -197,8 +196,8 @@ __device__ __forceinline__ u16 lane16(const uint4& v, int b) {
   return (u16)(((b < 4) ? lo64 : hi64) >> ((b & 3) * 16));
 }
 
-template <bool kSingle, int kStages>
-__global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
+template <bool kSingle, int kStages, int kWriters>
+__global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) {
   extern __shared__ __align__(128) u8 smem[];
   u8* data = smem;
   u64* full = reinterpret_cast<u64*>(smem + kStages * kStageBytes);
@@ -370,25 +369,38 @@ __global__ void __launch_bounds__(kXBlock, 2) k_extract(ExtractArgs a) {
       if (lane == 0 && m.count) atomicAdd((unsigned long long*)&a.counts[m.t], (unsigned long long)m.count);
       const u32* stg = ring + b * kSlotCap;
       if (!m.overflow) {
-        // 16 staged entries per lane in flight: 4 x 128-bit loads (the ring is L2-resident)
-        for (u32 q0 = 0; q0 < m.count; q0 += 512) {
-          uint4 e[4];
+        // lane l writes entries q0 + 32c + l: every store instruction covers 32 consecutive I (128 B) and
+        // V (64 B) slots; 16 staged entries per lane in flight, the next batch loaded before this one is
+        // stored (the ring is L2-resident)
+        constexpr int kE = 16;
+        const bool room = prefix + m.count <= a.cap;
+        u32 nx[kE];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) e[i] = *reinterpret_cast<const uint4*>(stg + q0 + i * 128 + 4 * lane);
+        for (int c = 0; c < kE; ++c) {
+          const u32 q = c * 32 + lane;
+          nx[c] = q < m.count ? stg[q] : 0u;
+        }
+        for (u32 q0 = 0; q0 < m.count; q0 += 32 * kE) {
+          u32 ev[kE];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const u32 ev[4] = {e[i].x, e[i].y, e[i].z, e[i].w};
+          for (int c = 0; c < kE; ++c) ev[c] = nx[c];
+          if (q0 + 32 * kE < m.count) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const u32 q = q0 + i * 128 + 4 * lane + c;
-              if (q < m.count) {
-                const u64 pos = prefix + q;
-                if (pos < a.cap) {
-                  a.I[pos] = (u32)(m.tile_base + (ev[c] & 0xFFFFu));
-                  a.V[pos] = (u16)(ev[c] >> 16);
-                } else {
-                  latch(a.status, SYNC_ERR_CAPACITY);
-                }
+            for (int c = 0; c < kE; ++c) {
+              const u32 q = q0 + 32 * kE + c * 32 + lane;
+              nx[c] = q < m.count ? stg[q] : 0u;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < kE; ++c) {
+            const u32 q = q0 + c * 32 + lane;
+            if (q < m.count) {
+              const u64 pos = prefix + q;
+              if (room || pos < a.cap) {
+                a.I[pos] = (u32)(m.tile_base + (ev[c] & 0xFFFFu));
+                a.V[pos] = (u16)(ev[c] >> 16);
+              } else {
+                latch(a.status, SYNC_ERR_CAPACITY);
               }
             }
           }
@@ -555,16 +567,18 @@ static size_t extract_smem() {
          kXQueue * sizeof(TileJob) + kSlots * sizeof(StagedTile) + 16 * 8;
 }
 
-template <bool kSingle, int kStages>
+template <bool kSingle, int kStages, int kWriters>
 static void launch_k(const ExtractArgs& a, cudaStream_t s) {
+  constexpr int kXBlock = xblock(kWriters);
   static int grid_cap = 0;
   const size_t sm = extract_smem<kStages>();
   if (!grid_cap) {
-    cudaFuncSetAttribute(k_extract<kSingle, kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_extract<kSingle, kStages, kWriters>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
     int dev = 0, n_sm = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_extract<kSingle, kStages>, kXBlock, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_extract<kSingle, kStages, kWriters>, kXBlock, sm);
     grid_cap = n_sm * (per > 0 ? per : 1);
     if (grid_cap > (int)kMaxExtractCtas) grid_cap = (int)kMaxExtractCtas;
   }
@@ -578,7 +592,7 @@ static void launch_k(const ExtractArgs& a, cudaStream_t s) {
     cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), s);
     b.prof = prof;
   }
-  k_extract<kSingle, kStages><<<(unsigned)grid, kXBlock, sm, s>>>(b);
+  k_extract<kSingle, kStages, kWriters><<<(unsigned)grid, kXBlock, sm, s>>>(b);
   count_launch();
   if (want_prof) {
     unsigned long long h[16];
@@ -593,17 +607,26 @@ static void launch_k(const ExtractArgs& a, cudaStream_t s) {
   }
 }
 
-// Stage count: 3 by default (two CTAs per SM); SS_XSTAGES=2|4 for experiments.
+// 3 stages (two CTAs per SM) and 3 writer warps by default (3 writers: +5% at 10% density, equal at 1%);
+// SS_XWRITERS=2|4 and (with 2 writers) SS_XSTAGES=2|4 select other instantiations for experiments.
 template <bool kSingle>
 static void launch(const ExtractArgs& a, cudaStream_t s) {
-  static int stages = 0;
+  static int stages = 0, writers = 0;
   if (!stages) {
     const char* e = getenv("SS_XSTAGES");
     stages = e ? atoi(e) : 3;
+    const char* w = getenv("SS_XWRITERS");
+    writers = w ? atoi(w) : 3;
   }
-  if (stages == 2) launch_k<kSingle, 2>(a, s);
-  else if (stages == 4) launch_k<kSingle, 4>(a, s);
-  else launch_k<kSingle, 3>(a, s);
+  if (writers == 2) {
+    if (stages == 2) launch_k<kSingle, 2, 2>(a, s);
+    else if (stages == 4) launch_k<kSingle, 4, 2>(a, s);
+    else launch_k<kSingle, 3, 2>(a, s);
+  } else if (writers == 4) {
+    launch_k<kSingle, 3, 4>(a, s);
+  } else {
+    launch_k<kSingle, 3, 3>(a, s);
+  }
 }
 
 void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, const u64* tile_prefix,
