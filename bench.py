@@ -153,7 +153,7 @@ class Clocks:
 
 # ============================================================================= distributed plumbing
 class Dist:
-    def __init__(self, n_gpus: int):
+    def __init__(self, n_gpus: int, topology: str = "ring", transport: str = "peer"):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -168,19 +168,23 @@ class Dist:
             dist.init_process_group("nccl", device_id=self.dev)
             self.ctrl = dist.new_group(backend="gloo")   # control plane (bucket manifests), cf. Ray in P:275
             self.dist = dist
-            # bring up the NCCL communicator and its P2P channels before the weight arenas take the HBM
+            # bring up the NCCL communicator (and, for the NCCL data plane, the P2P channels the topology
+            # uses) before the weight arenas take the HBM
             dist.barrier(device_ids=[self.local])
-            x = torch.zeros(1 << 20, dtype=torch.uint8, device=self.dev)
-            y = torch.empty_like(x)
-            ops = [dist.P2POp(dist.isend, x, (self.rank + 1) % self.world),
-                   dist.P2POp(dist.irecv, y, (self.rank - 1) % self.world)]
-            if self.world % 2 == 0:   # also every Trainer <-> Rollout pair of --topology pair/fanout/sharded
-                half = self.world // 2
-                peers = range(half, self.world) if self.rank < half else range(half)
-                for peer in peers:
-                    ops += [dist.P2POp(dist.isend, x, peer), dist.P2POp(dist.irecv, y, peer)]
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+            if transport == "nccl":
+                x = torch.zeros(1 << 20, dtype=torch.uint8, device=self.dev)
+                y = torch.empty_like(x)
+                W, half = self.world, self.world // 2
+                if topology == "ring":
+                    peers_out, peers_in = [(self.rank + 1) % W], [(self.rank - 1) % W]
+                elif topology == "fanout":
+                    peers_out, peers_in = (list(range(half, W)), []) if self.rank < half else ([], list(range(half)))
+                else:
+                    peers_out, peers_in = ([self.rank + half], []) if self.rank < half else ([], [self.rank - half])
+                ops = [dist.P2POp(dist.isend, x, p) for p in peers_out] + \
+                      [dist.P2POp(dist.irecv, y, p) for p in peers_in]
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
             torch.cuda.synchronize()
 
     def barrier(self):
@@ -320,6 +324,7 @@ class Rank:
         L, T, a = self.link, self.ss.transport, self.args
         G = self.G
         ring = a.topology == "ring"
+        peer = isinstance(L, T.PeerLink)
         ring_swap = ring and a.commit == "swap"
         for g in range(G):
             rec(3 * g)
@@ -332,21 +337,22 @@ class Rank:
                 blist = p.compress_pack()  # fused K2-K4 (blocking: host bucket plan)
                 rec(3 * g + 2)
                 if L is None:             # N = 1: the ring closes on itself
-                    rcv = self.receivers[0].parts[g]
-                    for b in range(len(blist)):
-                        rcv.apply(p.bucket(b))
+                    self.receivers[0].parts[g].apply_many([p.bucket(b) for b in range(len(blist))])
                 elif ring:
                     # under --commit swap group g's I array is dead until the next extract of group g:
                     # receive the peer's group-g buckets into it (saves payload-sized buffers at 183 GB of arenas)
                     src = (self.d.rank - 1) % self.d.world
-                    L.exchange(p.buckets, blist, self.receivers[src].parts[g].apply, tag=g,
+                    rp = self.receivers[src].parts[g]
+                    L.exchange(p.buckets, blist, rp.apply_many if peer else rp.apply, tag=g,
                                recv_buf=p.I.view(torch.uint8) if ring_swap else None)
                 else:
                     L.send(p.buckets, blist, tag=g)
             else:
                 rec(3 * g + 1)
                 rec(3 * g + 2)
-                if isinstance(L, (T.FanoutLink, T.PeerLink)):
+                if peer:
+                    L.receive({t: self.receivers[t].parts[g].apply_many for t in self.receivers}, tag=g)
+                elif isinstance(L, T.FanoutLink):
                     L.receive({t: self.receivers[t].parts[g].apply for t in self.receivers}, tag=g)
                 else:
                     src = next(iter(self.receivers))
@@ -452,7 +458,7 @@ def parse_records(bucket_bytes_list):
 
 def run_ours(args):
     import paper_2605_07330_b200 as ss
-    d = Dist(args.gpus)
+    d = Dist(args.gpus, args.topology, args.transport)
     peaks = measured_peaks()
     manifest = manifest_for(args.workload)
     r = Rank(args, d, manifest)

@@ -187,6 +187,12 @@ int sync_decompress(sync_ctx* ctx, const uint8_t* d_bucket, uint64_t bytes, uint
 int sync_decompress_apply(sync_ctx* ctx, const uint8_t* d_bucket, uint64_t bytes,
                           uint16_t* const* d_weight_ptrs, sync_stream_t stream);
 
+/* Batched form of sync_decompress_apply: h_buckets / h_bytes are HOST arrays of n_buckets device bucket
+ * addresses and sizes (e.g. the buckets of one transfer span); one kernel decodes up to 32 buckets, so many
+ * small buckets do not each pay a launch that fills a fraction of the GPU. Same validation and errors.   */
+int sync_decompress_apply_batched(sync_ctx* ctx, const uint8_t* const* h_buckets, const uint64_t* h_bytes,
+                                  uint32_t n_buckets, uint16_t* const* d_weight_ptrs, sync_stream_t stream);
+
 /* ---- a8 scatter-apply / a9 snapshot commit (Alg. 3 l.6) -----
  * d_W[d_I[k]] = d_V[k] for k < count (superset-safe, idempotent).
  * Indices >= numel are skipped and latch SYNC_ERR_INDEX_RANGE into *d_status

@@ -42,7 +42,7 @@ SYNC_CHUNK = 16384
 EXPORTS = [
     "sync_workspace_size", "sync_ctx_create", "sync_ctx_destroy", "sync_extract_workspace_size", "sync_extract",
     "sync_extract_status", "sync_extract_batched", "sync_enc_bound", "sync_compress", "sync_bucket_pack",
-    "sync_buckets_bound", "sync_compress_pack", "sync_bucket_unpack", "sync_decompress", "sync_decompress_apply", "sync_apply",
+    "sync_buckets_bound", "sync_compress_pack", "sync_bucket_unpack", "sync_decompress", "sync_decompress_apply", "sync_decompress_apply_batched", "sync_apply",
     "sync_commit_snapshot", "sync_commit_snapshot_batched", "sync_status", "sync_ctx_stats", "sync_strerror",
     "sync_launch_count",
 ]
@@ -104,6 +104,7 @@ def lib() -> ctypes.CDLL:
             "sync_bucket_unpack": [P, P, u64, P, u32, P, P],
             "sync_decompress": [P, P, u64, P, P, u64, P],
             "sync_decompress_apply": [P, P, u64, P, P],
+            "sync_decompress_apply_batched": [P, P, P, u32, P, P],
             "sync_apply": [P, P, P, u64, u64, P, P],
             "sync_commit_snapshot": [P, P, P, u64, u64, P, P],
             "sync_commit_snapshot_batched": [P, P, P, P, P, P],
@@ -320,6 +321,16 @@ class SyncContext:
     def sync_decompress_apply(self, bucket: torch.Tensor, nbytes: int, weight_ptrs: torch.Tensor, stream=None):
         _ck(lib().sync_decompress_apply(self._h, _dev_ptr(bucket), nbytes, _dev_ptr(weight_ptrs), _stream(stream)),
             "sync_decompress_apply")
+
+    def sync_decompress_apply_batched(self, buckets, weight_ptrs: torch.Tensor, stream=None):
+        """buckets: [(device address, nbytes)]; one kernel per 32 buckets."""
+        n = len(buckets)
+        if n == 0:
+            return
+        ptrs = (ctypes.c_void_p * n)(*[b[0] for b in buckets])
+        sizes = (ctypes.c_uint64 * n)(*[b[1] for b in buckets])
+        _ck(lib().sync_decompress_apply_batched(self._h, ptrs, sizes, n, _dev_ptr(weight_ptrs), _stream(stream)),
+            "sync_decompress_apply_batched")
 
     def sync_decompress_apply_ptr(self, bucket_ptr: int, nbytes: int, weight_ptrs: torch.Tensor, stream=None):
         """Same, for a raw device address (e.g. a bucket inside a peer GPU's mapped buffer)."""

@@ -28,7 +28,7 @@ struct Layout {
   u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, rec_dst, totals, recs, bks, views, nviews, crc, total;
 };
 
-u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4; }
+u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4 + 32; }  // + 32 bad flags
 
 Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_changed) {
   Layout L{};
@@ -478,13 +478,18 @@ int sync_compress_pack(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, co
 }
 
 // ------------------------------------------------------------------------ receive
-static int maybe_crc_check(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, cudaStream_t s, const u32** bad) {
+// CRC checks (flag on) of n <= 32 buckets: bad flags in crc scratch [0, 32), segment CRCs after them.
+constexpr u32 kCrcFlagSlots = 32;
+static int maybe_crc_check(sync_ctx* x, const uint8_t* const* d_buckets, const uint64_t* bytes, u32 n,
+                           cudaStream_t s, const u32** bad) {
   *bad = nullptr;
   if (!(x->cfg.flags & SYNC_FLAG_CRC)) return SYNC_OK;
-  if (crc_slots(bytes) + 1 > x->d.crc_n) return SYNC_ERR_CAPACITY;
+  for (u32 i = 0; i < n; ++i)
+    if (crc_slots(bytes[i]) > x->d.crc_n) return SYNC_ERR_CAPACITY;   // crc_slots includes the flags
   u32* scratch = reinterpret_cast<u32*>(x->ws + x->L.crc);
-  CK(cudaMemsetAsync(scratch, 0, 4, s));
-  launch_crc_check(d_bucket, bytes, scratch, x->plan.status, s);
+  CK(cudaMemsetAsync(scratch, 0, 4 * kCrcFlagSlots, s));
+  for (u32 i = 0; i < n; ++i)
+    launch_crc_check(d_buckets[i], bytes[i], scratch + kCrcFlagSlots, scratch + i, x->plan.status, s);
   *bad = scratch;
   return SYNC_OK;
 }
@@ -495,7 +500,7 @@ int sync_bucket_unpack(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, syn
   if (!aligned16(d_bucket)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
   const u32* bad;
-  int st = maybe_crc_check(x, d_bucket, bytes, s, &bad);
+  int st = maybe_crc_check(x, &d_bucket, &bytes, 1, s, &bad);
   if (st) return st;
   launch_unpack(d_bucket, bytes, x->d.T, x->plan.numel, d_views, max_views, d_n_records, x->plan.status, s);
   CK(cudaGetLastError());
@@ -508,12 +513,12 @@ int sync_decompress(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, uint32
   if (!aligned16(d_bucket)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
   const u32* bad;
-  int st = maybe_crc_check(x, d_bucket, bytes, s, &bad);
+  int st = maybe_crc_check(x, &d_bucket, &bytes, 1, s, &bad);
   if (st) return st;
   sync_record_view* views = reinterpret_cast<sync_record_view*>(x->ws + x->L.views);
   u32* nv = reinterpret_cast<u32*>(x->ws + x->L.nviews);
   launch_unpack(d_bucket, bytes, x->d.T, x->plan.numel, views, x->d.T, nv, x->plan.status, s);
-  launch_decode(d_bucket, bytes, x->d.T, x->plan.numel, nullptr, views, d_I, d_V, d_cap, x->plan.status, bad,
+  launch_decode(&d_bucket, &bytes, 1, x->d.T, x->plan.numel, nullptr, views, d_I, d_V, d_cap, x->plan.status, bad,
                 x->grid, s);
   CK(cudaGetLastError());
   return SYNC_OK;
@@ -525,10 +530,28 @@ int sync_decompress_apply(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, 
   if (!aligned16(d_bucket)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
   const u32* bad;
-  int st = maybe_crc_check(x, d_bucket, bytes, s, &bad);
+  int st = maybe_crc_check(x, &d_bucket, &bytes, 1, s, &bad);
   if (st) return st;
-  launch_decode(d_bucket, bytes, x->d.T, x->plan.numel, d_weight_ptrs, nullptr, nullptr, nullptr, 0,
+  launch_decode(&d_bucket, &bytes, 1, x->d.T, x->plan.numel, d_weight_ptrs, nullptr, nullptr, nullptr, 0,
                 x->plan.status, bad, x->grid, s);
+  CK(cudaGetLastError());
+  return SYNC_OK;
+}
+
+int sync_decompress_apply_batched(sync_ctx* x, const uint8_t* const* h_buckets, const uint64_t* h_bytes,
+                                  uint32_t n_buckets, uint16_t* const* d_weight_ptrs, sync_stream_t stream) {
+  if (!x || !d_weight_ptrs || (n_buckets && (!h_buckets || !h_bytes))) return SYNC_ERR_ARG;
+  for (u32 i = 0; i < n_buckets; ++i)
+    if (!h_buckets[i] || !aligned16(h_buckets[i])) return h_buckets[i] ? SYNC_ERR_ALIGNMENT : SYNC_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (u32 b0 = 0; b0 < n_buckets; b0 += kCrcFlagSlots) {
+    const u32 n = n_buckets - b0 < kCrcFlagSlots ? n_buckets - b0 : kCrcFlagSlots;
+    const u32* bad;
+    int st = maybe_crc_check(x, h_buckets + b0, h_bytes + b0, n, s, &bad);
+    if (st) return st;
+    launch_decode(h_buckets + b0, h_bytes + b0, n, x->d.T, x->plan.numel, d_weight_ptrs, nullptr, nullptr,
+                  nullptr, 0, x->plan.status, bad, x->grid, s);
+  }
   CK(cudaGetLastError());
   return SYNC_OK;
 }

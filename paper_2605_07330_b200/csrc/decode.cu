@@ -21,6 +21,13 @@ struct BucketHdr {
   u64 bytes;
 };
 
+constexpr u32 kDecodeBatch = 32;
+struct DecodeBatch {            // passed by value (kernel parameter)
+  const u8* bk[kDecodeBatch];
+  u64 bytes[kDecodeBatch];
+  u32 n;
+};
+
 __device__ __forceinline__ int read_bucket_header(const u8* bk, u64 avail, BucketHdr* h) {
   if (avail < 32) return SYNC_ERR_TRUNCATED;
   const u32* w = reinterpret_cast<const u32*>(bk);
@@ -141,24 +148,48 @@ struct DecodeModel {
   u16 cum[256];
 };
 
+// One launch decodes up to kDecodeBatch buckets (the chunks of all of them form one grid-stride range), so
+// many small buckets do not each pay a launch that fills a fraction of the GPU.
 template <bool kApply>
-__global__ void __launch_bounds__(256) k_decode(const u8* bk, u64 bytes, u32 n_tensors, const u64* numel,
+__global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, const u64* numel,
                                                u16* const* weights, const sync_record_view* views, u32* I_out,
                                                u16* V_out, u64 out_cap, u32* status, const u32* crc_bad) {
   __shared__ DecodeModel s_dm[8];
+  __shared__ BucketHdr s_h[kDecodeBatch];
+  __shared__ u64 s_pre[kDecodeBatch + 1];
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   DecodeModel& dm = s_dm[warp];
-  if (crc_bad && *crc_bad) return;
-  BucketHdr h;
-  int herr = read_bucket_header(bk, bytes, &h);
-  if (herr != SYNC_OK) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, herr);
-    return;
+  if (threadIdx.x < bb.n) {   // headers; a bucket with a bad header or failed CRC contributes no chunks
+    const u32 i = threadIdx.x;
+    BucketHdr h;
+    int herr = read_bucket_header(bb.bk[i], bb.bytes[i], &h);
+    if (herr != SYNC_OK) {
+      if (blockIdx.x == 0) latch(status, herr);
+      h.n_chunks = 0;
+    }
+    if (crc_bad && crc_bad[i]) h.n_chunks = 0;
+    if (h.n_records == 0) h.n_chunks = 0;
+    s_h[i] = h;
   }
-  const u32* dir = reinterpret_cast<const u32*>(bk + 32);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 acc = 0;
+    for (u32 i = 0; i < bb.n; ++i) {
+      s_pre[i] = acc;
+      acc += s_h[i].n_chunks;
+    }
+    s_pre[bb.n] = acc;
+  }
+  __syncthreads();
+  const u64 total = s_pre[bb.n];
   const u64 nwarps = (u64)gridDim.x * (blockDim.x >> 5);
-  for (u64 g = (u64)blockIdx.x * (blockDim.x >> 5) + warp; g < h.n_chunks; g += nwarps) {
-    if (h.n_records == 0) break;
+  for (u64 gg = (u64)blockIdx.x * (blockDim.x >> 5) + warp; gg < total; gg += nwarps) {
+    // bucket of global chunk gg: the last i with s_pre[i] <= gg (kDecodeBatch <= 32: one ballot)
+    const u32 bi = 31 - __clz(__ballot_sync(0xffffffffu, lane < bb.n && s_pre[lane] <= gg));
+    const u8* bk = bb.bk[bi];
+    const BucketHdr h = s_h[bi];
+    const u64 g = gg - s_pre[bi];
+    const u32* dir = reinterpret_cast<const u32*>(bk + 32);
     const u32 q = warp_upper_search(h.n_records, g, [&](u32 i) { return (u64)dir[2 * i + 1]; });
     const u32 ro = dir[2 * q];
     RecHdr r;
@@ -382,16 +413,23 @@ void launch_unpack(const u8* bucket, u64 bytes, u32 n_tensors, const u64* numel,
   count_launch();
 }
 
-void launch_decode(const u8* bucket, u64 bytes, u32 n_tensors, const u64* numel, u16* const* weights,
-                   const sync_record_view* views, u32* I_out, u16* V_out, u64 out_cap, u32* status,
-                   const u32* crc_bad, int grid, cudaStream_t s) {
-  if (weights)
-    k_decode<true><<<grid, 256, 0, s>>>(bucket, bytes, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0,
-                                        status, crc_bad);
-  else
-    k_decode<false><<<grid, 256, 0, s>>>(bucket, bytes, n_tensors, numel, nullptr, views, I_out, V_out, out_cap,
-                                         status, crc_bad);
-  count_launch();
+void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u32 n_tensors, const u64* numel,
+                   u16* const* weights, const sync_record_view* views, u32* I_out, u16* V_out, u64 out_cap,
+                   u32* status, const u32* crc_bad, int grid, cudaStream_t s) {
+  for (u32 b0 = 0; b0 < n_buckets; b0 += kDecodeBatch) {
+    DecodeBatch bb;
+    bb.n = n_buckets - b0 < kDecodeBatch ? n_buckets - b0 : kDecodeBatch;
+    for (u32 i = 0; i < bb.n; ++i) {
+      bb.bk[i] = buckets[b0 + i];
+      bb.bytes[i] = bytes[b0 + i];
+    }
+    const u32* bad = crc_bad ? crc_bad + b0 : nullptr;
+    if (weights)
+      k_decode<true><<<grid, 256, 0, s>>>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status, bad);
+    else
+      k_decode<false><<<grid, 256, 0, s>>>(bb, n_tensors, numel, nullptr, views, I_out, V_out, out_cap, status, bad);
+    count_launch();
+  }
 }
 
 }  // namespace ss

@@ -80,13 +80,18 @@ void launch_pack(const uint8_t* enc, uint8_t* buckets, const RecordDesc* recs, u
 void crc_fill(uint8_t* buckets, const BucketDesc* h_bks, uint32_t n_buckets, uint32_t* scratch, cudaStream_t s);
 
 // decode.cu
-void launch_crc_check(const uint8_t* bucket, uint64_t bytes, uint32_t* scratch, uint32_t* status, cudaStream_t s);
+// CRC-32 of one bucket vs its header: mismatch latches SYNC_ERR_CRC and sets *bad_flag (device u32).
+void launch_crc_check(const uint8_t* bucket, uint64_t bytes, uint32_t* seg_scratch, uint32_t* bad_flag,
+                      uint32_t* status, cudaStream_t s);
 void launch_unpack(const uint8_t* bucket, uint64_t bytes, uint32_t n_tensors, const uint64_t* numel,
                    sync_record_view* views, uint32_t max_views, uint32_t* n_records, uint32_t* status,
                    cudaStream_t s);
-void launch_decode(const uint8_t* bucket, uint64_t bytes, uint32_t n_tensors, const uint64_t* numel,
-                   uint16_t* const* weights, const sync_record_view* views, uint32_t* I_out, uint16_t* V_out,
-                   uint64_t out_cap, uint32_t* status, const uint32_t* crc_bad, int grid, cudaStream_t s);
+// buckets / bytes: HOST arrays of n_buckets device addresses and sizes; crc_bad: device flags [n_buckets]
+// (or null). One kernel per 32 buckets.
+void launch_decode(const uint8_t* const* buckets, const uint64_t* bytes, uint32_t n_buckets, uint32_t n_tensors,
+                   const uint64_t* numel, uint16_t* const* weights, const sync_record_view* views, uint32_t* I_out,
+                   uint16_t* V_out, uint64_t out_cap, uint32_t* status, const uint32_t* crc_bad, int grid,
+                   cudaStream_t s);
 
 // apply.cu
 void launch_apply(uint16_t* W, const uint32_t* I, const uint16_t* V, uint64_t count, uint64_t numel,

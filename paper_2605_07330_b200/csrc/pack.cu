@@ -5,17 +5,19 @@
 // needs anyway). These kernels then write every byte of the buckets:
 //  * k_pack_meta : header (32 B) + record directory + directory padding
 //  * k_pack_copy : records, 16 B units, enc -> bucket position
-//  * k_crc_seg / k_crc_fin : parallel CRC-32/IEEE of [32, bytes) — per-segment
-//    raw CRCs combined with multiplications by x^(8n) mod P (the CRC is linear
-//    over GF(2)), then the init/xorout terms.
+//  * k_crc_seg / k_crc_fin : parallel CRC-32/IEEE of [32, bytes) — slicing-by-4
+//    CRCs of 128-byte pieces, combined per 64 KB segment and then across segments
+//    with multiplications by x^(8n) mod P (the CRC is linear over GF(2)), then
+//    the init/xorout terms.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ss {
 
 constexpr u32 kPoly = 0xEDB88320u;  // reflected IEEE polynomial
-constexpr u32 kCrcSeg = 4096;       // bytes per segment (one CTA)
-constexpr int kCrcThreads = 128;    // 32 bytes per thread
+constexpr int kCrcThreads = 512;    // one CTA per segment
+constexpr u32 kCrcPiece = 128;      // bytes per thread (8 x 16-byte loads)
+constexpr u32 kCrcSeg = kCrcThreads * kCrcPiece;   // 64 KB per segment
 
 struct CrcTables {
   u32 x2n[32];  // x^(2^k) mod P, reflected
@@ -32,7 +34,7 @@ __host__ __device__ __forceinline__ u32 multmodp(u32 a, u32 b) {
 }
 
 // x^(8n) mod P
-__device__ __forceinline__ u32 x8n(const CrcTables& tb, u64 n) {
+__host__ __device__ __forceinline__ u32 x8n(const CrcTables& tb, u64 n) {
   u32 r = 1u << 31;
   int k = 3;
   while (n) {
@@ -43,51 +45,85 @@ __device__ __forceinline__ u32 x8n(const CrcTables& tb, u64 n) {
   return r;
 }
 
-// Raw CRC (init 0, no xorout) of each right-aligned segment of data[0, len):
-// segment s covers [len - (S - s)*kCrcSeg, len - (S - 1 - s)*kCrcSeg); bytes
-// before 0 are virtual zeros (leading zeros leave an init-0 CRC unchanged).
-__global__ void __launch_bounds__(kCrcThreads) k_crc_seg(const u8* data, u64 len, u32* seg_crc, CrcTables tb) {
-  __shared__ u32 table[256];
-  __shared__ u32 s_c[kCrcThreads];
+// x^(8 * kCrcPiece * (kCrcThreads - 1 - t)): shifts piece t's CRC to the end of its segment
+__constant__ u32 c_piece_shift[kCrcThreads];
+
+// The bytes [0, len) are viewed as a virtual stream of S * kCrcSeg bytes with pad = S*kCrcSeg - len
+// leading zero bytes (leading zeros leave an init-0 CRC unchanged). len is a multiple of 16, so every
+// 128-byte piece of the virtual stream starts 16-byte aligned in memory. Thread t of CTA s computes the
+// raw CRC (init 0, no xorout) of its piece with slicing-by-4 tables and shifts it to the segment end;
+// the XOR of the shifted pieces is the segment's raw CRC (the CRC is linear over GF(2)).
+__global__ void __launch_bounds__(kCrcThreads) k_crc_seg(const u8* data, u64 len, u64 pad, u32* seg_crc) {
+  __shared__ u32 T[4][256];
+  __shared__ u32 s_x[kCrcThreads / 32];
   for (u32 i = threadIdx.x; i < 256; i += blockDim.x) {
     u32 c = i;
     for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (kPoly & (0u - (c & 1u)));
-    table[i] = c;
+    T[0][i] = c;
   }
   __syncthreads();
-  const u64 S = (len + kCrcSeg - 1) / kCrcSeg;
-  const u64 s = blockIdx.x;
-  const long long seg_start = (long long)len - (long long)(S - s) * kCrcSeg;
-  const long long start = seg_start + (long long)threadIdx.x * 32;
+  for (u32 i = threadIdx.x; i < 256; i += blockDim.x) {
+    u32 c = T[0][i];
+    for (int k = 1; k < 4; ++k) {
+      c = (c >> 8) ^ T[0][c & 0xFFu];
+      T[k][i] = c;
+    }
+  }
+  __syncthreads();
+  const long long v0 = (long long)blockIdx.x * kCrcSeg + (long long)threadIdx.x * kCrcPiece - (long long)pad;
+  uint4 w[kCrcPiece / 16];
+#pragma unroll
+  for (int j = 0; j < (int)(kCrcPiece / 16); ++j) {
+    const long long o = v0 + 16 * j;
+    w[j] = o >= 0 ? *reinterpret_cast<const uint4*>(data + o) : make_uint4(0, 0, 0, 0);
+  }
   u32 c = 0;
-  for (int b = 0; b < 32; ++b) {
-    long long pos = start + b;
-    u32 byte = pos >= 0 ? data[pos] : 0u;
-    c = table[(c ^ byte) & 0xFFu] ^ (c >> 8);
+#pragma unroll
+  for (int j = 0; j < (int)(kCrcPiece / 16); ++j) {
+    const u32 ws[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      c ^= ws[k];
+      c = T[3][c & 0xFFu] ^ T[2][(c >> 8) & 0xFFu] ^ T[1][(c >> 16) & 0xFFu] ^ T[0][c >> 24];
+    }
   }
-  // ordered combine of 32-byte pieces: crc(A||B) = crc(A) * x^(8|B|) ^ crc(B)
-  s_c[threadIdx.x] = c;
+  c = multmodp(c, c_piece_shift[threadIdx.x]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) s_x[threadIdx.x >> 5] = c;
   __syncthreads();
-  for (u32 w = 1; w < kCrcThreads; w <<= 1) {
-    u32 v = 0;
-    bool active = (threadIdx.x % (2 * w)) == 0;
-    if (active) v = multmodp(s_c[threadIdx.x], x8n(tb, (u64)32 * w)) ^ s_c[threadIdx.x + w];
-    __syncthreads();
-    if (active) s_c[threadIdx.x] = v;
-    __syncthreads();
+  if (threadIdx.x < 32) {
+    c = threadIdx.x < kCrcThreads / 32 ? s_x[threadIdx.x] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
+    if (threadIdx.x == 0) seg_crc[blockIdx.x] = c;
   }
-  if (threadIdx.x == 0) seg_crc[s] = s_c[0];
 }
 
-// Combine segments and apply init/xorout; store into *out (or compare).
-__global__ void k_crc_fin(const u32* seg_crc, u64 len, CrcTables tb, u32* out, const u8* hdr_crc, u32* status,
-                          u32* bad) {
+// Combine the S segment CRCs (thread j: Horner over its block of consecutive segments, then one shift to
+// the stream end, XOR-reduced), apply the init / xorout terms of CRC-32/IEEE over the real len bytes, and
+// store into *out (or compare with the header's value).
+__global__ void __launch_bounds__(1024) k_crc_fin(const u32* seg_crc, u64 S, u64 len, CrcTables tb, u32* out,
+                                                  const u8* hdr_crc, u32* status, u32* bad) {
+  __shared__ u32 s_x[32];
+  const u64 B = (S + blockDim.x - 1) / blockDim.x;
+  const u64 s0 = (u64)threadIdx.x * B, s1 = s0 + B < S ? s0 + B : S;
+  u32 acc = 0;
+  if (s0 < S) {
+    const u32 shift = x8n(tb, kCrcSeg);
+    for (u64 s = s0; s < s1; ++s) acc = multmodp(acc, shift) ^ seg_crc[s];
+    acc = multmodp(acc, x8n(tb, (u64)kCrcSeg * (S - s1)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s_x[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  acc = threadIdx.x < blockDim.x / 32 ? s_x[threadIdx.x] : 0u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
   if (threadIdx.x != 0) return;
-  const u64 S = (len + kCrcSeg - 1) / kCrcSeg;
-  u32 raw = 0;
-  const u32 shift = x8n(tb, kCrcSeg);
-  for (u64 s = 0; s < S; ++s) raw = multmodp(raw, shift) ^ seg_crc[s];
-  u32 crc = raw ^ multmodp(0xFFFFFFFFu, x8n(tb, len)) ^ 0xFFFFFFFFu;
+  const u32 crc = acc ^ multmodp(0xFFFFFFFFu, x8n(tb, len)) ^ 0xFFFFFFFFu;
   if (out) *out = crc;
   if (hdr_crc) {
     u32 want = (u32)hdr_crc[0] | ((u32)hdr_crc[1] << 8) | ((u32)hdr_crc[2] << 16) | ((u32)hdr_crc[3] << 24);
@@ -106,20 +142,24 @@ static CrcTables host_crc_tables() {
   return tb;
 }
 
-// scratch: >= ceil(len / 4096) u32
+// scratch: >= ceil(len / kCrcSeg) u32
 static void crc_bucket(const u8* bucket, u64 bytes, u32* scratch, u32* out, const u8* hdr_crc, u32* status,
                        u32* bad, cudaStream_t s) {
   static const CrcTables tb = host_crc_tables();
-  u64 len = bytes > 32 ? bytes - 32 : 0;
-  if (len == 0) {
-    k_crc_fin<<<1, 32, 0, s>>>(scratch, 0, tb, out, hdr_crc, status, bad);
-    count_launch();
-    return;
+  static bool shifts = false;
+  if (!shifts) {
+    u32 h[kCrcThreads];
+    for (int t = 0; t < kCrcThreads; ++t) h[t] = x8n(tb, (u64)kCrcPiece * (kCrcThreads - 1 - t));
+    cudaMemcpyToSymbol(c_piece_shift, h, sizeof(h));
+    shifts = true;
   }
-  u64 S = (len + kCrcSeg - 1) / kCrcSeg;
-  k_crc_seg<<<(unsigned)S, kCrcThreads, 0, s>>>(bucket + 32, len, scratch, tb);
-  k_crc_fin<<<1, 32, 0, s>>>(scratch, len, tb, out, hdr_crc, status, bad);
-  count_launch();
+  const u64 len = bytes > 32 ? bytes - 32 : 0;   // bytes is a multiple of 16
+  const u64 S = (len + kCrcSeg - 1) / kCrcSeg;
+  if (S) {
+    k_crc_seg<<<(unsigned)S, kCrcThreads, 0, s>>>(bucket + 32, len, S * kCrcSeg - len, scratch);
+    count_launch();
+  }
+  k_crc_fin<<<1, 1024, 0, s>>>(scratch, S, len, tb, out, hdr_crc, status, bad);
   count_launch();
 }
 
@@ -187,9 +227,8 @@ void crc_fill(u8* buckets, const BucketDesc* h_bks, u32 n_buckets, u32* scratch,
   }
 }
 
-void launch_crc_check(const u8* bucket, u64 bytes, u32* scratch, u32* status, cudaStream_t s) {
-  // scratch[0] = bad flag, scratch[1..] = segment CRCs
-  crc_bucket(bucket, bytes, scratch + 1, nullptr, bucket + 20, status, scratch, s);
+void launch_crc_check(const u8* bucket, u64 bytes, u32* seg_scratch, u32* bad_flag, u32* status, cudaStream_t s) {
+  crc_bucket(bucket, bytes, seg_scratch, nullptr, bucket + 20, status, bad_flag, s);
 }
 
 }  // namespace ss

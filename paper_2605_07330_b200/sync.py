@@ -160,6 +160,12 @@ class SparseSyncReceiver:
         self.ctx.sync_decompress_apply(bucket, bucket.numel() if nbytes is None else nbytes, self.weight_ptrs,
                                        stream)
 
+    def apply_many(self, buckets, stream=None):
+        """Several buckets in one batched decode (sync_decompress_apply_batched); each a uint8 device tensor
+        or (device address, nbytes)."""
+        self.ctx.sync_decompress_apply_batched(
+            [b if isinstance(b, tuple) else (b.data_ptr(), b.numel()) for b in buckets], self.weight_ptrs, stream)
+
     def check(self, stream=None):
         self.ctx.check("receiver", stream)
 

@@ -281,7 +281,17 @@ class PeerLink:
         self.local_free: dict[tuple, object] = {}
         self.ack_works = []
         self.copy_stream = torch.cuda.Stream(device=self.device) if mode == "copy" else None
+        self.span_bytes = 64 << 20
+        self._events, self._ev_i = [], 0
         self.last_in: dict[int, list] = {}
+
+    def _event(self):
+        """A reusable CUDA event (a ring of 64: far more than the spans in flight between two host syncs)."""
+        if len(self._events) < 64:
+            self._events.append(torch.cuda.Event())
+            return self._events[-1]
+        self._ev_i = (self._ev_i + 1) % len(self._events)
+        return self._events[self._ev_i]
 
     @staticmethod
     def _tag(kind: int, tag: int) -> int:
@@ -335,8 +345,8 @@ class PeerLink:
 
     # ------------------------------------------------------------------ receiver
     def receive(self, apply_fns: dict, tag: int = 0):
-        """apply_fns: {src rank: fn(bucket)} where bucket is a uint8 tensor (copy mode) or (ptr, nbytes)
-        (direct mode)."""
+        """apply_fns: {src rank: fn([(device address, nbytes), ...])} — a batch of buckets per call (e.g.
+        SparseSyncReceiver.apply_many): one copy span (copy mode) or all of src's buckets (direct mode)."""
         import ctypes
         cur = torch.cuda.current_stream(self.device)
         incoming = {}
@@ -371,8 +381,7 @@ class PeerLink:
                 continue
             if self.mode == "direct":
                 _wait(cur.cuda_stream, self.peer_ready[key])
-                for o, z in blist:
-                    apply_fns[src]((remote + o, z))
+                apply_fns[src]([(remote + o, z) for o, z in blist])
                 continue
             need = max(o + z for o, z in blist)
             buf = self.local.get(key)
@@ -382,13 +391,21 @@ class PeerLink:
             cs = self.copy_stream
             cs.wait_stream(cur)                            # the previous decode from this buffer was enqueued
             _wait(cs.cuda_stream, self.peer_ready[key])    # the Trainer's encode of this sync is done
-            for o, z in blist:
-                _pck(_plib().sync_peer_copy(ctypes.c_void_p(buf.data_ptr() + o), ctypes.c_void_p(remote + o), z,
-                                            ctypes.c_void_p(cs.cuda_stream)), "sync_peer_copy")
-                ev = torch.cuda.Event()
+            # consecutive buckets are pulled in spans of >= span_bytes (one copy + one event per span), so small
+            # buckets do not pay a copy launch and an event each; bucket b is decoded as soon as its span landed
+            i = 0
+            while i < len(blist):
+                j, lo = i, blist[i][0]
+                while j + 1 < len(blist) and blist[j][0] + blist[j][1] - lo < self.span_bytes:
+                    j += 1
+                hi = blist[j][0] + blist[j][1]
+                _pck(_plib().sync_peer_copy(ctypes.c_void_p(buf.data_ptr() + lo), ctypes.c_void_p(remote + lo),
+                                            hi - lo, ctypes.c_void_p(cs.cuda_stream)), "sync_peer_copy")
+                ev = self._event()
                 ev.record(cs)
                 cur.wait_event(ev)
-                apply_fns[src](buf[o:o + z])
+                apply_fns[src]([(buf.data_ptr() + o, z) for o, z in blist[i:j + 1]])   # one batched decode
+                i = j + 1
         if tag not in self.consumed:
             self.consumed[tag] = _PeerEvent()
         self.consumed[tag].record(cur.cuda_stream)
@@ -403,7 +420,8 @@ class PeerLink:
         return incoming
 
     def exchange(self, send_buf, blist, apply_fn, tag: int = 0, recv_buf=None):
-        """Ring step: announce our buckets to the next rank, then receive and apply the previous rank's."""
+        """Ring step: announce our buckets to the next rank, then receive and apply the previous rank's
+        (apply_fn takes a batch, as in receive)."""
         self.send(send_buf, blist, tag)
         src = self.srcs[0]
         if recv_buf is not None and self.mode == "copy" and (src, tag) not in self.local:

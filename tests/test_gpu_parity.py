@@ -176,6 +176,48 @@ def test_gpu_decoder_applies_oracle_buckets():
             assert (host16(w) == n).all()
 
 
+@pytest.mark.parametrize("crc", [False, True])
+def test_batched_decoder_applies_oracle_buckets(crc):
+    """sync_decompress_apply_batched over > 32 oracle buckets (two launches), given in shuffled order:
+    the buckets of one sync touch disjoint records, so any order yields the new weights bit-exactly."""
+    m = mixed_manifest()
+    olds, news = synth.generate(m, seed=12, rho=0.05)
+    ref = oracle.sync_pack(olds, news, limit=1024, crc=crc)
+    assert ref.n_buckets > 32
+    W = [to_dev(o) for o in olds]
+    rcv = ss.SparseSyncReceiver(W, crc=crc, bucket_limit=1024)
+    dev = [torch.from_numpy(np.frombuffer(ref.bucket(b), np.uint8).copy()).to(DEV) for b in range(ref.n_buckets)]
+    order = np.random.default_rng(0).permutation(len(dev))
+    rcv.apply_many([dev[k] for k in order])
+    torch.cuda.synchronize()
+    rcv.check()
+    for w, n in zip(W, news):
+        assert (host16(w) == n).all()
+
+
+def test_batched_decoder_isolates_a_bad_bucket():
+    """With CRC on, a corrupted bucket inside a batch is rejected (SYNC_ERR_CRC, none of its records applied)
+    while the other buckets of the same launch are applied."""
+    m = mixed_manifest()
+    olds, news = synth.generate(m, seed=13, rho=0.05)
+    ref = oracle.sync_pack(olds, news, limit=4096, crc=True)
+    bks = [np.frombuffer(ref.bucket(b), np.uint8).copy() for b in range(ref.n_buckets)]
+    bad = len(bks) // 2
+    bks[bad][len(bks[bad]) // 2] ^= 1
+    W = [to_dev(o) for o in olds]
+    rcv = ss.SparseSyncReceiver(W, crc=True, bucket_limit=4096)
+    rcv.apply_many([torch.from_numpy(b).to(DEV) for b in bks])
+    torch.cuda.synchronize()
+    assert rcv.ctx.sync_status() == ss.SYNC_ERR_CRC
+    # expected: the oracle applies every bucket except the bad one
+    exp = [o.copy() for o in olds]
+    for b in range(ref.n_buckets):
+        if b != bad:
+            assert oracle.bucket_apply(ref.bucket(b), exp) == oracle.OK
+    for w, e in zip(W, exp):
+        assert (host16(w) == e).all()
+
+
 def test_decompress_emits_extract():
     m = mixed_manifest()
     olds, news = synth.generate(m, seed=3, rho=0.1)

@@ -57,7 +57,7 @@ def _worker(rank, port, mode, groups, q):
                 blist = p.compress_pack()
                 if step == 0:
                     first[g] = [p.bucket(b).cpu().numpy().tobytes() for b in range(len(blist))]
-                link.exchange(p.buckets, blist, rcv.parts[g].apply, tag=g)
+                link.exchange(p.buckets, blist, rcv.parts[g].apply_many, tag=g)
             snd.commit(mode="swap")   # the two buffers trade roles: the syncs go v0 -> v1 -> v0 -> v1
             X, Y = Y, X
         torch.cuda.synchronize()
