@@ -53,6 +53,10 @@ def lib():
         u64, u32, i32, i64 = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_int64
         sig = {
             "or_extract": (u64, [P, P, u64, P, P]),
+            "or_bf16_rne": (ctypes.c_uint16, [u32]),
+            "or_bf16_rne_array": (None, [P, P, u64]),
+            "or_cast_track": (u64, [P, P, P, u64]),
+            "or_extract_tracked": (u64, [P, P, u64, P, P]),
             "or_apply": (i32, [P, u64, P, P, u64]),
             "or_index_mode": (i32, [P, u64]),
             "or_encode_indices": (u64, [P, u64, i32, P]),
@@ -99,6 +103,33 @@ def extract(old: np.ndarray, new: np.ndarray):
     I = np.empty(max(n, 1), np.uint32)
     V = np.empty(max(n, 1), np.uint16)
     c = lib().or_extract(_p(old), _p(new), n, _p(I), _p(V))
+    return I[:c].copy(), V[:c].copy()
+
+
+# ----------------------------------------------------------------------------- f1 cast-fused tracking
+def bf16_rne(master: np.ndarray) -> np.ndarray:
+    """Alg. 1 l.5 round_BF16 of fp32 masters (float32 array) -> uint16 bf16 bit patterns."""
+    m = np.ascontiguousarray(np.ascontiguousarray(master, np.float32).view(np.uint32).reshape(-1))
+    out = np.empty(m.size, np.uint16)
+    lib().or_bf16_rne_array(_p(m), _p(out), m.size)
+    return out
+
+
+def cast_track(master: np.ndarray, W: np.ndarray, tracked: np.ndarray) -> int:
+    """Alg. 1 l.4-7 on one tensor: W <- round_BF16(master) in place, tracked |= (W changed).
+    master float32, W uint16 bits, tracked uint8 (0/1). Returns |I_t|."""
+    m = np.ascontiguousarray(master, np.float32).view(np.uint32)
+    assert W.dtype == np.uint16 and W.flags.c_contiguous and tracked.dtype == np.uint8
+    assert m.size == W.size == tracked.size
+    return int(lib().or_cast_track(_p(m), _p(W), _p(tracked), W.size))
+
+
+def extract_tracked(W: np.ndarray, tracked: np.ndarray):
+    """Alg. 2 l.4-5 on the tracked set: (I ascending, V = W[I]); clears tracked."""
+    n = W.size
+    I = np.empty(max(n, 1), np.uint32)
+    V = np.empty(max(n, 1), np.uint16)
+    c = lib().or_extract_tracked(_p(W), _p(tracked), n, _p(I), _p(V))
     return I[:c].copy(), V[:c].copy()
 
 

@@ -14,7 +14,7 @@
  * Pins (tests/test_oracle_*.py): SPEC examples, hand-derived rANS golden
  * vectors (tests/golden/), CRC-32 check value and zlib, round-trip identities,
  * exact Eq. (1) payload identity, entropy bounds.
- * Parity status: extract/apply/index codec/bucketing pinned; the exact rANS
+ * Parity status: extract/apply/index codec/bucketing/cast-tracking pinned; the exact rANS
  * byte string is pinned only by FORMAT + hand golden vectors
  * (the paper fixes no coder).
  */
@@ -67,6 +67,58 @@ uint64_t or_extract(const uint16_t* old_bits, const uint16_t* new_bits, uint64_t
       if (I) I[count] = (uint32_t)i;
       if (V) V[count] = new_bits[i];
       ++count;
+    }
+  }
+  return count;
+}
+
+/* ---------------------------------------------------------------------------
+ * f1 cast-fused tracking — Alg. 1, the paper's own hook.
+ *
+ * or_bf16_rne: round_BF16 of CastAndCopy (Alg. 1 l.5) on the fp32 bit
+ * pattern: round to nearest, ties to even, by adding 0x7FFF + lsb and keeping
+ * the top 16 bits; NaN -> 0x7FC0 (DESIGN C18: the cast the PyTorch/Megatron
+ * training stack performs). Overflow rounds to +-Inf by the same addition.
+ * ------------------------------------------------------------------------- */
+uint16_t or_bf16_rne(uint32_t f) {
+  if (((f >> 23) & 0xFFu) == 0xFFu && (f & 0x7FFFFFu) != 0) return 0x7FC0;
+  uint32_t lsb = (f >> 16) & 1u;
+  return (uint16_t)((f + 0x7FFFu + lsb) >> 16);
+}
+
+void or_bf16_rne_array(const uint32_t* f, uint16_t* out, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = or_bf16_rne(f[i]);
+}
+
+/* One optimizer-step epilogue for one tensor (Alg. 1 l.4-7):
+ *   W_prev <- W; W <- round_BF16(W_main); I_t = { i | W^(i) != W_prev^(i) } (bitwise, C1);
+ *   cumulative set: tracked[i] |= [i in I_t]   (tracked: one byte per element, 0/1).
+ * Returns |I_t|.                                                            */
+uint64_t or_cast_track(const uint32_t* master_bits, uint16_t* W, uint8_t* tracked, uint64_t n) {
+  uint64_t changed = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint16_t w_prev = W[i];
+    uint16_t w = or_bf16_rne(master_bits[i]);
+    W[i] = w;
+    if (w != w_prev) {
+      tracked[i] = 1;
+      ++changed;
+    }
+  }
+  return changed;
+}
+
+/* Sync point on the tracked set (Alg. 2 l.4-5): I = ascending { i | tracked[i] },
+ * V = W[I] (the current values, so a superset still reconstructs W bit-exactly); the set is
+ * cleared for the next interval (Alg. 1 l.1, I_0 = {} ). Returns |I|; I/V may be NULL to only count. */
+uint64_t or_extract_tracked(const uint16_t* W, uint8_t* tracked, uint64_t n, uint32_t* I, uint16_t* V) {
+  uint64_t count = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (tracked[i]) {
+      if (I) I[count] = (uint32_t)i;
+      if (V) V[count] = W[i];
+      ++count;
+      tracked[i] = 0;
     }
   }
   return count;
