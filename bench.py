@@ -65,6 +65,10 @@ def parse():
                    help="N=1 only. separate: a third arena is the Rollout replica; snapshot: the decode+apply "
                         "writes into the Trainer's snapshot (it IS the commit, SURVEY config 1 loopback) and a "
                         "write-only toggle of the changed bits makes the next update (2 arenas: fits 30B at 10%%)")
+    p.add_argument("--tracking", choices=["snapshot", "cast"], default="snapshot",
+                   help="snapshot: diff new weights against the last-synced snapshot (north_star); cast: f1, the "
+                        "paper's own hook (Alg. 1): the fp32->bf16 CastAndCopy tracks the changed elements into a "
+                        "bitmap and the sync gathers them (no snapshot; the cast runs inside the timed step)")
     p.add_argument("--groups", type=int, default=0,
                    help="tensor groups per Trainer, pipelined through transfer/apply (0: 1 for ring, 4 otherwise)")
     p.add_argument("--seed", type=int, default=0)
@@ -243,6 +247,8 @@ class Rank:
         kw = dict(bucket_limit=int(args.bucket_mb * (1 << 20)), codec=codec, crc=args.crc)
         self.X = self.Y = self.R = None
         self.sender = None
+        self.tracking = args.tracking == "cast"
+        self.kstep = 0
         self.receivers = {}    # source rank -> GroupedReceiver
         if self.is_trainer:
             if sharded_model:
@@ -252,12 +258,15 @@ class Rank:
                 mt, tid0, self.seed = manifest, 0, args.seed + 1000 * d.rank
             self.mt = mt
             total = mt.total
-            self.X, self.Xv = sg.arena(mt, dev)   # trainer snapshot (swaps with Y under --commit swap)
-            self.Y, self.Yv = sg.arena(mt, dev)   # trainer current weights
-            sg.fill_old(self.Xv, mt, self.seed, tid0=tid0)
-            sg.fill_new(self.Xv, self.Yv, mt, self.seed, args.rho, MASKS[args.mask], tid0=tid0)
-            self.sender = GroupedSender(self.Xv, self.Yv, groups=self.G,
-                                        max_changed=min(total, int(total * args.rho * 1.02) + (1 << 20)), **kw)
+            cap = min(total, int(total * args.rho * 1.02) + (1 << 20))
+            if self.tracking:
+                self._setup_tracking(mt, tid0, cap, kw)
+            else:
+                self.X, self.Xv = sg.arena(mt, dev)   # trainer snapshot (swaps with Y under --commit swap)
+                self.Y, self.Yv = sg.arena(mt, dev)   # trainer current weights
+                sg.fill_old(self.Xv, mt, self.seed, tid0=tid0)
+                sg.fill_new(self.Xv, self.Yv, mt, self.seed, args.rho, MASKS[args.mask], tid0=tid0)
+                self.sender = GroupedSender(self.Xv, self.Yv, groups=self.G, max_changed=cap, **kw)
         self.loop_snapshot = args.replica == "snapshot"
         if self.loop_snapshot and (W != 1 or topo != "ring"):
             raise SystemExit("--replica snapshot is the N=1 loopback layout")
@@ -309,15 +318,52 @@ class Rank:
         self.toggle_scratch = torch.empty(ntens + 1, dtype=torch.int64, device=dev)
         self.S = 2 * self.mt.total if self.is_trainer else 0   # weights this rank syncs per step (as the sender)
 
+    def _setup_tracking(self, mt, tid0, cap, kw):
+        """f1 (Alg. 1): bf16 model weights W + two fp32 master versions M0 / M1 (the optimizer's outputs of
+        consecutive steps; they alternate, as the two weight versions do under --commit swap). Per tensor: the
+        synthetic old / new bf16 values, each master = that value + a relative perturbation below 2^-10 (under
+        half a bf16 ULP, so round_BF16 recovers it exactly) where the value changed, M1 = M0 elsewhere.
+        Setup only, not timed. W = round_BF16(M0) = old; the Rollout replica starts there too."""
+        from paper_2605_07330_b200 import ptr_table
+        from paper_2605_07330_b200.sync import GroupedSender
+        sg, dev, args = self.sg, self.d.dev, self.args
+        self.W, self.Wv = sg.arena(mt, dev)
+        self.M, self.Mv = [], []
+        for _ in range(2):
+            buf, views = sg.arena(mt, dev, dtype=torch.float32)
+            self.M.append(buf)
+            self.Mv.append(views)
+        mx = max(mt.numel) if mt.tensors else 1
+        o_t = torch.empty(mx, dtype=torch.int16, device=dev)
+        n_t = torch.empty(mx, dtype=torch.int16, device=dev)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(self.seed + 77)
+        for k, t in enumerate(mt.tensors):
+            m1 = synth.Manifest("one", [t])
+            o, n = o_t[:t.numel], n_t[:t.numel]
+            sg.fill_old([o], m1, self.seed, tid0=tid0 + k)
+            sg.fill_new([o], [n], m1, self.seed, args.rho, MASKS[args.mask], tid0=tid0 + k)
+            self.Wv[k].copy_(o)
+            fo = o.view(torch.bfloat16).float()
+            fn = n.view(torch.bfloat16).float()
+            u = torch.rand(t.numel, device=dev, generator=gen) * 2 - 1
+            self.Mv[0][k].copy_(fo + fo.abs() * 2.0 ** -10 * u)
+            self.Mv[1][k].copy_(torch.where(n != o, fn + fn.abs() * 2.0 ** -10 * u, self.Mv[0][k]))
+        del o_t, n_t
+        self.X = self.W          # what a Rollout must match (digests)
+        self.sender = GroupedSender(None, self.Wv, groups=self.G, max_changed=cap, master=self.Mv[0], **kw)
+        self.master_tables = [[ptr_table(self.Mv[v][lo:hi], dev) for v in range(2)]
+                              for lo, hi in self.sender.ranges]
+
     def receivers_all(self):
         return [p for g in self.receivers.values() for p in g.parts]
 
     def n_events(self):
-        return 3 * self.G + 4
+        return 4 * self.G + 4
 
     def step(self, ev=None, toggle: bool = True):
-        """One sync. ev: n_events() CUDA events: per group (extract start, extract end, compress end), then
-        transfer/apply end, commit end, update end, and a spare. toggle=False skips the synthetic update
+        """One sync. ev: n_events() CUDA events: per group (start, cast_track end, extract end, compress end),
+        then transfer/apply end, commit end, update end, and a spare. toggle=False skips the synthetic update
         (the final verification sync)."""
         snd = self.sender
         rec = (lambda i: ev[i].record()) if ev else (lambda i: None)
@@ -325,17 +371,26 @@ class Rank:
         G = self.G
         ring = a.topology == "ring"
         peer = isinstance(L, T.PeerLink)
-        ring_swap = ring and a.commit == "swap"
+        ring_swap = ring and a.commit == "swap" and not self.tracking
+        self.kstep += 1
         for g in range(G):
-            rec(3 * g)
+            rec(4 * g)
             if snd is not None:
                 p = snd.parts[g]
-                p.ctx.sync_extract_batched(p.old_ptrs, p.new_ptrs, p.I, p.V, p.counts)
-                rec(3 * g + 1)
+                if self.tracking:
+                    # the optimizer-step epilogue (Alg. 1 l.5-7): the masters of this step are the other version
+                    p.master_ptrs = self.master_tables[g][self.kstep % 2]
+                    p.cast_track()
+                    rec(4 * g + 1)
+                    p.extract()                 # I = the tracked set, V = W[I]
+                else:
+                    rec(4 * g + 1)
+                    p.ctx.sync_extract_batched(p.old_ptrs, p.new_ptrs, p.I, p.V, p.counts)
+                rec(4 * g + 2)
                 if L is not None:
                     L.fence(g)            # the previous sync's sends of group g have left its bucket buffer
                 blist = p.compress_pack()  # fused K2-K4 (blocking: host bucket plan)
-                rec(3 * g + 2)
+                rec(4 * g + 3)
                 if L is None:             # N = 1: the ring closes on itself
                     self.receivers[0].parts[g].apply_many([p.bucket(b) for b in range(len(blist))])
                 elif ring:
@@ -348,8 +403,9 @@ class Rank:
                 else:
                     L.send(p.buckets, blist, tag=g)
             else:
-                rec(3 * g + 1)
-                rec(3 * g + 2)
+                rec(4 * g + 1)
+                rec(4 * g + 2)
+                rec(4 * g + 3)
                 if peer:
                     L.receive({t: self.receivers[t].parts[g].apply_many for t in self.receivers}, tag=g)
                 elif isinstance(L, T.FanoutLink):
@@ -357,31 +413,34 @@ class Rank:
                 else:
                     src = next(iter(self.receivers))
                     L.receive(self.receivers[src].parts[g].apply, tag=g)
-        rec(3 * G)
-        if self.loop_snapshot:
-            pass                        # the decode+apply above wrote the snapshot: committed
+        rec(4 * G)
+        if self.loop_snapshot or self.tracking:
+            pass                        # committed by the decode+apply (loopback) / nothing to commit (f1)
         elif snd is not None:
             snd.commit(mode=a.commit)
             if a.commit == "swap":
                 self.X, self.Y, self.Xv, self.Yv = self.Y, self.X, self.Yv, self.Xv
-        rec(3 * G + 1)
+        rec(4 * G + 1)
         if snd is not None and (a.commit == "scatter" or self.loop_snapshot) and toggle:
             # snapshot == current now: the synthetic "optimizer step" flips the changed bits again so the
             # next sync has a fresh update of the same density (write-only scatter, input generation)
             for p in snd.parts:
                 self.sg.toggle(p.new_ptrs, p.I, p.V, p.counts, len(p.numel), self.toggle_scratch)
         # under --commit swap the two trainer buffers hold the two model versions v0 / v1 and trade roles
-        # every step, so every step syncs a genuine update (v0 -> v1, then v1 -> v0) with no generator work
-        rec(3 * G + 2)
+        # every step, so every step syncs a genuine update (v0 -> v1, then v1 -> v0) with no generator work;
+        # under --tracking cast the two fp32 master versions alternate the same way
+        rec(4 * G + 2)
 
     def phase_ms(self, ev):
-        """extract, compress_pack (summed over groups), transfer_apply (the rest of the sync loop on this
-        rank's stream: waiting for and applying buckets), commit, synthetic_update."""
+        """extract (+ cast_track under --tracking cast), compress_pack (summed over groups), transfer_apply (the
+        rest of the sync loop on this rank's stream: waiting for and applying buckets), commit,
+        synthetic_update, cast_track."""
         G = self.G
         t = lambda i, j: ev[i].elapsed_time(ev[j])  # noqa: E731
-        ext = sum(t(3 * g, 3 * g + 1) for g in range(G))
-        cmp = sum(t(3 * g + 1, 3 * g + 2) for g in range(G))
-        return [ext, cmp, t(0, 3 * G) - ext - cmp, t(3 * G, 3 * G + 1), t(3 * G + 1, 3 * G + 2)]
+        cast = sum(t(4 * g, 4 * g + 1) for g in range(G))
+        ext = sum(t(4 * g + 1, 4 * g + 2) for g in range(G))
+        cmp = sum(t(4 * g + 2, 4 * g + 3) for g in range(G))
+        return [ext, cmp, t(0, 4 * G) - cast - ext - cmp, t(4 * G, 4 * G + 1), t(4 * G + 1, 4 * G + 2), cast]
 
     def digests(self):
         """(trainer snapshot digest, {source: rollout digest of that source's range}) for the bit-exact check."""
@@ -466,7 +525,7 @@ def run_ours(args):
     # ---- sampled full-size parity + CPU baseline (rank 0, N = 1 only; before any step mutates X/Y)
     cpu = None
     parity = None
-    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
+    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline and not r.tracking:
         cpu = cpu_baseline(args, manifest, r.seed, args.cpu_sample_elems)
         # inputs: GPU twin == CPU twin on the sampled tensors
         gen_ok = all(np.array_equal(r.Xv[k].cpu().numpy().view(np.uint16), cpu["olds"][k]) and
@@ -521,6 +580,7 @@ def run_ours(args):
     ms = d.max(ms_local)
     phases = np.mean([r.phase_ms(e) for e in evs], axis=0)
     ext_ms_local = phases[0]
+    cast_ms_local = phases[5]
     if d.world > 1:  # per phase, the max over ranks (pair: extract on Trainers, apply on Rollouts)
         g = [None] * d.world
         d.dist.all_gather_object(g, phases.tolist(), group=d.ctrl)
@@ -544,6 +604,27 @@ def run_ours(args):
                 "syncs": len(lat), "what": "one sync after a barrier, max over ranks (extract start -> last "
                                            "apply/commit)"} if lat else None)
 
+    # ---- f1: the plain CastAndCopy the tracking replaces (torch's fp32 -> bf16 copy kernel, a library kernel
+    #      timed only for comparison) over up to 2^29 elements of the masters, scaled to this rank's elements
+    track_cmp = None
+    if r.tracking and r.sender is not None:
+        n_el = r.S // 2
+        k = min(n_el, 1 << 29)
+        src = r.M[0][:k]
+        dst = torch.empty(k, dtype=torch.bfloat16, device=d.dev)
+        dst.copy_(src)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            dst.copy_(src)
+        e1.record()
+        torch.cuda.synchronize()
+        plain = e0.elapsed_time(e1) / 5 * n_el / k
+        del dst
+        track_cmp = {"cast_track_ms": round(float(cast_ms_local), 4), "plain_cast_ms": round(plain, 4),
+                     "overhead": round(float(cast_ms_local) / plain - 1, 4),
+                     "plain_cast_source": f"torch copy_ fp32->bf16 over {k:,} elements, scaled to {n_el:,}"}
+
     # ---- verification: rollout replica == the Trainer's committed snapshot (bit-exact)
     verify = None
     if not args.no_verify:
@@ -562,7 +643,10 @@ def run_ours(args):
 
     # ---- e2e through the public API with host buffers (H2D of the new weights, D2H of the result)
     e2e = None
-    if not args.no_e2e and args.e2e_steps > 0:
+    if r.tracking and not args.no_e2e:
+        e2e = {"value": None, "unit": UNIT, "reason": "not measured under --tracking cast (the inputs are fp32 "
+                                                      "masters produced on the device by the optimizer)"}
+    elif not args.no_e2e and args.e2e_steps > 0:
         e2e = run_e2e(args, d, r)
 
     total_S = d.sum(r.S)
@@ -570,6 +654,17 @@ def run_ours(args):
     nnz_t, payload_t, raw_t = d.sum(nnz), d.sum(payload), d.sum(raw_payload)
     vbytes_t, n16_t, n32_t, nb_t = d.sum(vbytes), d.sum(n16), d.sum(n32), d.sum(nb)
     achieved = local_alg_extract / (ext_ms_local / 1e3) / 1e9   # rank 0 (a Trainer), its own launch
+    roof_kernel, roof_bytes = "k_extract (K1)", local_alg_extract
+    if r.tracking:
+        # f1: the dominant kernel is the cast with tracking. Algorithmic bytes per launch: read the fp32 master
+        # and the bf16 weights (6 B / element), write the 32 B sectors that changed and the bitmap words that
+        # gained a bit (read + write)
+        n_el = r.S // 2
+        f_sec = 1 - (1 - args.rho) ** 16
+        f_word = 1 - (1 - args.rho) ** 32
+        roof_kernel = "k_cast_track (f1, Alg. 1 CastAndCopy + tracking)"
+        roof_bytes = int(6 * n_el + 32 * f_sec * n_el / 16 + 8 * f_word * n_el / 32)
+        achieved = roof_bytes / (cast_ms_local / 1e3) / 1e9
     peak = peaks.get("hbm_gbs", 6650.0)
     # ncu dram bytes / algorithmic bytes of the profiled extract launch (profiles/extract_traffic.json,
     # from `ncu --set full` on the 30b-slice workload), applied to this launch's algorithmic bytes
@@ -602,13 +697,15 @@ def run_ours(args):
                    "elements_per_trainer_rank": r.S // 2, "model_elements": manifest.total,
                    "tensors": len(manifest.tensors),
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
-                   "groups": r.G, "replica": args.replica, "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
+                   "groups": r.G, "replica": args.replica, "tracking": args.tracking, "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
                    "l2": "inputs larger than L2 (2 x S per Trainer); no flush"},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
-                         zip(["extract", "compress_pack", "transfer_apply", "commit", "synthetic_update"], phases)},
-        "roofline": {"bound": "hbm", "kernel": "k_extract (K1)", "achieved": round(achieved, 1),
-                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "bytes_per_launch": local_alg_extract, "traffic_source": traffic_src,
+                         zip(["extract", "compress_pack", "transfer_apply", "commit", "synthetic_update",
+                              "cast_track"], phases)},
+        "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": round(achieved, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic if not r.tracking else None,
+                     "bytes_per_launch": roof_bytes, "traffic_source": traffic_src if not r.tracking else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
         "payload": {"nnz": int(nnz_t), "rho_measured": round(nnz_t / max(total_S / 2, 1), 6), "buckets": int(nb_t),
                     "bytes": int(payload_t), "x_comp": round(total_S / max(payload_t, 1), 2),
@@ -619,6 +716,8 @@ def run_ours(args):
         "clocks": clk, "gpu_launches": int(launches), "bit_exact_replica": verify, "e2e": e2e,
         "latency_per_update": latency,
     }
+    if track_cmp is not None:
+        out["tracking_vs_plain_cast"] = track_cmp
     if parity is not None:
         out["parity_sampled"] = parity
     if cpu is not None:

@@ -207,6 +207,29 @@ int sync_commit_snapshot(uint16_t* d_snapshot, const uint32_t* d_I, const uint16
 int sync_commit_snapshot_batched(sync_ctx* ctx, uint16_t* const* d_snapshot_ptrs, const uint32_t* d_I,
                                  const uint16_t* d_V, const uint64_t* d_counts, sync_stream_t stream);
 
+/* ---- f1 cast-fused tracking (Alg. 1; hook P:386) ----------
+ * The paper's own hook: the changed indices are collected inside the optimizer-step epilogue that casts the
+ * fp32 master weights into the bf16 model weights, and accumulate across steps into the cumulative set
+ * I_T (Alg. 1 l.7), a superset of the true delta that is harmless because absolute values are sent.
+ * No snapshot is kept; the sync reads the set (1 bit per element) and gathers V = W[I].
+ * The set is a caller-allocated, 16-byte aligned device bitmap of sync_bitmap_words() u32 words (zero it
+ * once); tensor t owns ceil(numel_t / 32) consecutive words in manifest order, starting at a multiple of 4
+ * words; bit b of word w = element 32 w + b.
+ * sync_cast_track_batched: for every manifest tensor, W[i] <- round_BF16(master[i]) (round to nearest even
+ *   on the fp32 bits, NaN -> 0x7FC0, DESIGN C18) and bit i |= (bits(W[i]) changed) (Alg. 1 l.5-7).
+ *   d_master_ptrs / d_weight_ptrs: device arrays of per-tensor pointers (fp32 / bf16 bits); 16-byte aligned
+ *   tensors take the vector path, others a scalar one. Only W sectors that changed are written.
+ * sync_extract_tracked: I = ascending set bits of each tensor (tensor-local, records contiguous in manifest
+ *   order exactly like sync_extract_batched), V = W[I], d_counts[t] = |I_t|; clears the bitmap when `clear`
+ *   (next interval, Alg. 1 l.1). Capacity = max_changed: beyond it nothing is written out of bounds,
+ *   d_counts hold the true counts, SYNC_ERR_CAPACITY is latched and the bitmap is left intact (retry with
+ *   a larger context). The output feeds sync_compress(_pack).                                             */
+int sync_bitmap_words(sync_ctx* ctx, uint64_t* words);
+int sync_cast_track_batched(sync_ctx* ctx, const float* const* d_master_ptrs, uint16_t* const* d_weight_ptrs,
+                            uint32_t* d_bitmap, sync_stream_t stream);
+int sync_extract_tracked(sync_ctx* ctx, uint16_t* const* d_weight_ptrs, uint32_t* d_bitmap, uint32_t* d_I,
+                         uint16_t* d_V, uint64_t* d_counts, int clear, sync_stream_t stream);
+
 /* ---- status ----------------------------------------------------------------
  * sync_status: BLOCKING; synchronises `stream`, reads and clears the device
  * status word, returns SYNC_OK or the first latched error.

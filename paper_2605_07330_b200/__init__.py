@@ -44,7 +44,7 @@ EXPORTS = [
     "sync_extract_status", "sync_extract_batched", "sync_enc_bound", "sync_compress", "sync_bucket_pack",
     "sync_buckets_bound", "sync_compress_pack", "sync_bucket_unpack", "sync_decompress", "sync_decompress_apply", "sync_decompress_apply_batched", "sync_apply",
     "sync_commit_snapshot", "sync_commit_snapshot_batched", "sync_status", "sync_ctx_stats", "sync_strerror",
-    "sync_launch_count",
+    "sync_launch_count", "sync_bitmap_words", "sync_cast_track_batched", "sync_extract_tracked",
 ]
 # NVLink peer-memory plumbing (include/sparsesync_peer.h)
 PEER_EXPORTS = [
@@ -110,6 +110,9 @@ def lib() -> ctypes.CDLL:
             "sync_commit_snapshot_batched": [P, P, P, P, P, P],
             "sync_status": [P, P],
             "sync_ctx_stats": [P, P, P],
+            "sync_bitmap_words": [P, P],
+            "sync_cast_track_batched": [P, P, P, P, P],
+            "sync_extract_tracked": [P, P, P, P, P, P, i32, P],
             "sync_peer_mem_export": [P, P, P, P],
             "sync_peer_mem_open": [P, P],
             "sync_peer_mem_close": [P],
@@ -307,6 +310,22 @@ class SyncContext:
         _ck(lib().sync_commit_snapshot_batched(self._h, _dev_ptr(snap_ptrs), _ptr(I), _ptr(V), _dev_ptr(counts),
                                                _stream(stream)), "sync_commit_snapshot_batched")
 
+    # -- f1 cast-fused tracking (Alg. 1) ---------------------------------------
+    def bitmap_words(self) -> int:
+        w = ctypes.c_uint64()
+        _ck(lib().sync_bitmap_words(self._h, ctypes.byref(w)), "sync_bitmap_words")
+        return w.value
+
+    def sync_cast_track_batched(self, master_ptrs: torch.Tensor, weight_ptrs: torch.Tensor, bitmap: torch.Tensor,
+                                stream=None):
+        _ck(lib().sync_cast_track_batched(self._h, _dev_ptr(master_ptrs), _dev_ptr(weight_ptrs), _dev_ptr(bitmap),
+                                          _stream(stream)), "sync_cast_track_batched")
+
+    def sync_extract_tracked(self, weight_ptrs: torch.Tensor, bitmap: torch.Tensor, I: torch.Tensor,
+                             V: torch.Tensor, counts: torch.Tensor, clear: bool = True, stream=None):
+        _ck(lib().sync_extract_tracked(self._h, _dev_ptr(weight_ptrs), _dev_ptr(bitmap), _dev_ptr(I), _dev_ptr(V),
+                                       _dev_ptr(counts), 1 if clear else 0, _stream(stream)), "sync_extract_tracked")
+
     # -- receiver -------------------------------------------------------------
     def sync_bucket_unpack(self, bucket: torch.Tensor, nbytes: int, views: torch.Tensor, n_records: torch.Tensor,
                            stream=None):
@@ -350,4 +369,4 @@ class SyncContext:
         return {n: int(getattr(s, n)) for n, _ in _Stats._fields_}
 
 
-from .sync import SparseSyncReceiver, SparseSyncSender  # noqa: E402,F401
+from .sync import SparseSyncReceiver, SparseSyncSender, TrackedSender  # noqa: E402,F401

@@ -25,7 +25,8 @@ constexpr u64 kAlign = 256;
 
 struct Layout {
   u64 numel, tile_prefix, tile_tensor, misc, tile_state, stage_ring, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
-  u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, rec_dst, totals, recs, bks, views, nviews, crc, total;
+  u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, rec_dst, totals, recs, bks, views, nviews, crc;
+  u64 bm_off, group_sum, total;
 };
 
 u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4 + 32; }  // + 32 bad flags
@@ -62,6 +63,8 @@ Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_change
   L.views = take(sizeof(sync_record_view) * (u64)T);
   L.nviews = take(8);
   L.crc = take(4ull * crc_n);
+  L.bm_off = take(8ull * (T + 1));                       // f1: bitmap word offset per tensor
+  L.group_sum = take(8ull * (n_tiles / 1024 + 2));       // f1: tile-offset scan groups
   L.total = o;
   return L;
 }
@@ -126,6 +129,7 @@ struct sync_ctx {
   sync_config cfg;
   std::vector<u64> numel, tile_prefix;
   std::vector<u32> tile_tensor;
+  std::vector<u64> bm_off;   // f1: bitmap word offset of each tensor (ceil(numel / 32) words each)
   u8* ws;
   Layout L;
   Plan plan;
@@ -177,6 +181,13 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   x->tile_tensor.resize(acc);
   for (u32 t = 0; t < d.T; ++t)
     for (u64 k = x->tile_prefix[t]; k < x->tile_prefix[t + 1]; ++k) x->tile_tensor[k] = t;
+  x->bm_off.resize(d.T + 1);
+  u64 wacc = 0;
+  for (u32 t = 0; t < d.T; ++t) {
+    x->bm_off[t] = wacc;
+    wacc += pad_to((x->numel[t] + 31) / 32, 4);   // every tensor's words start 16-byte aligned
+  }
+  x->bm_off[d.T] = wacc;
   cudaStream_t s = (cudaStream_t)stream;
   u8* w = x->ws;
   if (d.T) {
@@ -184,7 +195,8 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
         cudaMemcpyAsync(w + L.tile_prefix, x->tile_prefix.data(), 8ull * (d.T + 1), cudaMemcpyHostToDevice, s) !=
             cudaSuccess ||
         (acc && cudaMemcpyAsync(w + L.tile_tensor, x->tile_tensor.data(), 4ull * acc, cudaMemcpyHostToDevice, s) !=
-                    cudaSuccess)) {
+                    cudaSuccess) ||
+        cudaMemcpyAsync(w + L.bm_off, x->bm_off.data(), 8ull * (d.T + 1), cudaMemcpyHostToDevice, s) != cudaSuccess) {
       delete x;
       return SYNC_ERR_CUDA;
     }
@@ -297,6 +309,53 @@ int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const u
                          reinterpret_cast<const u32*>(x->ws + x->L.tile_tensor), x->plan.numel, x->d.T, x->d.n_tiles, d_I, d_V, x->cfg.max_changed, d_counts,
                          reinterpret_cast<u64*>(x->ws + x->L.tile_state),
                          reinterpret_cast<u32*>(x->ws + x->L.stage_ring), x->misc + 1, s);
+  CK(cudaGetLastError());
+  return SYNC_OK;
+}
+
+// ------------------------------------------------------------------------ f1 cast-fused tracking
+static TrackArgs track_args(sync_ctx* x, uint32_t* d_bitmap) {
+  TrackArgs a{};
+  a.n_tiles = x->d.n_tiles;
+  a.n_tensors = x->d.T;
+  a.tile_tensor = reinterpret_cast<const u32*>(x->ws + x->L.tile_tensor);
+  a.tile_prefix = reinterpret_cast<const u64*>(x->ws + x->L.tile_prefix);
+  a.numel = x->plan.numel;
+  a.bm_off = reinterpret_cast<const u64*>(x->ws + x->L.bm_off);
+  a.bitmap = d_bitmap;
+  a.tile_off = reinterpret_cast<u64*>(x->ws + x->L.tile_state);
+  a.group_sum = reinterpret_cast<u64*>(x->ws + x->L.group_sum);
+  a.cap = x->cfg.max_changed;
+  a.totals = x->plan.totals;
+  a.status = x->misc + 1;
+  return a;
+}
+
+int sync_bitmap_words(sync_ctx* x, uint64_t* words) {
+  if (!x || !words) return SYNC_ERR_ARG;
+  *words = x->bm_off.empty() ? 0 : x->bm_off.back();
+  return SYNC_OK;
+}
+
+int sync_cast_track_batched(sync_ctx* x, const float* const* d_master_ptrs, uint16_t* const* d_weight_ptrs,
+                            uint32_t* d_bitmap, sync_stream_t stream) {
+  if (!x || (x->d.T && (!d_master_ptrs || !d_weight_ptrs || !d_bitmap))) return SYNC_ERR_ARG;
+  if (x->d.T && !aligned16(d_bitmap)) return SYNC_ERR_ALIGNMENT;
+  launch_cast_track(track_args(x, d_bitmap), d_master_ptrs, d_weight_ptrs, 8 * x->sm_count, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return SYNC_OK;
+}
+
+int sync_extract_tracked(sync_ctx* x, uint16_t* const* d_weight_ptrs, uint32_t* d_bitmap, uint32_t* d_I,
+                         uint16_t* d_V, uint64_t* d_counts, int clear, sync_stream_t stream) {
+  if (!x || (x->d.T && (!d_weight_ptrs || !d_bitmap || !d_counts))) return SYNC_ERR_ARG;
+  x->plan_valid = false;
+  if (x->d.T == 0) return SYNC_OK;
+  TrackArgs a = track_args(x, d_bitmap);
+  a.counts = d_counts;
+  a.I = d_I;
+  a.V = d_V;
+  launch_extract_tracked(a, d_weight_ptrs, clear, 16 * x->sm_count, (cudaStream_t)stream);
   CK(cudaGetLastError());
   return SYNC_OK;
 }

@@ -93,6 +93,27 @@ void launch_decode(const uint8_t* const* buckets, const uint64_t* bytes, uint32_
                    uint16_t* V_out, uint64_t out_cap, uint32_t* status, const uint32_t* crc_bad, int grid,
                    cudaStream_t s);
 
+// track.cu (f1 cast-fused tracking, Alg. 1)
+struct TrackArgs {
+  uint64_t n_tiles;
+  uint32_t n_tensors;
+  const uint32_t* tile_tensor;   // [n_tiles]
+  const uint64_t* tile_prefix;   // [T+1]
+  const uint64_t* numel;         // [T]
+  const uint64_t* bm_off;        // [T+1] bitmap word offset of each tensor
+  uint32_t* bitmap;
+  uint64_t* tile_off;            // [n_tiles] tile counts -> offsets within their group
+  uint64_t* group_sum;           // [n_groups+1]
+  uint64_t* counts;              // [T]
+  uint32_t* I;
+  uint16_t* V;
+  uint64_t cap;
+  uint64_t* totals;
+  uint32_t* status;
+};
+void launch_cast_track(const TrackArgs& a, const float* const* master, uint16_t* const* W, int grid, cudaStream_t s);
+void launch_extract_tracked(const TrackArgs& a, uint16_t* const* W, int clear, int grid, cudaStream_t s);
+
 // apply.cu
 void launch_apply(uint16_t* W, const uint32_t* I, const uint16_t* V, uint64_t count, uint64_t numel,
                   uint32_t* status, cudaStream_t s);

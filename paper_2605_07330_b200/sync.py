@@ -138,6 +138,60 @@ class SparseSyncSender:
         return self.ctx.stats(stream)
 
 
+class TrackedSender(SparseSyncSender):
+    """Trainer side with the paper's own hook (f1; Alg. 1): no snapshot. `cast_track()` is the
+    optimizer-step epilogue (CastAndCopy W <- round_BF16(W_main) that also ORs the changed elements into the
+    cumulative set); `sync()` extracts I from the set with V = W[I] (Alg. 2 l.4-5) and packs the buckets.
+
+    master: fp32 master weights (one tensor per manifest entry); weights: the bf16 model weights W."""
+
+    def __init__(self, master, weights, **kw):
+        w = _flat_bits(weights)
+        super().__init__(w, w, **kw)            # snapshot == current: the extract path is never used
+        self.master = [m.reshape(-1) for m in master]
+        for m, x in zip(self.master, w):
+            if m.dtype != torch.float32 or m.numel() != x.numel():
+                raise SyncError(-1, "master must be fp32 and match the weights")
+        self.master_ptrs = ptr_table(self.master, self.device)
+        self.weight_ptrs = self.new_ptrs
+        self.bitmap = torch.zeros(max(self.ctx.bitmap_words(), 4), dtype=torch.int32, device=self.device)
+
+    def cast_track(self, stream=None):
+        """Alg. 1 l.5-7: W <- round_BF16(master); changed elements join the cumulative set."""
+        self.ctx.sync_cast_track_batched(self.master_ptrs, self.weight_ptrs, self.bitmap, stream)
+
+    def extract(self, stream=None, clear: bool = True):
+        self.ctx.sync_extract_tracked(self.weight_ptrs, self.bitmap, self.I, self.V, self.counts, clear, stream)
+
+    def compress_pack(self, stream=None):
+        if self.buckets.numel() == 0:
+            self.buckets = torch.empty(int(3.5 * self.cap) + 64 * len(self.numel) + 4096, dtype=torch.uint8,
+                                       device=self.device)
+        for _ in range(3):
+            try:
+                self.bucket_list = self.ctx.sync_compress_pack(self.I, self.V, self.counts, self.buckets, stream)
+                return self.bucket_list
+            except SyncError as e:
+                if e.code != SYNC_ERR_CAPACITY:
+                    raise
+                self.ctx.sync_status(stream)
+                stats = self.ctx.stats(stream)
+                if stats["nnz"] > self.cap:   # the set was kept (nothing cleared): grow and extract again
+                    self._alloc(min(sum(self.numel), int(stats["nnz"] * 1.1) + 65536))
+                    self.extract(stream)
+                if getattr(e, "need", 0) > self.buckets.numel():
+                    self.buckets = torch.empty(int(e.need * 1.05) + 4096, dtype=torch.uint8, device=self.device)
+        raise SyncError(SYNC_ERR_CAPACITY, "sync_compress_pack: could not size the buffers")
+
+    def sync(self, stream=None, fused: bool = True):
+        self.extract(stream)
+        return self.compress_pack(stream)
+
+    def commit(self, stream=None, mode: str = "none"):
+        """Nothing to commit: the cumulative set was cleared by the extract (Alg. 1 l.1 of the next interval)."""
+        return
+
+
 class SparseSyncReceiver:
     """Rollout side: holds the weights and applies buckets in place (bit-exact)."""
 
@@ -177,9 +231,12 @@ class GroupedSender:
     side uses a GroupedReceiver built from the same tensor list and G."""
 
     def __init__(self, snapshot, current, groups: int = 1, max_changed: int | None = None,
-                 expected_density: float = 0.02, **kw):
+                 expected_density: float = 0.02, master=None, **kw):
+        """master: fp32 master weights -> every group is a TrackedSender (f1, Alg. 1) over (master, current);
+        `snapshot` is then unused."""
         from .transport import shard_ranges
-        snap, cur = list(snapshot), list(current)
+        cur = list(current)
+        snap = list(snapshot) if master is None else cur
         numel = [t.numel() for t in cur]
         self.ranges = shard_ranges(numel, max(1, min(groups, len(numel))))
         total = max(sum(numel), 1)
@@ -187,8 +244,12 @@ class GroupedSender:
         for lo, hi in self.ranges:
             n = sum(numel[lo:hi])
             cap = None if max_changed is None else min(n, int(max_changed * n / total) + (1 << 16))
-            self.parts.append(SparseSyncSender(snap[lo:hi], cur[lo:hi], max_changed=cap,
-                                               expected_density=expected_density, **kw))
+            if master is None:
+                self.parts.append(SparseSyncSender(snap[lo:hi], cur[lo:hi], max_changed=cap,
+                                                   expected_density=expected_density, **kw))
+            else:
+                self.parts.append(TrackedSender(list(master)[lo:hi], cur[lo:hi], max_changed=cap,
+                                                expected_density=expected_density, **kw))
 
     def commit(self, stream=None, mode: str = "scatter"):
         for p in self.parts:
