@@ -18,6 +18,7 @@
 //                   the words cleared (next interval, Alg. 1 l.1).
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace ss {
 
@@ -36,81 +37,166 @@ __device__ __forceinline__ u32 tile_words(u64 numel, u64 tile_base) {
   return (u32)((ne + 31) / 32);
 }
 
-// Warp-cooperative: a warp takes 1024 consecutive elements per iteration; lane l handles elements
-// 128k + 4l (k = 0..7): 16-byte fp32 loads and 8-byte bf16 loads, every load instruction covering 512 / 256
-// contiguous bytes. Change bits: a 4-bit nibble per lane and k; the 8 lanes of a 32-element word OR their
-// nibbles together (3 shuffles), lane 8j writes word j. Sectors (16 elements = 4 lanes) are stored whole when
-// any of their elements changed.
-__global__ void __launch_bounds__(kTT, 4) k_cast_track(TrackArgs a, const float* const* master, u16* const* W) {
-  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (u64 tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-    const u32 t = a.tile_tensor[tile];
-    const u64 n = a.numel[t];
-    const u64 base = (tile - a.tile_prefix[t]) * kTile;
-    const u64 ne = (n - base) < kTile ? (n - base) : kTile;
-    const float* M = master[t] + base;
-    u16* Wt = W[t] + base;
-    u32* bm = a.bitmap + a.bm_off[t] + base / 32;
-    const bool vec = ((((uintptr_t)M) & 15u) | (((uintptr_t)Wt) & 7u)) == 0;   // else the scalar path
-    for (u32 c = warp; c * 1024 < ne; c += kTT / 32) {
-      const u32 e0 = c * 1024;
-      uint4 m[8];
-      uint2 o[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const u32 e = e0 + 128 * k + 4 * lane;
-        if (vec && e + 4 <= ne) {
-          m[k] = *reinterpret_cast<const uint4*>(M + e);
-          o[k] = *reinterpret_cast<const uint2*>(Wt + e);
-        } else {
-          u32 mf[4] = {0, 0, 0, 0}, ow[4] = {0, 0, 0, 0};
-#pragma unroll
-          for (u32 q = 0; q < 4; ++q)
-            if (e + q < ne) {
-              mf[q] = __float_as_uint(M[e + q]);
-              ow[q] = Wt[e + q];
-            }
-          m[k] = make_uint4(mf[0], mf[1], mf[2], mf[3]);
-          o[k] = make_uint2(ow[0] | (ow[1] << 16), ow[2] | (ow[3] << 16));
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const u32 e = e0 + 128 * k + 4 * lane;
-        const u32 valid = e >= ne ? 0u : (e + 4 <= ne ? 0xFu : ((1u << (ne - e)) - 1u));
-        const u32 r0 = (u32)bf16_rne(m[k].x) | ((u32)bf16_rne(m[k].y) << 16);
-        const u32 r1 = (u32)bf16_rne(m[k].z) | ((u32)bf16_rne(m[k].w) << 16);
-        const u32 x0 = r0 ^ o[k].x, x1 = r1 ^ o[k].y;
-        const u32 nib = (((x0 & 0xFFFFu) ? 1u : 0u) | ((x0 >> 16) ? 2u : 0u) | ((x1 & 0xFFFFu) ? 4u : 0u) |
-                         ((x1 >> 16) ? 8u : 0u)) & valid;
-        // sector of 16 elements = lanes 4s..4s+3: store it whole if any of them changed
-        u32 sec = nib;
-        sec |= __shfl_xor_sync(0xffffffffu, sec, 1);
-        sec |= __shfl_xor_sync(0xffffffffu, sec, 2);
-        if (sec) {
-          if (vec && e + 4 <= ne) {
-            *reinterpret_cast<uint2*>(Wt + e) = make_uint2(r0, r1);
-          } else {
-            const u16 rv[4] = {(u16)r0, (u16)(r0 >> 16), (u16)r1, (u16)(r1 >> 16)};
-#pragma unroll
-            for (u32 q = 0; q < 4; ++q)
-              if (nib & (1u << q)) Wt[e + q] = rv[q];
-          }
-        }
-        // word of 32 elements = lanes 8j..8j+7 (4 bits each)
-        u32 word = nib << (4 * (lane & 7));
-        word |= __shfl_xor_sync(0xffffffffu, word, 1);
-        word |= __shfl_xor_sync(0xffffffffu, word, 2);
-        word |= __shfl_xor_sync(0xffffffffu, word, 4);
-        if ((lane & 7) == 0 && word) {
-          u32* wp = bm + (e0 + 128 * k) / 32 + (lane >> 3);
-          const u32 old = *wp;
-          if ((old | word) != old) *wp = old | word;
-        }
-      }
+// TMA-fed persistent kernel (the K1 pattern): a producer warp streams each tile's fp32 masters and bf16
+// weights in 4096-element stages (16 KB + 8 KB) into shared memory with cp.async.bulk + mbarrier
+// complete_tx (L2 evict-first); 16 consumer warps take 256 elements of a stage each: lane l handles elements
+// 128k + 4l (k = 0, 1) from shared memory, rounds to bf16, ORs the 4-bit change nibbles of the 8 lanes of a
+// 32-element word (3 shuffles; lane 8j writes word j) and stores the 32-byte sectors (4 lanes) that changed.
+constexpr int kCStages = 4;
+constexpr u32 kCSub = 4096;                               // elements per stage
+constexpr u32 kCStageBytes = kCSub * 6;                   // 16 KB fp32 + 8 KB bf16
+constexpr int kCConsumers = 512;
+constexpr int kCBlock = kCConsumers + 32;
+
+struct CastInfo {
+  const float* M;   // nullptr = no more work
+  u16* W;
+  u32* bm;
+  u32 n_valid;
+  u32 bulk;         // elements delivered by the bulk copies (multiple of 8)
+};
+
+__device__ __forceinline__ void cast_quad(const uint4& m, const uint2& o, u32 valid, u16* wdst, bool full,
+                                          u32* word_dst, u32 lane) {
+  const u32 r0 = (u32)bf16_rne(m.x) | ((u32)bf16_rne(m.y) << 16);
+  const u32 r1 = (u32)bf16_rne(m.z) | ((u32)bf16_rne(m.w) << 16);
+  const u32 x0 = r0 ^ o.x, x1 = r1 ^ o.y;
+  const u32 nib = (((x0 & 0xFFFFu) ? 1u : 0u) | ((x0 >> 16) ? 2u : 0u) | ((x1 & 0xFFFFu) ? 4u : 0u) |
+                   ((x1 >> 16) ? 8u : 0u)) & valid;
+  u32 sec = nib;   // sector of 16 elements = lanes 4s..4s+3: stored whole if any of them changed
+  sec |= __shfl_xor_sync(0xffffffffu, sec, 1);
+  sec |= __shfl_xor_sync(0xffffffffu, sec, 2);
+  if (sec) {
+    if (full) {
+      *reinterpret_cast<uint2*>(wdst) = make_uint2(r0, r1);
+    } else {
+      if (nib & 1u) wdst[0] = (u16)r0;
+      if (nib & 2u) wdst[1] = (u16)(r0 >> 16);
+      if (nib & 4u) wdst[2] = (u16)r1;
+      if (nib & 8u) wdst[3] = (u16)(r1 >> 16);
     }
   }
+  u32 word = nib << (4 * (lane & 7));   // word of 32 elements = lanes 8j..8j+7
+  word |= __shfl_xor_sync(0xffffffffu, word, 1);
+  word |= __shfl_xor_sync(0xffffffffu, word, 2);
+  word |= __shfl_xor_sync(0xffffffffu, word, 4);
+  // fire-and-forget OR (RED): no read round trip stalls the warp (a word has one writer per launch, the
+  // atomic only avoids the load of a plain read-modify-write)
+  if ((lane & 7) == 0 && word) atomicOr(word_dst, word);
 }
+
+__global__ void __launch_bounds__(kCBlock, 2) k_cast_track(TrackArgs a, const float* const* master,
+                                                           u16* const* W) {
+  extern __shared__ __align__(128) u8 smem[];
+  u64* full = reinterpret_cast<u64*>(smem + kCStages * kCStageBytes);
+  u64* empty = full + kCStages;
+  CastInfo* info = reinterpret_cast<CastInfo*>(empty + kCStages);
+  const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < kCStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kCConsumers / 32) {
+    // ---------------------------------------------------------------- producer warp
+    const u64 pol = policy_evict_first();
+    u32 it = 0;
+    for (u64 tile = blockIdx.x;; tile += gridDim.x) {
+      const bool done = tile >= a.n_tiles;
+      u32 t = 0;
+      u64 base = 0, ne = 0;
+      if (!done) {
+        t = a.tile_tensor[tile];
+        const u64 n = a.numel[t];
+        base = (tile - a.tile_prefix[t]) * kTile;
+        ne = (n - base) < kTile ? (n - base) : kTile;
+      }
+      const u32 n_sub = done ? 1u : (u32)((ne + kCSub - 1) / kCSub);
+      const float* M0 = done ? nullptr : master[t] + base;
+      u16* W0 = done ? nullptr : W[t] + base;
+      u32* bm0 = done ? nullptr : a.bitmap + a.bm_off[t] + base / 32;
+      const bool aligned = ((((uintptr_t)M0) | ((uintptr_t)W0)) & 15u) == 0;
+      for (u32 sub = 0; sub < n_sub; ++sub, ++it) {
+        const u32 s = it % kCStages;
+        if (it >= (u32)kCStages) mbar_wait(&empty[s], ((it / kCStages) - 1) & 1);
+        if (lane == 0) {
+          CastInfo ci;
+          if (done) {
+            ci.M = nullptr;
+            info[s] = ci;
+            mbar_arrive(&full[s]);
+          } else {
+            const u64 e0 = (u64)sub * kCSub;
+            const u32 nv = (u32)((ne - e0) < kCSub ? (ne - e0) : kCSub);
+            ci.M = M0 + e0;
+            ci.W = W0 + e0;
+            ci.bm = bm0 + e0 / 32;
+            ci.n_valid = nv;
+            ci.bulk = aligned ? (nv & ~7u) : 0u;
+            info[s] = ci;
+            u8* dst = smem + (size_t)s * kCStageBytes;
+            if (ci.bulk) {
+              mbar_arrive_tx(&full[s], 6u * ci.bulk);
+              bulk_g2s(dst, ci.M, 4u * ci.bulk, &full[s], pol);
+              bulk_g2s(dst + 4 * kCSub, ci.W, 2u * ci.bulk, &full[s], pol);
+            } else {
+              mbar_arrive(&full[s]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (done) break;
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumer warps
+  for (u32 it = 0;; ++it) {
+    const u32 s = it % kCStages;
+    mbar_wait(&full[s], (it / kCStages) & 1);
+    const CastInfo ci = info[s];
+    if (ci.M == nullptr) break;
+    const float* sm = reinterpret_cast<const float*>(smem + (size_t)s * kCStageBytes);
+    const u16* sw = reinterpret_cast<const u16*>(smem + (size_t)s * kCStageBytes + 4 * kCSub);
+    constexpr u32 kPerWarp = kCSub / (kCConsumers / 32);   // elements of a stage per consumer warp
+#pragma unroll
+    for (int k = 0; k < (int)(kPerWarp / 128); ++k) {
+      const u32 e = kPerWarp * warp + 128 * k + 4 * lane;
+      uint4 m = make_uint4(0, 0, 0, 0);
+      uint2 o = make_uint2(0, 0);
+      u32 valid = 0;
+      bool fullq = false;
+      if (e + 4 <= ci.bulk) {
+        m = *reinterpret_cast<const uint4*>(sm + e);
+        o = *reinterpret_cast<const uint2*>(sw + e);
+        valid = 0xFu;
+        fullq = true;
+      } else if (e < ci.n_valid) {   // tail / unaligned: straight from global
+        u32 mf[4] = {0, 0, 0, 0}, ow[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (u32 q = 0; q < 4; ++q)
+          if (e + q < ci.n_valid) {
+            mf[q] = __float_as_uint(ci.M[e + q]);
+            ow[q] = ci.W[e + q];
+            valid |= 1u << q;
+          }
+        m = make_uint4(mf[0], mf[1], mf[2], mf[3]);
+        o = make_uint2(ow[0] | (ow[1] << 16), ow[2] | (ow[3] << 16));
+        fullq = false;
+      }
+      cast_quad(m, o, valid, ci.W + e, fullq, ci.bm + (kPerWarp * warp + 128 * k) / 32 + (lane >> 3), lane);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+static size_t cast_smem() { return (size_t)kCStages * kCStageBytes + 2 * kCStages * 8 + kCStages * sizeof(CastInfo); }
 
 __device__ __forceinline__ u32 block_sum32(u32 v, u32* s) {
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -261,7 +347,19 @@ __global__ void __launch_bounds__(kTT) k_track_write(TrackArgs a, u16* const* W,
 
 void launch_cast_track(const TrackArgs& a, const float* const* master, u16* const* W, int grid, cudaStream_t s) {
   if (!a.n_tiles) return;
-  k_cast_track<<<grid, kTT, 0, s>>>(a, master, W);
+  static int cap = 0;
+  const size_t sm = cast_smem();
+  if (!cap) {
+    cudaFuncSetAttribute(k_cast_track, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int dev = 0, n_sm = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cast_track, kCBlock, sm);
+    cap = n_sm * (per > 0 ? per : 1);
+  }
+  (void)grid;
+  const u64 g = a.n_tiles < (u64)cap ? a.n_tiles : (u64)cap;   // persistent: every CTA resident
+  k_cast_track<<<(unsigned)g, kCBlock, sm, s>>>(a, master, W);
   count_launch();
 }
 
