@@ -53,6 +53,8 @@ def lib():
         u64, u32, i32, i64 = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_int64
         sig = {
             "or_extract": (u64, [P, P, u64, P, P]),
+            "or_full_record_bytes": (u64, [u64]),
+            "or_encode_full_record": (u64, [u32, P, u64, i32, P]),
             "or_bf16_rne": (ctypes.c_uint16, [u32]),
             "or_bf16_rne_array": (None, [P, P, u64]),
             "or_cast_track": (u64, [P, P, P, u64]),
@@ -187,6 +189,14 @@ def rans_decode(block: bytes, n: int):
 
 
 # ----------------------------------------------------------------------------- records
+def encode_full_record(tensor_id: int, W, codec: int = CODEC_COMPRESSED) -> bytes:
+    """f3 FULL record: the whole tensor's current values."""
+    W = _u16(W).ravel()
+    out = np.zeros(int(lib().or_full_record_bytes(W.size)), np.uint8)
+    n = lib().or_encode_full_record(tensor_id, _p(W), W.size, codec, _p(out))
+    return out[:n].tobytes()
+
+
 def encode_record(tensor_id: int, I, V, codec: int = CODEC_COMPRESSED) -> bytes:
     I = np.ascontiguousarray(I, np.uint32)
     V = np.ascontiguousarray(V, np.uint16)
@@ -226,7 +236,7 @@ class PackResult:
         self.buf = buf
         self.offsets = offsets
         self.sizes = sizes
-        self.stats = dict(zip(["nnz", "n_records", "delta16", "abs32", "payload_bytes", "value_bytes"],
+        self.stats = dict(zip(["nnz", "n_records", "delta16", "abs32", "payload_bytes", "value_bytes", "full"],
                               [int(s) for s in stats]))
 
     @property
@@ -239,8 +249,9 @@ class PackResult:
 
 
 def sync_pack(olds, news, codec: int = CODEC_COMPRESSED, limit: int = 256 << 20, crc: bool = False,
-              max_buckets: int = 1 << 16) -> PackResult:
-    """Sender path (Alg. 2) over a manifest of (old, new) uint16 arrays."""
+              max_buckets: int = 1 << 16, route: bool = False) -> PackResult:
+    """Sender path (Alg. 2) over a manifest of (old, new) uint16 arrays.
+    route: per-parameter routing (f3) — a record goes FULL when that is smaller (DESIGN C19)."""
     olds = [_u16(o).ravel() for o in olds]
     news = [_u16(n).ravel() for n in news]
     T = len(olds)
@@ -255,9 +266,10 @@ def sync_pack(olds, news, codec: int = CODEC_COMPRESSED, limit: int = 256 << 20,
     buf = np.zeros(cap, np.uint8)
     offs = np.zeros(max_buckets, np.uint64)
     sizes = np.zeros(max_buckets, np.uint64)
-    stats = np.zeros(6, np.uint64)
+    stats = np.zeros(7, np.uint64)
+    flags = (1 if crc else 0) | (2 if route else 0)
     nb = L.or_sync_pack(T, _p(numel), ctypes.cast(op, ctypes.c_void_p), ctypes.cast(np_, ctypes.c_void_p),
-                        codec, limit, 1 if crc else 0, _p(buf), cap, _p(offs), _p(sizes), max_buckets,
+                        codec, limit, flags, _p(buf), cap, _p(offs), _p(sizes), max_buckets,
                         _p(stats))
     if nb < 0:
         raise RuntimeError(f"or_sync_pack failed: {nb}")

@@ -380,6 +380,29 @@ uint64_t or_encode_record(uint32_t tensor_id, const uint32_t* I, const uint16_t*
   return total;
 }
 
+/* ---------------------------------------------------------------------------
+ * f3 per-parameter routing — WeightUpdater: "parameters that change on
+ * nearly every element each step are transmitted via a full-weight copy".
+ * FULL record (idx_mode 2): header {tensor_id, nnz field = numel,
+ * record_bytes, mode 2, dtype 1, codec} || numel x u16 LE current values || zero
+ * pad to 16. Routing rule (DESIGN C19): a record goes FULL iff its FULL size is
+ * strictly smaller than its sparse (I, V) record.
+ * ------------------------------------------------------------------------- */
+enum { OR_FULL = 2 };
+
+uint64_t or_full_record_bytes(uint64_t numel) { return pad_to(16 + 2 * numel, 16); }
+
+uint64_t or_encode_full_record(uint32_t tensor_id, const uint16_t* W, uint64_t numel, int codec, uint8_t* out) {
+  uint64_t total = or_full_record_bytes(numel);
+  for (uint64_t i = 0; i < numel; ++i) put16(out + 16 + 2 * i, W[i]);
+  memset(out + 16 + 2 * numel, 0, total - 16 - 2 * numel);
+  put32(out + 0, tensor_id);
+  put32(out + 4, (uint32_t)numel);
+  put32(out + 8, (uint32_t)total);
+  out[12] = OR_FULL; out[13] = 1; out[14] = (uint8_t)codec; out[15] = 0;
+  return total;
+}
+
 /* Decodes one record (exact inverse, Alg. 3 l.5) into I, V
  * (nnz entries). Returns 0 or an error; *tensor_id/*nnz filled. */
 int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, uint64_t* nnz_out,
@@ -388,10 +411,18 @@ int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, ui
   uint32_t tid = get32(rec), nnz = get32(rec + 4), rb = get32(rec + 8);
   uint8_t mode = rec[12], dtype = rec[13], codec = rec[14];
   if (rb > avail || rb < 16 || (rb % 16) != 0) return OR_ERR_TRUNCATED;
-  if (dtype != 1 || mode > 1 || codec > 1 || nnz == 0) return OR_ERR_CORRUPT;
+  if (dtype != 1 || mode > 2 || codec > 1 || nnz == 0) return OR_ERR_CORRUPT;
   *tensor_id = tid;
   *nnz_out = nnz;
   if (nnz > cap) return OR_ERR_CAPACITY;
+  if (mode == OR_FULL) {                /* every element, in order */
+    if (16 + 2ull * nnz > rb) return OR_ERR_CORRUPT;
+    for (uint64_t k = 0; k < nnz; ++k) {
+      I[k] = (uint32_t)k;
+      V[k] = get16(rec + 16 + 2 * k);
+    }
+    return OR_OK;
+  }
   if (codec == OR_CODEC_RAW) {
     if (mode != OR_ABS32 || 16 + 6ull * nnz > rb) return OR_ERR_CORRUPT;
     for (uint64_t k = 0; k < nnz; ++k) I[k] = get32(rec + 16 + 4 * k);
@@ -472,13 +503,14 @@ uint32_t or_bucketize(const uint64_t* rec_bytes, uint64_t n_records, uint64_t li
  * l.6) per tensor, in manifest order. Writes buckets into out (bucket b at
  * offsets[b], 256-aligned), sizes[b]. Returns n_buckets or a negative error.
  * stats (may be NULL): [0] total nnz, [1] n_records, [2] delta16 records,
- * [3] abs32 records, [4] payload bytes (Σ bucket bytes), [5] value-stream bytes.
+ * [3] abs32 records, [4] payload bytes (Σ bucket bytes), [5] value-stream bytes,
+ * [6] FULL records (flags bit 1 = routing, f3).
  * ------------------------------------------------------------------------- */
 int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const uint16_t* const* old_ptrs,
                      const uint16_t* const* new_ptrs, int codec, uint64_t limit, uint32_t flags,
                      uint8_t* out, uint64_t out_cap, uint64_t* offsets, uint64_t* sizes,
                      uint32_t max_buckets, uint64_t* stats) {
-  uint64_t st[6] = {0};
+  uint64_t st[7] = {0};
   /* 1. per tensor records into a scratch stream */
   uint64_t cap_total = 0;
   for (uint32_t t = 0; t < n_tensors; ++t) cap_total += or_record_bound(numel[t] ? numel[t] : 1);
@@ -494,13 +526,18 @@ int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const uint16_t* 
     uint64_t nnz = or_extract(old_ptrs[t], new_ptrs[t], n, I, V);
     if (nnz > 0) {
       uint64_t rb = or_encode_record(t, I, V, nnz, codec, stream + pos);
+      int full = (flags & 2u) && or_full_record_bytes(n) < rb;   /* routing, DESIGN C19 */
+      if (full) rb = or_encode_full_record(t, new_ptrs[t], n, codec, stream + pos);
       rec_bytes[n_records] = rb;
       rec_pos[n_records] = pos;
-      rec_chunks[n_records] = (uint32_t)((nnz + OR_C - 1) / OR_C);
+      rec_chunks[n_records] = (uint32_t)(((full ? n : nnz) + OR_C - 1) / OR_C);
       ++n_records;
       pos += rb;
       st[0] += nnz;
-      if (codec == OR_CODEC_COMPRESSED) {
+      if (full) {
+        st[6] += 1;
+        st[5] += rb - 16;
+      } else if (codec == OR_CODEC_COMPRESSED) {
         int mode = stream[pos - rb + 12];
         st[mode == OR_DELTA16 ? 2 : 3] += 1;
         uint64_t ib = (mode == OR_DELTA16 ? 2 : 4) * nnz;
