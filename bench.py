@@ -69,6 +69,8 @@ def parse():
                    help="snapshot: diff new weights against the last-synced snapshot (north_star); cast: f1, the "
                         "paper's own hook (Alg. 1): the fp32->bf16 CastAndCopy tracks the changed elements into a "
                         "bitmap and the sync gathers them (no snapshot; the cast runs inside the timed step)")
+    p.add_argument("--route", action="store_true",
+                   help="f3 per-parameter routing (P:389): records whose FULL copy is smaller go FULL")
     p.add_argument("--groups", type=int, default=0,
                    help="tensor groups per Trainer, pipelined through transfer/apply (0: 1 for ring, 4 otherwise)")
     p.add_argument("--seed", type=int, default=0)
@@ -245,6 +247,7 @@ class Rank:
         self.shards = transport.shard_ranges(manifest.numel, half) if sharded_model else None
         codec = ss.SYNC_CODEC_COMPRESSED if args.codec == "compressed" else ss.SYNC_CODEC_RAW
         kw = dict(bucket_limit=int(args.bucket_mb * (1 << 20)), codec=codec, crc=args.crc)
+        rkw = dict(kw, route=args.route)   # routing is a sender-side choice
         self.X = self.Y = self.R = None
         self.sender = None
         self.tracking = args.tracking == "cast"
@@ -260,13 +263,13 @@ class Rank:
             total = mt.total
             cap = min(total, int(total * args.rho * 1.02) + (1 << 20))
             if self.tracking:
-                self._setup_tracking(mt, tid0, cap, kw)
+                self._setup_tracking(mt, tid0, cap, rkw)
             else:
                 self.X, self.Xv = sg.arena(mt, dev)   # trainer snapshot (swaps with Y under --commit swap)
                 self.Y, self.Yv = sg.arena(mt, dev)   # trainer current weights
                 sg.fill_old(self.Xv, mt, self.seed, tid0=tid0)
                 sg.fill_new(self.Xv, self.Yv, mt, self.seed, args.rho, MASKS[args.mask], tid0=tid0)
-                self.sender = GroupedSender(self.Xv, self.Yv, groups=self.G, max_changed=cap, **kw)
+                self.sender = GroupedSender(self.Xv, self.Yv, groups=self.G, max_changed=cap, **rkw)
         self.loop_snapshot = args.replica == "snapshot"
         if self.loop_snapshot and (W != 1 or topo != "ring"):
             raise SystemExit("--replica snapshot is the N=1 loopback layout")
@@ -697,7 +700,8 @@ def run_ours(args):
                    "elements_per_trainer_rank": r.S // 2, "model_elements": manifest.total,
                    "tensors": len(manifest.tensors),
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
-                   "groups": r.G, "replica": args.replica, "tracking": args.tracking, "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
+                   "groups": r.G, "replica": args.replica, "tracking": args.tracking, "route": args.route,
+                   "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
                    "l2": "inputs larger than L2 (2 x S per Trainer); no flush"},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
                          zip(["extract", "compress_pack", "transfer_apply", "commit", "synthetic_update",

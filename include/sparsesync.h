@@ -54,6 +54,9 @@ typedef struct CUstream_st* sync_stream_t; /* == cudaStream_t; NULL = legacy def
 #define SYNC_CODEC_RAW 0         /* u32 I + u16 V: the paper's measured raw path */
 #define SYNC_CODEC_COMPRESSED 1  /* DELTA16/ABS32 indices + byte-plane rANS values (§3.3) */
 #define SYNC_FLAG_CRC 1u         /* per-bucket CRC-32/IEEE */
+#define SYNC_FLAG_ROUTE 2u       /* f3 per-parameter routing: a record goes FULL (the whole tensor,
+                                    idx_mode 2) when that is smaller than its sparse record (DESIGN C19);
+                                    needs sync_set_current()                                              */
 #define SYNC_CHUNK 16384u        /* values per chunk */
 
 /* Ordered tensor list = record order (model iteration order). Host memory. */
@@ -80,6 +83,7 @@ typedef struct {
   uint64_t enc_bytes;      /* Σ record_bytes (compressed or raw records) */
   uint64_t index_bytes;    /* Σ padded index-stream bytes */
   uint64_t value_bytes;    /* Σ (record_bytes - 16 - index bytes): α numerator (DESIGN C5) */
+  uint64_t n_full;         /* records routed FULL (SYNC_FLAG_ROUTE, f3) */
 } sync_stats;
 
 /* Record view produced by sync_bucket_unpack (device memory, 32 B). */
@@ -206,6 +210,12 @@ int sync_commit_snapshot(uint16_t* d_snapshot, const uint32_t* d_I, const uint16
 /* Batched commit over the manifest from the raw output of sync_extract_batched. */
 int sync_commit_snapshot_batched(sync_ctx* ctx, uint16_t* const* d_snapshot_ptrs, const uint32_t* d_I,
                                  const uint16_t* d_V, const uint64_t* d_counts, sync_stream_t stream);
+
+/* ---- f3 routing: the current weights a FULL record copies ---------------------------------------------
+ * d_new_ptrs: device array of the manifest's current-weight pointers (the `new` of sync_extract_batched, or
+ * W under f1 tracking), read by sync_compress / sync_compress_pack for records routed FULL. Required when
+ * the context was created with SYNC_FLAG_ROUTE (else those calls return SYNC_ERR_ARG); kept until replaced. */
+int sync_set_current(sync_ctx* ctx, const uint16_t* const* d_new_ptrs);
 
 /* ---- f1 cast-fused tracking (Alg. 1; hook P:386) ----------
  * The paper's own hook: the changed indices are collected inside the optimizer-step epilogue that casts the

@@ -37,6 +37,7 @@ SYNC_ERR_CRC = -12
 SYNC_CODEC_RAW = 0
 SYNC_CODEC_COMPRESSED = 1
 SYNC_FLAG_CRC = 1
+SYNC_FLAG_ROUTE = 2
 SYNC_CHUNK = 16384
 
 EXPORTS = [
@@ -45,6 +46,7 @@ EXPORTS = [
     "sync_buckets_bound", "sync_compress_pack", "sync_bucket_unpack", "sync_decompress", "sync_decompress_apply", "sync_decompress_apply_batched", "sync_apply",
     "sync_commit_snapshot", "sync_commit_snapshot_batched", "sync_status", "sync_ctx_stats", "sync_strerror",
     "sync_launch_count", "sync_bitmap_words", "sync_cast_track_batched", "sync_extract_tracked",
+    "sync_set_current",
 ]
 # NVLink peer-memory plumbing (include/sparsesync_peer.h)
 PEER_EXPORTS = [
@@ -71,7 +73,8 @@ class _Config(ctypes.Structure):
 
 class _Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in ["nnz", "n_records", "n_delta16", "n_abs32", "n_chunks",
-                                                "n_chunks_rans", "enc_bytes", "index_bytes", "value_bytes"]]
+                                                "n_chunks_rans", "enc_bytes", "index_bytes", "value_bytes",
+                                                "n_full"]]
 
 
 RECORD_VIEW_BYTES = 32
@@ -111,6 +114,7 @@ def lib() -> ctypes.CDLL:
             "sync_status": [P, P],
             "sync_ctx_stats": [P, P, P],
             "sync_bitmap_words": [P, P],
+            "sync_set_current": [P, P],
             "sync_cast_track_batched": [P, P, P, P, P],
             "sync_extract_tracked": [P, P, P, P, P, P, i32, P],
             "sync_peer_mem_export": [P, P, P, P],
@@ -232,15 +236,16 @@ class SyncContext:
     """A manifest (ordered tensor sizes) + config + device workspace, for sender and receiver calls."""
 
     def __init__(self, numel, bucket_limit: int = 256 << 20, max_changed: int | None = None,
-                 codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, device=None):
+                 codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, device=None, route: bool = False):
         self.numel = [int(n) for n in numel]
         self.device = torch.device(device or "cuda")
         self.T = len(self.numel)
         self.max_changed = int(max_changed if max_changed is not None else sum(self.numel))
         self._numel_arr = (ctypes.c_uint64 * max(self.T, 1))(*self.numel)
         self._m = _Manifest(self.T, self._numel_arr)
-        self._c = _Config(int(bucket_limit), self.max_changed, int(codec), SYNC_FLAG_CRC if crc else 0)
-        self.codec, self.crc, self.bucket_limit = codec, crc, bucket_limit
+        self._c = _Config(int(bucket_limit), self.max_changed, int(codec),
+                          (SYNC_FLAG_CRC if crc else 0) | (SYNC_FLAG_ROUTE if route else 0))
+        self.codec, self.crc, self.bucket_limit, self.route = codec, crc, bucket_limit, route
         need = ctypes.c_size_t()
         _ck(lib().sync_workspace_size(ctypes.byref(self._m), ctypes.byref(self._c), ctypes.byref(need)),
             "sync_workspace_size")
@@ -309,6 +314,11 @@ class SyncContext:
                                      counts: torch.Tensor, stream=None):
         _ck(lib().sync_commit_snapshot_batched(self._h, _dev_ptr(snap_ptrs), _ptr(I), _ptr(V), _dev_ptr(counts),
                                                _stream(stream)), "sync_commit_snapshot_batched")
+
+    def sync_set_current(self, new_ptrs: torch.Tensor):
+        """f3: the current-weight pointer table FULL records copy from (kept alive by this object)."""
+        self._cur = new_ptrs
+        _ck(lib().sync_set_current(self._h, _dev_ptr(new_ptrs)), "sync_set_current")
 
     # -- f1 cast-fused tracking (Alg. 1) ---------------------------------------
     def bitmap_words(self) -> int:

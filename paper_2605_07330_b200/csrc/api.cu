@@ -139,6 +139,7 @@ struct sync_ctx {
   const u64* plan_counts;
   bool plan_valid;
   pvec<u64> h_rec_bytes, h_chunk_off, h_enc_off, h_totals, h_rec_dst;
+  pvec<u32> h_rec_mode;
   pvec<RecordDesc> h_recs;
   pvec<BucketDesc> h_bks;
 };
@@ -209,6 +210,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   x->misc = reinterpret_cast<u32*>(w + L.misc);
   try {   // pinned host tables, sized once
     x->h_rec_bytes.reserve(d.T);
+    x->h_rec_mode.reserve(d.T);
     x->h_chunk_off.reserve(d.T + 1);
     x->h_enc_off.reserve(d.T + 1);
     x->h_totals.reserve(16);
@@ -223,6 +225,8 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   p.n_tensors = d.T;
   p.cap = c->max_changed;
   p.codec = c->codec;
+  p.route = (c->flags & SYNC_FLAG_ROUTE) ? 1 : 0;
+  p.cur = nullptr;
   p.max_chunks = d.max_chunks;
   p.numel = reinterpret_cast<const u64*>(w + L.numel);
   p.rec_off = reinterpret_cast<u64*>(w + L.rec_off);
@@ -331,6 +335,12 @@ static TrackArgs track_args(sync_ctx* x, uint32_t* d_bitmap) {
   return a;
 }
 
+int sync_set_current(sync_ctx* x, const uint16_t* const* d_new_ptrs) {
+  if (!x) return SYNC_ERR_ARG;
+  x->plan.cur = d_new_ptrs;
+  return SYNC_OK;
+}
+
 int sync_bitmap_words(sync_ctx* x, uint64_t* words) {
   if (!x || !words) return SYNC_ERR_ARG;
   *words = x->bm_off.empty() ? 0 : x->bm_off.back();
@@ -373,6 +383,7 @@ int sync_enc_bound(const sync_manifest* m, const sync_config* c, uint64_t* bytes
 int sync_compress(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts, uint8_t* d_enc,
                   uint64_t enc_cap, sync_stream_t stream) {
   if (!x || (x->d.T && (!d_counts || !d_enc))) return SYNC_ERR_ARG;
+  if (x->plan.route && !x->plan.cur) return SYNC_ERR_ARG;   // SYNC_FLAG_ROUTE needs sync_set_current
   if (!aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
   x->plan.enc_cap = enc_cap;
@@ -391,11 +402,13 @@ int sync_compress(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const u
 static int read_plan(sync_ctx* x, cudaStream_t s) {
   const u32 T = x->d.T;
   x->h_rec_bytes.resize(T);
+  x->h_rec_mode.resize(T);
   x->h_chunk_off.resize(T + 1);
   x->h_enc_off.resize(T + 1);
   x->h_totals.resize(16);
   if (T) {
     CK(cudaMemcpyAsync(x->h_rec_bytes.data(), x->plan.rec_bytes, 8ull * T, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(x->h_rec_mode.data(), x->plan.rec_mode, 4ull * T, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(x->h_chunk_off.data(), x->plan.chunk_off, 8ull * (T + 1), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(x->h_enc_off.data(), x->plan.enc_off, 8ull * (T + 1), cudaMemcpyDeviceToHost, s));
   }
@@ -448,7 +461,9 @@ static int plan_buckets(sync_ctx* x, uint64_t buckets_cap, uint32_t max_buckets,
     r.dst = cur_sum;  // provisional: offset within the record area
     x->h_recs.push_back(r);
     cur.n_records++;
-    cur.n_chunks += (u32)(x->h_chunk_off[t + 1] - x->h_chunk_off[t]);
+    // chunks of a record on the wire = ceil(nnz field / C); a FULL record's nnz field is numel
+    cur.n_chunks += x->h_rec_mode[t] == kModeFull ? (u32)((x->numel[t] + kChunk - 1) / kChunk)
+                                                  : (u32)(x->h_chunk_off[t + 1] - x->h_chunk_off[t]);
     cur_sum += rb;
   }
   close();
@@ -507,6 +522,7 @@ int sync_compress_pack(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, co
                        uint8_t* d_buckets, uint64_t buckets_cap, uint32_t* n_buckets, uint64_t* h_offsets,
                        uint64_t* h_sizes, uint32_t max_buckets, uint64_t* h_need, sync_stream_t stream) {
   if (!x || !n_buckets || (x->d.T && !d_counts)) return SYNC_ERR_ARG;
+  if (x->plan.route && !x->plan.cur) return SYNC_ERR_ARG;   // SYNC_FLAG_ROUTE needs sync_set_current
   if (!aligned16(d_buckets)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
   *n_buckets = 0;
@@ -670,6 +686,7 @@ int sync_ctx_stats(sync_ctx* x, sync_stats* out, sync_stream_t stream) {
   out->enc_bytes = t[kTotEnc];
   out->index_bytes = t[kTotIndexBytes];
   out->value_bytes = t[kTotValueBytes];
+  out->n_full = t[kTotFull];
   return SYNC_OK;
 }
 

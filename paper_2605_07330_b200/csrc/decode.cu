@@ -56,8 +56,9 @@ __device__ __forceinline__ bool read_record(const u8* bk, const BucketHdr& h, u3
   r->dtype = (w[3] >> 8) & 0xFFu;
   r->codec = (w[3] >> 16) & 0xFFu;
   if (r->rb < 16 || (r->rb & 15u) || (u64)ro + r->rb > h.bytes) return false;
-  if (r->tid >= n_tensors || r->dtype != 1 || r->mode > 1 || r->codec > 1 || r->nnz == 0) return false;
+  if (r->tid >= n_tensors || r->dtype != 1 || r->mode > 2 || r->codec > 1 || r->nnz == 0) return false;
   if ((u64)r->nnz > numel[r->tid]) return false;
+  if (r->mode == kModeFull) return (u64)r->nnz == numel[r->tid] && 16 + 2ull * r->nnz <= r->rb;
   if (r->codec == SYNC_CODEC_RAW) return r->mode == 1 && 16 + 6ull * r->nnz <= r->rb;
   const u64 nch = (r->nnz + kChunk - 1) / kChunk;
   const u64 ib = (r->mode ? 4ull : 2ull) * r->nnz;
@@ -221,6 +222,20 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
       Vo = V_out + oo;
     }
     bool bad = false;
+
+    if (r.mode == kModeFull) {   // f3 FULL record: element i of the tensor = the i-th value
+      const u16* Vr = reinterpret_cast<const u16*>(rec + 16);
+      for (u32 qq = lane; qq < nk; qq += 32) {
+        const u64 i = p0 + qq;
+        if (kApply) {
+          W[i] = Vr[i];
+        } else {
+          Io[qq] = (u32)i;
+          Vo[qq] = Vr[i];
+        }
+      }
+      continue;
+    }
 
     if (r.codec == SYNC_CODEC_RAW) {
       const u32* Ir = reinterpret_cast<const u32*>(rec + 16) + p0;

@@ -44,9 +44,29 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
     if (k == 0 && tid == 0) {
       u32* h = reinterpret_cast<u32*>(rec);
       h[0] = t;
-      h[1] = (u32)nnz;
+      h[1] = mode == kModeFull ? (u32)p.numel[t] : (u32)nnz;
       h[2] = (u32)rb;
       h[3] = mode | (1u << 8) | ((comp ? 1u : 0u) << 16);
+    }
+
+    if (mode == kModeFull) {
+      // f3 FULL record: the tensor's current values. The record's n_ch chunks (counted
+      // from its nnz) split the copy at multiples of 8 elements (16-byte stores into the 16-aligned body).
+      const u64 numel = p.numel[t];
+      const u16* src = p.cur[t];
+      u16* dst = reinterpret_cast<u16*>(rec + 16);
+      const u64 lo = (numel * k / n_ch) & ~7ull;
+      const u64 hi = last ? numel : ((numel * (k + 1) / n_ch) & ~7ull);
+      if ((((uintptr_t)src) & 15u) == 0) {
+        const u64 v_end = lo + ((hi - lo) & ~7ull);
+        for (u64 q = lo + 8ull * tid; q < v_end; q += 8ull * kCThreads)
+          *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<const uint4*>(src + q);
+        for (u64 q = v_end + tid; q < hi; q += kCThreads) dst[q] = src[q];
+      } else {
+        for (u64 q = lo + tid; q < hi; q += kCThreads) dst[q] = src[q];
+      }
+      if (last) zero_bytes(rec + 16 + 2 * numel, rb - (16 + 2 * numel));
+      continue;
     }
 
     if (!comp) {

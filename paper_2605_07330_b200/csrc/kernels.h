@@ -20,7 +20,7 @@ struct Plan {
   uint64_t* rec_off;             // [T+1] value offset of tensor t in I/V
   uint64_t* chunk_off;           // [T+1] first global chunk of tensor t
   uint32_t* maxgap;              // [T]
-  uint32_t* rec_mode;            // [T] DELTA16 / ABS32
+  uint32_t* rec_mode;            // [T] DELTA16 / ABS32 / FULL
   uint64_t* rec_bytes;           // [T]
   uint64_t* enc_off;             // [T+1]
   const uint64_t* rec_dst;       // [T] where k_encode writes record t (enc_off, or bucket positions)
@@ -32,12 +32,15 @@ struct Plan {
   uint64_t* totals;              // [16]
   uint32_t* status;
   int prof;                      // debug instrumentation switch
+  int route;                     // f3: SYNC_FLAG_ROUTE
+  const uint16_t* const* cur;    // f3: current weights (FULL records), device pointer table
 };
 
 enum TotalsIdx {
   kTotNnz = 0, kTotChunks = 1, kTotRecords = 2, kTotEnc = 3, kTotDelta16 = 4, kTotAbs32 = 5,
-  kTotRansChunks = 6, kTotOverflow = 7, kTotIndexBytes = 8, kTotValueBytes = 9
+  kTotRansChunks = 6, kTotOverflow = 7, kTotIndexBytes = 8, kTotValueBytes = 9, kTotFull = 10
 };
+constexpr uint32_t kModeFull = 2;  // record idx_mode of a FULL record (f3)
 
 void launch_extract_batched(const uint16_t* const* d_old, const uint16_t* const* d_new, const uint64_t* tile_prefix,
                             const uint32_t* tile_tensor, const uint64_t* numel, uint32_t n_tensors, uint64_t n_tiles, uint32_t* I, uint16_t* V,

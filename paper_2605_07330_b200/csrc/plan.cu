@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
   }
   const u64 rans = block_sum64(rans_local, s_w2);
   // 2. record sizes and offsets
-  u64 carry_enc = 0, n16 = 0, n32 = 0, ib_tot = 0, vb_tot = 0;
+  u64 carry_enc = 0, n16 = 0, n32 = 0, ib_tot = 0, vb_tot = 0, nfull = 0;
   for (u32 b = 0; b < T; b += (u32)kRound) {
     const u32 t0 = b + threadIdx.x * kPer;
     u64 bytes[kPer];
@@ -318,8 +318,17 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
           ib = 4 * c;
           by = pad_to(16 + 6 * c, 16);
         }
-        if (mode) n32++;
-        else n16++;
+        const u64 full = pad_to(16 + 2 * p.numel[t], 16);   // f3 routing (DESIGN C19)
+        if (p.route && full < by) {
+          mode = kModeFull;
+          by = full;
+          ib = 0;
+          nfull++;
+        } else if (mode) {
+          n32++;
+        } else {
+          n16++;
+        }
         ib_tot += ib;
         vb_tot += by - 16 - ib;
       }
@@ -345,6 +354,7 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
   n32 = block_sum64(n32, s_w2);
   ib_tot = block_sum64(ib_tot, s_w);
   vb_tot = block_sum64(vb_tot, s_w2);
+  nfull = block_sum64(nfull, s_w);
   if (threadIdx.x == 0) {
     p.enc_off[T] = carry_enc;
     if (carry_enc > p.enc_cap) {
@@ -358,6 +368,7 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
     p.totals[kTotRansChunks] = rans;
     p.totals[kTotIndexBytes] = ib_tot;
     p.totals[kTotValueBytes] = vb_tot;
+    p.totals[kTotFull] = nfull;
   }
 }
 

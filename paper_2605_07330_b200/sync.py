@@ -23,7 +23,9 @@ class SparseSyncSender:
     """Trainer side. `snapshot` = last-synced copy (W_prev), `current` = new weights W."""
 
     def __init__(self, snapshot, current, bucket_limit: int = 256 << 20, max_changed: int | None = None,
-                 codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, expected_density: float = 0.02):
+                 codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, expected_density: float = 0.02,
+                 route: bool = False):
+        """route: per-parameter routing (f3): a record whose FULL copy is smaller goes FULL."""
         self.snapshot = _flat_bits(snapshot)
         self.current = _flat_bits(current)
         assert len(self.snapshot) == len(self.current)
@@ -34,7 +36,7 @@ class SparseSyncSender:
         self.numel = [t.numel() for t in self.current]
         total = sum(self.numel)
         cap = int(max_changed if max_changed is not None else min(total, int(total * expected_density) + 65536))
-        self._cfg = dict(bucket_limit=bucket_limit, codec=codec, crc=crc)
+        self._cfg = dict(bucket_limit=bucket_limit, codec=codec, crc=crc, route=route)
         self.old_ptrs = ptr_table(self.snapshot, self.device)
         self.new_ptrs = ptr_table(self.current, self.device)
         self.counts = torch.zeros(max(len(self.numel), 1), dtype=torch.int64, device=self.device)
@@ -45,6 +47,8 @@ class SparseSyncSender:
     def _alloc(self, cap: int):
         """(Re)size the changed-element capacity: context workspace, I/V and the encoded stream."""
         self.ctx = SyncContext(self.numel, max_changed=cap, device=self.device, **self._cfg)
+        if self._cfg.get("route"):
+            self.ctx.sync_set_current(self.new_ptrs)
         self.cap = cap
         self.I = torch.empty(max(cap, 1), dtype=torch.int32, device=self.device)
         self.V = torch.empty(max(cap, 1), dtype=torch.int16, device=self.device)
@@ -99,6 +103,8 @@ class SparseSyncSender:
         if mode == "swap":
             self.snapshot, self.current = self.current, self.snapshot
             self.old_ptrs, self.new_ptrs = self.new_ptrs, self.old_ptrs
+            if self._cfg.get("route"):
+                self.ctx.sync_set_current(self.new_ptrs)
             return
         self.ctx.sync_commit_snapshot_batched(self.old_ptrs, self.I, self.V, self.counts, stream)
 

@@ -145,6 +145,66 @@ def test_bucket_bytes_and_apply_bit_exact(codec, limit, crc, rho, mask, fused):
     assert st["nnz"] == ref.stats["nnz"] and st["n_records"] == ref.stats["n_records"]
 
 
+@pytest.mark.parametrize("codec", [ss.SYNC_CODEC_COMPRESSED, ss.SYNC_CODEC_RAW])
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("crc", [False, True])
+def test_routing_full_records_bit_exact(codec, fused, crc):
+    """f3: tensors updated on (nearly) every element go FULL — GPU bucket bytes == oracle's, the
+    replica applies them, and the sender's snapshot commit is unaffected."""
+    m = mixed_manifest()
+    olds, news = synth.generate(m, seed=21, rho=0.02)
+    rng = np.random.default_rng(21)
+    for k in (0, 5, 6, len(news) - 1):            # dense updates: LoRA-like / fully retrained tensors
+        if news[k].size:
+            news[k] = olds[k] ^ np.uint16(1)
+    k = 9                                          # a 50%-dense expert: FULL for raw, sparse or FULL otherwise
+    idx = rng.choice(news[k].size, news[k].size // 2, replace=False)
+    news[k] = olds[k].copy()
+    news[k][idx] ^= np.uint16(2)
+    ref = oracle.sync_pack(olds, news, codec=codec, limit=64 << 10, crc=crc, route=True)
+    assert ref.stats["full"] >= 3
+    old_d = [to_dev(o) for o in olds]
+    new_d = [to_dev(n) for n in news]
+    rol_d = [to_dev(o) for o in olds]
+    snd = ss.SparseSyncSender(old_d, new_d, bucket_limit=64 << 10, codec=codec, crc=crc, route=True,
+                              max_changed=sum(o.size for o in olds))
+    rcv = ss.SparseSyncReceiver(rol_d, bucket_limit=64 << 10, codec=codec, crc=crc)
+    bl = snd.sync(fused=fused)
+    got = [snd.bucket(b).cpu().numpy().tobytes() for b in range(len(bl))]
+    assert got == [ref.bucket(b) for b in range(ref.n_buckets)]
+    assert snd.stats()["n_full"] == ref.stats["full"]
+    rcv.apply_many([snd.bucket(b) for b in range(len(bl))])
+    snd.commit()
+    torch.cuda.synchronize()
+    snd.check()
+    rcv.check()
+    for r, o, n in zip(rol_d, old_d, news):
+        assert (host16(r) == n).all() and (host16(o) == n).all()
+    # the EMIT debug path returns every element of a FULL record, like the oracle's decoder
+    b0 = torch.from_numpy(np.frombuffer(ref.bucket(0), np.uint8).copy()).to(DEV)
+    st, recs = oracle.bucket_decode(ref.bucket(0), cap=sum(o.size for o in olds))
+    n_out = sum(r[1].size for r in recs)
+    I = torch.empty(max(n_out, 1), dtype=torch.int32, device=DEV)
+    V = torch.empty(max(n_out, 1), dtype=torch.int16, device=DEV)
+    rcv.ctx.sync_decompress(b0, b0.numel(), I, V)
+    torch.cuda.synchronize()
+    rcv.check()
+    assert (I[:n_out].cpu().numpy().view(np.uint32) == np.concatenate([r[1] for r in recs])).all()
+    assert (V[:n_out].cpu().numpy().view(np.uint16) == np.concatenate([r[2] for r in recs])).all()
+
+
+def test_routing_needs_current_weights():
+    m = mixed_manifest()
+    ctx = ss.SyncContext(m.numel, route=True, device=DEV, max_changed=1000)
+    I = torch.zeros(1000, dtype=torch.int32, device=DEV)
+    V = torch.zeros(1000, dtype=torch.int16, device=DEV)
+    counts = torch.zeros(len(m.numel), dtype=torch.int64, device=DEV)
+    buf = torch.zeros(1 << 16, dtype=torch.uint8, device=DEV)
+    with pytest.raises(ss.SyncError) as e:
+        ctx.sync_compress_pack(I, V, counts, buf)
+    assert e.value.code == ss.SYNC_ERR_ARG
+
+
 def test_delta16_abs32_boundary():
     # gap of exactly 32767 stays DELTA16, 32768 forces ABS32 (P:360, DESIGN C4)
     n = 70_000
