@@ -30,6 +30,7 @@ ERR_TRUNCATED = -11
 ERR_CRC = -12
 
 DELTA16, ABS32 = 0, 1
+DTYPE_BF16, DTYPE_FP16 = 1, 2
 CODEC_RAW, CODEC_COMPRESSED = 0, 1
 CHUNK = 16384
 
@@ -54,7 +55,7 @@ def lib():
         sig = {
             "or_extract": (u64, [P, P, u64, P, P]),
             "or_full_record_bytes": (u64, [u64]),
-            "or_encode_full_record": (u64, [u32, P, u64, i32, P]),
+            "or_encode_full_record": (u64, [u32, P, u64, i32, P, i32]),
             "or_bf16_rne": (ctypes.c_uint16, [u32]),
             "or_bf16_rne_array": (None, [P, P, u64]),
             "or_cast_track": (u64, [P, P, P, u64]),
@@ -67,11 +68,11 @@ def lib():
             "or_rans_encode": (u32, [P, u32, P]),
             "or_rans_decode": (i32, [P, u32, u32, P]),
             "or_record_bound": (u64, [u64]),
-            "or_encode_record": (u64, [u32, P, P, u64, i32, P]),
+            "or_encode_record": (u64, [u32, P, P, u64, i32, P, i32]),
             "or_decode_record": (i32, [P, u64, P, P, P, P, u64]),
             "or_crc32": (u32, [P, u64]),
             "or_bucketize": (u32, [P, u64, u64, P]),
-            "or_sync_pack": (i64, [u32, P, P, P, i32, u64, u32, P, u64, P, P, u32, P]),
+            "or_sync_pack": (i64, [u32, P, P, P, i32, u64, u32, P, u64, P, P, u32, P, i32]),
             "or_bucket_apply": (i32, [P, u64, u32, P, P]),
             "or_bucket_decode": (i32, [P, u64, P, P, u64, P, u32, P]),
             "or_eq1_sparse_bytes": (ctypes.c_double, [ctypes.c_double] * 5),
@@ -189,20 +190,20 @@ def rans_decode(block: bytes, n: int):
 
 
 # ----------------------------------------------------------------------------- records
-def encode_full_record(tensor_id: int, W, codec: int = CODEC_COMPRESSED) -> bytes:
+def encode_full_record(tensor_id: int, W, codec: int = CODEC_COMPRESSED, dtype: int = 1) -> bytes:
     """f3 FULL record: the whole tensor's current values."""
     W = _u16(W).ravel()
     out = np.zeros(int(lib().or_full_record_bytes(W.size)), np.uint8)
-    n = lib().or_encode_full_record(tensor_id, _p(W), W.size, codec, _p(out))
+    n = lib().or_encode_full_record(tensor_id, _p(W), W.size, codec, _p(out), dtype)
     return out[:n].tobytes()
 
 
-def encode_record(tensor_id: int, I, V, codec: int = CODEC_COMPRESSED) -> bytes:
+def encode_record(tensor_id: int, I, V, codec: int = CODEC_COMPRESSED, dtype: int = 1) -> bytes:
     I = np.ascontiguousarray(I, np.uint32)
     V = np.ascontiguousarray(V, np.uint16)
     assert I.size == V.size and I.size > 0
     out = np.zeros(lib().or_record_bound(I.size), np.uint8)
-    n = lib().or_encode_record(tensor_id, _p(I), _p(V), I.size, codec, _p(out))
+    n = lib().or_encode_record(tensor_id, _p(I), _p(V), I.size, codec, _p(out), dtype)
     return out[:n].tobytes()
 
 
@@ -249,7 +250,7 @@ class PackResult:
 
 
 def sync_pack(olds, news, codec: int = CODEC_COMPRESSED, limit: int = 256 << 20, crc: bool = False,
-              max_buckets: int = 1 << 16, route: bool = False) -> PackResult:
+              max_buckets: int = 1 << 16, route: bool = False, dtype: int = 1) -> PackResult:
     """Sender path (Alg. 2) over a manifest of (old, new) uint16 arrays.
     route: per-parameter routing (f3) — a record goes FULL when that is smaller (DESIGN C19)."""
     olds = [_u16(o).ravel() for o in olds]
@@ -270,7 +271,7 @@ def sync_pack(olds, news, codec: int = CODEC_COMPRESSED, limit: int = 256 << 20,
     flags = (1 if crc else 0) | (2 if route else 0)
     nb = L.or_sync_pack(T, _p(numel), ctypes.cast(op, ctypes.c_void_p), ctypes.cast(np_, ctypes.c_void_p),
                         codec, limit, flags, _p(buf), cap, _p(offs), _p(sizes), max_buckets,
-                        _p(stats))
+                        _p(stats), dtype)
     if nb < 0:
         raise RuntimeError(f"or_sync_pack failed: {nb}")
     return PackResult(buf, offs[:nb].copy(), sizes[:nb].copy(), stats)

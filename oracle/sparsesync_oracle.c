@@ -40,6 +40,8 @@
 enum { OR_DELTA16 = 0, OR_ABS32 = 1 };
 enum { OR_CODEC_RAW = 0, OR_CODEC_COMPRESSED = 1 };
 enum { OR_CHUNK_RAW = 0, OR_CHUNK_RANS = 1 };
+/* record dtype byte (f2): the 16-bit element types share every encoding; only the tag differs */
+enum { OR_DTYPE_BF16 = 1, OR_DTYPE_FP16 = 2 };
 
 static uint64_t pad_to(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
@@ -324,7 +326,7 @@ uint64_t or_record_bound(uint64_t nnz) {
 
 /* Encodes one record; returns record_bytes (multiple of 16). nnz >= 1. */
 uint64_t or_encode_record(uint32_t tensor_id, const uint32_t* I, const uint16_t* V, uint64_t nnz,
-                          int codec, uint8_t* out) {
+                          int codec, uint8_t* out, int dtype) {
   uint8_t* rec = out;
   uint64_t off = 16;
   if (codec == OR_CODEC_RAW) {
@@ -337,7 +339,7 @@ uint64_t or_encode_record(uint32_t tensor_id, const uint32_t* I, const uint16_t*
     put32(rec + 0, tensor_id);
     put32(rec + 4, (uint32_t)nnz);
     put32(rec + 8, (uint32_t)total);
-    rec[12] = OR_ABS32; rec[13] = 1; rec[14] = OR_CODEC_RAW; rec[15] = 0;
+    rec[12] = OR_ABS32; rec[13] = (uint8_t)dtype; rec[14] = OR_CODEC_RAW; rec[15] = 0;
     return total;
   }
   int mode = or_index_mode(I, nnz);
@@ -376,7 +378,7 @@ uint64_t or_encode_record(uint32_t tensor_id, const uint32_t* I, const uint16_t*
   put32(rec + 0, tensor_id);
   put32(rec + 4, (uint32_t)nnz);
   put32(rec + 8, (uint32_t)total);
-  rec[12] = (uint8_t)mode; rec[13] = 1; rec[14] = OR_CODEC_COMPRESSED; rec[15] = 0;
+  rec[12] = (uint8_t)mode; rec[13] = (uint8_t)dtype; rec[14] = OR_CODEC_COMPRESSED; rec[15] = 0;
   return total;
 }
 
@@ -392,14 +394,15 @@ enum { OR_FULL = 2 };
 
 uint64_t or_full_record_bytes(uint64_t numel) { return pad_to(16 + 2 * numel, 16); }
 
-uint64_t or_encode_full_record(uint32_t tensor_id, const uint16_t* W, uint64_t numel, int codec, uint8_t* out) {
+uint64_t or_encode_full_record(uint32_t tensor_id, const uint16_t* W, uint64_t numel, int codec, uint8_t* out,
+                               int dtype) {
   uint64_t total = or_full_record_bytes(numel);
   for (uint64_t i = 0; i < numel; ++i) put16(out + 16 + 2 * i, W[i]);
   memset(out + 16 + 2 * numel, 0, total - 16 - 2 * numel);
   put32(out + 0, tensor_id);
   put32(out + 4, (uint32_t)numel);
   put32(out + 8, (uint32_t)total);
-  out[12] = OR_FULL; out[13] = 1; out[14] = (uint8_t)codec; out[15] = 0;
+  out[12] = OR_FULL; out[13] = (uint8_t)dtype; out[14] = (uint8_t)codec; out[15] = 0;
   return total;
 }
 
@@ -411,7 +414,8 @@ int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, ui
   uint32_t tid = get32(rec), nnz = get32(rec + 4), rb = get32(rec + 8);
   uint8_t mode = rec[12], dtype = rec[13], codec = rec[14];
   if (rb > avail || rb < 16 || (rb % 16) != 0) return OR_ERR_TRUNCATED;
-  if (dtype != 1 || mode > 2 || codec > 1 || nnz == 0) return OR_ERR_CORRUPT;
+  if ((dtype != OR_DTYPE_BF16 && dtype != OR_DTYPE_FP16) || mode > 2 || codec > 1 || nnz == 0)
+    return OR_ERR_CORRUPT;
   *tensor_id = tid;
   *nnz_out = nnz;
   if (nnz > cap) return OR_ERR_CAPACITY;
@@ -509,7 +513,7 @@ uint32_t or_bucketize(const uint64_t* rec_bytes, uint64_t n_records, uint64_t li
 int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const uint16_t* const* old_ptrs,
                      const uint16_t* const* new_ptrs, int codec, uint64_t limit, uint32_t flags,
                      uint8_t* out, uint64_t out_cap, uint64_t* offsets, uint64_t* sizes,
-                     uint32_t max_buckets, uint64_t* stats) {
+                     uint32_t max_buckets, uint64_t* stats, int dtype) {
   uint64_t st[7] = {0};
   /* 1. per tensor records into a scratch stream */
   uint64_t cap_total = 0;
@@ -525,9 +529,9 @@ int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const uint16_t* 
     uint16_t* V = (uint16_t*)malloc(sizeof(uint16_t) * (n ? n : 1));
     uint64_t nnz = or_extract(old_ptrs[t], new_ptrs[t], n, I, V);
     if (nnz > 0) {
-      uint64_t rb = or_encode_record(t, I, V, nnz, codec, stream + pos);
+      uint64_t rb = or_encode_record(t, I, V, nnz, codec, stream + pos, dtype);
       int full = (flags & 2u) && or_full_record_bytes(n) < rb;   /* routing, DESIGN C19 */
-      if (full) rb = or_encode_full_record(t, new_ptrs[t], n, codec, stream + pos);
+      if (full) rb = or_encode_full_record(t, new_ptrs[t], n, codec, stream + pos, dtype);
       rec_bytes[n_records] = rb;
       rec_pos[n_records] = pos;
       rec_chunks[n_records] = (uint32_t)(((full ? n : nnz) + OR_C - 1) / OR_C);

@@ -62,6 +62,25 @@ def threshold(p: float) -> int:
 _TABLE = None
 
 
+DTYPE_BF16, DTYPE_FP16 = 1, 2
+ONE = {DTYPE_BF16: 0x3F80, DTYPE_FP16: 0x3C00}   # bit patterns of 1.0 (RMSNorm weights)
+_TABLE16 = None
+
+
+def fp16_table() -> np.ndarray:
+    """65536 fp16 bit patterns: RNE (numpy's float16 cast) of SIGMA * Phi^-1((k + 0.5) / 65536)."""
+    global _TABLE16
+    if _TABLE16 is None:
+        from scipy.special import ndtri
+        q = (np.arange(65536, dtype=np.float64) + 0.5) / 65536.0
+        _TABLE16 = (SIGMA * ndtri(q)).astype(np.float32).astype(np.float16).view(np.uint16)
+    return _TABLE16
+
+
+def table(dtype: int = DTYPE_BF16) -> np.ndarray:
+    return fp16_table() if dtype == DTYPE_FP16 else bf16_table()
+
+
 def bf16_table() -> np.ndarray:
     """65536 bf16 bit patterns: RNE of SIGMA * Phi^-1((k + 0.5) / 65536), ascending k."""
     global _TABLE
@@ -174,11 +193,11 @@ def shard(manifest: Manifest, rank: int, world: int) -> Manifest:
 
 
 # ----------------------------------------------------------------------------- generation
-def gen_old(t: Tensor, tid: int, seed: int) -> np.ndarray:
+def gen_old(t: Tensor, tid: int, seed: int, dtype: int = DTYPE_BF16) -> np.ndarray:
     if t.kind == KIND_NORM:
-        return np.full(t.numel, 0x3F80, np.uint16)
+        return np.full(t.numel, ONE[dtype], np.uint16)
     i = np.arange(t.numel, dtype=np.uint64)
-    return bf16_table()[(h(S_VAL, seed, tid, i) >> np.uint64(48)).astype(np.int64)]
+    return table(dtype)[(h(S_VAL, seed, tid, i) >> np.uint64(48)).astype(np.int64)]
 
 
 def gen_mask(t: Tensor, tid: int, seed: int, rho: float, mask: int = MASK_U) -> np.ndarray:
@@ -206,11 +225,12 @@ def gen_new(old: np.ndarray, t: Tensor, tid: int, seed: int, rho: float, mask: i
     return np.where(m, old ^ d, old).astype(np.uint16)
 
 
-def generate(manifest: Manifest, seed: int = 0, rho: float = 0.01, mask: int = MASK_U, tid0: int = 0):
+def generate(manifest: Manifest, seed: int = 0, rho: float = 0.01, mask: int = MASK_U, tid0: int = 0,
+             dtype: int = DTYPE_BF16):
     """Lists (olds, news) of uint16 arrays; tensor ids start at tid0 (global manifest ids)."""
     olds, news = [], []
     for k, t in enumerate(manifest.tensors):
-        o = gen_old(t, tid0 + k, seed)
+        o = gen_old(t, tid0 + k, seed, dtype)
         olds.append(o)
         news.append(gen_new(o, t, tid0 + k, seed, rho, mask))
     return olds, news

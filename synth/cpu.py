@@ -8,7 +8,7 @@ import subprocess
 import numpy as np
 
 from . import (KIND_NORM, MASK_E, MASK_R, S_EXP, S_MASK, S_PERT, S_ROW, S_VAL, EXPERT_F, ROW_Q, Manifest, h, key,
-               threshold, bf16_table)
+               threshold, bf16_table, table, ONE, DTYPE_BF16)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gen_cpu.c")
@@ -40,16 +40,18 @@ def _p(a):
     return ctypes.c_void_p(a.ctypes.data)
 
 
-def generate(manifest: Manifest, seed: int = 0, rho: float = 0.01, mask: int = 0, tid0: int = 0):
+def generate(manifest: Manifest, seed: int = 0, rho: float = 0.01, mask: int = 0, tid0: int = 0,
+             dtype: int = DTYPE_BF16):
     """Same output as synth.generate (numpy), ~50x faster."""
-    tab = bf16_table()
+    tab = table(dtype)
     olds, news = [], []
     for k, t in enumerate(manifest.tensors):
         tid = tid0 + k
         o = np.empty(t.numel, np.uint16)
         n = np.empty(t.numel, np.uint16)
         if t.numel:
-            lib().synth_cpu_fill_old(_p(o), t.numel, int(t.kind == KIND_NORM), key(S_VAL, seed, tid), _p(tab))
+            lib().synth_cpu_fill_old(_p(o), t.numel, ONE[dtype] if t.kind == KIND_NORM else 0,
+                                     key(S_VAL, seed, tid), _p(tab))
             mode, active, thr = 0, 1, threshold(rho)
             key_row, thr_row, cols = 0, 0, 1
             if mask == MASK_R and len(t.shape) == 2:

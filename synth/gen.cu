@@ -20,7 +20,7 @@ __device__ __forceinline__ u64 mix(u64 z) {
 
 __global__ void k_fill_old(u16* out, u64 n, int norm, u64 key_val, const u16* table) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
-    out[i] = norm ? (u16)0x3F80 : table[mix(key_val ^ i) >> 48];
+    out[i] = norm ? (u16)norm : table[mix(key_val ^ i) >> 48];   // norm: the bits of 1.0 (0 = none)
 }
 
 // mode 0 = U, 1 = R (row clustered), 2 = E (expert gate already folded into `active`)

@@ -10,7 +10,7 @@ static inline uint64_t mix(uint64_t z) {
 }
 
 void synth_cpu_fill_old(uint16_t* out, uint64_t n, int norm, uint64_t key_val, const uint16_t* table) {
-  for (uint64_t i = 0; i < n; ++i) out[i] = norm ? (uint16_t)0x3F80 : table[mix(key_val ^ i) >> 48];
+  for (uint64_t i = 0; i < n; ++i) out[i] = norm ? (uint16_t)norm : table[mix(key_val ^ i) >> 48];
 }
 
 void synth_cpu_fill_new(const uint16_t* old, uint16_t* nw, uint64_t n, int mode, int active, uint64_t key_mask,

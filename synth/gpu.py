@@ -9,7 +9,7 @@ import numpy as np
 import torch
 
 from . import (KIND_NORM, MASK_E, MASK_R, S_EXP, S_MASK, S_PERT, S_ROW, S_VAL, EXPERT_F, ROW_Q, Manifest, h, key,
-               threshold, bf16_table)
+               threshold, bf16_table, table, ONE, DTYPE_BF16)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gen.cu")
@@ -43,10 +43,10 @@ def lib():
 _tables = {}
 
 
-def _table(device) -> torch.Tensor:
-    k = str(device)
+def _table(device, dtype: int = DTYPE_BF16) -> torch.Tensor:
+    k = (str(device), dtype)
     if k not in _tables:
-        _tables[k] = torch.from_numpy(bf16_table().view(np.int16).copy()).to(device)
+        _tables[k] = torch.from_numpy(table(dtype).view(np.int16).copy()).to(device)
     return _tables[k]
 
 
@@ -65,10 +65,10 @@ def arena(manifest: Manifest, device, dtype=torch.int16):
     return buf, views
 
 
-def fill_old(views, manifest: Manifest, seed: int, tid0: int = 0):
-    tab = _table(views[0].device) if views else None
+def fill_old(views, manifest: Manifest, seed: int, tid0: int = 0, dtype: int = DTYPE_BF16):
+    tab = _table(views[0].device, dtype) if views else None
     for k, (v, t) in enumerate(zip(views, manifest.tensors)):
-        rc = lib().synth_fill_old(ctypes.c_void_p(v.data_ptr()), v.numel(), int(t.kind == KIND_NORM),
+        rc = lib().synth_fill_old(ctypes.c_void_p(v.data_ptr()), v.numel(), ONE[dtype] if t.kind == KIND_NORM else 0,
                                   key(S_VAL, seed, tid0 + k), ctypes.c_void_p(tab.data_ptr()), _s())
         assert rc == 0
 

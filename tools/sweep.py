@@ -54,6 +54,8 @@ SETS = {
         ("fanout4_r01_E_b64", 4, ["--topology", "fanout", "--mask", "E", "--bucket-mb", "64"]),
         ("fanout4_r01_E_b256", 4, ["--topology", "fanout", "--mask", "E"]),
         ("fanout4_r01_E_b1024", 4, ["--topology", "fanout", "--mask", "E", "--bucket-mb", "1024"]),
+        ("fanout4_r01_cast", 4, ["--topology", "fanout", "--tracking", "cast"]),
+        ("pair4_4b_r01", 4, ["--topology", "pair", "--workload", "qwen3-4b"]),
     ],
     "n2": [
         ("ring2_r01", 2, ["--topology", "ring"]),
@@ -72,6 +74,8 @@ SETS = {
         ("one_r01_E", 1, ["--mask", "E"]),
         ("one_r01_raw", 1, ["--codec", "raw"]),
         ("one_r01_crc", 1, ["--crc"]),
+        ("one_r01_route", 1, ["--route"]),
+        ("one_4b_cast", 1, ["--workload", "qwen3-4b", "--tracking", "cast"]),
     ],
 }
 
