@@ -69,6 +69,8 @@ def parse():
                    help="snapshot: diff new weights against the last-synced snapshot (north_star); cast: f1, the "
                         "paper's own hook (Alg. 1): the fp32->bf16 CastAndCopy tracks the changed elements into a "
                         "bitmap and the sync gathers them (no snapshot; the cast runs inside the timed step)")
+    p.add_argument("--dtype", choices=["bf16", "fp16"], default="bf16",
+                   help="synchronisation precision (f2, P:190): 16-bit element type of the weights")
     p.add_argument("--route", action="store_true",
                    help="f3 per-parameter routing (P:389): records whose FULL copy is smaller go FULL")
     p.add_argument("--groups", type=int, default=0,
@@ -246,11 +248,14 @@ class Rank:
         sharded_model = topo in ("fanout", "sharded")
         self.shards = transport.shard_ranges(manifest.numel, half) if sharded_model else None
         codec = ss.SYNC_CODEC_COMPRESSED if args.codec == "compressed" else ss.SYNC_CODEC_RAW
-        kw = dict(bucket_limit=int(args.bucket_mb * (1 << 20)), codec=codec, crc=args.crc)
+        self.dtype = synth.DTYPE_FP16 if args.dtype == "fp16" else synth.DTYPE_BF16
+        kw = dict(bucket_limit=int(args.bucket_mb * (1 << 20)), codec=codec, crc=args.crc, dtype=self.dtype)
         rkw = dict(kw, route=args.route)   # routing is a sender-side choice
         self.X = self.Y = self.R = None
         self.sender = None
         self.tracking = args.tracking == "cast"
+        if self.tracking and args.dtype != "bf16":
+            raise SystemExit("--tracking cast implements Alg. 1's round_BF16 cast (bf16 only)")
         self.kstep = 0
         self.receivers = {}    # source rank -> GroupedReceiver
         if self.is_trainer:
@@ -267,7 +272,7 @@ class Rank:
             else:
                 self.X, self.Xv = sg.arena(mt, dev)   # trainer snapshot (swaps with Y under --commit swap)
                 self.Y, self.Yv = sg.arena(mt, dev)   # trainer current weights
-                sg.fill_old(self.Xv, mt, self.seed, tid0=tid0)
+                sg.fill_old(self.Xv, mt, self.seed, tid0=tid0, dtype=self.dtype)
                 sg.fill_new(self.Xv, self.Yv, mt, self.seed, args.rho, MASKS[args.mask], tid0=tid0)
                 self.sender = GroupedSender(self.Xv, self.Yv, groups=self.G, max_changed=cap, **rkw)
         self.loop_snapshot = args.replica == "snapshot"
@@ -293,7 +298,7 @@ class Rank:
                 mr, tid0, rseed = manifest.slice(lo, hi), lo, args.seed
             self.mr = mr
             self.R, self.Rv = sg.arena(mr, dev)
-            sg.fill_old(self.Rv, mr, rseed, tid0=tid0)
+            sg.fill_old(self.Rv, mr, rseed, tid0=tid0, dtype=self.dtype)
             # one receiver per source Trainer (its records carry ids local to its shard and group)
             for src, (lo, hi) in srcs.items():
                 self.receivers[src] = GroupedReceiver(self.Rv[lo:hi], groups=self.G, **kw)
@@ -483,7 +488,8 @@ def cpu_baseline(args, manifest: synth.Manifest, seed: int, sample_elems: float,
         tot += manifest.tensors[k].numel
         k += 1
     sub = manifest.slice(0, k, f"{manifest.name}[:{k}]")
-    olds, news = sc.generate(sub, seed=seed, rho=args.rho, mask=MASKS[args.mask])
+    dt = synth.DTYPE_FP16 if args.dtype == "fp16" else synth.DTYPE_BF16
+    olds, news = sc.generate(sub, seed=seed, rho=args.rho, mask=MASKS[args.mask], dtype=dt)
     codec = oracle.CODEC_COMPRESSED if args.codec == "compressed" else oracle.CODEC_RAW
     limit = int(args.bucket_mb * (1 << 20))
     R = [o.copy() for o in olds]
@@ -492,7 +498,7 @@ def cpu_baseline(args, manifest: synth.Manifest, seed: int, sample_elems: float,
     pk = None
     for _ in range(steps):
         t0 = time.perf_counter()
-        pk = oracle.sync_pack(olds, news, codec=codec, limit=limit, crc=args.crc)
+        pk = oracle.sync_pack(olds, news, codec=codec, limit=limit, crc=args.crc, route=args.route, dtype=dt)
         for b in range(pk.n_buckets):
             assert oracle.bucket_apply(pk.bucket(b), R) == oracle.OK
         for b in range(pk.n_buckets):          # snapshot commit (same scatter)
@@ -692,7 +698,7 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": d.world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms / K, 4), "higher_is_better": True,
         "scaling": "strong" if strong else "weak",
-        "vs_baseline": None, "dtype": "u16 (bf16 bit patterns; integer/bit work only)",
+        "vs_baseline": None, "dtype": f"u16 ({args.dtype} bit patterns; integer/bit work only)",
         "data": "synthetic: random-init bf16 weights of the named architecture (N(0,0.02) quantile table), "
                 f"{args.mask}-mask sparse perturbations, seeded",
         "config": {"workload": f"{manifest.name} bf16, {100 * (1 - args.rho):.1f}% sparsity, {args.mask} mask",
@@ -701,6 +707,7 @@ def run_ours(args):
                    "tensors": len(manifest.tensors),
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
                    "groups": r.G, "replica": args.replica, "tracking": args.tracking, "route": args.route,
+                   "element_dtype": args.dtype,
                    "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
                    "l2": "inputs larger than L2 (2 x S per Trainer); no flush"},
         "ms_per_phase": {n: round(float(v), 4) for n, v in

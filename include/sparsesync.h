@@ -39,7 +39,7 @@ typedef struct CUstream_st* sync_stream_t; /* == cudaStream_t; NULL = legacy def
 #define SYNC_OK 0
 #define SYNC_ERR_ARG -1          /* bad argument (NULL, size out of range) */
 #define SYNC_ERR_ALIGNMENT -2    /* device pointer not 16-byte aligned */
-#define SYNC_ERR_DTYPE -3        /* dtype other than BF16 */
+#define SYNC_ERR_DTYPE -3        /* unsupported dtype, or a record whose dtype tag differs from the context's */
 #define SYNC_ERR_WORKSPACE -4    /* workspace too small */
 #define SYNC_ERR_CUDA -5         /* a CUDA runtime call failed */
 #define SYNC_ERR_INDEX_RANGE -6  /* an index >= numel (S:327 IndexOutOfRange); no OOB write happened */
@@ -70,7 +70,13 @@ typedef struct {
   uint64_t max_changed;    /* capacity of the caller's I/V arrays (elements) */
   uint32_t codec;          /* SYNC_CODEC_* */
   uint32_t flags;          /* SYNC_FLAG_* */
+  uint32_t dtype;          /* SYNC_DTYPE_* of every manifest tensor (0 = BF16) */
 } sync_config;
+
+/* Element types (f2). Both are 16-bit patterns: every step is the same integer work and the record's
+ * dtype byte carries the tag; a receiver context only accepts records of its own dtype. */
+#define SYNC_DTYPE_BF16 1u
+#define SYNC_DTYPE_FP16 2u
 
 /* Per-sync statistics, filled by sync_ctx_stats() (blocking). */
 typedef struct {
@@ -102,7 +108,7 @@ typedef struct sync_ctx sync_ctx;   /* opaque host object */
 /* ---- context --------------------------------------------------------------
  * sync_workspace_size: device bytes the context needs (tile look-back states,
  * manifest tables, record/chunk plan, status word).
- * sync_ctx_create: validates the manifest (numel < 2^31, dtype BF16 implied),
+ * sync_ctx_create: validates the manifest (numel < 2^31) and the dtype (BF16 or FP16),
  * uploads its tables into d_workspace on `stream`, and returns a host object.
  * The same context serves a sender (extract/compress/pack/commit) and a
  * receiver (unpack/decompress/apply) over the same manifest (the

@@ -38,6 +38,8 @@ SYNC_CODEC_RAW = 0
 SYNC_CODEC_COMPRESSED = 1
 SYNC_FLAG_CRC = 1
 SYNC_FLAG_ROUTE = 2
+SYNC_DTYPE_BF16 = 1
+SYNC_DTYPE_FP16 = 2
 SYNC_CHUNK = 16384
 
 EXPORTS = [
@@ -68,7 +70,7 @@ class _Manifest(ctypes.Structure):
 
 class _Config(ctypes.Structure):
     _fields_ = [("bucket_limit", ctypes.c_uint64), ("max_changed", ctypes.c_uint64),
-                ("codec", ctypes.c_uint32), ("flags", ctypes.c_uint32)]
+                ("codec", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("dtype", ctypes.c_uint32)]
 
 
 class _Stats(ctypes.Structure):
@@ -167,12 +169,12 @@ def _dev_ptr(t: torch.Tensor) -> ctypes.c_void_p:
 
 
 def _bits(t: torch.Tensor) -> torch.Tensor:
-    """bf16 / int16 / uint16 tensor -> its 16-bit patterns (a view, no copy)."""
-    if t.dtype == torch.bfloat16:
+    """bf16 / fp16 / int16 / uint16 tensor -> its 16-bit patterns (a view, no copy)."""
+    if t.dtype in (torch.bfloat16, torch.float16):
         return t.view(torch.int16)
     if t.dtype in (torch.int16, torch.uint16):
         return t
-    raise SyncError(SYNC_ERR_DTYPE, f"dtype {t.dtype} (BF16 only)")
+    raise SyncError(SYNC_ERR_DTYPE, f"dtype {t.dtype} (16-bit element types only)")
 
 
 def ptr_table(tensors, device) -> torch.Tensor:
@@ -236,7 +238,8 @@ class SyncContext:
     """A manifest (ordered tensor sizes) + config + device workspace, for sender and receiver calls."""
 
     def __init__(self, numel, bucket_limit: int = 256 << 20, max_changed: int | None = None,
-                 codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, device=None, route: bool = False):
+                 codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, device=None, route: bool = False,
+                 dtype: int = SYNC_DTYPE_BF16):
         self.numel = [int(n) for n in numel]
         self.device = torch.device(device or "cuda")
         self.T = len(self.numel)
@@ -244,7 +247,7 @@ class SyncContext:
         self._numel_arr = (ctypes.c_uint64 * max(self.T, 1))(*self.numel)
         self._m = _Manifest(self.T, self._numel_arr)
         self._c = _Config(int(bucket_limit), self.max_changed, int(codec),
-                          (SYNC_FLAG_CRC if crc else 0) | (SYNC_FLAG_ROUTE if route else 0))
+                          (SYNC_FLAG_CRC if crc else 0) | (SYNC_FLAG_ROUTE if route else 0), int(dtype))
         self.codec, self.crc, self.bucket_limit, self.route = codec, crc, bucket_limit, route
         need = ctypes.c_size_t()
         _ck(lib().sync_workspace_size(ctypes.byref(self._m), ctypes.byref(self._c), ctypes.byref(need)),

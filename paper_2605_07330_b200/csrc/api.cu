@@ -77,6 +77,7 @@ struct Dims {
 int check_manifest(const sync_manifest* m, const sync_config* c, Dims* d) {
   if (!m || !c || (m->n_tensors && !m->numel)) return SYNC_ERR_ARG;
   if (c->codec > SYNC_CODEC_COMPRESSED || c->bucket_limit < 64) return SYNC_ERR_ARG;
+  if (c->dtype > SYNC_DTYPE_FP16) return SYNC_ERR_DTYPE;
   d->T = m->n_tensors;
   d->n_tiles = 0;
   u64 maxn = 0;
@@ -226,6 +227,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   p.cap = c->max_changed;
   p.codec = c->codec;
   p.route = (c->flags & SYNC_FLAG_ROUTE) ? 1 : 0;
+  p.dtype = c->dtype ? c->dtype : SYNC_DTYPE_BF16;
   p.cur = nullptr;
   p.max_chunks = d.max_chunks;
   p.numel = reinterpret_cast<const u64*>(w + L.numel);
@@ -351,6 +353,7 @@ int sync_cast_track_batched(sync_ctx* x, const float* const* d_master_ptrs, uint
                             uint32_t* d_bitmap, sync_stream_t stream) {
   if (!x || (x->d.T && (!d_master_ptrs || !d_weight_ptrs || !d_bitmap))) return SYNC_ERR_ARG;
   if (x->d.T && !aligned16(d_bitmap)) return SYNC_ERR_ALIGNMENT;
+  if (x->plan.dtype != SYNC_DTYPE_BF16) return SYNC_ERR_DTYPE;   // the cast is round_BF16 (Alg. 1 l.5)
   launch_cast_track(track_args(x, d_bitmap), d_master_ptrs, d_weight_ptrs, 8 * x->sm_count, (cudaStream_t)stream);
   CK(cudaGetLastError());
   return SYNC_OK;
@@ -577,7 +580,8 @@ int sync_bucket_unpack(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, syn
   const u32* bad;
   int st = maybe_crc_check(x, &d_bucket, &bytes, 1, s, &bad);
   if (st) return st;
-  launch_unpack(d_bucket, bytes, x->d.T, x->plan.numel, d_views, max_views, d_n_records, x->plan.status, s);
+  launch_unpack(d_bucket, bytes, x->d.T, x->plan.numel, d_views, max_views, d_n_records, x->plan.status,
+                x->plan.dtype, s);
   CK(cudaGetLastError());
   return SYNC_OK;
 }
@@ -592,9 +596,9 @@ int sync_decompress(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, uint32
   if (st) return st;
   sync_record_view* views = reinterpret_cast<sync_record_view*>(x->ws + x->L.views);
   u32* nv = reinterpret_cast<u32*>(x->ws + x->L.nviews);
-  launch_unpack(d_bucket, bytes, x->d.T, x->plan.numel, views, x->d.T, nv, x->plan.status, s);
+  launch_unpack(d_bucket, bytes, x->d.T, x->plan.numel, views, x->d.T, nv, x->plan.status, x->plan.dtype, s);
   launch_decode(&d_bucket, &bytes, 1, x->d.T, x->plan.numel, nullptr, views, d_I, d_V, d_cap, x->plan.status, bad,
-                x->grid, s);
+                x->plan.dtype, x->grid, s);
   CK(cudaGetLastError());
   return SYNC_OK;
 }
@@ -608,7 +612,7 @@ int sync_decompress_apply(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, 
   int st = maybe_crc_check(x, &d_bucket, &bytes, 1, s, &bad);
   if (st) return st;
   launch_decode(&d_bucket, &bytes, 1, x->d.T, x->plan.numel, d_weight_ptrs, nullptr, nullptr, nullptr, 0,
-                x->plan.status, bad, x->grid, s);
+                x->plan.status, bad, x->plan.dtype, x->grid, s);
   CK(cudaGetLastError());
   return SYNC_OK;
 }
@@ -625,7 +629,7 @@ int sync_decompress_apply_batched(sync_ctx* x, const uint8_t* const* h_buckets, 
     int st = maybe_crc_check(x, h_buckets + b0, h_bytes + b0, n, s, &bad);
     if (st) return st;
     launch_decode(h_buckets + b0, h_bytes + b0, n, x->d.T, x->plan.numel, d_weight_ptrs, nullptr, nullptr,
-                  nullptr, 0, x->plan.status, bad, x->grid, s);
+                  nullptr, 0, x->plan.status, bad, x->plan.dtype, x->grid, s);
   }
   CK(cudaGetLastError());
   return SYNC_OK;

@@ -46,7 +46,7 @@ struct RecHdr {
 };
 
 __device__ __forceinline__ bool read_record(const u8* bk, const BucketHdr& h, u32 ro, u32 n_tensors,
-                                            const u64* numel, RecHdr* r) {
+                                            const u64* numel, RecHdr* r, u32 dtype) {
   if ((ro & 15u) || (u64)ro + 16 > h.bytes) return false;
   const u32* w = reinterpret_cast<const u32*>(bk + ro);
   r->tid = w[0];
@@ -56,7 +56,7 @@ __device__ __forceinline__ bool read_record(const u8* bk, const BucketHdr& h, u3
   r->dtype = (w[3] >> 8) & 0xFFu;
   r->codec = (w[3] >> 16) & 0xFFu;
   if (r->rb < 16 || (r->rb & 15u) || (u64)ro + r->rb > h.bytes) return false;
-  if (r->tid >= n_tensors || r->dtype != 1 || r->mode > 2 || r->codec > 1 || r->nnz == 0) return false;
+  if (r->tid >= n_tensors || r->dtype != dtype || r->mode > 2 || r->codec > 1 || r->nnz == 0) return false;
   if ((u64)r->nnz > numel[r->tid]) return false;
   if (r->mode == kModeFull) return (u64)r->nnz == numel[r->tid] && 16 + 2ull * r->nnz <= r->rb;
   if (r->codec == SYNC_CODEC_RAW) return r->mode == 1 && 16 + 6ull * r->nnz <= r->rb;
@@ -67,7 +67,8 @@ __device__ __forceinline__ bool read_record(const u8* bk, const BucketHdr& h, u3
 
 // ---------------------------------------------------------------------------- unpack
 __global__ void __launch_bounds__(1024) k_unpack(const u8* bk, u64 bytes, u32 n_tensors, const u64* numel,
-                                                 sync_record_view* views, u32 max_views, u32* n_out, u32* status) {
+                                                 sync_record_view* views, u32 max_views, u32* n_out, u32* status,
+                                                 u32 dtype) {
   __shared__ u64 s_w[33];
   __shared__ int s_err;
   BucketHdr h;
@@ -90,8 +91,8 @@ __global__ void __launch_bounds__(1024) k_unpack(const u8* bk, u64 bytes, u32 n_
     u64 nnz = 0;
     if (q < h.n_records) {
       u32 ro = dir[2 * q];
-      if (!read_record(bk, h, ro, n_tensors, numel, &r)) {
-        s_err = 1;
+      if (!read_record(bk, h, ro, n_tensors, numel, &r, dtype)) {
+        s_err = (ro + 16 <= h.bytes && bk[ro + 13] != dtype) ? 2 : 1;
       } else {
         nnz = r.nnz;
         sync_record_view v;
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(1024) k_unpack(const u8* bk, u64 bytes, u32 n_
   __syncthreads();
   if (threadIdx.x == 0) {
     if (s_err || chunk_carry != h.n_chunks) {
-      latch(status, SYNC_ERR_CORRUPT);
+      latch(status, s_err == 2 ? SYNC_ERR_DTYPE : SYNC_ERR_CORRUPT);
       *n_out = 0;
     } else {
       *n_out = h.n_records;
@@ -154,7 +155,8 @@ struct DecodeModel {
 template <bool kApply>
 __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, const u64* numel,
                                                u16* const* weights, const sync_record_view* views, u32* I_out,
-                                               u16* V_out, u64 out_cap, u32* status, const u32* crc_bad) {
+                                               u16* V_out, u64 out_cap, u32* status, const u32* crc_bad,
+                                               u32 dtype) {
   __shared__ DecodeModel s_dm[8];
   __shared__ BucketHdr s_h[kDecodeBatch];
   __shared__ u64 s_pre[kDecodeBatch + 1];
@@ -195,11 +197,12 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
     const u32 ro = dir[2 * q];
     RecHdr r;
     const u64 fc = dir[2 * q + 1];
-    bool ok = read_record(bk, h, ro, n_tensors, numel, &r);
+    bool ok = read_record(bk, h, ro, n_tensors, numel, &r, dtype);
     const u64 nch = ok ? (r.nnz + kChunk - 1) / kChunk : 0;
     const u64 k = g - fc;
     if (!ok || k >= nch) {
-      if (lane == 0) latch(status, SYNC_ERR_CORRUPT);
+      const bool tag = (u64)ro + 16 <= h.bytes && bk[ro + 13] != dtype;   // another element type
+      if (lane == 0) latch(status, tag ? SYNC_ERR_DTYPE : SYNC_ERR_CORRUPT);
       continue;
     }
     const u8* rec = bk + ro;
@@ -423,14 +426,14 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
 }
 
 void launch_unpack(const u8* bucket, u64 bytes, u32 n_tensors, const u64* numel, sync_record_view* views,
-                   u32 max_views, u32* n_records, u32* status, cudaStream_t s) {
-  k_unpack<<<1, 1024, 0, s>>>(bucket, bytes, n_tensors, numel, views, max_views, n_records, status);
+                   u32 max_views, u32* n_records, u32* status, u32 dtype, cudaStream_t s) {
+  k_unpack<<<1, 1024, 0, s>>>(bucket, bytes, n_tensors, numel, views, max_views, n_records, status, dtype);
   count_launch();
 }
 
 void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u32 n_tensors, const u64* numel,
                    u16* const* weights, const sync_record_view* views, u32* I_out, u16* V_out, u64 out_cap,
-                   u32* status, const u32* crc_bad, int grid, cudaStream_t s) {
+                   u32* status, const u32* crc_bad, u32 dtype, int grid, cudaStream_t s) {
   for (u32 b0 = 0; b0 < n_buckets; b0 += kDecodeBatch) {
     DecodeBatch bb;
     bb.n = n_buckets - b0 < kDecodeBatch ? n_buckets - b0 : kDecodeBatch;
@@ -440,9 +443,11 @@ void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u3
     }
     const u32* bad = crc_bad ? crc_bad + b0 : nullptr;
     if (weights)
-      k_decode<true><<<grid, 256, 0, s>>>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status, bad);
+      k_decode<true><<<grid, 256, 0, s>>>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status, bad,
+                                          dtype);
     else
-      k_decode<false><<<grid, 256, 0, s>>>(bb, n_tensors, numel, nullptr, views, I_out, V_out, out_cap, status, bad);
+      k_decode<false><<<grid, 256, 0, s>>>(bb, n_tensors, numel, nullptr, views, I_out, V_out, out_cap, status, bad,
+                                           dtype);
     count_launch();
   }
 }

@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
       h[0] = t;
       h[1] = mode == kModeFull ? (u32)p.numel[t] : (u32)nnz;
       h[2] = (u32)rb;
-      h[3] = mode | (1u << 8) | ((comp ? 1u : 0u) << 16);
+      h[3] = mode | (p.dtype << 8) | ((comp ? 1u : 0u) << 16);
     }
 
     if (mode == kModeFull) {

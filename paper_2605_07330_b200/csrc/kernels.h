@@ -33,6 +33,7 @@ struct Plan {
   uint32_t* status;
   int prof;                      // debug instrumentation switch
   int route;                     // f3: SYNC_FLAG_ROUTE
+  uint32_t dtype;                // record dtype tag (SYNC_DTYPE_*)
   const uint16_t* const* cur;    // f3: current weights (FULL records), device pointer table
 };
 
@@ -88,13 +89,13 @@ void launch_crc_check(const uint8_t* bucket, uint64_t bytes, uint32_t* seg_scrat
                       uint32_t* status, cudaStream_t s);
 void launch_unpack(const uint8_t* bucket, uint64_t bytes, uint32_t n_tensors, const uint64_t* numel,
                    sync_record_view* views, uint32_t max_views, uint32_t* n_records, uint32_t* status,
-                   cudaStream_t s);
+                   uint32_t dtype, cudaStream_t s);
 // buckets / bytes: HOST arrays of n_buckets device addresses and sizes; crc_bad: device flags [n_buckets]
 // (or null). One kernel per 32 buckets.
 void launch_decode(const uint8_t* const* buckets, const uint64_t* bytes, uint32_t n_buckets, uint32_t n_tensors,
                    const uint64_t* numel, uint16_t* const* weights, const sync_record_view* views, uint32_t* I_out,
-                   uint16_t* V_out, uint64_t out_cap, uint32_t* status, const uint32_t* crc_bad, int grid,
-                   cudaStream_t s);
+                   uint16_t* V_out, uint64_t out_cap, uint32_t* status, const uint32_t* crc_bad, uint32_t dtype,
+                   int grid, cudaStream_t s);
 
 // track.cu (f1 cast-fused tracking, Alg. 1)
 struct TrackArgs {

@@ -24,8 +24,9 @@ class SparseSyncSender:
 
     def __init__(self, snapshot, current, bucket_limit: int = 256 << 20, max_changed: int | None = None,
                  codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, expected_density: float = 0.02,
-                 route: bool = False):
-        """route: per-parameter routing (f3): a record whose FULL copy is smaller goes FULL."""
+                 route: bool = False, dtype: int = 1):
+        """route: per-parameter routing (f3): a record whose FULL copy is smaller goes FULL.
+        dtype: SYNC_DTYPE_BF16 / SYNC_DTYPE_FP16 (f2): the record tag; the work is the same."""
         self.snapshot = _flat_bits(snapshot)
         self.current = _flat_bits(current)
         assert len(self.snapshot) == len(self.current)
@@ -36,7 +37,7 @@ class SparseSyncSender:
         self.numel = [t.numel() for t in self.current]
         total = sum(self.numel)
         cap = int(max_changed if max_changed is not None else min(total, int(total * expected_density) + 65536))
-        self._cfg = dict(bucket_limit=bucket_limit, codec=codec, crc=crc, route=route)
+        self._cfg = dict(bucket_limit=bucket_limit, codec=codec, crc=crc, route=route, dtype=dtype)
         self.old_ptrs = ptr_table(self.snapshot, self.device)
         self.new_ptrs = ptr_table(self.current, self.device)
         self.counts = torch.zeros(max(len(self.numel), 1), dtype=torch.int64, device=self.device)
@@ -202,13 +203,13 @@ class SparseSyncReceiver:
     """Rollout side: holds the weights and applies buckets in place (bit-exact)."""
 
     def __init__(self, weights, bucket_limit: int = 256 << 20, codec: int = SYNC_CODEC_COMPRESSED,
-                 crc: bool = False):
+                 crc: bool = False, dtype: int = 1):
         self.weights = _flat_bits(weights)
         self.device = self.weights[0].device if self.weights else torch.device("cuda")
         numel = [t.numel() for t in self.weights]
         # a receiver never extracts or encodes: no changed-element capacity needed
         self.ctx = SyncContext(numel, bucket_limit=bucket_limit, max_changed=0, codec=codec, crc=crc,
-                               device=self.device)
+                               device=self.device, dtype=dtype)
         self.weight_ptrs = ptr_table(self.weights, self.device)
 
     def apply(self, bucket, nbytes: int | None = None, stream=None):

@@ -205,6 +205,39 @@ def test_routing_needs_current_weights():
     assert e.value.code == ss.SYNC_ERR_ARG
 
 
+@pytest.mark.parametrize("codec", [ss.SYNC_CODEC_COMPRESSED, ss.SYNC_CODEC_RAW])
+def test_fp16_bit_exact_and_tag_checked(codec):
+    """f2 FP16: synthetic FP16 weights (GPU generator == CPU twin), GPU buckets == the oracle's FP16
+    buckets, an FP16 replica reconstructs them; a BF16 receiver rejects them (SYNC_ERR_DTYPE, no write)."""
+    import synth.gpu as sg
+    m = mixed_manifest()
+    olds, news = synth.generate(m, seed=31, rho=0.03, dtype=synth.DTYPE_FP16)
+    _, views = sg.arena(m, DEV)
+    _, nviews = sg.arena(m, DEV)
+    sg.fill_old(views, m, 31, dtype=synth.DTYPE_FP16)
+    sg.fill_new(views, nviews, m, 31, 0.03)
+    assert all((host16(v) == o).all() for v, o in zip(views, olds))
+    assert all((host16(v) == n).all() for v, n in zip(nviews, news))
+    ref = oracle.sync_pack(olds, news, codec=codec, limit=32 << 10, dtype=oracle.DTYPE_FP16)
+    snd = ss.SparseSyncSender(views, nviews, bucket_limit=32 << 10, codec=codec, dtype=ss.SYNC_DTYPE_FP16,
+                              max_changed=sum(o.size for o in olds))
+    bl = snd.sync()
+    got = [snd.bucket(b).cpu().numpy().tobytes() for b in range(len(bl))]
+    assert got == [ref.bucket(b) for b in range(ref.n_buckets)]
+    R = [to_dev(o) for o in olds]
+    rcv = ss.SparseSyncReceiver(R, bucket_limit=32 << 10, codec=codec, dtype=ss.SYNC_DTYPE_FP16)
+    rcv.apply_many([snd.bucket(b) for b in range(len(bl))])
+    torch.cuda.synchronize()
+    rcv.check()
+    assert all((host16(r) == n).all() for r, n in zip(R, news))
+    B = [to_dev(o) for o in olds]
+    wrong = ss.SparseSyncReceiver(B, bucket_limit=32 << 10, codec=codec)     # a BF16 context
+    wrong.apply_many([snd.bucket(b) for b in range(len(bl))])
+    torch.cuda.synchronize()
+    assert wrong.ctx.sync_status() == ss.SYNC_ERR_DTYPE
+    assert all((host16(b) == o).all() for b, o in zip(B, olds))
+
+
 def test_delta16_abs32_boundary():
     # gap of exactly 32767 stays DELTA16, 32768 forces ABS32 (P:360, DESIGN C4)
     n = 70_000
