@@ -31,6 +31,7 @@ ERR_CRC = -12
 
 DELTA16, ABS32 = 0, 1
 DTYPE_BF16, DTYPE_FP16 = 1, 2
+DELTA16E = 3
 CODEC_RAW, CODEC_COMPRESSED = 0, 1
 CHUNK = 16384
 
@@ -69,6 +70,11 @@ def lib():
             "or_rans_decode": (i32, [P, u32, u32, P]),
             "or_record_bound": (u64, [u64]),
             "or_encode_record": (u64, [u32, P, P, u64, i32, P, i32]),
+            "or_encode_record_ex": (u64, [u32, P, P, u64, i32, P, i32, i32]),
+            "or_count_escapes": (u64, [P, u64]),
+            "or_index_mode_escape": (i32, [P, u64]),
+            "or_encode_indices_escape": (u64, [P, u64, P]),
+            "or_decode_indices_escape": (u64, [P, u64, u64, P]),
             "or_decode_record": (i32, [P, u64, P, P, P, P, u64]),
             "or_crc32": (u32, [P, u64]),
             "or_bucketize": (u32, [P, u64, u64, P]),
@@ -198,12 +204,31 @@ def encode_full_record(tensor_id: int, W, codec: int = CODEC_COMPRESSED, dtype: 
     return out[:n].tobytes()
 
 
-def encode_record(tensor_id: int, I, V, codec: int = CODEC_COMPRESSED, dtype: int = 1) -> bytes:
+def encode_indices_escape(I) -> bytes:
+    """f4 DELTA16E index stream."""
+    I = np.ascontiguousarray(I, np.uint32)
+    out = np.zeros(4 * max(I.size, 1), np.uint8)
+    n = lib().or_encode_indices_escape(_p(I), I.size, _p(out))
+    return out[:n].tobytes()
+
+
+def decode_indices_escape(stream: bytes, nnz: int):
+    """Inverse; returns (I, words consumed) or (None, None) on a truncated stream."""
+    buf = np.frombuffer(stream, np.uint8).copy()
+    I = np.zeros(max(nnz, 1), np.uint32)
+    w = lib().or_decode_indices_escape(_p(buf), len(stream) // 2, nnz, _p(I))
+    if w == (1 << 64) - 1:
+        return None, None
+    return I[:nnz].copy(), int(w)
+
+
+def encode_record(tensor_id: int, I, V, codec: int = CODEC_COMPRESSED, dtype: int = 1,
+                  escape: bool = False) -> bytes:
     I = np.ascontiguousarray(I, np.uint32)
     V = np.ascontiguousarray(V, np.uint16)
     assert I.size == V.size and I.size > 0
     out = np.zeros(lib().or_record_bound(I.size), np.uint8)
-    n = lib().or_encode_record(tensor_id, _p(I), _p(V), I.size, codec, _p(out), dtype)
+    n = lib().or_encode_record_ex(tensor_id, _p(I), _p(V), I.size, codec, _p(out), dtype, 1 if escape else 0)
     return out[:n].tobytes()
 
 
@@ -237,7 +262,8 @@ class PackResult:
         self.buf = buf
         self.offsets = offsets
         self.sizes = sizes
-        self.stats = dict(zip(["nnz", "n_records", "delta16", "abs32", "payload_bytes", "value_bytes", "full"],
+        self.stats = dict(zip(["nnz", "n_records", "delta16", "abs32", "payload_bytes", "value_bytes", "full",
+                               "delta16e"],
                               [int(s) for s in stats]))
 
     @property
@@ -250,9 +276,11 @@ class PackResult:
 
 
 def sync_pack(olds, news, codec: int = CODEC_COMPRESSED, limit: int = 256 << 20, crc: bool = False,
-              max_buckets: int = 1 << 16, route: bool = False, dtype: int = 1) -> PackResult:
+              max_buckets: int = 1 << 16, route: bool = False, dtype: int = 1,
+              escape: bool = False) -> PackResult:
     """Sender path (Alg. 2) over a manifest of (old, new) uint16 arrays.
-    route: per-parameter routing (f3) — a record goes FULL when that is smaller (DESIGN C19)."""
+    route: per-parameter routing (f3) — a record goes FULL when that is smaller (DESIGN C19).
+    escape: escape-coded DELTA16 (f4) for records with gaps > 32767."""
     olds = [_u16(o).ravel() for o in olds]
     news = [_u16(n).ravel() for n in news]
     T = len(olds)
@@ -267,8 +295,8 @@ def sync_pack(olds, news, codec: int = CODEC_COMPRESSED, limit: int = 256 << 20,
     buf = np.zeros(cap, np.uint8)
     offs = np.zeros(max_buckets, np.uint64)
     sizes = np.zeros(max_buckets, np.uint64)
-    stats = np.zeros(7, np.uint64)
-    flags = (1 if crc else 0) | (2 if route else 0)
+    stats = np.zeros(8, np.uint64)
+    flags = (1 if crc else 0) | (2 if route else 0) | (4 if escape else 0)
     nb = L.or_sync_pack(T, _p(numel), ctypes.cast(op, ctypes.c_void_p), ctypes.cast(np_, ctypes.c_void_p),
                         codec, limit, flags, _p(buf), cap, _p(offs), _p(sizes), max_buckets,
                         _p(stats), dtype)

@@ -168,6 +168,67 @@ uint64_t or_encode_indices(const uint32_t* I, uint64_t nnz, int mode, uint8_t* o
   return 4 * nnz;
 }
 
+/* ---------------------------------------------------------------------------
+ * f4 escape-coded DELTA16 (P:360 keeps int32 whenever a gap
+ * does not fit — for clustered masks that is every record). DELTA16E (idx_mode 3,
+ * DESIGN §3.6): per element one u16 word Δ_k when Δ_k <= 32767, else two words
+ * (0x8000 | Δ_k >> 16), (Δ_k & 0xFFFF) — an escape. Δ_0 = I_0 as in DELTA16.
+ * ------------------------------------------------------------------------- */
+enum { OR_DELTA16E = 3 };
+
+uint64_t or_count_escapes(const uint32_t* I, uint64_t nnz) {
+  uint64_t e = 0;
+  uint32_t prev = 0;
+  for (uint64_t k = 0; k < nnz; ++k) {
+    if (I[k] - prev > 32767u) ++e;
+    prev = I[k];
+  }
+  return e;
+}
+
+/* Mode with the escape option (flags bit 2): DELTA16 if no gap escapes; else DELTA16E when its stream
+ * (2 (nnz + escapes) bytes) is smaller than ABS32's (4 nnz), i.e. escapes < nnz; else ABS32. */
+int or_index_mode_escape(const uint32_t* I, uint64_t nnz) {
+  uint64_t e = or_count_escapes(I, nnz);
+  if (e == 0) return OR_DELTA16;
+  return e < nnz ? OR_DELTA16E : OR_ABS32;
+}
+
+uint64_t or_encode_indices_escape(const uint32_t* I, uint64_t nnz, uint8_t* out) {
+  uint64_t w = 0;
+  uint32_t prev = 0;
+  for (uint64_t k = 0; k < nnz; ++k) {
+    uint32_t d = I[k] - prev;
+    prev = I[k];
+    if (d <= 32767u) {
+      put16(out + 2 * w++, (uint16_t)d);
+    } else {
+      put16(out + 2 * w++, (uint16_t)(0x8000u | (d >> 16)));
+      put16(out + 2 * w++, (uint16_t)(d & 0xFFFFu));
+    }
+  }
+  return 2 * w;
+}
+
+/* Inverse of or_encode_indices_escape; returns the words consumed, or UINT64_MAX if the stream (words
+ * available) ends inside an element. */
+uint64_t or_decode_indices_escape(const uint8_t* in, uint64_t words, uint64_t nnz, uint32_t* I) {
+  uint64_t w = 0;
+  uint32_t acc = 0;
+  for (uint64_t k = 0; k < nnz; ++k) {
+    if (w >= words) return UINT64_MAX;
+    uint16_t a = get16(in + 2 * w++);
+    uint32_t d = a;
+    if (a & 0x8000u) {
+      if (w >= words) return UINT64_MAX;
+      d = ((uint32_t)(a & 0x7FFFu) << 16) | get16(in + 2 * w++);
+    }
+    acc += d;
+    I[k] = acc;
+  }
+  return w;
+}
+
 /* Inverse: DELTA16 running sum from 0; ABS32 copy. */
 void or_decode_indices(const uint8_t* in, uint64_t nnz, int mode, uint32_t* I) {
   if (mode == OR_DELTA16) {
@@ -325,8 +386,17 @@ uint64_t or_record_bound(uint64_t nnz) {
 }
 
 /* Encodes one record; returns record_bytes (multiple of 16). nnz >= 1. */
+uint64_t or_encode_record_ex(uint32_t tensor_id, const uint32_t* I, const uint16_t* V, uint64_t nnz,
+                             int codec, uint8_t* out, int dtype, int escape);
 uint64_t or_encode_record(uint32_t tensor_id, const uint32_t* I, const uint16_t* V, uint64_t nnz,
                           int codec, uint8_t* out, int dtype) {
+  return or_encode_record_ex(tensor_id, I, V, nnz, codec, out, dtype, 0);
+}
+
+/* escape != 0: the f4 DELTA16E option (flags bit 2). A DELTA16E record adds, after the chunk directory,
+ * n_chunks x u32: the word offset of each chunk's first index word (so chunks decode independently). */
+uint64_t or_encode_record_ex(uint32_t tensor_id, const uint32_t* I, const uint16_t* V, uint64_t nnz,
+                             int codec, uint8_t* out, int dtype, int escape) {
   uint8_t* rec = out;
   uint64_t off = 16;
   if (codec == OR_CODEC_RAW) {
@@ -342,8 +412,9 @@ uint64_t or_encode_record(uint32_t tensor_id, const uint32_t* I, const uint16_t*
     rec[12] = OR_ABS32; rec[13] = (uint8_t)dtype; rec[14] = OR_CODEC_RAW; rec[15] = 0;
     return total;
   }
-  int mode = or_index_mode(I, nnz);
-  uint64_t ib = or_encode_indices(I, nnz, mode, rec + off);
+  int mode = escape ? or_index_mode_escape(I, nnz) : or_index_mode(I, nnz);
+  uint64_t ib = mode == OR_DELTA16E ? or_encode_indices_escape(I, nnz, rec + off)
+                                    : or_encode_indices(I, nnz, mode, rec + off);
   memset(rec + off + ib, 0, pad_to(ib, 4) - ib);
   off += pad_to(ib, 4);
   for (uint64_t k = 0; k < nnz; ++k) rec[off + k] = (uint8_t)(V[k] & 0xFFu);
@@ -352,6 +423,16 @@ uint64_t or_encode_record(uint32_t tensor_id, const uint32_t* I, const uint16_t*
   uint64_t n_chunks = (nnz + OR_C - 1) / OR_C;
   uint64_t dir = off;
   off += 16 * n_chunks;
+  if (mode == OR_DELTA16E) {   /* word offset of each chunk's first index */
+    uint64_t w = 0;
+    uint32_t prev = 0;
+    for (uint64_t k = 0; k < nnz; ++k) {
+      if (k % OR_C == 0) put32(rec + off + 4 * (k / OR_C), (uint32_t)w);
+      w += (I[k] - prev > 32767u) ? 2 : 1;
+      prev = I[k];
+    }
+    off += 4 * n_chunks;
+  }
   uint8_t* hi = (uint8_t*)malloc(OR_C);
   for (uint64_t k = 0; k < n_chunks; ++k) {
     uint64_t p0 = k * OR_C;
@@ -364,7 +445,7 @@ uint64_t or_encode_record(uint32_t tensor_id, const uint32_t* I, const uint16_t*
       hb = nk;
       chunk_mode = OR_CHUNK_RAW;
     }
-    uint32_t base = (mode == OR_DELTA16 && k > 0) ? I[p0 - 1] : 0u;
+    uint32_t base = ((mode == OR_DELTA16 || mode == OR_DELTA16E) && k > 0) ? I[p0 - 1] : 0u;
     put32(rec + dir + 16 * k + 0, (uint32_t)off);
     put32(rec + dir + 16 * k + 4, hb);
     put32(rec + dir + 16 * k + 8, chunk_mode);
@@ -407,14 +488,14 @@ uint64_t or_encode_full_record(uint32_t tensor_id, const uint16_t* W, uint64_t n
 }
 
 /* Decodes one record (exact inverse, Alg. 3 l.5) into I, V
- * (nnz entries). Returns 0 or an error; *tensor_id/*nnz filled. */
+ * (nnz entries). Returns 0 or an error; *tensor_id and *nnz filled. */
 int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, uint64_t* nnz_out,
                      uint32_t* I, uint16_t* V, uint64_t cap) {
   if (avail < 16) return OR_ERR_TRUNCATED;
   uint32_t tid = get32(rec), nnz = get32(rec + 4), rb = get32(rec + 8);
   uint8_t mode = rec[12], dtype = rec[13], codec = rec[14];
   if (rb > avail || rb < 16 || (rb % 16) != 0) return OR_ERR_TRUNCATED;
-  if ((dtype != OR_DTYPE_BF16 && dtype != OR_DTYPE_FP16) || mode > 2 || codec > 1 || nnz == 0)
+  if ((dtype != OR_DTYPE_BF16 && dtype != OR_DTYPE_FP16) || mode > 3 || codec > 1 || nnz == 0)
     return OR_ERR_CORRUPT;
   *tensor_id = tid;
   *nnz_out = nnz;
@@ -434,14 +515,34 @@ int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, ui
     return OR_OK;
   }
   uint64_t off = 16;
-  uint64_t ib = (mode == OR_DELTA16 ? 2ull : 4ull) * nnz;
   uint64_t n_chunks = (nnz + OR_C - 1) / OR_C;
-  if (off + pad_to(ib, 4) + pad_to(nnz, 4) + 16 * n_chunks > rb) return OR_ERR_CORRUPT;
-  or_decode_indices(rec + off, nnz, mode, I);
+  uint64_t ib;
+  if (mode == OR_DELTA16E) {
+    /* the stream length follows from the escapes; the lo plane starts after it (padded to 4). The
+       words available are bounded by the record: parse, then check the layout. */
+    uint64_t words = (rb - 16) / 2;
+    uint64_t used = or_decode_indices_escape(rec + off, words, nnz, I);
+    if (used == UINT64_MAX) return OR_ERR_CORRUPT;
+    ib = 2 * used;
+  } else {
+    ib = (mode == OR_DELTA16 ? 2ull : 4ull) * nnz;
+  }
+  uint64_t table = mode == OR_DELTA16E ? 4 * n_chunks : 0;
+  if (off + pad_to(ib, 4) + pad_to(nnz, 4) + 16 * n_chunks + table > rb) return OR_ERR_CORRUPT;
+  if (mode != OR_DELTA16E) or_decode_indices(rec + off, nnz, mode, I);
   off += pad_to(ib, 4);
   const uint8_t* lo = rec + off;
   off += pad_to(nnz, 4);
   const uint8_t* dir = rec + off;
+  if (mode == OR_DELTA16E) {   /* the chunk word offsets must match the stream */
+    uint64_t w = 0;
+    uint32_t prev = 0;
+    for (uint64_t k = 0; k < nnz; ++k) {
+      if (k % OR_C == 0 && get32(dir + 16 * n_chunks + 4 * (k / OR_C)) != w) return OR_ERR_CORRUPT;
+      w += (I[k] - prev > 32767u) ? 2 : 1;
+      prev = I[k];
+    }
+  }
   uint8_t* hi = (uint8_t*)malloc(OR_C);
   int st = OR_OK;
   for (uint64_t k = 0; k < n_chunks && st == OR_OK; ++k) {
@@ -449,7 +550,7 @@ int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, ui
     uint32_t nk = (uint32_t)((nnz - p0) < OR_C ? (nnz - p0) : OR_C);
     uint32_t ho = get32(dir + 16 * k), hb = get32(dir + 16 * k + 4), cm = get32(dir + 16 * k + 8);
     uint32_t base = get32(dir + 16 * k + 12);
-    uint32_t expect_base = (mode == OR_DELTA16 && k > 0) ? I[p0 - 1] : 0u;
+    uint32_t expect_base = ((mode == OR_DELTA16 || mode == OR_DELTA16E) && k > 0) ? I[p0 - 1] : 0u;
     if (base != expect_base || (uint64_t)ho + hb > rb) { st = OR_ERR_CORRUPT; break; }
     if (cm == OR_CHUNK_RAW) {
       if (hb != nk) { st = OR_ERR_CORRUPT; break; }
@@ -508,13 +609,13 @@ uint32_t or_bucketize(const uint64_t* rec_bytes, uint64_t n_records, uint64_t li
  * offsets[b], 256-aligned), sizes[b]. Returns n_buckets or a negative error.
  * stats (may be NULL): [0] total nnz, [1] n_records, [2] delta16 records,
  * [3] abs32 records, [4] payload bytes (Σ bucket bytes), [5] value-stream bytes,
- * [6] FULL records (flags bit 1 = routing, f3).
+ * [6] FULL records (flags bit 1 = routing, f3), [7] DELTA16E records (flags bit 2 = escapes, f4).
  * ------------------------------------------------------------------------- */
 int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const uint16_t* const* old_ptrs,
                      const uint16_t* const* new_ptrs, int codec, uint64_t limit, uint32_t flags,
                      uint8_t* out, uint64_t out_cap, uint64_t* offsets, uint64_t* sizes,
                      uint32_t max_buckets, uint64_t* stats, int dtype) {
-  uint64_t st[7] = {0};
+  uint64_t st[8] = {0};
   /* 1. per tensor records into a scratch stream */
   uint64_t cap_total = 0;
   for (uint32_t t = 0; t < n_tensors; ++t) cap_total += or_record_bound(numel[t] ? numel[t] : 1);
@@ -529,7 +630,7 @@ int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const uint16_t* 
     uint16_t* V = (uint16_t*)malloc(sizeof(uint16_t) * (n ? n : 1));
     uint64_t nnz = or_extract(old_ptrs[t], new_ptrs[t], n, I, V);
     if (nnz > 0) {
-      uint64_t rb = or_encode_record(t, I, V, nnz, codec, stream + pos, dtype);
+      uint64_t rb = or_encode_record_ex(t, I, V, nnz, codec, stream + pos, dtype, (flags & 4u) != 0);
       int full = (flags & 2u) && or_full_record_bytes(n) < rb;   /* routing, DESIGN C19 */
       if (full) rb = or_encode_full_record(t, new_ptrs[t], n, codec, stream + pos, dtype);
       rec_bytes[n_records] = rb;
@@ -543,8 +644,16 @@ int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const uint16_t* 
         st[5] += rb - 16;
       } else if (codec == OR_CODEC_COMPRESSED) {
         int mode = stream[pos - rb + 12];
-        st[mode == OR_DELTA16 ? 2 : 3] += 1;
-        uint64_t ib = (mode == OR_DELTA16 ? 2 : 4) * nnz;
+        uint64_t ib = (mode == OR_ABS32 ? 4 : 2) * nnz;
+        if (mode == OR_DELTA16E) {
+          uint64_t e = 0;
+          uint32_t prev = 0;
+          for (uint64_t k = 0; k < nnz; ++k) { e += (I[k] - prev > 32767u); prev = I[k]; }
+          ib = 2 * (nnz + e);
+          st[7] += 1;
+        } else {
+          st[mode == OR_DELTA16 ? 2 : 3] += 1;
+        }
         st[5] += rb - 16 - pad_to(ib, 4);
       } else {
         st[3] += 1;
