@@ -393,8 +393,9 @@ uint64_t or_encode_record(uint32_t tensor_id, const uint32_t* I, const uint16_t*
   return or_encode_record_ex(tensor_id, I, V, nnz, codec, out, dtype, 0);
 }
 
-/* escape != 0: the f4 DELTA16E option (flags bit 2). A DELTA16E record adds, after the chunk directory,
- * n_chunks x u32: the word offset of each chunk's first index word (so chunks decode independently). */
+/* escape != 0: the f4 DELTA16E option (flags bit 2). A DELTA16E record carries, between its header and its
+ * index stream, (n_chunks + 1) x u32: the word offset of each chunk's first index word (so chunks decode
+ * independently) and the stream's total word count (so the planes after it can be located). */
 uint64_t or_encode_record_ex(uint32_t tensor_id, const uint32_t* I, const uint16_t* V, uint64_t nnz,
                              int codec, uint8_t* out, int dtype, int escape) {
   uint8_t* rec = out;
@@ -413,17 +414,8 @@ uint64_t or_encode_record_ex(uint32_t tensor_id, const uint32_t* I, const uint16
     return total;
   }
   int mode = escape ? or_index_mode_escape(I, nnz) : or_index_mode(I, nnz);
-  uint64_t ib = mode == OR_DELTA16E ? or_encode_indices_escape(I, nnz, rec + off)
-                                    : or_encode_indices(I, nnz, mode, rec + off);
-  memset(rec + off + ib, 0, pad_to(ib, 4) - ib);
-  off += pad_to(ib, 4);
-  for (uint64_t k = 0; k < nnz; ++k) rec[off + k] = (uint8_t)(V[k] & 0xFFu);
-  memset(rec + off + nnz, 0, pad_to(nnz, 4) - nnz);
-  off += pad_to(nnz, 4);
   uint64_t n_chunks = (nnz + OR_C - 1) / OR_C;
-  uint64_t dir = off;
-  off += 16 * n_chunks;
-  if (mode == OR_DELTA16E) {   /* word offset of each chunk's first index */
+  if (mode == OR_DELTA16E) {   /* word offset of each chunk's first index word, then the total */
     uint64_t w = 0;
     uint32_t prev = 0;
     for (uint64_t k = 0; k < nnz; ++k) {
@@ -431,8 +423,18 @@ uint64_t or_encode_record_ex(uint32_t tensor_id, const uint32_t* I, const uint16
       w += (I[k] - prev > 32767u) ? 2 : 1;
       prev = I[k];
     }
-    off += 4 * n_chunks;
+    put32(rec + off + 4 * n_chunks, (uint32_t)w);
+    off += 4 * (n_chunks + 1);
   }
+  uint64_t ib = mode == OR_DELTA16E ? or_encode_indices_escape(I, nnz, rec + off)
+                                    : or_encode_indices(I, nnz, mode, rec + off);
+  memset(rec + off + ib, 0, pad_to(ib, 4) - ib);
+  off += pad_to(ib, 4);
+  for (uint64_t k = 0; k < nnz; ++k) rec[off + k] = (uint8_t)(V[k] & 0xFFu);
+  memset(rec + off + nnz, 0, pad_to(nnz, 4) - nnz);
+  off += pad_to(nnz, 4);
+  uint64_t dir = off;
+  off += 16 * n_chunks;
   uint8_t* hi = (uint8_t*)malloc(OR_C);
   for (uint64_t k = 0; k < n_chunks; ++k) {
     uint64_t p0 = k * OR_C;
@@ -517,32 +519,33 @@ int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, ui
   uint64_t off = 16;
   uint64_t n_chunks = (nnz + OR_C - 1) / OR_C;
   uint64_t ib;
+  const uint8_t* table = NULL;
   if (mode == OR_DELTA16E) {
-    /* the stream length follows from the escapes; the lo plane starts after it (padded to 4). The
-       words available are bounded by the record: parse, then check the layout. */
-    uint64_t words = (rb - 16) / 2;
-    uint64_t used = or_decode_indices_escape(rec + off, words, nnz, I);
-    if (used == UINT64_MAX) return OR_ERR_CORRUPT;
-    ib = 2 * used;
+    if (off + 4 * (n_chunks + 1) > rb) return OR_ERR_CORRUPT;
+    table = rec + off;
+    off += 4 * (n_chunks + 1);
+    uint64_t total = get32(table + 4 * n_chunks);
+    if (total < nnz || total > 2ull * nnz || off + 2 * total > rb) return OR_ERR_CORRUPT;
+    if (or_decode_indices_escape(rec + off, total, nnz, I) != total) return OR_ERR_CORRUPT;
+    ib = 2 * total;
   } else {
     ib = (mode == OR_DELTA16 ? 2ull : 4ull) * nnz;
   }
-  uint64_t table = mode == OR_DELTA16E ? 4 * n_chunks : 0;
-  if (off + pad_to(ib, 4) + pad_to(nnz, 4) + 16 * n_chunks + table > rb) return OR_ERR_CORRUPT;
+  if (off + pad_to(ib, 4) + pad_to(nnz, 4) + 16 * n_chunks > rb) return OR_ERR_CORRUPT;
   if (mode != OR_DELTA16E) or_decode_indices(rec + off, nnz, mode, I);
-  off += pad_to(ib, 4);
-  const uint8_t* lo = rec + off;
-  off += pad_to(nnz, 4);
-  const uint8_t* dir = rec + off;
-  if (mode == OR_DELTA16E) {   /* the chunk word offsets must match the stream */
+  if (table) {   /* the chunk word offsets must match the stream */
     uint64_t w = 0;
     uint32_t prev = 0;
     for (uint64_t k = 0; k < nnz; ++k) {
-      if (k % OR_C == 0 && get32(dir + 16 * n_chunks + 4 * (k / OR_C)) != w) return OR_ERR_CORRUPT;
+      if (k % OR_C == 0 && get32(table + 4 * (k / OR_C)) != w) return OR_ERR_CORRUPT;
       w += (I[k] - prev > 32767u) ? 2 : 1;
       prev = I[k];
     }
   }
+  off += pad_to(ib, 4);
+  const uint8_t* lo = rec + off;
+  off += pad_to(nnz, 4);
+  const uint8_t* dir = rec + off;
   uint8_t* hi = (uint8_t*)malloc(OR_C);
   int st = OR_OK;
   for (uint64_t k = 0; k < n_chunks && st == OR_OK; ++k) {

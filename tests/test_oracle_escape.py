@@ -4,8 +4,8 @@ gap does not fit in int16, which for row-clustered masks is every record).
 * hand-worked streams at the 32767 / 32768 threshold and at the largest gap 2^31 - 1;
 * round trip on random gap mixtures; stream length = 2 (nnz + escapes);
 * the mode rule: no escape -> DELTA16, escapes < nnz -> DELTA16E, else ABS32;
-* each chunk decodes on its own from the word-offset table + its directory base (what a chunk-parallel
-  decoder relies on);
+* each chunk decodes on its own from the word-offset table (after the header, with the total word count
+  last) + its directory base (what a chunk-parallel decoder relies on);
 * on the R (clustered-row) mask every ABS32 record becomes DELTA16E, the payload shrinks, the replica is
   bit-exact; without the flag the bytes are the v1 format unchanged.
 """
@@ -69,10 +69,12 @@ def test_chunks_decode_independently():
     nch = (n + oracle.CHUNK - 1) // oracle.CHUNK
     esc = int(lib_count(I))
     ib = 2 * (n + esc)
-    lo_off = 16 + ib + (-ib) % 4
+    table = rec[16:16 + 4 * (nch + 1)].view(np.uint32)
+    assert table[nch] == n + esc
+    s0 = 16 + 4 * (nch + 1)
+    lo_off = s0 + ib + (-ib) % 4
     dir_off = lo_off + n + (-n) % 4
-    table = rec[dir_off + 16 * nch:dir_off + 20 * nch].view(np.uint32)
-    stream = rec[16:16 + ib].tobytes()
+    stream = rec[s0:s0 + ib].tobytes()
     for k in range(nch):
         p0 = k * oracle.CHUNK
         nk = min(oracle.CHUNK, n - p0)
