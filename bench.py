@@ -71,6 +71,8 @@ def parse():
                         "bitmap and the sync gathers them (no snapshot; the cast runs inside the timed step)")
     p.add_argument("--dtype", choices=["bf16", "fp16"], default="bf16",
                    help="synchronisation precision (f2, P:190): 16-bit element type of the weights")
+    p.add_argument("--escape", action="store_true",
+                   help="f4 escape-coded DELTA16 for records with index gaps > 32767 (clustered masks)")
     p.add_argument("--route", action="store_true",
                    help="f3 per-parameter routing (P:389): records whose FULL copy is smaller go FULL")
     p.add_argument("--groups", type=int, default=0,
@@ -250,7 +252,7 @@ class Rank:
         codec = ss.SYNC_CODEC_COMPRESSED if args.codec == "compressed" else ss.SYNC_CODEC_RAW
         self.dtype = synth.DTYPE_FP16 if args.dtype == "fp16" else synth.DTYPE_BF16
         kw = dict(bucket_limit=int(args.bucket_mb * (1 << 20)), codec=codec, crc=args.crc, dtype=self.dtype)
-        rkw = dict(kw, route=args.route)   # routing is a sender-side choice
+        rkw = dict(kw, route=args.route, escape=args.escape)   # routing / escapes are sender-side choices
         self.X = self.Y = self.R = None
         self.sender = None
         self.tracking = args.tracking == "cast"
@@ -498,7 +500,8 @@ def cpu_baseline(args, manifest: synth.Manifest, seed: int, sample_elems: float,
     pk = None
     for _ in range(steps):
         t0 = time.perf_counter()
-        pk = oracle.sync_pack(olds, news, codec=codec, limit=limit, crc=args.crc, route=args.route, dtype=dt)
+        pk = oracle.sync_pack(olds, news, codec=codec, limit=limit, crc=args.crc, route=args.route, dtype=dt,
+                              escape=args.escape)
         for b in range(pk.n_buckets):
             assert oracle.bucket_apply(pk.bucket(b), R) == oracle.OK
         for b in range(pk.n_buckets):          # snapshot commit (same scatter)
@@ -554,7 +557,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         r.step()
     torch.cuda.synchronize()
-    nnz = payload = nb = raw_payload = vbytes = n16 = n32 = 0
+    nnz = payload = nb = raw_payload = vbytes = n16 = n32 = n16e = 0
     if r.sender is not None:   # rank 0 is always a Trainer
         st = [p.ctx.sync_status() for p in r.sender.parts]
         assert not any(st), f"sender status {st}"
@@ -563,6 +566,7 @@ def run_ours(args):
         nb = len(bl)
         payload = sum(z for _, z in bl)
         nnz, vbytes, n16, n32 = stats["nnz"], stats["value_bytes"], stats["n_delta16"], stats["n_abs32"]
+        n16e = stats.get("n_delta16e", 0)
         counts = [c for p in r.sender.parts for c in p.counts.cpu().tolist()]
         raw_payload = sum(((16 + 6 * c + 15) // 16) * 16 for c in counts if c) + 48 * max(nb, 1)
     local_alg_extract = 2 * r.S + 6 * nnz
@@ -662,6 +666,7 @@ def run_ours(args):
     value = total_S * K / (ms / 1e3) / 1e9
     nnz_t, payload_t, raw_t = d.sum(nnz), d.sum(payload), d.sum(raw_payload)
     vbytes_t, n16_t, n32_t, nb_t = d.sum(vbytes), d.sum(n16), d.sum(n32), d.sum(nb)
+    n16e_t = d.sum(n16e)
     achieved = local_alg_extract / (ext_ms_local / 1e3) / 1e9   # rank 0 (a Trainer), its own launch
     roof_kernel, roof_bytes = "k_extract (K1)", local_alg_extract
     if r.tracking:
@@ -707,7 +712,7 @@ def run_ours(args):
                    "tensors": len(manifest.tensors),
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
                    "groups": r.G, "replica": args.replica, "tracking": args.tracking, "route": args.route,
-                   "element_dtype": args.dtype,
+                   "element_dtype": args.dtype, "escape": args.escape,
                    "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
                    "l2": "inputs larger than L2 (2 x S per Trainer); no flush"},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
@@ -722,7 +727,7 @@ def run_ours(args):
                     "bytes": int(payload_t), "x_comp": round(total_S / max(payload_t, 1), 2),
                     "x_raw_eq1": round(total_S / max(raw_t, 1), 2),
                     "alpha": round(vbytes_t / max(2 * nnz_t, 1), 4),
-                    "delta16_records": int(n16_t), "abs32_records": int(n32_t),
+                    "delta16_records": int(n16_t), "abs32_records": int(n32_t), "delta16e_records": int(n16e_t),
                     "paper_context": "paper: 32-54x raw, ~60-101x compressed on H100 clusters (P:22, P:380)"},
         "clocks": clk, "gpu_launches": int(launches), "bit_exact_replica": verify, "e2e": e2e,
         "latency_per_update": latency,

@@ -57,6 +57,9 @@ typedef struct CUstream_st* sync_stream_t; /* == cudaStream_t; NULL = legacy def
 #define SYNC_FLAG_ROUTE 2u       /* f3 per-parameter routing: a record goes FULL (the whole tensor,
                                     idx_mode 2) when that is smaller than its sparse record (DESIGN C19);
                                     needs sync_set_current()                                              */
+#define SYNC_FLAG_ESCAPE 4u      /* f4 escape-coded DELTA16: a record with gaps > 32767 keeps
+                                    2-byte deltas plus one escape word per large gap (idx_mode 3) instead
+                                    of falling back to 4-byte absolute indices, when that is smaller       */
 #define SYNC_CHUNK 16384u        /* values per chunk */
 
 /* Ordered tensor list = record order (model iteration order). Host memory. */
@@ -90,6 +93,7 @@ typedef struct {
   uint64_t index_bytes;    /* Σ padded index-stream bytes */
   uint64_t value_bytes;    /* Σ (record_bytes - 16 - index bytes): α numerator (DESIGN C5) */
   uint64_t n_full;         /* records routed FULL (SYNC_FLAG_ROUTE, f3) */
+  uint64_t n_delta16e;     /* records coded DELTA16E (SYNC_FLAG_ESCAPE, f4) */
 } sync_stats;
 
 /* Record view produced by sync_bucket_unpack (device memory, 32 B). */

@@ -38,6 +38,7 @@ SYNC_CODEC_RAW = 0
 SYNC_CODEC_COMPRESSED = 1
 SYNC_FLAG_CRC = 1
 SYNC_FLAG_ROUTE = 2
+SYNC_FLAG_ESCAPE = 4
 SYNC_DTYPE_BF16 = 1
 SYNC_DTYPE_FP16 = 2
 SYNC_CHUNK = 16384
@@ -76,7 +77,7 @@ class _Config(ctypes.Structure):
 class _Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in ["nnz", "n_records", "n_delta16", "n_abs32", "n_chunks",
                                                 "n_chunks_rans", "enc_bytes", "index_bytes", "value_bytes",
-                                                "n_full"]]
+                                                "n_full", "n_delta16e"]]
 
 
 RECORD_VIEW_BYTES = 32
@@ -239,7 +240,7 @@ class SyncContext:
 
     def __init__(self, numel, bucket_limit: int = 256 << 20, max_changed: int | None = None,
                  codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, device=None, route: bool = False,
-                 dtype: int = SYNC_DTYPE_BF16):
+                 dtype: int = SYNC_DTYPE_BF16, escape: bool = False):
         self.numel = [int(n) for n in numel]
         self.device = torch.device(device or "cuda")
         self.T = len(self.numel)
@@ -247,7 +248,8 @@ class SyncContext:
         self._numel_arr = (ctypes.c_uint64 * max(self.T, 1))(*self.numel)
         self._m = _Manifest(self.T, self._numel_arr)
         self._c = _Config(int(bucket_limit), self.max_changed, int(codec),
-                          (SYNC_FLAG_CRC if crc else 0) | (SYNC_FLAG_ROUTE if route else 0), int(dtype))
+                          (SYNC_FLAG_CRC if crc else 0) | (SYNC_FLAG_ROUTE if route else 0) |
+                          (SYNC_FLAG_ESCAPE if escape else 0), int(dtype))
         self.codec, self.crc, self.bucket_limit, self.route = codec, crc, bucket_limit, route
         need = ctypes.c_size_t()
         _ck(lib().sync_workspace_size(ctypes.byref(self._m), ctypes.byref(self._c), ctypes.byref(need)),

@@ -26,7 +26,7 @@ constexpr u64 kAlign = 256;
 struct Layout {
   u64 numel, tile_prefix, tile_tensor, misc, tile_state, stage_ring, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
   u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, rec_dst, totals, recs, bks, views, nviews, crc;
-  u64 bm_off, group_sum, total;
+  u64 bm_off, group_sum, chunk_esc, chunk_escoff, total;
 };
 
 u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4 + 32; }  // + 32 bad flags
@@ -65,6 +65,8 @@ Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_change
   L.crc = take(4ull * crc_n);
   L.bm_off = take(8ull * (T + 1));                       // f1: bitmap word offset per tensor
   L.group_sum = take(8ull * (n_tiles / 1024 + 2));       // f1: tile-offset scan groups
+  L.chunk_esc = take(4ull * max_chunks);                   // f4: escapes per chunk
+  L.chunk_escoff = take(8ull * (max_chunks + 1));          // f4: their exclusive prefix
   L.total = o;
   return L;
 }
@@ -228,6 +230,9 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   p.codec = c->codec;
   p.route = (c->flags & SYNC_FLAG_ROUTE) ? 1 : 0;
   p.dtype = c->dtype ? c->dtype : SYNC_DTYPE_BF16;
+  p.escape = (c->flags & SYNC_FLAG_ESCAPE) ? 1 : 0;
+  p.chunk_esc = reinterpret_cast<u32*>(w + L.chunk_esc);
+  p.chunk_escoff = reinterpret_cast<u64*>(w + L.chunk_escoff);
   p.cur = nullptr;
   p.max_chunks = d.max_chunks;
   p.numel = reinterpret_cast<const u64*>(w + L.numel);
@@ -691,6 +696,7 @@ int sync_ctx_stats(sync_ctx* x, sync_stats* out, sync_stream_t stream) {
   out->index_bytes = t[kTotIndexBytes];
   out->value_bytes = t[kTotValueBytes];
   out->n_full = t[kTotFull];
+  out->n_delta16e = t[kTotDelta16E];
   return SYNC_OK;
 }
 

@@ -56,11 +56,19 @@ __device__ __forceinline__ bool read_record(const u8* bk, const BucketHdr& h, u3
   r->dtype = (w[3] >> 8) & 0xFFu;
   r->codec = (w[3] >> 16) & 0xFFu;
   if (r->rb < 16 || (r->rb & 15u) || (u64)ro + r->rb > h.bytes) return false;
-  if (r->tid >= n_tensors || r->dtype != dtype || r->mode > 2 || r->codec > 1 || r->nnz == 0) return false;
+  if (r->tid >= n_tensors || r->dtype != dtype || r->mode > 3 || r->codec > 1 || r->nnz == 0) return false;
+  if (r->mode == kModeDelta16E && r->codec != SYNC_CODEC_COMPRESSED) return false;
   if ((u64)r->nnz > numel[r->tid]) return false;
   if (r->mode == kModeFull) return (u64)r->nnz == numel[r->tid] && 16 + 2ull * r->nnz <= r->rb;
   if (r->codec == SYNC_CODEC_RAW) return r->mode == 1 && 16 + 6ull * r->nnz <= r->rb;
   const u64 nch = (r->nnz + kChunk - 1) / kChunk;
+  if (r->mode == kModeDelta16E) {   // f4: word-offset table + total words after the header
+    const u64 s0 = 16 + 4 * (nch + 1);
+    if (s0 > r->rb) return false;
+    const u64 total = reinterpret_cast<const u32*>(bk + ro + 16)[nch];
+    if (total < r->nnz || total > 2ull * r->nnz) return false;
+    return s0 + pad_to(2 * total, 4) + pad_to(r->nnz, 4) + 16 * nch <= r->rb;
+  }
   const u64 ib = (r->mode ? 4ull : 2ull) * r->nnz;
   return 16 + pad_to(ib, 4) + pad_to(r->nnz, 4) + 16 * nch <= r->rb;
 }
@@ -258,8 +266,11 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
       continue;
     }
 
-    const u64 ib = (r.mode ? 4ull : 2ull) * nnz;
-    const u64 lo_off = 16 + pad_to(ib, 4);
+    const bool esc = r.mode == kModeDelta16E;
+    const u32* tbl = reinterpret_cast<const u32*>(rec + 16);
+    const u64 s0 = esc ? 16 + 4 * (nch + 1) : 16;
+    const u64 ib = esc ? 2ull * tbl[nch] : (r.mode ? 4ull : 2ull) * nnz;
+    const u64 lo_off = s0 + pad_to(ib, 4);
     const u64 dir_off = lo_off + pad_to(nnz, 4);
     const u32* de = reinterpret_cast<const u32*>(rec + dir_off + 16 * k);
     const u32 hi_off = de[0], hb = de[1], cm = de[2], base = de[3];
@@ -269,6 +280,11 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
     const u16* D = reinterpret_cast<const u16*>(rec + 16) + p0;
     const u32* A = reinterpret_cast<const u32*>(rec + 16) + p0;
 
+    // f4 DELTA16E: this chunk's words [tbl[k], tbl[k+1]) of the escape-coded stream
+    const u16* Ws = reinterpret_cast<const u16*>(rec + s0);
+    u32 wptr = esc ? tbl[k] : 0u;
+    const u32 wend = esc ? tbl[k + 1] : 0u;   // tbl[nch] = total words
+    bool esc_bad = esc && (wptr > wend || (u64)wend > (ib >> 1));
     u32 x = kLow, nwords = 0;
     const u16* words = nullptr;
     if (!corrupt && cm == 1) {
@@ -346,7 +362,7 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
 
     const u32 G = (nk + 31) / 32;
     u32 ptr = 0;
-    u32 carry = (r.mode == 0) ? base : 0u;
+    u32 carry = (r.mode == 0 || esc) ? base : 0u;
     bool range_bad = false, word_bad = false;
     // software pipeline: the lo bytes and the index words (DELTA16 delta or
     // ABS32 index) of the next 8 steps are loaded while the current 8 decode
@@ -358,7 +374,7 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
         const u32 qq = (g0 + i) * 32 + lane;
         const bool act = qq < nk;
         lb_[i] = act ? (u32)lo[qq] : 0u;
-        dd_[i] = act ? (r.mode == 0 ? (u32)D[qq] : A[qq]) : 0u;
+        dd_[i] = (act && !esc) ? (r.mode == 0 ? (u32)D[qq] : A[qq]) : 0u;
       }
     };
     load_block(0, nlb, ndd);
@@ -401,6 +417,45 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
         if (r.mode == 0) {
           idx = carry + warp_incl_scan(dd[i]);
           carry = __shfl_sync(0xffffffffu, idx, 31);
+        } else if (esc) {
+          // parse the 32 elements of this step: lane l reads word wptr + l, shifted by one word for every
+          // escape (two-word element) among the lanes before it; one ballot per escape in the step
+          u32 pos = wptr + lane, dv = 0;
+          bool done = !act;
+          while (true) {
+            const bool in = !done && pos < wend;
+            if (!done && !in) {
+              esc_bad = true;
+              done = true;
+            }
+            const u32 w = in ? (u32)Ws[pos] : 0u;
+            const u32 m = __ballot_sync(0xffffffffu, in && (w & 0x8000u));
+            if (m == 0) {
+              if (in) dv = w;
+              break;
+            }
+            const u32 e = __ffs(m) - 1;
+            if (in && lane < e) {
+              dv = w;
+              done = true;
+            } else if (lane == e) {
+              if (pos + 1 < wend) dv = ((w & 0x7FFFu) << 16) | Ws[pos + 1];
+              else esc_bad = true;
+              done = true;
+            } else if (in) {
+              pos += 1;
+            }
+          }
+          const u32 end = act ? pos + (dv > 32767u ? 2u : 1u) : 0u;
+          u32 mx = end;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const u32 y = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = y > mx ? y : mx;
+          }
+          wptr = mx > wptr ? mx : wptr;
+          idx = carry + warp_incl_scan(dv);
+          carry = __shfl_sync(0xffffffffu, idx, 31);
         } else {
           idx = dd[i];
         }
@@ -421,6 +476,7 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
       bool endbad = word_bad || x != kLow || ptr != nwords;
       if (__any_sync(0xffffffffu, endbad) && lane == 0) latch(status, SYNC_ERR_CORRUPT);
     }
+    if (esc && __any_sync(0xffffffffu, esc_bad || wptr != wend) && lane == 0) latch(status, SYNC_ERR_CORRUPT);
     if (__any_sync(0xffffffffu, range_bad) && lane == 0) latch(status, SYNC_ERR_INDEX_RANGE);
   }
 }

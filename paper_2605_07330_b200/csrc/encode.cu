@@ -82,11 +82,72 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
 
     // ---- index stream + lo plane slices: groups of 4 positions per thread, kG groups in flight
     //      (DELTA16: one 64-bit store of 4 deltas; ABS32: one 128-bit store; lo: one 32-bit store)
-    const u64 ib = (mode ? 4 : 2) * nnz;
-    const u64 lo_off = 16 + pad_to(ib, 4);
+    const bool esc = mode == kModeDelta16E;
+    const u64 ch0 = p.chunk_off[t];
+    const u64 ne_rec = esc ? p.chunk_escoff[ch0 + n_ch] - p.chunk_escoff[ch0] : 0;
+    const u64 s0 = esc ? 16 + 4 * (n_ch + 1) : 16;          // f4: word-offset table after the header
+    const u64 ib = esc ? 2 * (nnz + ne_rec) : (mode ? 4 : 2) * nnz;
+    const u64 lo_off = s0 + pad_to(ib, 4);
     const u64 dir_off = lo_off + pad_to(nnz, 4);
     const u64 hi_base = dir_off + 16 * n_ch;
-    {
+    if (esc) {
+      // f4 DELTA16E: rounds of 4 positions per thread; a block scan of the word counts (1, or
+      // 2 for an escape) places every thread's words after the chunk's first word w0
+      __shared__ u32 s_ws[kCThreads / 32 + 1];
+      const u64 w0 = (u64)p0 + (p.chunk_escoff[g] - p.chunk_escoff[ch0]);
+      u32* tbl = reinterpret_cast<u32*>(rec + 16);
+      if (tid == 0) {
+        tbl[k] = (u32)w0;
+        if (last) tbl[n_ch] = (u32)(nnz + ne_rec);
+      }
+      u16* Ws = reinterpret_cast<u16*>(rec + s0);
+      u8* L = rec + lo_off + p0;
+      u64 wrun = w0;
+      for (u32 r0 = 0; r0 < nk; r0 += 4 * kCThreads) {
+        const u32 q = r0 + 4 * tid;
+        u32 d[4];
+        u32 cnt = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const u64 pp = p0 + q + j;
+          d[j] = 0;
+          if (q + j < nk) {
+            d[j] = Ir[pp] - (pp ? Ir[pp - 1] : 0u);
+            cnt += d[j] > 32767u ? 2u : 1u;
+            L[q + j] = (u8)(Vc[q + j] & 0xFFu);
+          }
+        }
+        // exclusive block scan of cnt (kCThreads threads)
+        const u32 lane = tid & 31, wp = tid >> 5;
+        const u32 inc = warp_incl_scan(cnt);
+        if (lane == 31) s_ws[wp] = inc;
+        __syncthreads();
+        if (tid == 0) {
+          u32 acc = 0;
+          for (u32 i = 0; i < kCThreads / 32; ++i) {
+            const u32 v = s_ws[i];
+            s_ws[i] = acc;
+            acc += v;
+          }
+          s_ws[kCThreads / 32] = acc;
+        }
+        __syncthreads();
+        u64 w = wrun + s_ws[wp] + inc - cnt;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (q + j < nk) {
+            if (d[j] <= 32767u) {
+              Ws[w++] = (u16)d[j];
+            } else {
+              Ws[w++] = (u16)(0x8000u | (d[j] >> 16));
+              Ws[w++] = (u16)(d[j] & 0xFFFFu);
+            }
+          }
+        }
+        wrun += s_ws[kCThreads / 32];
+        __syncthreads();
+      }
+    } else {
       constexpr int kG = 4;
       u8* L = rec + lo_off + p0;
       for (u32 q0 = 4 * tid; q0 < nk; q0 += 4 * kCThreads * kG) {
@@ -131,7 +192,7 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
       }
     }
     if (last) {
-      zero_bytes(rec + 16 + ib, pad_to(ib, 4) - ib);
+      zero_bytes(rec + s0 + ib, pad_to(ib, 4) - ib);
       zero_bytes(rec + lo_off + nnz, pad_to(nnz, 4) - nnz);
     }
     // ---- directory entry + hi block
@@ -143,7 +204,7 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
       d[0] = (u32)hi_off;
       d[1] = hb;
       d[2] = cm;
-      d[3] = (mode == 0 && k > 0) ? Ir[p0 - 1] : 0u;
+      d[3] = ((mode == 0 || mode == kModeDelta16E) && k > 0) ? Ir[p0 - 1] : 0u;
     }
     u8* blk = rec + hi_off;
     if (last) {

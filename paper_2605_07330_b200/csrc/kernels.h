@@ -34,14 +34,19 @@ struct Plan {
   int prof;                      // debug instrumentation switch
   int route;                     // f3: SYNC_FLAG_ROUTE
   uint32_t dtype;                // record dtype tag (SYNC_DTYPE_*)
+  int escape;                    // f4: SYNC_FLAG_ESCAPE
+  uint32_t* chunk_esc;           // [max_chunks] index gaps > 32767 in the chunk (f4)
+  uint64_t* chunk_escoff;        // [max_chunks+1] exclusive prefix of chunk_esc
   const uint16_t* const* cur;    // f3: current weights (FULL records), device pointer table
 };
 
 enum TotalsIdx {
   kTotNnz = 0, kTotChunks = 1, kTotRecords = 2, kTotEnc = 3, kTotDelta16 = 4, kTotAbs32 = 5,
-  kTotRansChunks = 6, kTotOverflow = 7, kTotIndexBytes = 8, kTotValueBytes = 9, kTotFull = 10
+  kTotRansChunks = 6, kTotOverflow = 7, kTotIndexBytes = 8, kTotValueBytes = 9, kTotFull = 10,
+  kTotDelta16E = 11
 };
-constexpr uint32_t kModeFull = 2;  // record idx_mode of a FULL record (f3)
+constexpr uint32_t kModeFull = 2;     // record idx_mode of a FULL record (f3)
+constexpr uint32_t kModeDelta16E = 3;  // record idx_mode of an escape-coded DELTA16 record (f4)
 
 void launch_extract_batched(const uint16_t* const* d_old, const uint16_t* const* d_new, const uint64_t* tile_prefix,
                             const uint32_t* tile_tensor, const uint64_t* numel, uint32_t n_tensors, uint64_t n_tiles, uint32_t* I, uint16_t* V,

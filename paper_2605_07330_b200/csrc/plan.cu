@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
     //      block is consumed, and the element before each 32-group comes from the previous group
     for (u32 sym = lane; sym < 256; sym += 32) m.hist[sym] = 0;
     __syncwarp();
-    u32 gmax = 0;
+    u32 gmax = 0, nesc = 0;
     u32 carry = (lane == 0 && p0) ? Ic[-1] : 0u;   // I of the element before the chunk (Δ_0 = I_0 if none)
     carry = __shfl_sync(0xffffffffu, carry, 0);
     u32 hv[kWPF], cur[kWPF], hn[kWPF], cn[kWPF];
@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
         carry = __shfl_sync(0xffffffffu, cur[u], 31);
         const u32 d = q < nk ? cur[u] - prev : 0u;
         gmax = d > gmax ? d : gmax;
+        nesc += d > 32767u ? 1u : 0u;
       }
     }
 #pragma unroll
@@ -156,6 +157,9 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
       gmax = x > gmax ? x : gmax;
     }
     if (lane == 0 && gmax) atomicMax(&p.maxgap[t], gmax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nesc += __shfl_xor_sync(0xffffffffu, nesc, o);
+    if (lane == 0) p.chunk_esc[g] = nesc;   // f4: gaps that need an escape word
     __syncwarp();
     const long long t2 = clock64();
     if (!comp) continue;
@@ -267,36 +271,47 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
   const bool over = p.totals[kTotOverflow] != 0;
   constexpr u64 kRound = (u64)kScanThreads * kPer;
   // 1. exclusive prefix of padded hi block sizes over all chunks (+ RANS chunk count)
-  u64 carry = 0, rans_local = 0;
+  u64 carry = 0, rans_local = 0, ecarry = 0;
   if (comp) {
     for (u64 b = 0; b < n_chunks; b += kRound) {
       const u64 g0 = b + (u64)threadIdx.x * kPer;
-      u64 v[kPer];
-      u64 sum = 0;
+      u64 v[kPer], es[kPer];
+      u64 sum = 0, esum = 0;
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
         const u64 g = g0 + k;
         v[k] = g < n_chunks ? pad_to(p.chunk_hi[g], 4) : 0;
+        es[k] = (p.escape && g < n_chunks) ? p.chunk_esc[g] : 0;
         rans_local += g < n_chunks ? p.chunk_mode[g] : 0;
         sum += v[k];
+        esum += es[k];
       }
-      u64 e;
+      u64 e, ee;
       const u64 tot = block_excl_scan64(sum, &e, s_w);
-      u64 run = carry + e;
+      const u64 etot = block_excl_scan64(esum, &ee, s_w2);
+      u64 run = carry + e, erun = ecarry + ee;
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
         const u64 g = g0 + k;
-        if (g < n_chunks) p.chunk_hioff[g] = run;
+        if (g < n_chunks) {
+          p.chunk_hioff[g] = run;
+          p.chunk_escoff[g] = erun;
+        }
         run += v[k];
+        erun += es[k];
       }
       carry += tot;
+      ecarry += etot;
     }
-    if (threadIdx.x == 0) p.chunk_hioff[n_chunks] = carry;
+    if (threadIdx.x == 0) {
+      p.chunk_hioff[n_chunks] = carry;
+      p.chunk_escoff[n_chunks] = ecarry;
+    }
     __syncthreads();
   }
   const u64 rans = block_sum64(rans_local, s_w2);
   // 2. record sizes and offsets
-  u64 carry_enc = 0, n16 = 0, n32 = 0, ib_tot = 0, vb_tot = 0, nfull = 0;
+  u64 carry_enc = 0, n16 = 0, n32 = 0, ib_tot = 0, vb_tot = 0, nfull = 0, n16e = 0;
   for (u32 b = 0; b < T; b += (u32)kRound) {
     const u32 t0 = b + threadIdx.x * kPer;
     u64 bytes[kPer];
@@ -309,11 +324,20 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
       u32 mode = 1;
       if (c) {
         if (comp) {
-          mode = p.maxgap[t] <= 32767u ? 0u : 1u;
-          ib = pad_to((mode ? 4 : 2) * c, 4);
           const u64 ch0 = p.chunk_off[t], ch1 = p.chunk_off[t + 1];
+          mode = p.maxgap[t] <= 32767u ? 0u : 1u;
+          u64 table = 0;
+          if (mode && p.escape) {   // f4: escapes < nnz -> DELTA16E beats ABS32
+            const u64 ne = p.chunk_escoff[ch1] - p.chunk_escoff[ch0];
+            if (ne < c) {
+              mode = kModeDelta16E;
+              table = 4 * (ch1 - ch0 + 1);
+              ib = pad_to(2 * (c + ne), 4);
+            }
+          }
+          if (mode != kModeDelta16E) ib = pad_to((mode ? 4 : 2) * c, 4);
           const u64 hi = p.chunk_hioff[ch1] - p.chunk_hioff[ch0];
-          by = pad_to(16 + ib + pad_to(c, 4) + 16 * (ch1 - ch0) + hi, 16);
+          by = pad_to(16 + table + ib + pad_to(c, 4) + 16 * (ch1 - ch0) + hi, 16);
         } else {
           ib = 4 * c;
           by = pad_to(16 + 6 * c, 16);
@@ -324,6 +348,8 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
           by = full;
           ib = 0;
           nfull++;
+        } else if (mode == kModeDelta16E) {
+          n16e++;
         } else if (mode) {
           n32++;
         } else {
@@ -355,6 +381,7 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
   ib_tot = block_sum64(ib_tot, s_w);
   vb_tot = block_sum64(vb_tot, s_w2);
   nfull = block_sum64(nfull, s_w);
+  n16e = block_sum64(n16e, s_w2);
   if (threadIdx.x == 0) {
     p.enc_off[T] = carry_enc;
     if (carry_enc > p.enc_cap) {
@@ -369,6 +396,7 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
     p.totals[kTotIndexBytes] = ib_tot;
     p.totals[kTotValueBytes] = vb_tot;
     p.totals[kTotFull] = nfull;
+    p.totals[kTotDelta16E] = n16e;
   }
 }
 

@@ -24,9 +24,10 @@ class SparseSyncSender:
 
     def __init__(self, snapshot, current, bucket_limit: int = 256 << 20, max_changed: int | None = None,
                  codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, expected_density: float = 0.02,
-                 route: bool = False, dtype: int = 1):
+                 route: bool = False, dtype: int = 1, escape: bool = False):
         """route: per-parameter routing (f3): a record whose FULL copy is smaller goes FULL.
-        dtype: SYNC_DTYPE_BF16 / SYNC_DTYPE_FP16 (f2): the record tag; the work is the same."""
+        dtype: SYNC_DTYPE_BF16 / SYNC_DTYPE_FP16 (f2): the record tag; the work is the same.
+        escape: escape-coded DELTA16 (f4) for records with index gaps > 32767."""
         self.snapshot = _flat_bits(snapshot)
         self.current = _flat_bits(current)
         assert len(self.snapshot) == len(self.current)
@@ -37,7 +38,7 @@ class SparseSyncSender:
         self.numel = [t.numel() for t in self.current]
         total = sum(self.numel)
         cap = int(max_changed if max_changed is not None else min(total, int(total * expected_density) + 65536))
-        self._cfg = dict(bucket_limit=bucket_limit, codec=codec, crc=crc, route=route, dtype=dtype)
+        self._cfg = dict(bucket_limit=bucket_limit, codec=codec, crc=crc, route=route, dtype=dtype, escape=escape)
         self.old_ptrs = ptr_table(self.snapshot, self.device)
         self.new_ptrs = ptr_table(self.current, self.device)
         self.counts = torch.zeros(max(len(self.numel), 1), dtype=torch.int64, device=self.device)

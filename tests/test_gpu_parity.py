@@ -238,6 +238,64 @@ def test_fp16_bit_exact_and_tag_checked(codec):
     assert all((host16(b) == o).all() for b, o in zip(B, olds))
 
 
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("crc", [False, True])
+def test_escape_delta16_bit_exact(fused, crc):
+    """f4: on the clustered-row mask, records with gaps > 32767 are coded DELTA16E — GPU buckets
+    == the oracle's, the replica applies them, the EMIT path returns the oracle's (I, V), and a damaged
+    word-offset table is detected."""
+    m = synth.Manifest("r", [synth.Tensor(f"w{k}", (300, 2048)) for k in range(3)] +
+                       [synth.Tensor("n", (2048,), synth.KIND_NORM), synth.Tensor("big", (64, 40000))])
+    olds, news = synth.generate(m, seed=41, rho=0.02, mask=synth.MASK_R)
+    ref = oracle.sync_pack(olds, news, limit=96 << 10, crc=crc, escape=True)
+    assert ref.stats["delta16e"] >= 3
+    old_d = [to_dev(o) for o in olds]
+    new_d = [to_dev(n) for n in news]
+    rol_d = [to_dev(o) for o in olds]
+    snd = ss.SparseSyncSender(old_d, new_d, bucket_limit=96 << 10, crc=crc, escape=True,
+                              max_changed=sum(o.size for o in olds))
+    rcv = ss.SparseSyncReceiver(rol_d, bucket_limit=96 << 10, crc=crc)
+    bl = snd.sync(fused=fused)
+    got = [snd.bucket(b).cpu().numpy().tobytes() for b in range(len(bl))]
+    assert got == [ref.bucket(b) for b in range(ref.n_buckets)]
+    assert snd.stats()["n_delta16e"] == ref.stats["delta16e"]
+    rcv.apply_many([snd.bucket(b) for b in range(len(bl))])
+    snd.commit()
+    torch.cuda.synchronize()
+    snd.check()
+    rcv.check()
+    for r, o, n in zip(rol_d, old_d, news):
+        assert (host16(r) == n).all() and (host16(o) == n).all()
+    for b in range(ref.n_buckets):
+        st, recs = oracle.bucket_decode(ref.bucket(b), cap=sum(o.size for o in olds))
+        n_out = sum(r[1].size for r in recs)
+        I = torch.empty(max(n_out, 1), dtype=torch.int32, device=DEV)
+        V = torch.empty(max(n_out, 1), dtype=torch.int16, device=DEV)
+        bk = torch.from_numpy(np.frombuffer(ref.bucket(b), np.uint8).copy()).to(DEV)
+        rcv.ctx.sync_decompress(bk, bk.numel(), I, V)
+        torch.cuda.synchronize()
+        rcv.check()
+        assert (I[:n_out].cpu().numpy().view(np.uint32) == np.concatenate([r[1] for r in recs])).all()
+        assert (V[:n_out].cpu().numpy().view(np.uint16) == np.concatenate([r[2] for r in recs])).all()
+    if not crc:   # damage the first DELTA16E record's chunk-1 word offset
+        for b in range(ref.n_buckets):
+            a = np.frombuffer(ref.bucket(b), np.uint8).copy()
+            nrec = int(a[12:16].view(np.uint32)[0])
+            ros = [int(x) for x in a[32:32 + 8 * nrec].view(np.uint32)[0::2]]
+            hit = [ro for ro in ros if a[ro + 12] == 3 and int(a[ro + 4:ro + 8].view(np.uint32)[0]) > 16384]
+            if hit:
+                ro = hit[0]
+                a[ro + 20] ^= 1
+                W = [to_dev(o) for o in olds]
+                bad = ss.SparseSyncReceiver(W, bucket_limit=96 << 10)
+                bad.apply(torch.from_numpy(a).to(DEV))
+                torch.cuda.synchronize()
+                assert bad.ctx.sync_status() == ss.SYNC_ERR_CORRUPT
+                break
+        else:
+            pytest.fail("no multi-chunk DELTA16E record to damage")
+
+
 def test_delta16_abs32_boundary():
     # gap of exactly 32767 stays DELTA16, 32768 forces ABS32 (P:360, DESIGN C4)
     n = 70_000
