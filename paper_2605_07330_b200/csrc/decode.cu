@@ -152,10 +152,12 @@ __global__ void __launch_bounds__(1024) k_unpack(const u8* bk, u64 bytes, u32 n_
 }
 
 // ---------------------------------------------------------------------------- decode
+constexpr int kEscWin = 320;   // f4: index words staged per 8-step block (256 elements + 64 escapes; more: global)
 struct DecodeModel {
   u8 slot2sym[kM];
   u16 freq[256];
   u16 cum[256];
+  u16 win[kEscWin];            // f4: the block's escape-coded index words
 };
 
 // One launch decodes up to kDecodeBatch buckets (the chunks of all of them form one grid-stride range), so
@@ -388,6 +390,18 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
       if (g0 + kPF < G) load_block(g0 + kPF, nlb, ndd);
       if (cm == 1 && lane < 8 && ptr + 64 * (lane + 1) < nwords)  // warm L1 with the next words
         asm volatile("prefetch.global.L1 [%0];" ::"l"(words + ptr + 64 * (lane + 1)));
+      // f4: stage this block's index words (from wptr) in shared memory, one coalesced pass, so the
+      // per-step parse below reads shared memory instead of waiting on a global load every step
+      const u32 wbase = wptr;
+      if (esc) {
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kEscWin / 32; ++j) {
+          const u32 o = (u32)j * 32 + lane;
+          dm.win[o] = (wbase + o < wend) ? Ws[wbase + o] : (u16)0;
+        }
+        __syncwarp();
+      }
 #pragma unroll
       for (int i = 0; i < kPF; ++i) {
         const u32 gs = g0 + i;
@@ -428,7 +442,7 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
               esc_bad = true;
               done = true;
             }
-            const u32 w = in ? (u32)Ws[pos] : 0u;
+            const u32 w = in ? (u32)(pos - wbase < (u32)kEscWin ? dm.win[pos - wbase] : Ws[pos]) : 0u;
             const u32 m = __ballot_sync(0xffffffffu, in && (w & 0x8000u));
             if (m == 0) {
               if (in) dv = w;
@@ -439,7 +453,8 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
               dv = w;
               done = true;
             } else if (lane == e) {
-              if (pos + 1 < wend) dv = ((w & 0x7FFFu) << 16) | Ws[pos + 1];
+              if (pos + 1 < wend)
+                dv = ((w & 0x7FFFu) << 16) | (pos + 1 - wbase < (u32)kEscWin ? dm.win[pos + 1 - wbase] : Ws[pos + 1]);
               else esc_bad = true;
               done = true;
             } else if (in) {

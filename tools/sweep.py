@@ -59,6 +59,8 @@ SETS = {
     ],
     "n2": [
         ("ring2_r01", 2, ["--topology", "ring"]),
+        ("ring2_r001", 2, ["--topology", "ring", "--rho", "0.001"]),
+        ("fanout2_r01", 2, ["--topology", "fanout"]),
         ("pair2_4b_r01", 2, ["--topology", "pair", "--workload", "qwen3-4b"]),
         ("pair2_r01", 2, ["--topology", "pair"]),
         ("pair2_r10", 2, ["--topology", "pair", "--rho", "0.1"]),
