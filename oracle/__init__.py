@@ -30,7 +30,7 @@ ERR_TRUNCATED = -11
 ERR_CRC = -12
 
 DELTA16, ABS32 = 0, 1
-DTYPE_BF16, DTYPE_FP16 = 1, 2
+DTYPE_BF16, DTYPE_FP16, DTYPE_FP8 = 1, 2, 3
 DELTA16E = 3
 CODEC_RAW, CODEC_COMPRESSED = 0, 1
 CHUNK = 16384
@@ -56,6 +56,9 @@ def lib():
         sig = {
             "or_extract": (u64, [P, P, u64, P, P]),
             "or_full_record_bytes": (u64, [u64]),
+            "or_full_record_bytes_dt": (u64, [u64, i32]),
+            "or_extract8": (u64, [P, P, u64, P, P]),
+            "or_apply8": (i32, [P, u64, P, P, u64]),
             "or_encode_full_record": (u64, [u32, P, u64, i32, P, i32]),
             "or_bf16_rne": (ctypes.c_uint16, [u32]),
             "or_bf16_rne_array": (None, [P, P, u64]),
@@ -96,6 +99,11 @@ def lib():
 
 def _p(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p) if a.size else None
+
+
+def _u8(a) -> np.ndarray:
+    a = np.asarray(a)
+    return np.ascontiguousarray(a.view(np.uint8) if a.dtype != np.uint8 else a)
 
 
 def _u16(a) -> np.ndarray:
@@ -139,6 +147,16 @@ def extract_tracked(W: np.ndarray, tracked: np.ndarray):
     I = np.empty(max(n, 1), np.uint32)
     V = np.empty(max(n, 1), np.uint16)
     c = lib().or_extract_tracked(_p(W), _p(tracked), n, _p(I), _p(V))
+    return I[:c].copy(), V[:c].copy()
+
+
+def extract8(old: np.ndarray, new: np.ndarray):
+    """FP8 (f2): Alg. 1 l.6 + Alg. 2 l.5 on 8-bit elements: (I, V as uint16 holding the byte)."""
+    old, new = _u8(old).ravel(), _u8(new).ravel()
+    n = old.size
+    I = np.empty(max(n, 1), np.uint32)
+    V = np.empty(max(n, 1), np.uint16)
+    c = lib().or_extract8(_p(old), _p(new), n, _p(I), _p(V))
     return I[:c].copy(), V[:c].copy()
 
 
@@ -197,9 +215,9 @@ def rans_decode(block: bytes, n: int):
 
 # ----------------------------------------------------------------------------- records
 def encode_full_record(tensor_id: int, W, codec: int = CODEC_COMPRESSED, dtype: int = 1) -> bytes:
-    """f3 FULL record: the whole tensor's current values."""
-    W = _u16(W).ravel()
-    out = np.zeros(int(lib().or_full_record_bytes(W.size)), np.uint8)
+    """f3 FULL record: the whole tensor's current values (uint8 for FP8)."""
+    W = (_u8(W) if dtype == DTYPE_FP8 else _u16(W)).ravel()
+    out = np.zeros(int(lib().or_full_record_bytes_dt(W.size, dtype)), np.uint8)
     n = lib().or_encode_full_record(tensor_id, _p(W), W.size, codec, _p(out), dtype)
     return out[:n].tobytes()
 
@@ -281,12 +299,13 @@ def sync_pack(olds, news, codec: int = CODEC_COMPRESSED, limit: int = 256 << 20,
     """Sender path (Alg. 2) over a manifest of (old, new) uint16 arrays.
     route: per-parameter routing (f3) — a record goes FULL when that is smaller (DESIGN C19).
     escape: escape-coded DELTA16 (f4) for records with gaps > 32767."""
-    olds = [_u16(o).ravel() for o in olds]
-    news = [_u16(n).ravel() for n in news]
+    conv = _u8 if dtype == DTYPE_FP8 else _u16   # FP8 (f2): 8-bit elements
+    olds = [conv(o).ravel() for o in olds]
+    news = [conv(n).ravel() for n in news]
     T = len(olds)
     numel = np.array([o.size for o in olds], np.uint64)
-    keep = [np.zeros(1, np.uint16) if o.size == 0 else o for o in olds] + \
-           [np.zeros(1, np.uint16) if n.size == 0 else n for n in news]
+    keep = [np.zeros(1, o.dtype) if o.size == 0 else o for o in olds] + \
+           [np.zeros(1, n.dtype) if n.size == 0 else n for n in news]
     op = (ctypes.c_void_p * max(T, 1))(*[k.ctypes.data for k in keep[:T]])
     np_ = (ctypes.c_void_p * max(T, 1))(*[k.ctypes.data for k in keep[T:]])
     L = lib()
@@ -306,13 +325,14 @@ def sync_pack(olds, news, codec: int = CODEC_COMPRESSED, limit: int = 256 << 20,
 
 
 def bucket_apply(bucket: bytes, weights) -> int:
-    """Receiver path (Alg. 3): decode + scatter into weights (list of uint16 arrays)."""
+    """Receiver path (Alg. 3): decode + scatter into weights (list of uint16 arrays; uint8 for
+    FP8-tagged records)."""
     buf = np.frombuffer(bucket, np.uint8).copy()
     T = len(weights)
     numel = np.array([w.size for w in weights], np.uint64)
     for w in weights:
-        assert w.dtype == np.uint16 and w.flags.c_contiguous
-    keep = [w if w.size else np.zeros(1, np.uint16) for w in weights]
+        assert w.dtype in (np.uint16, np.uint8) and w.flags.c_contiguous
+    keep = [w if w.size else np.zeros(1, w.dtype) for w in weights]
     wp = (ctypes.c_void_p * max(T, 1))(*[k.ctypes.data for k in keep])
     return lib().or_bucket_apply(_p(buf), len(bucket), T, _p(numel), ctypes.cast(wp, ctypes.c_void_p))
 

@@ -41,7 +41,11 @@ enum { OR_DELTA16 = 0, OR_ABS32 = 1 };
 enum { OR_CODEC_RAW = 0, OR_CODEC_COMPRESSED = 1 };
 enum { OR_CHUNK_RAW = 0, OR_CHUNK_RANS = 1 };
 /* record dtype byte (f2): the 16-bit element types share every encoding; only the tag differs */
-enum { OR_DTYPE_BF16 = 1, OR_DTYPE_FP16 = 2 };
+enum { OR_DTYPE_BF16 = 1, OR_DTYPE_FP16 = 2, OR_DTYPE_FP8 = 3 };
+/* FP8 E4M3 (f2): 8-bit elements. V arrays stay u16 with the byte in the low half;
+ * a record has one value plane (the byte itself, rANS-coded per chunk, no lo plane); RAW records carry
+ * u8 values; FULL records one byte per element. */
+static int is8(int dtype) { return dtype == OR_DTYPE_FP8; }
 
 static uint64_t pad_to(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
@@ -124,6 +128,28 @@ uint64_t or_extract_tracked(const uint16_t* W, uint8_t* tracked, uint64_t n, uin
     }
   }
   return count;
+}
+
+/* 8-bit elements (FP8, f2): the same definitions on bytes; V holds the byte in the low half. */
+uint64_t or_extract8(const uint8_t* old_bits, const uint8_t* new_bits, uint64_t n, uint32_t* I, uint16_t* V) {
+  uint64_t count = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (old_bits[i] != new_bits[i]) {
+      if (I) I[count] = (uint32_t)i;
+      if (V) V[count] = new_bits[i];
+      ++count;
+    }
+  }
+  return count;
+}
+
+int or_apply8(uint8_t* W, uint64_t numel, const uint32_t* I, const uint16_t* V, uint64_t count) {
+  int status = OR_OK;
+  for (uint64_t k = 0; k < count; ++k) {
+    if ((uint64_t)I[k] >= numel) { status = OR_ERR_INDEX_RANGE; continue; }
+    W[I[k]] = (uint8_t)V[k];
+  }
+  return status;
 }
 
 /* ---------------------------------------------------------------------------
@@ -403,8 +429,13 @@ uint64_t or_encode_record_ex(uint32_t tensor_id, const uint32_t* I, const uint16
   if (codec == OR_CODEC_RAW) {
     for (uint64_t k = 0; k < nnz; ++k) put32(rec + off + 4 * k, I[k]);
     off += 4 * nnz;
-    for (uint64_t k = 0; k < nnz; ++k) put16(rec + off + 2 * k, V[k]);
-    off += 2 * nnz;
+    if (is8(dtype)) {
+      for (uint64_t k = 0; k < nnz; ++k) rec[off + k] = (uint8_t)V[k];
+      off += nnz;
+    } else {
+      for (uint64_t k = 0; k < nnz; ++k) put16(rec + off + 2 * k, V[k]);
+      off += 2 * nnz;
+    }
     uint64_t total = pad_to(off, 16);
     memset(rec + off, 0, total - off);
     put32(rec + 0, tensor_id);
@@ -430,16 +461,18 @@ uint64_t or_encode_record_ex(uint32_t tensor_id, const uint32_t* I, const uint16
                                     : or_encode_indices(I, nnz, mode, rec + off);
   memset(rec + off + ib, 0, pad_to(ib, 4) - ib);
   off += pad_to(ib, 4);
-  for (uint64_t k = 0; k < nnz; ++k) rec[off + k] = (uint8_t)(V[k] & 0xFFu);
-  memset(rec + off + nnz, 0, pad_to(nnz, 4) - nnz);
-  off += pad_to(nnz, 4);
+  if (!is8(dtype)) {   /* lo plane (16-bit elements only) */
+    for (uint64_t k = 0; k < nnz; ++k) rec[off + k] = (uint8_t)(V[k] & 0xFFu);
+    memset(rec + off + nnz, 0, pad_to(nnz, 4) - nnz);
+    off += pad_to(nnz, 4);
+  }
   uint64_t dir = off;
   off += 16 * n_chunks;
   uint8_t* hi = (uint8_t*)malloc(OR_C);
   for (uint64_t k = 0; k < n_chunks; ++k) {
     uint64_t p0 = k * OR_C;
     uint32_t nk = (uint32_t)((nnz - p0) < OR_C ? (nnz - p0) : OR_C);
-    for (uint32_t p = 0; p < nk; ++p) hi[p] = (uint8_t)(V[p0 + p] >> 8);
+    for (uint32_t p = 0; p < nk; ++p) hi[p] = is8(dtype) ? (uint8_t)V[p0 + p] : (uint8_t)(V[p0 + p] >> 8);
     uint32_t hb = or_rans_encode(hi, nk, rec + off);
     uint32_t chunk_mode = OR_CHUNK_RANS;
     if (hb >= nk) {                       /* never-expand */
@@ -476,12 +509,18 @@ uint64_t or_encode_record_ex(uint32_t tensor_id, const uint32_t* I, const uint16
 enum { OR_FULL = 2 };
 
 uint64_t or_full_record_bytes(uint64_t numel) { return pad_to(16 + 2 * numel, 16); }
+uint64_t or_full_record_bytes_dt(uint64_t numel, int dtype) {
+  return pad_to(16 + (is8(dtype) ? 1 : 2) * numel, 16);
+}
 
-uint64_t or_encode_full_record(uint32_t tensor_id, const uint16_t* W, uint64_t numel, int codec, uint8_t* out,
+/* W: the tensor's current elements (u16, or u8 for FP8). */
+uint64_t or_encode_full_record(uint32_t tensor_id, const void* Wv, uint64_t numel, int codec, uint8_t* out,
                                int dtype) {
-  uint64_t total = or_full_record_bytes(numel);
-  for (uint64_t i = 0; i < numel; ++i) put16(out + 16 + 2 * i, W[i]);
-  memset(out + 16 + 2 * numel, 0, total - 16 - 2 * numel);
+  uint64_t total = or_full_record_bytes_dt(numel, dtype);
+  uint64_t eb = is8(dtype) ? 1 : 2;
+  if (is8(dtype)) memcpy(out + 16, Wv, numel);
+  else for (uint64_t i = 0; i < numel; ++i) put16(out + 16 + 2 * i, ((const uint16_t*)Wv)[i]);
+  memset(out + 16 + eb * numel, 0, total - 16 - eb * numel);
   put32(out + 0, tensor_id);
   put32(out + 4, (uint32_t)numel);
   put32(out + 8, (uint32_t)total);
@@ -497,23 +536,26 @@ int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, ui
   uint32_t tid = get32(rec), nnz = get32(rec + 4), rb = get32(rec + 8);
   uint8_t mode = rec[12], dtype = rec[13], codec = rec[14];
   if (rb > avail || rb < 16 || (rb % 16) != 0) return OR_ERR_TRUNCATED;
-  if ((dtype != OR_DTYPE_BF16 && dtype != OR_DTYPE_FP16) || mode > 3 || codec > 1 || nnz == 0)
+  if ((dtype != OR_DTYPE_BF16 && dtype != OR_DTYPE_FP16 && dtype != OR_DTYPE_FP8) || mode > 3 || codec > 1 ||
+      nnz == 0)
     return OR_ERR_CORRUPT;
+  const uint64_t eb = is8(dtype) ? 1 : 2;
   *tensor_id = tid;
   *nnz_out = nnz;
   if (nnz > cap) return OR_ERR_CAPACITY;
   if (mode == OR_FULL) {                /* every element, in order */
-    if (16 + 2ull * nnz > rb) return OR_ERR_CORRUPT;
+    if (16 + eb * nnz > rb) return OR_ERR_CORRUPT;
     for (uint64_t k = 0; k < nnz; ++k) {
       I[k] = (uint32_t)k;
-      V[k] = get16(rec + 16 + 2 * k);
+      V[k] = eb == 1 ? rec[16 + k] : get16(rec + 16 + 2 * k);
     }
     return OR_OK;
   }
   if (codec == OR_CODEC_RAW) {
-    if (mode != OR_ABS32 || 16 + 6ull * nnz > rb) return OR_ERR_CORRUPT;
+    if (mode != OR_ABS32 || 16 + (4 + eb) * nnz > rb) return OR_ERR_CORRUPT;
     for (uint64_t k = 0; k < nnz; ++k) I[k] = get32(rec + 16 + 4 * k);
-    for (uint64_t k = 0; k < nnz; ++k) V[k] = get16(rec + 16 + 4ull * nnz + 2 * k);
+    for (uint64_t k = 0; k < nnz; ++k)
+      V[k] = eb == 1 ? rec[16 + 4ull * nnz + k] : get16(rec + 16 + 4ull * nnz + 2 * k);
     return OR_OK;
   }
   uint64_t off = 16;
@@ -531,7 +573,8 @@ int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, ui
   } else {
     ib = (mode == OR_DELTA16 ? 2ull : 4ull) * nnz;
   }
-  if (off + pad_to(ib, 4) + pad_to(nnz, 4) + 16 * n_chunks > rb) return OR_ERR_CORRUPT;
+  const uint64_t lo_bytes = eb == 1 ? 0 : pad_to(nnz, 4);   /* no lo plane for 8-bit elements */
+  if (off + pad_to(ib, 4) + lo_bytes + 16 * n_chunks > rb) return OR_ERR_CORRUPT;
   if (mode != OR_DELTA16E) or_decode_indices(rec + off, nnz, mode, I);
   if (table) {   /* the chunk word offsets must match the stream */
     uint64_t w = 0;
@@ -544,7 +587,7 @@ int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, ui
   }
   off += pad_to(ib, 4);
   const uint8_t* lo = rec + off;
-  off += pad_to(nnz, 4);
+  off += lo_bytes;
   const uint8_t* dir = rec + off;
   uint8_t* hi = (uint8_t*)malloc(OR_C);
   int st = OR_OK;
@@ -564,7 +607,7 @@ int or_decode_record(const uint8_t* rec, uint64_t avail, uint32_t* tensor_id, ui
       st = OR_ERR_CORRUPT;
     }
     for (uint32_t p = 0; p < nk && st == OR_OK; ++p)
-      V[p0 + p] = (uint16_t)(((uint16_t)hi[p] << 8) | lo[p0 + p]);
+      V[p0 + p] = eb == 1 ? hi[p] : (uint16_t)(((uint16_t)hi[p] << 8) | lo[p0 + p]);
   }
   free(hi);
   return st;
@@ -614,8 +657,8 @@ uint32_t or_bucketize(const uint64_t* rec_bytes, uint64_t n_records, uint64_t li
  * [3] abs32 records, [4] payload bytes (Σ bucket bytes), [5] value-stream bytes,
  * [6] FULL records (flags bit 1 = routing, f3), [7] DELTA16E records (flags bit 2 = escapes, f4).
  * ------------------------------------------------------------------------- */
-int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const uint16_t* const* old_ptrs,
-                     const uint16_t* const* new_ptrs, int codec, uint64_t limit, uint32_t flags,
+int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const void* const* old_ptrs,
+                     const void* const* new_ptrs, int codec, uint64_t limit, uint32_t flags,
                      uint8_t* out, uint64_t out_cap, uint64_t* offsets, uint64_t* sizes,
                      uint32_t max_buckets, uint64_t* stats, int dtype) {
   uint64_t st[8] = {0};
@@ -631,10 +674,11 @@ int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const uint16_t* 
     uint64_t n = numel[t];
     uint32_t* I = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
     uint16_t* V = (uint16_t*)malloc(sizeof(uint16_t) * (n ? n : 1));
-    uint64_t nnz = or_extract(old_ptrs[t], new_ptrs[t], n, I, V);
+    uint64_t nnz = is8(dtype) ? or_extract8((const uint8_t*)old_ptrs[t], (const uint8_t*)new_ptrs[t], n, I, V)
+                              : or_extract((const uint16_t*)old_ptrs[t], (const uint16_t*)new_ptrs[t], n, I, V);
     if (nnz > 0) {
       uint64_t rb = or_encode_record_ex(t, I, V, nnz, codec, stream + pos, dtype, (flags & 4u) != 0);
-      int full = (flags & 2u) && or_full_record_bytes(n) < rb;   /* routing, DESIGN C19 */
+      int full = (flags & 2u) && or_full_record_bytes_dt(n, dtype) < rb;   /* routing, DESIGN C19 */
       if (full) rb = or_encode_full_record(t, new_ptrs[t], n, codec, stream + pos, dtype);
       rec_bytes[n_records] = rb;
       rec_pos[n_records] = pos;
@@ -660,7 +704,7 @@ int64_t or_sync_pack(uint32_t n_tensors, const uint64_t* numel, const uint16_t* 
         st[5] += rb - 16 - pad_to(ib, 4);
       } else {
         st[3] += 1;
-        st[5] += 2 * nnz;
+        st[5] += (is8(dtype) ? 1 : 2) * nnz;
       }
     }
     free(I);
@@ -717,8 +761,9 @@ done:
  * Receiver: Alg. 3 for one bucket — validate header (and CRC),
  * decode every record, scatter into weights[tensor_id]. Returns 0 or error.
  * ------------------------------------------------------------------------- */
+/* weights: per-tensor element arrays (u16; u8 for records tagged FP8). */
 int or_bucket_apply(const uint8_t* bk, uint64_t avail, uint32_t n_tensors, const uint64_t* numel,
-                    uint16_t* const* weights) {
+                    void* const* weights) {
   if (avail < 32) return OR_ERR_TRUNCATED;
   if (get32(bk) != 0x424C5253u) return OR_ERR_BAD_MAGIC;
   if (get16(bk + 4) != 1) return OR_ERR_VERSION;
@@ -739,7 +784,8 @@ int or_bucket_apply(const uint8_t* bk, uint64_t avail, uint32_t n_tensors, const
     int st = or_decode_record(bk + ro, bytes - ro, &tid, &nnz, I, V, nnz_hdr);
     if (st == OR_OK) {
       if (tid >= n_tensors) st = OR_ERR_CORRUPT;
-      else st = or_apply(weights[tid], numel[tid], I, V, nnz);
+      else if (bk[ro + 13] == OR_DTYPE_FP8) st = or_apply8((uint8_t*)weights[tid], numel[tid], I, V, nnz);
+      else st = or_apply((uint16_t*)weights[tid], numel[tid], I, V, nnz);
     }
     free(I);
     free(V);

@@ -62,9 +62,23 @@ def threshold(p: float) -> int:
 _TABLE = None
 
 
-DTYPE_BF16, DTYPE_FP16 = 1, 2
-ONE = {DTYPE_BF16: 0x3F80, DTYPE_FP16: 0x3C00}   # bit patterns of 1.0 (RMSNorm weights)
+DTYPE_BF16, DTYPE_FP16, DTYPE_FP8 = 1, 2, 3
+ONE = {DTYPE_BF16: 0x3F80, DTYPE_FP16: 0x3C00, DTYPE_FP8: 0x38}   # bit patterns of 1.0 (RMSNorm weights)
 _TABLE16 = None
+_TABLE8 = None
+
+
+def fp8_table() -> np.ndarray:
+    """65536 FP8 E4M3 bytes: torch's float8_e4m3fn cast (round to nearest even, saturating) of
+    SIGMA * Phi^-1((k + 0.5) / 65536) — the same quantiles as the 16-bit tables, at 8-bit precision."""
+    global _TABLE8
+    if _TABLE8 is None:
+        import torch
+        from scipy.special import ndtri
+        q = (np.arange(65536, dtype=np.float64) + 0.5) / 65536.0
+        f32 = torch.from_numpy((SIGMA * ndtri(q)).astype(np.float32))
+        _TABLE8 = f32.to(torch.float8_e4m3fn).view(torch.uint8).numpy().copy()
+    return _TABLE8
 
 
 def fp16_table() -> np.ndarray:
@@ -78,6 +92,8 @@ def fp16_table() -> np.ndarray:
 
 
 def table(dtype: int = DTYPE_BF16) -> np.ndarray:
+    if dtype == DTYPE_FP8:
+        return fp8_table()
     return fp16_table() if dtype == DTYPE_FP16 else bf16_table()
 
 
@@ -195,7 +211,7 @@ def shard(manifest: Manifest, rank: int, world: int) -> Manifest:
 # ----------------------------------------------------------------------------- generation
 def gen_old(t: Tensor, tid: int, seed: int, dtype: int = DTYPE_BF16) -> np.ndarray:
     if t.kind == KIND_NORM:
-        return np.full(t.numel, ONE[dtype], np.uint16)
+        return np.full(t.numel, ONE[dtype], np.uint8 if dtype == DTYPE_FP8 else np.uint16)
     i = np.arange(t.numel, dtype=np.uint64)
     return table(dtype)[(h(S_VAL, seed, tid, i) >> np.uint64(48)).astype(np.int64)]
 
@@ -221,8 +237,8 @@ def gen_mask(t: Tensor, tid: int, seed: int, rho: float, mask: int = MASK_U) -> 
 def gen_new(old: np.ndarray, t: Tensor, tid: int, seed: int, rho: float, mask: int = MASK_U) -> np.ndarray:
     m = gen_mask(t, tid, seed, rho, mask)
     i = np.arange(t.numel, dtype=np.uint64)
-    d = (np.uint64(1) + h(S_PERT, seed, tid, i) % np.uint64(3)).astype(np.uint16)
-    return np.where(m, old ^ d, old).astype(np.uint16)
+    d = (np.uint64(1) + h(S_PERT, seed, tid, i) % np.uint64(3)).astype(old.dtype)
+    return np.where(m, old ^ d, old).astype(old.dtype)
 
 
 def generate(manifest: Manifest, seed: int = 0, rho: float = 0.01, mask: int = MASK_U, tid0: int = 0,

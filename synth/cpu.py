@@ -8,7 +8,7 @@ import subprocess
 import numpy as np
 
 from . import (KIND_NORM, MASK_E, MASK_R, S_EXP, S_MASK, S_PERT, S_ROW, S_VAL, EXPERT_F, ROW_Q, Manifest, h, key,
-               threshold, bf16_table, table, ONE, DTYPE_BF16)
+               threshold, bf16_table, table, ONE, DTYPE_BF16, DTYPE_FP8)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gen_cpu.c")
@@ -32,6 +32,10 @@ def lib():
         L.synth_cpu_fill_new.argtypes = [P, P, u64, i32, i32, u64, u64, u64, u64, u64, u64]
         L.synth_cpu_fill_old.restype = None
         L.synth_cpu_fill_new.restype = None
+        L.synth_cpu_fill_old8.argtypes = [P, u64, i32, u64, P]
+        L.synth_cpu_fill_new8.argtypes = [P, P, u64, i32, i32, u64, u64, u64, u64, u64, u64]
+        L.synth_cpu_fill_old8.restype = None
+        L.synth_cpu_fill_new8.restype = None
         _lib = L
     return _lib
 
@@ -47,10 +51,11 @@ def generate(manifest: Manifest, seed: int = 0, rho: float = 0.01, mask: int = 0
     olds, news = [], []
     for k, t in enumerate(manifest.tensors):
         tid = tid0 + k
-        o = np.empty(t.numel, np.uint16)
-        n = np.empty(t.numel, np.uint16)
+        e8 = dtype == DTYPE_FP8
+        o = np.empty(t.numel, np.uint8 if e8 else np.uint16)
+        n = np.empty(t.numel, np.uint8 if e8 else np.uint16)
         if t.numel:
-            lib().synth_cpu_fill_old(_p(o), t.numel, ONE[dtype] if t.kind == KIND_NORM else 0,
+            (lib().synth_cpu_fill_old8 if e8 else lib().synth_cpu_fill_old)(_p(o), t.numel, ONE[dtype] if t.kind == KIND_NORM else 0,
                                      key(S_VAL, seed, tid), _p(tab))
             mode, active, thr = 0, 1, threshold(rho)
             key_row, thr_row, cols = 0, 0, 1
@@ -61,7 +66,8 @@ def generate(manifest: Manifest, seed: int = 0, rho: float = 0.01, mask: int = 0
                 e = np.array([t.expert], np.uint64)
                 active = int((h(S_EXP, seed, t.layer, e) >> np.uint64(32))[0] < np.uint64(threshold(EXPERT_F)))
                 thr = threshold(min(1.0, rho / EXPERT_F))
-            lib().synth_cpu_fill_new(_p(o), _p(n), t.numel, mode, active, key(S_MASK, seed, tid), thr,
+            (lib().synth_cpu_fill_new8 if e8 else lib().synth_cpu_fill_new)(
+                _p(o), _p(n), t.numel, mode, active, key(S_MASK, seed, tid), thr,
                                      key(S_PERT, seed, tid), key_row, thr_row, cols)
         olds.append(o)
         news.append(n)

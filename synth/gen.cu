@@ -34,6 +34,22 @@ __global__ void k_fill_new(const u16* old, u16* nw, u64 n, int mode, int active,
   }
 }
 
+// 8-bit elements (FP8 E4M3, f2): the same recipe on bytes
+__global__ void k_fill_old8(uint8_t* out, u64 n, int norm, u64 key_val, const uint8_t* table) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    out[i] = norm ? (uint8_t)norm : table[mix(key_val ^ i) >> 48];
+}
+
+__global__ void k_fill_new8(const uint8_t* old, uint8_t* nw, u64 n, int mode, int active, u64 key_mask, u64 thr,
+                            u64 key_pert, u64 key_row, u64 thr_row, u64 cols) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    bool m = active && (mix(key_mask ^ i) >> 32) < thr;
+    if (mode == 1) m = m && ((mix(key_row ^ (i / cols)) >> 32) < thr_row);
+    uint8_t o = old[i];
+    nw[i] = m ? (uint8_t)(o ^ (uint8_t)(1 + mix(key_pert ^ i) % 3)) : o;
+  }
+}
+
 // offsets[t] = exclusive prefix of counts (single CTA of 1024 threads)
 __global__ void __launch_bounds__(1024) k_prefix(const u64* counts, u32 T, u64* offsets) {
   __shared__ u64 s_w[32];
@@ -129,6 +145,24 @@ int synth_fill_new(const void* old, void* nw, u64 n, int mode, int active, u64 k
   int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
   k_fill_new<<<grid, 256, 0, (cudaStream_t)stream>>>((const u16*)old, (u16*)nw, n, mode, active, key_mask, thr,
                                                       key_pert, key_row, thr_row, cols ? cols : 1);
+  return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+int synth_fill_old8(void* out, u64 n, int norm, u64 key_val, const void* table, void* stream) {
+  if (!n) return 0;
+  u64 blocks = (n + 255) / 256;
+  int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
+  k_fill_old8<<<grid, 256, 0, (cudaStream_t)stream>>>((uint8_t*)out, n, norm, key_val, (const uint8_t*)table);
+  return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+int synth_fill_new8(const void* old, void* nw, u64 n, int mode, int active, u64 key_mask, u64 thr, u64 key_pert,
+                    u64 key_row, u64 thr_row, u64 cols, void* stream) {
+  if (!n) return 0;
+  u64 blocks = (n + 255) / 256;
+  int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
+  k_fill_new8<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)old, (uint8_t*)nw, n, mode, active, key_mask,
+                                                       thr, key_pert, key_row, thr_row, cols ? cols : 1);
   return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 

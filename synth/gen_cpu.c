@@ -23,3 +23,19 @@ void synth_cpu_fill_new(const uint16_t* old, uint16_t* nw, uint64_t n, int mode,
     nw[i] = m ? (uint16_t)(o ^ (uint16_t)(1 + mix(key_pert ^ i) % 3)) : o;
   }
 }
+
+/* 8-bit elements (FP8 E4M3, f2) */
+void synth_cpu_fill_old8(uint8_t* out, uint64_t n, int norm, uint64_t key_val, const uint8_t* table) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = norm ? (uint8_t)norm : table[mix(key_val ^ i) >> 48];
+}
+
+void synth_cpu_fill_new8(const uint8_t* old, uint8_t* nw, uint64_t n, int mode, int active, uint64_t key_mask,
+                         uint64_t thr, uint64_t key_pert, uint64_t key_row, uint64_t thr_row, uint64_t cols) {
+  if (!cols) cols = 1;
+  for (uint64_t i = 0; i < n; ++i) {
+    int m = active && (mix(key_mask ^ i) >> 32) < thr;
+    if (mode == 1) m = m && ((mix(key_row ^ (i / cols)) >> 32) < thr_row);
+    uint8_t o = old[i];
+    nw[i] = m ? (uint8_t)(o ^ (uint8_t)(1 + mix(key_pert ^ i) % 3)) : o;
+  }
+}

@@ -9,7 +9,7 @@ import numpy as np
 import torch
 
 from . import (KIND_NORM, MASK_E, MASK_R, S_EXP, S_MASK, S_PERT, S_ROW, S_VAL, EXPERT_F, ROW_Q, Manifest, h, key,
-               threshold, bf16_table, table, ONE, DTYPE_BF16)
+               threshold, bf16_table, table, ONE, DTYPE_BF16, DTYPE_FP8)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gen.cu")
@@ -34,7 +34,9 @@ def lib():
         L.synth_fill_old.argtypes = [P, u64, i32, u64, P, P]
         L.synth_fill_new.argtypes = [P, P, u64, i32, i32, u64, u64, u64, u64, u64, u64, P]
         L.synth_toggle.argtypes = [P, P, P, P, u32, P, P]
-        for f in (L.synth_fill_old, L.synth_fill_new, L.synth_toggle):
+        L.synth_fill_old8.argtypes = [P, u64, i32, u64, P, P]
+        L.synth_fill_new8.argtypes = [P, P, u64, i32, i32, u64, u64, u64, u64, u64, u64, P]
+        for f in (L.synth_fill_old, L.synth_fill_new, L.synth_toggle, L.synth_fill_old8, L.synth_fill_new8):
             f.restype = i32
         _lib = L
     return _lib
@@ -46,7 +48,8 @@ _tables = {}
 def _table(device, dtype: int = DTYPE_BF16) -> torch.Tensor:
     k = (str(device), dtype)
     if k not in _tables:
-        _tables[k] = torch.from_numpy(table(dtype).view(np.int16).copy()).to(device)
+        tb = table(dtype)
+        _tables[k] = torch.from_numpy(tb.copy() if tb.dtype == np.uint8 else tb.view(np.int16).copy()).to(device)
     return _tables[k]
 
 
@@ -68,7 +71,8 @@ def arena(manifest: Manifest, device, dtype=torch.int16):
 def fill_old(views, manifest: Manifest, seed: int, tid0: int = 0, dtype: int = DTYPE_BF16):
     tab = _table(views[0].device, dtype) if views else None
     for k, (v, t) in enumerate(zip(views, manifest.tensors)):
-        rc = lib().synth_fill_old(ctypes.c_void_p(v.data_ptr()), v.numel(), ONE[dtype] if t.kind == KIND_NORM else 0,
+        f = lib().synth_fill_old8 if dtype == DTYPE_FP8 else lib().synth_fill_old
+        rc = f(ctypes.c_void_p(v.data_ptr()), v.numel(), ONE[dtype] if t.kind == KIND_NORM else 0,
                                   key(S_VAL, seed, tid0 + k), ctypes.c_void_p(tab.data_ptr()), _s())
         assert rc == 0
 
@@ -85,7 +89,8 @@ def fill_new(old_views, new_views, manifest: Manifest, seed: int, rho: float, ma
             e = np.array([t.expert], np.uint64)
             active = int((h(S_EXP, seed, t.layer, e) >> np.uint64(32))[0] < np.uint64(threshold(EXPERT_F)))
             thr = threshold(min(1.0, rho / EXPERT_F))
-        rc = lib().synth_fill_new(ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(n.data_ptr()), o.numel(), mode,
+        f = lib().synth_fill_new8 if o.element_size() == 1 else lib().synth_fill_new
+        rc = f(ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(n.data_ptr()), o.numel(), mode,
                                   active, key(S_MASK, seed, tid), thr, key(S_PERT, seed, tid), key_row, thr_row,
                                   cols, _s())
         assert rc == 0
