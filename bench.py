@@ -69,7 +69,7 @@ def parse():
                    help="snapshot: diff new weights against the last-synced snapshot (north_star); cast: f1, the "
                         "paper's own hook (Alg. 1): the fp32->bf16 CastAndCopy tracks the changed elements into a "
                         "bitmap and the sync gathers them (no snapshot; the cast runs inside the timed step)")
-    p.add_argument("--dtype", choices=["bf16", "fp16"], default="bf16",
+    p.add_argument("--dtype", choices=["bf16", "fp16", "fp8"], default="bf16",
                    help="synchronisation precision (f2, P:190): 16-bit element type of the weights")
     p.add_argument("--escape", action="store_true",
                    help="f4 escape-coded DELTA16 for records with index gaps > 32767 (clustered masks)")
@@ -250,7 +250,10 @@ class Rank:
         sharded_model = topo in ("fanout", "sharded")
         self.shards = transport.shard_ranges(manifest.numel, half) if sharded_model else None
         codec = ss.SYNC_CODEC_COMPRESSED if args.codec == "compressed" else ss.SYNC_CODEC_RAW
-        self.dtype = synth.DTYPE_FP16 if args.dtype == "fp16" else synth.DTYPE_BF16
+        self.dtype = {"bf16": synth.DTYPE_BF16, "fp16": synth.DTYPE_FP16, "fp8": synth.DTYPE_FP8}[args.dtype]
+        adt = torch.uint8 if args.dtype == "fp8" else torch.int16   # arena element type
+        if args.dtype == "fp8" and (args.commit != "swap" or args.replica != "separate"):
+            raise SystemExit("--dtype fp8 runs with --commit swap and a separate replica")
         kw = dict(bucket_limit=int(args.bucket_mb * (1 << 20)), codec=codec, crc=args.crc, dtype=self.dtype)
         rkw = dict(kw, route=args.route, escape=args.escape)   # routing / escapes are sender-side choices
         self.X = self.Y = self.R = None
@@ -272,8 +275,8 @@ class Rank:
             if self.tracking:
                 self._setup_tracking(mt, tid0, cap, rkw)
             else:
-                self.X, self.Xv = sg.arena(mt, dev)   # trainer snapshot (swaps with Y under --commit swap)
-                self.Y, self.Yv = sg.arena(mt, dev)   # trainer current weights
+                self.X, self.Xv = sg.arena(mt, dev, dtype=adt)   # trainer snapshot (swaps with Y under swap)
+                self.Y, self.Yv = sg.arena(mt, dev, dtype=adt)   # trainer current weights
                 sg.fill_old(self.Xv, mt, self.seed, tid0=tid0, dtype=self.dtype)
                 sg.fill_new(self.Xv, self.Yv, mt, self.seed, args.rho, MASKS[args.mask], tid0=tid0)
                 self.sender = GroupedSender(self.Xv, self.Yv, groups=self.G, max_changed=cap, **rkw)
@@ -299,7 +302,7 @@ class Rank:
                 srcs = {d.rank - half: (0, hi - lo)}
                 mr, tid0, rseed = manifest.slice(lo, hi), lo, args.seed
             self.mr = mr
-            self.R, self.Rv = sg.arena(mr, dev)
+            self.R, self.Rv = sg.arena(mr, dev, dtype=adt)
             sg.fill_old(self.Rv, mr, rseed, tid0=tid0, dtype=self.dtype)
             # one receiver per source Trainer (its records carry ids local to its shard and group)
             for src, (lo, hi) in srcs.items():
@@ -326,7 +329,9 @@ class Rank:
                 self.link = transport.PairLink(d.rank, W, dev, trainer=t, rollout=t + half, ctrl=d.ctrl)
         ntens = len(self.mt.tensors) if self.is_trainer else 1
         self.toggle_scratch = torch.empty(ntens + 1, dtype=torch.int64, device=dev)
-        self.S = 2 * self.mt.total if self.is_trainer else 0   # weights this rank syncs per step (as the sender)
+        self.N = self.mt.total if self.is_trainer else 0
+        eb = 1 if args.dtype == "fp8" else 2
+        self.S = eb * self.N   # bytes of weights this rank syncs per step (as the sender)
 
     def _setup_tracking(self, mt, tid0, cap, kw):
         """f1 (Alg. 1): bf16 model weights W + two fp32 master versions M0 / M1 (the optimizer's outputs of
@@ -464,14 +469,14 @@ class Rank:
             mine_r = {}
             for src, gr in self.receivers.items():
                 w = gr.parts[0].weights[0]
-                lo = (w.data_ptr() - self.R.data_ptr()) // 2
+                lo = (w.data_ptr() - self.R.data_ptr()) // self.R.element_size()
                 n = sum(sum(x.numel() for x in p.weights) for p in gr.parts)
                 mine_r[src] = chunked_digest(self.R[lo:lo + n])
         return mine_x, mine_r
 
 
 def chunked_digest(t: torch.Tensor, chunk: int = 1 << 24) -> tuple:
-    """Order-sensitive digest of an int16 tensor (verification only, outside the timed region)."""
+    """Order-sensitive digest of an int16 / uint8 tensor (verification only, outside the timed region)."""
     a = b = 0
     for s in range(0, t.numel(), chunk):
         c = t[s:s + chunk].to(torch.int64) & 0xFFFF
@@ -490,7 +495,7 @@ def cpu_baseline(args, manifest: synth.Manifest, seed: int, sample_elems: float,
         tot += manifest.tensors[k].numel
         k += 1
     sub = manifest.slice(0, k, f"{manifest.name}[:{k}]")
-    dt = synth.DTYPE_FP16 if args.dtype == "fp16" else synth.DTYPE_BF16
+    dt = {"bf16": synth.DTYPE_BF16, "fp16": synth.DTYPE_FP16, "fp8": synth.DTYPE_FP8}[args.dtype]
     olds, news = sc.generate(sub, seed=seed, rho=args.rho, mask=MASKS[args.mask], dtype=dt)
     codec = oracle.CODEC_COMPRESSED if args.codec == "compressed" else oracle.CODEC_RAW
     limit = int(args.bucket_mb * (1 << 20))
@@ -540,8 +545,8 @@ def run_ours(args):
     if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline and not r.tracking:
         cpu = cpu_baseline(args, manifest, r.seed, args.cpu_sample_elems)
         # inputs: GPU twin == CPU twin on the sampled tensors
-        gen_ok = all(np.array_equal(r.Xv[k].cpu().numpy().view(np.uint16), cpu["olds"][k]) and
-                     np.array_equal(r.Yv[k].cpu().numpy().view(np.uint16), cpu["news"][k])
+        hv = (lambda x: x.cpu().numpy()) if r.X.element_size() == 1 else (lambda x: x.cpu().numpy().view(np.uint16))
+        gen_ok = all(np.array_equal(hv(r.Xv[k]), cpu["olds"][k]) and np.array_equal(hv(r.Yv[k]), cpu["news"][k])
                      for k in range(min(cpu["k"], 64)))
         p0 = r.sender.parts[0]   # group 0 starts at tensor 0: its record ids are the oracle's
         p0.sync()
@@ -568,7 +573,8 @@ def run_ours(args):
         nnz, vbytes, n16, n32 = stats["nnz"], stats["value_bytes"], stats["n_delta16"], stats["n_abs32"]
         n16e = stats.get("n_delta16e", 0)
         counts = [c for p in r.sender.parts for c in p.counts.cpu().tolist()]
-        raw_payload = sum(((16 + 6 * c + 15) // 16) * 16 for c in counts if c) + 48 * max(nb, 1)
+        vb = 5 if args.dtype == "fp8" else 6   # raw (I, V) bytes per change: u32 index + element
+        raw_payload = sum(((16 + vb * c + 15) // 16) * 16 for c in counts if c) + 48 * max(nb, 1)
     local_alg_extract = 2 * r.S + 6 * nnz
 
     # ---- timed region
@@ -621,7 +627,7 @@ def run_ours(args):
     #      timed only for comparison) over up to 2^29 elements of the masters, scaled to this rank's elements
     track_cmp = None
     if r.tracking and r.sender is not None:
-        n_el = r.S // 2
+        n_el = r.N
         k = min(n_el, 1 << 29)
         src = r.M[0][:k]
         dst = torch.empty(k, dtype=torch.bfloat16, device=d.dev)
@@ -669,11 +675,13 @@ def run_ours(args):
     n16e_t = d.sum(n16e)
     achieved = local_alg_extract / (ext_ms_local / 1e3) / 1e9   # rank 0 (a Trainer), its own launch
     roof_kernel, roof_bytes = "k_extract (K1)", local_alg_extract
+    if args.dtype == "fp8":
+        roof_kernel = "k_diff8 + tracked compaction (FP8 extract)"
     if r.tracking:
         # f1: the dominant kernel is the cast with tracking. Algorithmic bytes per launch: read the fp32 master
         # and the bf16 weights (6 B / element), write the 32 B sectors that changed and the bitmap words that
         # gained a bit (read + write)
-        n_el = r.S // 2
+        n_el = r.N
         f_sec = 1 - (1 - args.rho) ** 16
         f_word = 1 - (1 - args.rho) ** 32
         roof_kernel = "k_cast_track (f1, Alg. 1 CastAndCopy + tracking)"
@@ -703,12 +711,13 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": d.world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms / K, 4), "higher_is_better": True,
         "scaling": "strong" if strong else "weak",
-        "vs_baseline": None, "dtype": f"u16 ({args.dtype} bit patterns; integer/bit work only)",
+        "vs_baseline": None,
+        "dtype": f"{'u8' if args.dtype == 'fp8' else 'u16'} ({args.dtype} bit patterns; integer/bit work only)",
         "data": "synthetic: random-init bf16 weights of the named architecture (N(0,0.02) quantile table), "
                 f"{args.mask}-mask sparse perturbations, seeded",
         "config": {"workload": f"{manifest.name} bf16, {100 * (1 - args.rho):.1f}% sparsity, {args.mask} mask",
                    "topology_mode": args.topology,
-                   "elements_per_trainer_rank": r.S // 2, "model_elements": manifest.total,
+                   "elements_per_trainer_rank": r.N, "model_elements": manifest.total,
                    "tensors": len(manifest.tensors),
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
                    "groups": r.G, "replica": args.replica, "tracking": args.tracking, "route": args.route,
@@ -720,13 +729,14 @@ def run_ours(args):
                               "cast_track"], phases)},
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic if not r.tracking else None,
-                     "bytes_per_launch": roof_bytes, "traffic_source": traffic_src if not r.tracking else None,
+                     "traffic": traffic if not (r.tracking or args.dtype == "fp8") else None,
+                     "bytes_per_launch": roof_bytes,
+                     "traffic_source": traffic_src if not (r.tracking or args.dtype == "fp8") else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
-        "payload": {"nnz": int(nnz_t), "rho_measured": round(nnz_t / max(total_S / 2, 1), 6), "buckets": int(nb_t),
+        "payload": {"nnz": int(nnz_t), "rho_measured": round(nnz_t / max(d.sum(r.N), 1), 6), "buckets": int(nb_t),
                     "bytes": int(payload_t), "x_comp": round(total_S / max(payload_t, 1), 2),
                     "x_raw_eq1": round(total_S / max(raw_t, 1), 2),
-                    "alpha": round(vbytes_t / max(2 * nnz_t, 1), 4),
+                    "alpha": round(vbytes_t / max((1 if args.dtype == "fp8" else 2) * nnz_t, 1), 4),
                     "delta16_records": int(n16_t), "abs32_records": int(n32_t), "delta16e_records": int(n16e_t),
                     "paper_context": "paper: 32-54x raw, ~60-101x compressed on H100 clusters (P:22, P:380)"},
         "clocks": clk, "gpu_launches": int(launches), "bit_exact_replica": verify, "e2e": e2e,

@@ -76,10 +76,15 @@ typedef struct {
   uint32_t dtype;          /* SYNC_DTYPE_* of every manifest tensor (0 = BF16) */
 } sync_config;
 
-/* Element types (f2). Both are 16-bit patterns: every step is the same integer work and the record's
- * dtype byte carries the tag; a receiver context only accepts records of its own dtype. */
+/* Element types (f2). BF16 / FP16 are 16-bit patterns: every step is the same integer work and the
+ * record's dtype byte carries the tag; a receiver context only accepts records of its own dtype. */
 #define SYNC_DTYPE_BF16 1u
 #define SYNC_DTYPE_FP16 2u
+/* FP8 E4M3 (8-bit elements): every pointer table / weight argument of an FP8 context points at
+ * byte tensors (cast to the uint16_t* parameter types); V arrays still hold one value per u16 slot (the byte
+ * in the low half). Records have one value plane. Not supported by sync_extract / sync_apply /
+ * sync_commit_snapshot (single-tensor 16-bit calls) nor by the f1 tracking calls (round_BF16).           */
+#define SYNC_DTYPE_FP8 3u
 
 /* Per-sync statistics, filled by sync_ctx_stats() (blocking). */
 typedef struct {

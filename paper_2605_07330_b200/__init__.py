@@ -41,6 +41,7 @@ SYNC_FLAG_ROUTE = 2
 SYNC_FLAG_ESCAPE = 4
 SYNC_DTYPE_BF16 = 1
 SYNC_DTYPE_FP16 = 2
+SYNC_DTYPE_FP8 = 3
 SYNC_CHUNK = 16384
 
 EXPORTS = [
@@ -170,11 +171,13 @@ def _dev_ptr(t: torch.Tensor) -> ctypes.c_void_p:
 
 
 def _bits(t: torch.Tensor) -> torch.Tensor:
-    """bf16 / fp16 / int16 / uint16 tensor -> its 16-bit patterns (a view, no copy)."""
+    """bf16 / fp16 / int16 / uint16 tensor -> its 16-bit patterns; fp8 / uint8 / int8 -> its bytes (views)."""
     if t.dtype in (torch.bfloat16, torch.float16):
         return t.view(torch.int16)
-    if t.dtype in (torch.int16, torch.uint16):
+    if t.dtype in (torch.int16, torch.uint16, torch.uint8):
         return t
+    if t.dtype in (torch.float8_e4m3fn, torch.int8):
+        return t.view(torch.uint8)
     raise SyncError(SYNC_ERR_DTYPE, f"dtype {t.dtype} (16-bit element types only)")
 
 

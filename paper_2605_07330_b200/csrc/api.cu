@@ -26,12 +26,12 @@ constexpr u64 kAlign = 256;
 struct Layout {
   u64 numel, tile_prefix, tile_tensor, misc, tile_state, stage_ring, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
   u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, rec_dst, totals, recs, bks, views, nviews, crc;
-  u64 bm_off, group_sum, chunk_esc, chunk_escoff, total;
+  u64 bm_off, group_sum, chunk_esc, chunk_escoff, bitmap8, total;
 };
 
 u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4 + 32; }  // + 32 bad flags
 
-Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_changed) {
+Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_changed, u64 bm8_words = 0) {
   Layout L{};
   u64 o = 0;
   auto take = [&](u64 bytes) {
@@ -67,19 +67,20 @@ Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_change
   L.group_sum = take(8ull * (n_tiles / 1024 + 2));       // f1: tile-offset scan groups
   L.chunk_esc = take(4ull * max_chunks);                   // f4: escapes per chunk
   L.chunk_escoff = take(8ull * (max_chunks + 1));          // f4: their exclusive prefix
+  L.bitmap8 = take(4ull * bm8_words);                      // FP8: change bitmap of the extract
   L.total = o;
   return L;
 }
 
 struct Dims {
   u32 T;
-  u64 n_tiles, max_chunks, max_record, crc_n;
+  u64 n_tiles, max_chunks, max_record, crc_n, bm8_words;
 };
 
 int check_manifest(const sync_manifest* m, const sync_config* c, Dims* d) {
   if (!m || !c || (m->n_tensors && !m->numel)) return SYNC_ERR_ARG;
   if (c->codec > SYNC_CODEC_COMPRESSED || c->bucket_limit < 64) return SYNC_ERR_ARG;
-  if (c->dtype > SYNC_DTYPE_FP16) return SYNC_ERR_DTYPE;
+  if (c->dtype > SYNC_DTYPE_FP8) return SYNC_ERR_DTYPE;
   d->T = m->n_tensors;
   d->n_tiles = 0;
   u64 maxn = 0;
@@ -88,6 +89,9 @@ int check_manifest(const sync_manifest* m, const sync_config* c, Dims* d) {
     d->n_tiles += (m->numel[t] + kTile - 1) / kTile;
     maxn = m->numel[t] > maxn ? m->numel[t] : maxn;
   }
+  d->bm8_words = 0;   // FP8 contexts extract through a change bitmap (same per-tensor word layout as f1)
+  if (c->dtype == SYNC_DTYPE_FP8)
+    for (u32 t = 0; t < m->n_tensors; ++t) d->bm8_words += pad_to((m->numel[t] + 31) / 32, 4);
   d->max_chunks = (c->max_changed + kChunk - 1) / kChunk + d->T + 1;
   // largest possible record (one tensor fully changed): bounds a received bucket for the CRC scratch
   d->max_record = 6 * maxn + 20 * ((maxn + kChunk - 1) / kChunk) + 64;
@@ -154,7 +158,7 @@ int sync_workspace_size(const sync_manifest* m, const sync_config* c, size_t* by
   int st = check_manifest(m, c, &d);
   if (st) return st;
   if (!bytes) return SYNC_ERR_ARG;
-  *bytes = make_layout(d.T, d.n_tiles, d.max_chunks, d.crc_n, c->max_changed).total;
+  *bytes = make_layout(d.T, d.n_tiles, d.max_chunks, d.crc_n, c->max_changed, d.bm8_words).total;
   return SYNC_OK;
 }
 
@@ -165,7 +169,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   Dims d;
   int st = check_manifest(m, c, &d);
   if (st) return st;
-  Layout L = make_layout(d.T, d.n_tiles, d.max_chunks, d.crc_n, c->max_changed);
+  Layout L = make_layout(d.T, d.n_tiles, d.max_chunks, d.crc_n, c->max_changed, d.bm8_words);
   if (!d_workspace || workspace_bytes < L.total) return SYNC_ERR_WORKSPACE;
   if (!aligned16(d_workspace)) return SYNC_ERR_ALIGNMENT;
   sync_ctx* x = new (std::nothrow) sync_ctx();
@@ -307,6 +311,8 @@ int sync_extract_status(void* d_workspace, sync_stream_t stream) {
   return -(int)v;
 }
 
+static TrackArgs track_args(sync_ctx* x, uint32_t* d_bitmap);
+
 int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const uint16_t* const* d_new_ptrs,
                          uint32_t* d_I, uint16_t* d_V, uint64_t* d_counts, sync_stream_t stream) {
   if (!x || (x->d.T && (!d_old_ptrs || !d_new_ptrs || !d_counts))) return SYNC_ERR_ARG;
@@ -315,6 +321,16 @@ int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const u
   if (x->d.T == 0) return SYNC_OK;
   CK(cudaMemsetAsync(x->misc, 0, 4, s));
   CK(cudaMemsetAsync(d_counts, 0, 8ull * x->d.T, s));
+  if (x->plan.dtype == SYNC_DTYPE_FP8) {   // 8-bit elements: diff into a bitmap, then compact
+    TrackArgs a = track_args(x, reinterpret_cast<u32*>(x->ws + x->L.bitmap8));
+    a.counts = d_counts;
+    a.I = d_I;
+    a.V = d_V;
+    launch_extract8(a, reinterpret_cast<const uint8_t* const*>(d_old_ptrs),
+                    reinterpret_cast<const uint8_t* const*>(d_new_ptrs), 16 * x->sm_count, s);
+    CK(cudaGetLastError());
+    return SYNC_OK;
+  }
   if (x->d.n_tiles) CK(cudaMemsetAsync(x->ws + x->L.tile_state, 0, 8 * x->d.n_tiles, s));
   launch_extract_batched(d_old_ptrs, d_new_ptrs, reinterpret_cast<const u64*>(x->ws + x->L.tile_prefix),
                          reinterpret_cast<const u32*>(x->ws + x->L.tile_tensor), x->plan.numel, x->d.T, x->d.n_tiles, d_I, d_V, x->cfg.max_changed, d_counts,

@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(256) k_apply(u16* W, const u32* I, const u16* 
   if (bad) latch(status, SYNC_ERR_INDEX_RANGE);
 }
 
+template <typename E>   // element type: u16 (BF16 / FP16) or u8 (FP8)
 __global__ void __launch_bounds__(256) k_commit_batched(Plan p, u16* const* snaps, const u32* I, const u16* V) {
   // CTA per chunk; warp w takes the contiguous changes [w*2048, (w+1)*2048) of the
   // chunk (contiguous per-warp ranges measured 3-16% faster than CTA-strided ones
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(256) k_commit_batched(Plan p, u16* const* snap
     const u32 nk = (u32)((nnz - p0) < kChunk ? (nnz - p0) : kChunk);
     const u32* Ir = I + p.rec_off[t] + p0;
     const u16* Vr = V + p.rec_off[t] + p0;
-    u16* S = snaps[t];
+    E* S = reinterpret_cast<E*>(snaps[t]);
     const u64 lim = p.numel[t];
     bool bad = false;
     const u32 wb = warp * kPerWarp, we = wb + kPerWarp < nk ? wb + kPerWarp : nk;
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(256) k_commit_batched(Plan p, u16* const* snap
       for (int u = 0; u < kU; ++u) {
         const u32 q = q0 + u * 32;
         if (q < we) {
-          if (idx[u] < lim) S[idx[u]] = val[u];
+          if (idx[u] < lim) S[idx[u]] = (E)val[u];
           else bad = true;
         }
       }
@@ -100,7 +101,8 @@ void launch_apply(u16* W, const u32* I, const u16* V, u64 count, u64 numel, u32*
 }
 
 void launch_commit_batched(const Plan& p, u16* const* snaps, const u32* I, const u16* V, int grid, cudaStream_t s) {
-  k_commit_batched<<<grid * 2, 256, 0, s>>>(p, snaps, I, V);
+  if (p.dtype == SYNC_DTYPE_FP8) k_commit_batched<uint8_t><<<grid * 2, 256, 0, s>>>(p, snaps, I, V);
+  else k_commit_batched<u16><<<grid * 2, 256, 0, s>>>(p, snaps, I, V);
   count_launch();
 }
 

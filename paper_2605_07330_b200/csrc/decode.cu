@@ -59,18 +59,20 @@ __device__ __forceinline__ bool read_record(const u8* bk, const BucketHdr& h, u3
   if (r->tid >= n_tensors || r->dtype != dtype || r->mode > 3 || r->codec > 1 || r->nnz == 0) return false;
   if (r->mode == kModeDelta16E && r->codec != SYNC_CODEC_COMPRESSED) return false;
   if ((u64)r->nnz > numel[r->tid]) return false;
-  if (r->mode == kModeFull) return (u64)r->nnz == numel[r->tid] && 16 + 2ull * r->nnz <= r->rb;
-  if (r->codec == SYNC_CODEC_RAW) return r->mode == 1 && 16 + 6ull * r->nnz <= r->rb;
+  const u64 eb = dtype == SYNC_DTYPE_FP8 ? 1 : 2;           // element bytes
+  const u64 lo = eb == 1 ? 0 : pad_to(r->nnz, 4);            // lo plane (16-bit elements only)
+  if (r->mode == kModeFull) return (u64)r->nnz == numel[r->tid] && 16 + eb * r->nnz <= r->rb;
+  if (r->codec == SYNC_CODEC_RAW) return r->mode == 1 && 16 + (4 + eb) * r->nnz <= r->rb;
   const u64 nch = (r->nnz + kChunk - 1) / kChunk;
   if (r->mode == kModeDelta16E) {   // f4: word-offset table + total words after the header
     const u64 s0 = 16 + 4 * (nch + 1);
     if (s0 > r->rb) return false;
     const u64 total = reinterpret_cast<const u32*>(bk + ro + 16)[nch];
     if (total < r->nnz || total > 2ull * r->nnz) return false;
-    return s0 + pad_to(2 * total, 4) + pad_to(r->nnz, 4) + 16 * nch <= r->rb;
+    return s0 + pad_to(2 * total, 4) + lo + 16 * nch <= r->rb;
   }
   const u64 ib = (r->mode ? 4ull : 2ull) * r->nnz;
-  return 16 + pad_to(ib, 4) + pad_to(r->nnz, 4) + 16 * nch <= r->rb;
+  return 16 + pad_to(ib, 4) + lo + 16 * nch <= r->rb;
 }
 
 // ---------------------------------------------------------------------------- unpack
@@ -172,6 +174,7 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
   __shared__ u64 s_pre[kDecodeBatch + 1];
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   DecodeModel& dm = s_dm[warp];
+  const bool e8 = dtype == SYNC_DTYPE_FP8;   // FP8: one value plane (the byte), no lo plane, byte stores
   if (threadIdx.x < bb.n) {   // headers; a bucket with a bad header or failed CRC contributes no chunks
     const u32 i = threadIdx.x;
     BucketHdr h;
@@ -238,13 +241,16 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
 
     if (r.mode == kModeFull) {   // f3 FULL record: element i of the tensor = the i-th value
       const u16* Vr = reinterpret_cast<const u16*>(rec + 16);
+      const u8* Vr8 = rec + 16;
       for (u32 qq = lane; qq < nk; qq += 32) {
         const u64 i = p0 + qq;
+        const u16 v = e8 ? (u16)Vr8[i] : Vr[i];
         if (kApply) {
-          W[i] = Vr[i];
+          if (e8) reinterpret_cast<u8*>(W)[i] = (u8)v;
+          else W[i] = v;
         } else {
           Io[qq] = (u32)i;
-          Vo[qq] = Vr[i];
+          Vo[qq] = v;
         }
       }
       continue;
@@ -253,12 +259,17 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
     if (r.codec == SYNC_CODEC_RAW) {
       const u32* Ir = reinterpret_cast<const u32*>(rec + 16) + p0;
       const u16* Vr = reinterpret_cast<const u16*>(rec + 16 + 4 * nnz) + p0;
+      const u8* Vr8 = rec + 16 + 4 * nnz + p0;
       for (u32 qq = lane; qq < nk; qq += 32) {
         u32 idx = Ir[qq];
-        u16 v = Vr[qq];
+        u16 v = e8 ? (u16)Vr8[qq] : Vr[qq];
         if (kApply) {
-          if (idx < lim) W[idx] = v;
-          else bad = true;
+          if (idx < lim) {
+            if (e8) reinterpret_cast<u8*>(W)[idx] = (u8)v;
+            else W[idx] = v;
+          } else {
+            bad = true;
+          }
         } else {
           Io[qq] = idx;
           Vo[qq] = v;
@@ -273,7 +284,7 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
     const u64 s0 = esc ? 16 + 4 * (nch + 1) : 16;
     const u64 ib = esc ? 2ull * tbl[nch] : (r.mode ? 4ull : 2ull) * nnz;
     const u64 lo_off = s0 + pad_to(ib, 4);
-    const u64 dir_off = lo_off + pad_to(nnz, 4);
+    const u64 dir_off = lo_off + (e8 ? 0 : pad_to(nnz, 4));   // FP8: no lo plane
     const u32* de = reinterpret_cast<const u32*>(rec + dir_off + 16 * k);
     const u32 hi_off = de[0], hb = de[1], cm = de[2], base = de[3];
     bool corrupt = ((u64)hi_off + hb > r.rb) || (hi_off & 3u) || cm > 1 || (cm == 0 && hb != nk);
@@ -375,7 +386,7 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
       for (int i = 0; i < kPF; ++i) {
         const u32 qq = (g0 + i) * 32 + lane;
         const bool act = qq < nk;
-        lb_[i] = act ? (u32)lo[qq] : 0u;
+        lb_[i] = (act && !e8) ? (u32)lo[qq] : 0u;
         dd_[i] = (act && !esc) ? (r.mode == 0 ? (u32)D[qq] : A[qq]) : 0u;
       }
     };
@@ -475,10 +486,14 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
           idx = dd[i];
         }
         if (act) {
-          const u16 v = (u16)((s << 8) | lb[i]);
+          const u16 v = e8 ? (u16)s : (u16)((s << 8) | lb[i]);
           if (kApply) {
-            if (idx < lim) W[idx] = v;
-            else range_bad = true;
+            if (idx < lim) {
+              if (e8) reinterpret_cast<u8*>(W)[idx] = (u8)v;
+              else W[idx] = v;
+            } else {
+              range_bad = true;
+            }
           } else {
             Io[qq] = idx;
             Vo[qq] = v;

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
   const u32 tid = threadIdx.x;
   const u64 n_chunks = p.totals[kTotChunks];
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
+  const bool e8 = p.dtype == SYNC_DTYPE_FP8;   // FP8: one value plane (the byte), no lo plane
   for (u64 g = blockIdx.x; g < n_chunks; g += gridDim.x) {
     __syncthreads();
     const ChunkPos c = locate_chunk(p, counts, g, s_t, I, V);
@@ -53,10 +54,17 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
       // f3 FULL record: the tensor's current values. The record's n_ch chunks (counted
       // from its nnz) split the copy at multiples of 8 elements (16-byte stores into the 16-aligned body).
       const u64 numel = p.numel[t];
+      const u64 lo = (numel * k / n_ch) & ~15ull;
+      const u64 hi = last ? numel : ((numel * (k + 1) / n_ch) & ~15ull);
+      if (e8) {   // bytes
+        const u8* src8 = reinterpret_cast<const u8*>(p.cur[t]);
+        u8* dst8 = rec + 16;
+        for (u64 q = lo + tid; q < hi; q += kCThreads) dst8[q] = src8[q];
+        if (last) zero_bytes(rec + 16 + numel, rb - (16 + numel));
+        continue;
+      }
       const u16* src = p.cur[t];
       u16* dst = reinterpret_cast<u16*>(rec + 16);
-      const u64 lo = (numel * k / n_ch) & ~7ull;
-      const u64 hi = last ? numel : ((numel * (k + 1) / n_ch) & ~7ull);
       if ((((uintptr_t)src) & 15u) == 0) {
         const u64 v_end = lo + ((hi - lo) & ~7ull);
         for (u64 q = lo + 8ull * tid; q < v_end; q += 8ull * kCThreads)
@@ -71,12 +79,14 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
 
     if (!comp) {
       u32* Io = reinterpret_cast<u32*>(rec + 16) + p0;
-      u16* Vo = reinterpret_cast<u16*>(rec + 16 + 4 * nnz) + p0;
+      u8* Vb = rec + 16 + 4 * nnz;
       for (u32 q = tid; q < nk; q += kCThreads) {
         Io[q] = Ir[p0 + q];
-        Vo[q] = Vc[q];
+        if (e8) Vb[p0 + q] = (u8)Vc[q];
+        else reinterpret_cast<u16*>(Vb)[p0 + q] = Vc[q];
       }
-      if (last) zero_bytes(rec + 16 + 6 * nnz, rb - (16 + 6 * nnz));
+      const u64 used = 16 + (e8 ? 5 : 6) * nnz;
+      if (last) zero_bytes(rec + used, rb - used);
       continue;
     }
 
@@ -88,7 +98,7 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
     const u64 s0 = esc ? 16 + 4 * (n_ch + 1) : 16;          // f4: word-offset table after the header
     const u64 ib = esc ? 2 * (nnz + ne_rec) : (mode ? 4 : 2) * nnz;
     const u64 lo_off = s0 + pad_to(ib, 4);
-    const u64 dir_off = lo_off + pad_to(nnz, 4);
+    const u64 dir_off = lo_off + (e8 ? 0 : pad_to(nnz, 4));
     const u64 hi_base = dir_off + 16 * n_ch;
     if (esc) {
       // f4 DELTA16E: rounds of 4 positions per thread; a block scan of the word counts (1, or
@@ -114,7 +124,7 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
           if (q + j < nk) {
             d[j] = Ir[pp] - (pp ? Ir[pp - 1] : 0u);
             cnt += d[j] > 32767u ? 2u : 1u;
-            L[q + j] = (u8)(Vc[q + j] & 0xFFu);
+            if (!e8) L[q + j] = (u8)(Vc[q + j] & 0xFFu);
           }
         }
         // exclusive block scan of cnt (kCThreads threads)
@@ -177,15 +187,16 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
               *reinterpret_cast<uint4*>(reinterpret_cast<u32*>(rec + 16) + p0 + q) =
                   make_uint4(iv[j][1], iv[j][2], iv[j][3], iv[j][4]);
             }
-            *reinterpret_cast<u32*>(L + q) = (u32)(vv[j][0] & 0xFFu) | ((u32)(vv[j][1] & 0xFFu) << 8) |
-                                             ((u32)(vv[j][2] & 0xFFu) << 16) | ((u32)(vv[j][3] & 0xFFu) << 24);
+            if (!e8)
+              *reinterpret_cast<u32*>(L + q) = (u32)(vv[j][0] & 0xFFu) | ((u32)(vv[j][1] & 0xFFu) << 8) |
+                                               ((u32)(vv[j][2] & 0xFFu) << 16) | ((u32)(vv[j][3] & 0xFFu) << 24);
           } else {
             for (u32 e = 0; q + e < nk; ++e) {  // chunk tail: reload (keeps the arrays in registers)
               const u64 pe = p0 + q + e;
               const u32 cur = Ir[pe], prev = pe ? Ir[pe - 1] : 0u;
               if (mode == 0) reinterpret_cast<u16*>(rec + 16)[pe] = (u16)(cur - prev);
               else reinterpret_cast<u32*>(rec + 16)[pe] = cur;
-              L[q + e] = (u8)(Vc[q + e] & 0xFFu);
+              if (!e8) L[q + e] = (u8)(Vc[q + e] & 0xFFu);
             }
           }
         }
@@ -193,7 +204,7 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
     }
     if (last) {
       zero_bytes(rec + s0 + ib, pad_to(ib, 4) - ib);
-      zero_bytes(rec + lo_off + nnz, pad_to(nnz, 4) - nnz);
+      if (!e8) zero_bytes(rec + lo_off + nnz, pad_to(nnz, 4) - nnz);
     }
     // ---- directory entry + hi block
     const u32 hb = p.chunk_hi[g];
@@ -212,7 +223,7 @@ __global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, cons
       zero_bytes(rec + hi_end, rb - hi_end);
     }
     if (cm == 0) {
-      for (u32 q = tid; q < nk; q += kCThreads) blk[q] = (u8)(Vc[q] >> 8);
+      for (u32 q = tid; q < nk; q += kCThreads) blk[q] = e8 ? (u8)Vc[q] : (u8)(Vc[q] >> 8);
       zero_bytes(blk + nk, pad_to(nk, 4) - nk);
       continue;
     }

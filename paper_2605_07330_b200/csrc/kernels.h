@@ -121,7 +121,11 @@ struct TrackArgs {
   uint32_t* status;
 };
 void launch_cast_track(const TrackArgs& a, const float* const* master, uint16_t* const* W, int grid, cudaStream_t s);
-void launch_extract_tracked(const TrackArgs& a, uint16_t* const* W, int clear, int grid, cudaStream_t s);
+void launch_extract_tracked(const TrackArgs& a, uint16_t* const* W, int clear, int grid, cudaStream_t s,
+                            bool k8 = false);
+// FP8 (8-bit elements): bitwise diff into the bitmap, then the tracked compaction (V = new[I] bytes)
+void launch_extract8(const TrackArgs& a, const uint8_t* const* olds, const uint8_t* const* news, int grid,
+                     cudaStream_t s);
 
 // apply.cu
 void launch_apply(uint16_t* W, const uint32_t* I, const uint16_t* V, uint64_t count, uint64_t numel,

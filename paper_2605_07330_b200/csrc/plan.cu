@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
   const u64 n_chunks = p.totals[kTotChunks];
   const u64 nwarps = (u64)gridDim.x * 8;
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
+  // the coded value plane: the hi byte of a 16-bit element, the whole byte of an FP8 one (V's low half)
+  const u32 sh = p.dtype == SYNC_DTYPE_FP8 ? 0u : 8u;
   for (u64 g = (u64)blockIdx.x * 8 + warp; g < n_chunks; g += nwarps) {
     const long long t0 = clock64();
     const u64* co = p.chunk_off;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
 #pragma unroll
       for (int u = 0; u < kWPF; ++u) {
         const u32 q = b0 + u * 32 + lane;
-        h[u] = q < nk ? (u32)(Vc[q] >> 8) : 0x100u;
+        h[u] = q < nk ? (u32)(Vc[q] >> sh) : 0x100u;
         c[u] = q < nk ? Ic[q] : 0u;
       }
     };
@@ -181,7 +183,7 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
       for (int u = 0; u < kWPF; ++u) {
         const int gg = top - u;
         const u32 q = (u32)gg * 32 + lane;
-        dst[u] = (gg >= 0 && q < nk) ? (u32)(Vc[q] >> 8) : 0x100u;
+        dst[u] = (gg >= 0 && q < nk) ? (u32)(Vc[q] >> sh) : 0x100u;
       }
     };
     load_block((int)G - 1, nxt);
@@ -267,6 +269,7 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
   __shared__ u64 s_w2[33];
   const u32 T = p.n_tensors;
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
+  const bool e8 = p.dtype == SYNC_DTYPE_FP8;
   const u64 n_chunks = p.totals[kTotChunks];
   const bool over = p.totals[kTotOverflow] != 0;
   constexpr u64 kRound = (u64)kScanThreads * kPer;
@@ -337,12 +340,12 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
           }
           if (mode != kModeDelta16E) ib = pad_to((mode ? 4 : 2) * c, 4);
           const u64 hi = p.chunk_hioff[ch1] - p.chunk_hioff[ch0];
-          by = pad_to(16 + table + ib + pad_to(c, 4) + 16 * (ch1 - ch0) + hi, 16);
+          by = pad_to(16 + table + ib + (e8 ? 0 : pad_to(c, 4)) + 16 * (ch1 - ch0) + hi, 16);   // FP8: no lo plane
         } else {
           ib = 4 * c;
-          by = pad_to(16 + 6 * c, 16);
+          by = pad_to(16 + (e8 ? 5 : 6) * c, 16);
         }
-        const u64 full = pad_to(16 + 2 * p.numel[t], 16);   // f3 routing (DESIGN C19)
+        const u64 full = pad_to(16 + (e8 ? 1 : 2) * p.numel[t], 16);   // f3 routing (DESIGN C19)
         if (p.route && full < by) {
           mode = kModeFull;
           by = full;

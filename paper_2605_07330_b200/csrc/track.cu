@@ -23,7 +23,6 @@
 namespace ss {
 
 constexpr int kTT = 256;                         // threads per CTA
-constexpr u32 kWordsPerTile = (u32)(kTile / 32); // 1024
 constexpr u32 kGroup = 1024;                     // tiles per scan group
 
 __device__ __forceinline__ u16 bf16_rne(u32 f) {
@@ -298,6 +297,7 @@ __global__ void k_track_counts(TrackArgs a) {
 
 // Thread i owns words 4i..4i+3 of the tile (one 16-byte load): one block scan per tile gives each thread its
 // first output position, and its set bits are written in ascending element order.
+template <bool k8>   // k8: 8-bit elements (FP8): V = the byte, zero-extended
 __global__ void __launch_bounds__(kTT) k_track_write(TrackArgs a, u16* const* W, int clear) {
   __shared__ u64 s[33];
   const bool fits = tile_offset(a, a.n_tiles) <= a.cap;   // on overflow the set is kept for a retry
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kTT) k_track_write(TrackArgs a, u16* const* W,
         const u32 idx = (u32)(base + 32ull * (w0 + j) + b);
         if (pos < a.cap) {
           a.I[pos] = idx;
-          a.V[pos] = Wt[idx];
+          a.V[pos] = k8 ? (u16)reinterpret_cast<const uint8_t*>(Wt)[idx] : Wt[idx];
         }
         ++pos;
       }
@@ -363,7 +363,51 @@ void launch_cast_track(const TrackArgs& a, const float* const* master, u16* cons
   count_launch();
 }
 
-void launch_extract_tracked(const TrackArgs& a, u16* const* W, int clear, int grid, cudaStream_t s) {
+// FP8 extraction (f2, 8-bit elements): per tile, the change bitmap of old vs new (bitwise, C1) — thread
+// owns 32-element words: two 16-byte loads of each array — then the tracked compaction below gathers
+// V = new[I] (bytes).
+__global__ void __launch_bounds__(kTT) k_diff8(TrackArgs a, const uint8_t* const* olds, const uint8_t* const* news) {
+  for (u64 tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+    const u32 t = a.tile_tensor[tile];
+    const u64 n = a.numel[t];
+    const u64 base = (tile - a.tile_prefix[t]) * kTile;
+    const u32 nw = tile_words(n, base);
+    const uint8_t* O = olds[t] + base;
+    const uint8_t* N = news[t] + base;
+    u32* bm = a.bitmap + a.bm_off[t] + base / 32;
+    const bool vec = ((((uintptr_t)O) | ((uintptr_t)N)) & 15u) == 0;
+    for (u32 w = threadIdx.x; w < nw; w += kTT) {
+      const u64 e0 = (u64)w * 32;
+      u32 mask = 0;
+      if (vec && base + e0 + 32 <= n) {
+        const uint4* o4 = reinterpret_cast<const uint4*>(O + e0);
+        const uint4* n4 = reinterpret_cast<const uint4*>(N + e0);
+        const uint4 oa = o4[0], ob = o4[1], na = n4[0], nb = n4[1];
+        const u32 x[8] = {oa.x ^ na.x, oa.y ^ na.y, oa.z ^ na.z, oa.w ^ na.w,
+                          ob.x ^ nb.x, ob.y ^ nb.y, ob.z ^ nb.z, ob.w ^ nb.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            mask |= (((x[j] >> (8 * b)) & 0xFFu) ? 1u : 0u) << (4 * j + b);
+      } else {
+        for (u32 k = 0; k < 32 && base + e0 + k < n; ++k) mask |= (O[e0 + k] != N[e0 + k] ? 1u : 0u) << k;
+      }
+      bm[w] = mask;
+    }
+  }
+}
+
+void launch_extract8(const TrackArgs& a, const uint8_t* const* olds, const uint8_t* const* news, int grid,
+                     cudaStream_t s) {
+  if (a.n_tiles) {
+    k_diff8<<<grid, kTT, 0, s>>>(a, olds, news);
+    count_launch();
+  }
+  launch_extract_tracked(a, (u16* const*)news, 0, grid, s, true);   // read-only: V = new[I]
+}
+
+void launch_extract_tracked(const TrackArgs& a, u16* const* W, int clear, int grid, cudaStream_t s, bool k8) {
   if (!a.n_tiles) {
     if (a.n_tensors) {
       k_track_counts<<<1, 256, 0, s>>>(a);
@@ -376,7 +420,8 @@ void launch_extract_tracked(const TrackArgs& a, u16* const* W, int clear, int gr
   k_track_scan_groups<<<(unsigned)n_groups, kTT, 0, s>>>(a);
   k_track_scan_top<<<1, kTT, 0, s>>>(a, n_groups);
   k_track_counts<<<(a.n_tensors + 255) / 256, 256, 0, s>>>(a);
-  k_track_write<<<grid, kTT, 0, s>>>(a, W, clear);
+  if (k8) k_track_write<true><<<grid, kTT, 0, s>>>(a, W, clear);
+  else k_track_write<false><<<grid, kTT, 0, s>>>(a, W, clear);
   for (int i = 0; i < 5; ++i) count_launch();
 }
 

@@ -296,6 +296,47 @@ def test_escape_delta16_bit_exact(fused, crc):
             pytest.fail("no multi-chunk DELTA16E record to damage")
 
 
+@pytest.mark.parametrize("codec,escape,route,crc", [(ss.SYNC_CODEC_COMPRESSED, False, False, False),
+                                                     (ss.SYNC_CODEC_COMPRESSED, True, True, True),
+                                                     (ss.SYNC_CODEC_RAW, False, True, False)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_fp8_bit_exact(codec, escape, route, crc, fused):
+    """f2 FP8 E4M3 (8-bit elements): GPU generator == CPU twin; extraction, one-plane records,
+    FULL / escape records, CRC: GPU buckets == the oracle's; replica and snapshot commit bit-exact."""
+    import synth.gpu as sg
+    m = synth.Manifest("f8", [synth.Tensor("a", (300, 512)), synth.Tensor("n", (64,), synth.KIND_NORM),
+                              synth.Tensor("b", (70_000,)), synth.Tensor("c", (64, 40000)), synth.Tensor("z", (0,)),
+                              synth.Tensor("t", (33,))])
+    mask = synth.MASK_R if escape else synth.MASK_U
+    olds, news = synth.generate(m, seed=51, rho=0.03, mask=mask, dtype=synth.DTYPE_FP8)
+    _, ov = sg.arena(m, DEV, dtype=torch.uint8)
+    _, nv = sg.arena(m, DEV, dtype=torch.uint8)
+    sg.fill_old(ov, m, 51, dtype=synth.DTYPE_FP8)
+    sg.fill_new(ov, nv, m, 51, 0.03, mask)
+    h8 = lambda x: x.cpu().numpy().reshape(-1)  # noqa: E731
+    assert all((h8(v) == o).all() for v, o in zip(ov, olds))
+    assert all((h8(v) == n).all() for v, n in zip(nv, news))
+    if route:
+        news[0] = olds[0] ^ np.uint8(1)
+        nv[0].copy_(torch.from_numpy(news[0]))
+    ref = oracle.sync_pack(olds, news, codec=codec, limit=32 << 10, crc=crc, route=route, escape=escape,
+                           dtype=oracle.DTYPE_FP8)
+    snd = ss.SparseSyncSender(ov, nv, bucket_limit=32 << 10, codec=codec, crc=crc, route=route, escape=escape,
+                              dtype=ss.SYNC_DTYPE_FP8, max_changed=sum(o.size for o in olds))
+    bl = snd.sync(fused=fused)
+    got = [snd.bucket(b).cpu().numpy().tobytes() for b in range(len(bl))]
+    assert got == [ref.bucket(b) for b in range(ref.n_buckets)]
+    R = [torch.from_numpy(o.copy()).to(DEV) for o in olds]
+    rcv = ss.SparseSyncReceiver(R, bucket_limit=32 << 10, codec=codec, crc=crc, dtype=ss.SYNC_DTYPE_FP8)
+    rcv.apply_many([snd.bucket(b) for b in range(len(bl))])
+    snd.commit()
+    torch.cuda.synchronize()
+    snd.check()
+    rcv.check()
+    assert all((h8(r) == n).all() for r, n in zip(R, news))
+    assert all((h8(o) == n).all() for o, n in zip(ov, news))
+
+
 def test_delta16_abs32_boundary():
     # gap of exactly 32767 stays DELTA16, 32768 forces ABS32 (P:360, DESIGN C4)
     n = 70_000
