@@ -79,7 +79,7 @@ def test_host_side_argument_errors(lib):
     assert lib.sync_workspace_size(ctypes.byref(m), ctypes.byref(c), ctypes.byref(need)) == ss.SYNC_ERR_ARG
     c.bucket_limit = 1 << 20
     for dt, want in ((0, ss.SYNC_OK), (ss.SYNC_DTYPE_BF16, ss.SYNC_OK), (ss.SYNC_DTYPE_FP16, ss.SYNC_OK),
-                     (3, ss.SYNC_ERR_DTYPE)):
+                     (ss.SYNC_DTYPE_FP8, ss.SYNC_OK), (4, ss.SYNC_ERR_DTYPE)):
         c.dtype = dt
         assert lib.sync_workspace_size(ctypes.byref(m), ctypes.byref(c), ctypes.byref(need)) == want
 
