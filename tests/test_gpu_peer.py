@@ -98,3 +98,82 @@ def test_peer_ring_world2(mode, groups):
         res[r] = ok
     assert res == {0: True, 1: True}
     assert all(p.exitcode == 0 for p in ps)
+
+
+def _worker_fanout(rank, world, port, q):
+    """ranks 0, 1: Trainers of shards 0, 1 of one model (2 groups each); ranks 2, 3: full-replica Rollouts
+    (fanout). Every process on cuda:(rank % device count)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", rank % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        import synth.gpu as sg
+        from paper_2605_07330_b200 import transport
+        from paper_2605_07330_b200.sync import GroupedReceiver, GroupedSender
+        m = synth.Manifest("m", [synth.Tensor("a", (512, 700)), synth.Tensor("n", (64,), synth.KIND_NORM),
+                                 synth.Tensor("b", (300_000,)), synth.Tensor("c", (96, 1000)),
+                                 synth.Tensor("d", (20_000,))])
+        shards = transport.shard_ranges(m.numel, 2)
+        ok = True
+        if rank < 2:
+            lo, hi = shards[rank]
+            ms = m.slice(lo, hi)
+            X, Xv = sg.arena(ms, dev)
+            Y, Yv = sg.arena(ms, dev)
+            sg.fill_old(Xv, ms, 7, tid0=lo)
+            sg.fill_new(Xv, Yv, ms, 7, 0.03, tid0=lo)
+            snd = GroupedSender(Xv, Yv, groups=2, bucket_limit=32 << 10)
+            link = transport.PeerLink(rank, world, dev, [2, 3], [])
+            for step in range(3):
+                for g, p in enumerate(snd.parts):
+                    p.ctx.sync_extract_batched(p.old_ptrs, p.new_ptrs, p.I, p.V, p.counts)
+                    link.fence(g)
+                    blist = p.compress_pack()
+                    link.send(p.buckets, blist, tag=g)
+                snd.commit(mode="swap")
+                X, Y = Y, X
+            for g in range(2):
+                link.fence(g)
+            torch.cuda.synchronize()
+            both = [None] * world
+            dist.all_gather_object(both, X.cpu().numpy().tobytes())
+        else:
+            R, Rv = sg.arena(m, dev)
+            sg.fill_old(Rv, m, 7)
+            rcvs = {t: GroupedReceiver(Rv[lo:hi], groups=2, bucket_limit=32 << 10) for t, (lo, hi) in enumerate(shards)}
+            link = transport.PeerLink(rank, world, dev, [], [0, 1])
+            for step in range(3):
+                for g in range(2):
+                    link.receive({t: rcvs[t].parts[g].apply_many for t in rcvs}, tag=g)
+            torch.cuda.synchronize()
+            ok = all(p.ctx.sync_status() == 0 for r in rcvs.values() for p in r.parts)
+            both = [None] * world
+            dist.all_gather_object(both, None)
+            got = R.cpu().numpy().tobytes()
+            ok = ok and got == both[0] + both[1]    # the replica = the two Trainers' committed shards
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_fanout_world4():
+    """Send-only / receive-only PeerLink roles: 2 sharded Trainers fan out to 2 full replicas (3 syncs)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_fanout, args=(r, 4, port, q)) for r in range(4)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(300)
+    res = dict(q.get(timeout=30) for _ in range(4))
+    assert res == {r: True for r in range(4)}
+    assert all(p.exitcode == 0 for p in ps)
