@@ -321,7 +321,7 @@ int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const u
   if (x->d.T == 0) return SYNC_OK;
   CK(cudaMemsetAsync(x->misc, 0, 4, s));
   CK(cudaMemsetAsync(d_counts, 0, 8ull * x->d.T, s));
-  if (x->plan.dtype == SYNC_DTYPE_FP8) {   // 8-bit elements: diff into a bitmap, then compact
+  if (x->plan.dtype == SYNC_DTYPE_FP8 && getenv("SS_FP8_BITMAP")) {   // alternative: diff bitmap + compaction
     TrackArgs a = track_args(x, reinterpret_cast<u32*>(x->ws + x->L.bitmap8));
     a.counts = d_counts;
     a.I = d_I;
@@ -335,7 +335,8 @@ int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const u
   launch_extract_batched(d_old_ptrs, d_new_ptrs, reinterpret_cast<const u64*>(x->ws + x->L.tile_prefix),
                          reinterpret_cast<const u32*>(x->ws + x->L.tile_tensor), x->plan.numel, x->d.T, x->d.n_tiles, d_I, d_V, x->cfg.max_changed, d_counts,
                          reinterpret_cast<u64*>(x->ws + x->L.tile_state),
-                         reinterpret_cast<u32*>(x->ws + x->L.stage_ring), x->misc + 1, s);
+                         reinterpret_cast<u32*>(x->ws + x->L.stage_ring), x->misc + 1, s,
+                         x->plan.dtype == SYNC_DTYPE_FP8 ? 1 : 2);
   CK(cudaGetLastError());
   return SYNC_OK;
 }

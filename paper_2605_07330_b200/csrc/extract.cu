@@ -157,13 +157,42 @@ __device__ __forceinline__ u32 change_mask(const uint4& o, const uint4& n) {
          ((x3 & 0xFFFFu) ? 64u : 0u) | ((x3 >> 16) ? 128u : 0u);
 }
 
+// 8-bit elements (FP8, f2): 16 bytes per vector
+__device__ __forceinline__ uint4 load16_direct8(const uint8_t* p, u64 e, u64 n) {
+  u32 w[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (e + k < n) w[k >> 2] |= (u32)p[e + k] << (8 * (k & 3));
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ u32 change_mask8(const uint4& o, const uint4& n) {
+  const u32 x[4] = {o.x ^ n.x, o.y ^ n.y, o.z ^ n.z, o.w ^ n.w};
+  u32 m = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) m |= (((x[j] >> (8 * b)) & 0xFFu) ? 1u : 0u) << (4 * j + b);
+  return m;
+}
+
+__device__ __forceinline__ u16 lane8(const uint4& v, int b) {
+  const u32 w[4] = {v.x, v.y, v.z, v.w};
+  return (u16)((w[b >> 2] >> (8 * (b & 3))) & 0xFFu);
+}
+
 __device__ __forceinline__ u16 lane16(const uint4& v, int b) {
   const u64 lo64 = v.x | ((u64)v.y << 32), hi64 = v.z | ((u64)v.w << 32);
   return (u16)(((b < 4) ? lo64 : hi64) >> ((b & 3) * 16));
 }
 
-template <bool kSingle, int kStages, int kWriters>
+// kB = element bytes: 2 (BF16 / FP16) or 1 (FP8, f2). A 16-byte vector holds kEPV = 16 / kB elements; a
+// sub-tile (one stage: 16 KB of old + 16 KB of new) holds kSubE = 256 threads x 4 vectors x kEPV elements;
+// a tile is always kTile = 32768 elements (local indices fit 16 bits; the tile tables are shared).
+template <bool kSingle, int kStages, int kWriters, int kB = 2>
 __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) {
+  constexpr u32 kEPV = 16 / kB;
+  constexpr u64 kSubE = (u64)kXThreads * kXVec * kEPV;
   extern __shared__ __align__(128) u8 smem[];
   u8* data = smem;
   u64* full = reinterpret_cast<u64*>(smem + kStages * kStageBytes);
@@ -233,7 +262,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
         j.t = t;
         const u64 rem = n - j.base;
         const u64 nv = rem < kTile ? rem : kTile;
-        j.n_sub = (u32)((nv + kSub - 1) / kSub);
+        j.n_sub = (u32)((nv + kSubE - 1) / kSubE);
         jobs[q] = j;
         mbar_arrive(&qfull[q]);
       }
@@ -270,10 +299,10 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
             info[s] = si;
             mbar_arrive(&full[s]);
           } else {
-            const u64 sb = j.base + (u64)sub * kSub;
+            const u64 sb = j.base + (u64)sub * kSubE;
             const u64 rem = j.n - sb;
-            const u32 n_valid = (u32)(rem < kSub ? rem : kSub);
-            const u32 bulk = aligned ? (n_valid & ~7u) : 0u;
+            const u32 n_valid = (u32)(rem < kSubE ? rem : kSubE);
+            const u32 bulk = aligned ? (n_valid & ~(kEPV - 1)) : 0u;   // whole 16-byte vectors
             si.tile = j.tile;
             si.base = sb;
             si.po = j.po;
@@ -286,9 +315,11 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
             info[s] = si;
             u8* dst = data + (size_t)s * kStageBytes;
             if (bulk) {
-              mbar_arrive_tx(&full[s], 4u * bulk);
-              bulk_g2s(dst, j.po + sb, 2u * bulk, &full[s], pol);
-              bulk_g2s(dst + kSub * 2, j.pn + sb, 2u * bulk, &full[s], pol);
+              const u8* po8 = reinterpret_cast<const u8*>(j.po) + kB * sb;
+              const u8* pn8 = reinterpret_cast<const u8*>(j.pn) + kB * sb;
+              mbar_arrive_tx(&full[s], 2u * kB * bulk);
+              bulk_g2s(dst, po8, kB * bulk, &full[s], pol);
+              bulk_g2s(dst + kStageBytes / 2, pn8, kB * bulk, &full[s], pol);
             } else {
               mbar_arrive(&full[s]);
             }
@@ -374,11 +405,19 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       } else {
         // slow path (tile denser than a slot): re-read it from global
         u64 run = prefix;
-        for (u64 e0 = m.tile_base; e0 < m.tile_end; e0 += 256) {
-          const u64 e = e0 + lane * 8;
-          const uint4 vo = load8_direct(m.po, e, m.tile_end);
-          const uint4 vd = load8_direct(m.pn, e, m.tile_end);
-          u32 mk = change_mask(vo, vd);
+        for (u64 e0 = m.tile_base; e0 < m.tile_end; e0 += 32 * kEPV) {
+          const u64 e = e0 + lane * kEPV;
+          uint4 vo, vd;
+          u32 mk;
+          if (kB == 1) {
+            vo = load16_direct8(reinterpret_cast<const u8*>(m.po), e, m.tile_end);
+            vd = load16_direct8(reinterpret_cast<const u8*>(m.pn), e, m.tile_end);
+            mk = change_mask8(vo, vd);
+          } else {
+            vo = load8_direct(m.po, e, m.tile_end);
+            vd = load8_direct(m.pn, e, m.tile_end);
+            mk = change_mask(vo, vd);
+          }
           const u32 c = __popc(mk);
           const u32 inc = warp_incl_scan(c);
           u64 pos = run + inc - c;
@@ -387,7 +426,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
             mk &= mk - 1;
             if (pos < a.cap) {
               a.I[pos] = (u32)(e + bb);
-              a.V[pos] = lane16(vd, bb);
+              a.V[pos] = kB == 1 ? lane8(vd, bb) : lane16(vd, bb);
             } else {
               latch(a.status, SYNC_ERR_CAPACITY);
             }
@@ -441,32 +480,39 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       overflow = false;
     }
     const uint4* so = reinterpret_cast<const uint4*>(data + (size_t)s * kStageBytes);
-    const uint4* sn = reinterpret_cast<const uint4*>(data + (size_t)s * kStageBytes + kSub * 2);
-    const u16* sn16 = reinterpret_cast<const u16*>(data + (size_t)s * kStageBytes + kSub * 2);
+    const uint4* sn = reinterpret_cast<const uint4*>(data + (size_t)s * kStageBytes + kStageBytes / 2);
+    const u16* sn16 = reinterpret_cast<const u16*>(data + (size_t)s * kStageBytes + kStageBytes / 2);
+    const u8* sn8 = data + (size_t)s * kStageBytes + kStageBytes / 2;
 
     // Thread t owns the 4 consecutive vectors 4t..4t+3 (elements 32t..32t+31), so
     // thread order == index order and one u32 scan places every change. Load u
     // reads vector 4t + ((t/2 + u) & 3): the 8 threads of each LDS.128 phase hit
     // 8 distinct 16-byte columns (conflict-free).
-    u32 masks = 0;  // bit 8j + b <-> element 32t + 8j + b
+    // bit kEPV*j + b <-> element 4*kEPV*t + kEPV*j + b (32 elements per thread for 16-bit, 64 for 8-bit)
+    u64 masks = 0;
     const u32 rot = (tid >> 1) & 3;
 #pragma unroll
     for (int u = 0; u < kXVec; ++u) {
       const u32 j = (rot + (u32)u) & 3;
       const u32 v = 4 * tid + j;  // vector index within the sub-tile
       uint4 vo, vd;
-      if (v * 8 + 8 <= si.bulk) {
+      if (v * kEPV + kEPV <= si.bulk) {
         vo = so[v];
         vd = sn[v];
-      } else if (v * 8 < si.n_valid) {
-        vo = load8_direct(si.po, si.base + v * 8, si.base + si.n_valid);
-        vd = load8_direct(si.pn, si.base + v * 8, si.base + si.n_valid);
+      } else if (v * kEPV < si.n_valid) {
+        if (kB == 1) {
+          vo = load16_direct8(reinterpret_cast<const u8*>(si.po), si.base + v * kEPV, si.base + si.n_valid);
+          vd = load16_direct8(reinterpret_cast<const u8*>(si.pn), si.base + v * kEPV, si.base + si.n_valid);
+        } else {
+          vo = load8_direct(si.po, si.base + v * 8, si.base + si.n_valid);
+          vd = load8_direct(si.pn, si.base + v * 8, si.base + si.n_valid);
+        }
       } else {
         vo = vd = make_uint4(0, 0, 0, 0);
       }
-      masks |= change_mask(vo, vd) << (8 * j);
+      masks |= (u64)(kB == 1 ? change_mask8(vo, vd) : change_mask(vo, vd)) << (kEPV * j);
     }
-    const u32 cnt = __popc(masks);
+    const u32 cnt = __popcll(masks);
     // block exclusive scan (one barrier; s_wsum double-buffered by sub-tile parity)
     const u32 incl = warp_incl_scan(cnt);
     u32* wsum = reinterpret_cast<u32*>(s_wsum) + (it & 1) * 8;
@@ -482,14 +528,20 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
     if (!overflow && tile_cnt + st_total <= kSlotCap) {
       u32* stg = ring + b * kSlotCap;
       u32 pos = tile_cnt + wexcl + incl - cnt;
-      const u32 local = (u32)si.sub * (u32)kSub + 32 * tid;
-      u32 mk = masks;
+      constexpr u32 kPerT = 4 * kEPV;   // elements per thread
+      const u32 local = (u32)si.sub * (u32)kSubE + kPerT * tid;
+      u64 mk = masks;
       while (mk) {
-        const int bb = __ffs(mk) - 1;
+        const int bb = __ffsll(mk) - 1;
         mk &= mk - 1;
         u16 val;
-        if (32 * tid + bb + 1 <= si.bulk) val = sn16[32 * tid + bb];
-        else val = si.pn[si.base + 32 * tid + bb];
+        if (kB == 1) {
+          if (kPerT * tid + bb + 1 <= si.bulk) val = sn8[kPerT * tid + bb];
+          else val = reinterpret_cast<const u8*>(si.pn)[si.base + kPerT * tid + bb];
+        } else {
+          if (kPerT * tid + bb + 1 <= si.bulk) val = sn16[kPerT * tid + bb];
+          else val = si.pn[si.base + kPerT * tid + bb];
+        }
         stg[pos++] = (local + bb) | ((u32)val << 16);
       }
     } else {
@@ -506,7 +558,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       publish_count(a.tile_state, si.tile, tile_cnt);
       StagedTile m;
       m.tile = si.tile;
-      m.tile_base = si.base - (u64)si.sub * kSub;
+      m.tile_base = si.base - (u64)si.sub * kSubE;
       m.tile_end = si.base + si.n_valid;
       m.po = si.po;
       m.pn = si.pn;
@@ -533,18 +585,18 @@ static size_t extract_smem() {
          kXQueue * sizeof(TileJob) + kSlots * sizeof(StagedTile) + 16 * 8;
 }
 
-template <bool kSingle, int kStages, int kWriters>
+template <bool kSingle, int kStages, int kWriters, int kB = 2>
 static void launch_k(const ExtractArgs& a, cudaStream_t s) {
   constexpr int kXBlock = xblock(kWriters);
   static int grid_cap = 0;
   const size_t sm = extract_smem<kStages>();
   if (!grid_cap) {
-    cudaFuncSetAttribute(k_extract<kSingle, kStages, kWriters>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_extract<kSingle, kStages, kWriters, kB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
     int dev = 0, n_sm = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_extract<kSingle, kStages, kWriters>, kXBlock, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_extract<kSingle, kStages, kWriters, kB>, kXBlock, sm);
     grid_cap = n_sm * (per > 0 ? per : 1);
     if (grid_cap > (int)kMaxExtractCtas) grid_cap = (int)kMaxExtractCtas;
   }
@@ -558,7 +610,7 @@ static void launch_k(const ExtractArgs& a, cudaStream_t s) {
     cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), s);
     b.prof = prof;
   }
-  k_extract<kSingle, kStages, kWriters><<<(unsigned)grid, kXBlock, sm, s>>>(b);
+  k_extract<kSingle, kStages, kWriters, kB><<<(unsigned)grid, kXBlock, sm, s>>>(b);
   count_launch();
   if (want_prof) {
     unsigned long long h[16];
@@ -597,7 +649,8 @@ static void launch(const ExtractArgs& a, cudaStream_t s) {
 
 void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, const u64* tile_prefix,
                             const u32* tile_tensor, const u64* numel, u32 n_tensors, u64 n_tiles, u32* I, u16* V,
-                            u64 cap, u64* counts, u64* tile_state, u32* stage_ring, u32* status, cudaStream_t s) {
+                            u64 cap, u64* counts, u64* tile_state, u32* stage_ring, u32* status, cudaStream_t s,
+                            int elem_bytes) {
   if (n_tiles == 0) return;
   ExtractArgs a{};
   a.old_ptrs = d_old;
@@ -614,7 +667,8 @@ void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, co
   a.tile_state = tile_state;
   a.stage_ring = stage_ring;
   a.status = status;
-  launch<false>(a, s);
+  if (elem_bytes == 1) launch_k<false, 3, 3, 1>(a, s);   // FP8: the same pipeline on 8-bit elements
+  else launch<false>(a, s);
 }
 
 void launch_extract_single(const u16* d_old, const u16* d_new, u64 n, u32* I, u16* V, u64 cap, u64* count,

@@ -51,7 +51,7 @@ constexpr uint32_t kModeDelta16E = 3;  // record idx_mode of an escape-coded DEL
 void launch_extract_batched(const uint16_t* const* d_old, const uint16_t* const* d_new, const uint64_t* tile_prefix,
                             const uint32_t* tile_tensor, const uint64_t* numel, uint32_t n_tensors, uint64_t n_tiles, uint32_t* I, uint16_t* V,
                             uint64_t cap, uint64_t* counts, uint64_t* tile_state, uint32_t* stage_ring,
-                            uint32_t* status, cudaStream_t s);
+                            uint32_t* status, cudaStream_t s, int elem_bytes = 2);   // 1: FP8
 void launch_extract_single(const uint16_t* d_old, const uint16_t* d_new, uint64_t n, uint32_t* I, uint16_t* V,
                            uint64_t cap, uint64_t* count, uint64_t* tile_state, uint32_t* stage_ring,
                            uint32_t* status, cudaStream_t s);
