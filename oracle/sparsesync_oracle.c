@@ -14,8 +14,9 @@
  * Pins (tests/test_oracle_*.py): SPEC examples, hand-derived rANS golden
  * vectors (tests/golden/), CRC-32 check value and zlib, round-trip identities,
  * exact Eq. (1) payload identity, entropy bounds.
- * Parity status: extract/apply/index codec/bucketing/cast-tracking pinned; the exact rANS
- * byte string is pinned only by FORMAT + hand golden vectors
+ * Parity status: extract/apply, index codec (incl. f4 escapes), bucketing, f1 cast
+ * tracking, f3 FULL routing and the f2 FP16/FP8 tags and layouts are pinned; the exact
+ * rANS byte string is pinned only by FORMAT + hand golden vectors
  * (the paper fixes no coder).
  */
 #include <stdint.h>
