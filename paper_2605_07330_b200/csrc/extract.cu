@@ -26,6 +26,7 @@
 // All CTAs are resident and each counts its tiles in increasing order, so
 // every count a writer waits for is eventually published.
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -489,7 +490,8 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
     // reads vector 4t + ((t/2 + u) & 3): the 8 threads of each LDS.128 phase hit
     // 8 distinct 16-byte columns (conflict-free).
     // bit kEPV*j + b <-> element 4*kEPV*t + kEPV*j + b (32 elements per thread for 16-bit, 64 for 8-bit)
-    u64 masks = 0;
+    using MaskT = typename std::conditional<kB == 1, u64, u32>::type;
+    MaskT masks = 0;
     const u32 rot = (tid >> 1) & 3;
 #pragma unroll
     for (int u = 0; u < kXVec; ++u) {
@@ -510,9 +512,9 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       } else {
         vo = vd = make_uint4(0, 0, 0, 0);
       }
-      masks |= (u64)(kB == 1 ? change_mask8(vo, vd) : change_mask(vo, vd)) << (kEPV * j);
+      masks |= (MaskT)(kB == 1 ? change_mask8(vo, vd) : change_mask(vo, vd)) << (kEPV * j);
     }
-    const u32 cnt = __popcll(masks);
+    const u32 cnt = kB == 1 ? (u32)__popcll((u64)masks) : (u32)__popc((u32)masks);
     // block exclusive scan (one barrier; s_wsum double-buffered by sub-tile parity)
     const u32 incl = warp_incl_scan(cnt);
     u32* wsum = reinterpret_cast<u32*>(s_wsum) + (it & 1) * 8;
@@ -530,9 +532,9 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       u32 pos = tile_cnt + wexcl + incl - cnt;
       constexpr u32 kPerT = 4 * kEPV;   // elements per thread
       const u32 local = (u32)si.sub * (u32)kSubE + kPerT * tid;
-      u64 mk = masks;
+      MaskT mk = masks;
       while (mk) {
-        const int bb = __ffsll(mk) - 1;
+        const int bb = (kB == 1 ? __ffsll((long long)mk) : __ffs((int)mk)) - 1;
         mk &= mk - 1;
         u16 val;
         if (kB == 1) {
