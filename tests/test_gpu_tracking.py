@@ -153,3 +153,14 @@ def test_empty_interval_and_capacity():
     snd.check()
     assert int(snd.counts.sum().item()) == want and len(blist) >= 1
     assert snd.bitmap.count_nonzero().item() == 0
+
+
+def test_tracking_is_bf16_only():
+    """Alg. 1's cast is round_BF16: an FP16 / FP8 context refuses the tracking calls (SYNC_ERR_DTYPE)."""
+    ms = masters(4, sizes=[1000, 64])
+    W0 = [oracle.bf16_rne(m) for m in ms]
+    for dt in (ss.SYNC_DTYPE_FP16, ss.SYNC_DTYPE_FP8):
+        with pytest.raises(ss.SyncError) as e:
+            snd, _, _ = make_sender(ms, W0, dtype=dt)
+            snd.cast_track()
+        assert e.value.code == ss.SYNC_ERR_DTYPE
