@@ -147,23 +147,6 @@ struct WarpModel {
   uint2 fr[257];
 };
 
-// Histogram of hi bytes hi(p) for p < n into m.hist (warp-aggregated smem atomics).
-template <typename HiAt>
-__device__ __forceinline__ void warp_histogram(WarpModel& m, u32 n, HiAt hi_at) {
-  const u32 lane = lane_id();
-  for (u32 s = lane; s < 256; s += 32) m.hist[s] = 0;
-  __syncwarp();
-  for (u32 base = 0; base < n; base += 32) {
-    u32 p = base + lane;
-    bool act = p < n;
-    u32 s = act ? hi_at(p) : 0x100u + lane;  // inactive lanes never match an active symbol
-    u32 peers = __match_any_sync(0xffffffffu, s);
-    if (act && (__ffs(peers) - 1) == lane) atomicAdd(&m.hist[s], __popc(peers));
-  }
-  __syncwarp();
-}
-
-// Frequency normalisation to 4096 (DESIGN §3.3 steps 1-3), warp-parallel;
 // fills freq, cum, rcp; returns nsym.
 __device__ __forceinline__ u32 warp_normalize(WarpModel& m, u32 n) {
   const u32 lane = lane_id();
