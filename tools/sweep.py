@@ -78,6 +78,10 @@ SETS = {
         ("one_r01_crc", 1, ["--crc"]),
         ("one_r01_route", 1, ["--route"]),
         ("one_4b_cast", 1, ["--workload", "qwen3-4b", "--tracking", "cast"]),
+        ("one_r01_fp16", 1, ["--dtype", "fp16"]),
+        ("one_r01_fp8", 1, ["--dtype", "fp8"]),
+        ("one_r10_fp8", 1, ["--dtype", "fp8", "--rho", "0.1"]),
+        ("one_r01_R_escape", 1, ["--mask", "R", "--escape"]),
     ],
 }
 
