@@ -135,6 +135,7 @@ struct sync_ctx {
   Dims d;
   sync_config cfg;
   std::vector<u64> numel, tile_prefix;
+  u64 total_elems = 0;   // sum of numel (decode variant choice)
   std::vector<u32> tile_tensor;
   std::vector<u64> bm_off;   // f1: bitmap word offset of each tensor (ceil(numel / 32) words each)
   u8* ws;
@@ -179,6 +180,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   x->ws = static_cast<u8*>(d_workspace);
   x->L = L;
   x->numel.assign(m->numel, m->numel + d.T);
+  for (u64 n : x->numel) x->total_elems += n;
   x->tile_prefix.resize(d.T + 1);
   u64 acc = 0;
   for (u32 t = 0; t < d.T; ++t) {
@@ -620,7 +622,7 @@ int sync_decompress(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, uint32
   u32* nv = reinterpret_cast<u32*>(x->ws + x->L.nviews);
   launch_unpack(d_bucket, bytes, x->d.T, x->plan.numel, views, x->d.T, nv, x->plan.status, x->plan.dtype, s);
   launch_decode(&d_bucket, &bytes, 1, x->d.T, x->plan.numel, nullptr, views, d_I, d_V, d_cap, x->plan.status, bad,
-                x->plan.dtype, x->grid, s);
+                x->plan.dtype, x->grid, decode_is_dense(&bytes, 1, x->total_elems), s);
   CK(cudaGetLastError());
   return SYNC_OK;
 }
@@ -634,7 +636,7 @@ int sync_decompress_apply(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, 
   int st = maybe_crc_check(x, &d_bucket, &bytes, 1, s, &bad);
   if (st) return st;
   launch_decode(&d_bucket, &bytes, 1, x->d.T, x->plan.numel, d_weight_ptrs, nullptr, nullptr, nullptr, 0,
-                x->plan.status, bad, x->plan.dtype, x->grid, s);
+                x->plan.status, bad, x->plan.dtype, x->grid, decode_is_dense(&bytes, 1, x->total_elems), s);
   CK(cudaGetLastError());
   return SYNC_OK;
 }
@@ -645,13 +647,14 @@ int sync_decompress_apply_batched(sync_ctx* x, const uint8_t* const* h_buckets, 
   for (u32 i = 0; i < n_buckets; ++i)
     if (!h_buckets[i] || !aligned16(h_buckets[i])) return h_buckets[i] ? SYNC_ERR_ALIGNMENT : SYNC_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
+  const bool dense = decode_is_dense(h_bytes, n_buckets, x->total_elems);
   for (u32 b0 = 0; b0 < n_buckets; b0 += kCrcFlagSlots) {
     const u32 n = n_buckets - b0 < kCrcFlagSlots ? n_buckets - b0 : kCrcFlagSlots;
     const u32* bad;
     int st = maybe_crc_check(x, h_buckets + b0, h_bytes + b0, n, s, &bad);
     if (st) return st;
     launch_decode(h_buckets + b0, h_bytes + b0, n, x->d.T, x->plan.numel, d_weight_ptrs, nullptr, nullptr,
-                  nullptr, 0, x->plan.status, bad, x->plan.dtype, x->grid, s);
+                  nullptr, 0, x->plan.status, bad, x->plan.dtype, x->grid, dense, s);
   }
   CK(cudaGetLastError());
   return SYNC_OK;

@@ -11,6 +11,8 @@
 // V = hi << 8 | lo is scattered straight into the weights (APPLY) or written
 // out as (I, V) (EMIT, the debug path). Every chunk checks the end states
 // (all lanes back at 2^16) and that every word was consumed.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -164,8 +166,8 @@ struct DecodeModel {
 
 // One launch decodes up to kDecodeBatch buckets (the chunks of all of them form one grid-stride range), so
 // many small buckets do not each pay a launch that fills a fraction of the GPU.
-template <bool kApply>
-__global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, const u64* numel,
+template <bool kApply, int kMinB, int kPF>
+__global__ void __launch_bounds__(256, kMinB) k_decode(DecodeBatch bb, u32 n_tensors, const u64* numel,
                                                u16* const* weights, const sync_record_view* views, u32* I_out,
                                                u16* V_out, u64 out_cap, u32* status, const u32* crc_bad,
                                                u32 dtype) {
@@ -379,7 +381,6 @@ __global__ void __launch_bounds__(256) k_decode(DecodeBatch bb, u32 n_tensors, c
     bool range_bad = false, word_bad = false;
     // software pipeline: the lo bytes and the index words (DELTA16 delta or
     // ABS32 index) of the next 8 steps are loaded while the current 8 decode
-    constexpr int kPF = 8;
     u32 nlb[kPF], ndd[kPF];
     auto load_block = [&](u32 g0, u32* lb_, u32* dd_) {
 #pragma unroll
@@ -517,9 +518,21 @@ void launch_unpack(const u8* bucket, u64 bytes, u32 n_tensors, const u64* numel,
   count_launch();
 }
 
+template <int kMinB, int kPF>
+static void run_decode(const DecodeBatch& bb, u32 n_tensors, const u64* numel, u16* const* weights,
+                       const sync_record_view* views, u32* I_out, u16* V_out, u64 out_cap, u32* status,
+                       const u32* bad, u32 dtype, int grid, cudaStream_t s) {
+  if (weights)
+    k_decode<true, kMinB, kPF><<<grid, 256, 0, s>>>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0,
+                                                    status, bad, dtype);
+  else
+    k_decode<false, kMinB, kPF><<<grid, 256, 0, s>>>(bb, n_tensors, numel, nullptr, views, I_out, V_out, out_cap,
+                                                     status, bad, dtype);
+}
+
 void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u32 n_tensors, const u64* numel,
                    u16* const* weights, const sync_record_view* views, u32* I_out, u16* V_out, u64 out_cap,
-                   u32* status, const u32* crc_bad, u32 dtype, int grid, cudaStream_t s) {
+                   u32* status, const u32* crc_bad, u32 dtype, int grid, bool dense, cudaStream_t s) {
   for (u32 b0 = 0; b0 < n_buckets; b0 += kDecodeBatch) {
     DecodeBatch bb;
     bb.n = n_buckets - b0 < kDecodeBatch ? n_buckets - b0 : kDecodeBatch;
@@ -528,12 +541,12 @@ void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u3
       bb.bytes[i] = bytes[b0 + i];
     }
     const u32* bad = crc_bad ? crc_bad + b0 : nullptr;
-    if (weights)
-      k_decode<true><<<grid, 256, 0, s>>>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status, bad,
-                                          dtype);
+    // dense syncs are decode-bound: the 3-CTA / 4-deep variant keeps more chunks in flight; sparse ones are
+    // scatter-bound and keep the 8-deep load pipeline
+    if (dense)
+      run_decode<3, 4>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad, dtype, grid, s);
     else
-      k_decode<false><<<grid, 256, 0, s>>>(bb, n_tensors, numel, nullptr, views, I_out, V_out, out_cap, status, bad,
-                                           dtype);
+      run_decode<1, 8>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad, dtype, grid, s);
     count_launch();
   }
 }

@@ -100,7 +100,13 @@ void launch_unpack(const uint8_t* bucket, uint64_t bytes, uint32_t n_tensors, co
 void launch_decode(const uint8_t* const* buckets, const uint64_t* bytes, uint32_t n_buckets, uint32_t n_tensors,
                    const uint64_t* numel, uint16_t* const* weights, const sync_record_view* views, uint32_t* I_out,
                    uint16_t* V_out, uint64_t out_cap, uint32_t* status, const uint32_t* crc_bad, uint32_t dtype,
-                   int grid, cudaStream_t s);
+                   int grid, bool dense, cudaStream_t s);
+// a decode call is "dense" when its buckets carry >= 0.1 byte per model element (rho >~ 3%)
+inline bool decode_is_dense(const uint64_t* bytes, uint32_t n, uint64_t model_elems) {
+  uint64_t t = 0;
+  for (uint32_t i = 0; i < n; ++i) t += bytes[i];
+  return t * 10 >= model_elems && t > 0;
+}
 
 // track.cu (f1 cast-fused tracking, Alg. 1)
 struct TrackArgs {

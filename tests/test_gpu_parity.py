@@ -387,6 +387,29 @@ def test_batched_decoder_applies_oracle_buckets(crc):
         assert (host16(w) == n).all()
 
 
+@pytest.mark.parametrize("rho", [0.004, 0.3])
+def test_decoder_variants_apply_oracle_buckets(rho):
+    """Both decode launch variants (chosen per call from payload bytes per model element, so one
+    call over all buckets of a dense sync takes the high-occupancy one and a call per small bucket the other)
+    apply the oracle's buckets bit-exactly."""
+    m = mixed_manifest()
+    olds, news = synth.generate(m, seed=21, rho=rho)
+    ref = oracle.sync_pack(olds, news, limit=16 << 10)
+    dev = [torch.from_numpy(np.frombuffer(ref.bucket(b), np.uint8).copy()).to(DEV) for b in range(ref.n_buckets)]
+    for batched in (True, False):
+        W = [to_dev(o) for o in olds]
+        rcv = ss.SparseSyncReceiver(W, bucket_limit=16 << 10)
+        if batched:
+            rcv.apply_many(dev)
+        else:
+            for bk in dev:
+                rcv.apply(bk)
+        torch.cuda.synchronize()
+        rcv.check()
+        for w, n in zip(W, news):
+            assert (host16(w) == n).all()
+
+
 def test_batched_decoder_isolates_a_bad_bucket():
     """With CRC on, a corrupted bucket inside a batch is rejected (SYNC_ERR_CRC, none of its records applied)
     while the other buckets of the same launch are applied."""
