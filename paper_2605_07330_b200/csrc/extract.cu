@@ -533,6 +533,18 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       constexpr u32 kPerT = 4 * kEPV;   // elements per thread
       const u32 local = (u32)si.sub * (u32)kSubE + kPerT * tid;
       MaskT mk = masks;
+      if (kB == 2 && kPerT * tid + kPerT <= si.bulk) {
+        // all 32 of this thread's elements are in the stage: values from shared memory, a running
+        // ring pointer, (local | value << 16) in one byte permute (local < 2^15 within a tile)
+        const u16* vrow = sn16 + kPerT * tid;
+        u32* sp = stg + pos;
+        while (mk) {
+          const int bb = __ffs((int)mk) - 1;
+          mk &= mk - 1;
+          *sp++ = __byte_perm(local + (u32)bb, (u32)vrow[bb], 0x5410);
+        }
+        mk = 0;
+      }
       while (mk) {
         const int bb = (kB == 1 ? __ffsll((long long)mk) : __ffs((int)mk)) - 1;
         mk &= mk - 1;
