@@ -167,14 +167,16 @@ __device__ __forceinline__ uint4 load16_direct8(const uint8_t* p, u64 e, u64 n) 
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// bit 4j + b <-> byte b of word j differs. Per word: the high bit of every nonzero byte of x
+// ((x & 0x7F..) + 0x7F.. sets it for nonzero low 7 bits, | x for the top bit), then one multiply
+// gathers bits 7, 15, 23, 31 into bits 28..31 (the partial products land on distinct bits: no carries).
+__device__ __forceinline__ u32 byte_nz4(u32 x) {
+  const u32 t = (((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+  return (t * 0x00204081u) >> 28;
+}
 __device__ __forceinline__ u32 change_mask8(const uint4& o, const uint4& n) {
-  const u32 x[4] = {o.x ^ n.x, o.y ^ n.y, o.z ^ n.z, o.w ^ n.w};
-  u32 m = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) m |= (((x[j] >> (8 * b)) & 0xFFu) ? 1u : 0u) << (4 * j + b);
-  return m;
+  return byte_nz4(o.x ^ n.x) | (byte_nz4(o.y ^ n.y) << 4) | (byte_nz4(o.z ^ n.z) << 8) |
+         (byte_nz4(o.w ^ n.w) << 12);
 }
 
 __device__ __forceinline__ u16 lane8(const uint4& v, int b) {
@@ -533,17 +535,16 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       constexpr u32 kPerT = 4 * kEPV;   // elements per thread
       const u32 local = (u32)si.sub * (u32)kSubE + kPerT * tid;
       MaskT mk = masks;
-      if (kB == 2 && kPerT * tid + kPerT <= si.bulk) {
-        // all 32 of this thread's elements are in the stage: values from shared memory, a running
+      if (kPerT * tid + kPerT <= si.bulk) {
+        // all of this thread's elements are in the stage: values from shared memory, a running
         // ring pointer, (local | value << 16) in one byte permute (local < 2^15 within a tile)
-        const u16* vrow = sn16 + kPerT * tid;
         u32* sp = stg + pos;
         while (mk) {
-          const int bb = __ffs((int)mk) - 1;
+          const int bb = (kB == 1 ? __ffsll((long long)mk) : __ffs((int)mk)) - 1;
           mk &= mk - 1;
-          *sp++ = __byte_perm(local + (u32)bb, (u32)vrow[bb], 0x5410);
+          const u32 val = kB == 1 ? (u32)sn8[kPerT * tid + bb] : (u32)sn16[kPerT * tid + bb];
+          *sp++ = __byte_perm(local + (u32)bb, val, 0x5410);
         }
-        mk = 0;
       }
       while (mk) {
         const int bb = (kB == 1 ? __ffsll((long long)mk) : __ffs((int)mk)) - 1;
