@@ -98,7 +98,7 @@ __device__ unsigned long long g_cprof[8];  // debug cycle counters (SS_CPROF=1)
 // No hi plane in shared memory: ~32 independent rANS chains per SM (a CTA-per-chunk
 // variant with the hi plane staged in shared memory measured 1.2-1.7x slower).
 constexpr int kWPF = 8;
-__global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
+__global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
   __shared__ WarpModel s_m[8];
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpModel& m = s_m[warp];
@@ -125,11 +125,23 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
     u32 carry = (lane == 0 && p0) ? Ic[-1] : 0u;   // I of the element before the chunk (Δ_0 = I_0 if none)
     carry = __shfl_sync(0xffffffffu, carry, 0);
     u32 hv[kWPF], cur[kWPF], hn[kWPF], cn[kWPF];
+    // the coded byte of V[q] is byte 2q + vb of the V array (vb = 1: the hi byte of a 16-bit element)
+    const u8* Vb = reinterpret_cast<const u8*>(Vc) + (sh ? 1 : 0);
     auto load = [&](u32 b0, u32* h, u32* c) {
+      if (b0 + 32 * kWPF <= nk) {   // whole block inside the chunk: plain loads at constant offsets
+        const u8* vp = Vb + 2 * (b0 + lane);
+        const u32* ip = Ic + b0 + lane;
+#pragma unroll
+        for (int u = 0; u < kWPF; ++u) {
+          h[u] = vp[64 * u];
+          c[u] = ip[32 * u];
+        }
+        return;
+      }
 #pragma unroll
       for (int u = 0; u < kWPF; ++u) {
         const u32 q = b0 + u * 32 + lane;
-        h[u] = q < nk ? (u32)(Vc[q] >> sh) : 0x100u;
+        h[u] = q < nk ? (u32)Vb[2 * q] : 0x100u;
         c[u] = q < nk ? Ic[q] : 0u;
       }
     };
@@ -179,11 +191,17 @@ __global__ void __launch_bounds__(256) k_chunk_stats(Plan p, const u32* I, const
     const uint2* const fr = m.fr;
     u32 nxt[kWPF];
     auto load_block = [&](int top, u32* dst) {  // steps top, top-1, ..., top-7
+      if (top >= kWPF - 1 && (u32)(top + 1) * 32 <= nk) {   // all 8 steps full
+        const u8* vp = Vb + 2 * ((u32)top * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < kWPF; ++u) dst[u] = vp[-64 * u];
+        return;
+      }
 #pragma unroll
       for (int u = 0; u < kWPF; ++u) {
         const int gg = top - u;
         const u32 q = (u32)gg * 32 + lane;
-        dst[u] = (gg >= 0 && q < nk) ? (u32)(Vc[q] >> sh) : 0x100u;
+        dst[u] = (gg >= 0 && q < nk) ? (u32)Vb[2 * q] : 0x100u;
       }
     };
     load_block((int)G - 1, nxt);
