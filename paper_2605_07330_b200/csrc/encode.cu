@@ -21,7 +21,7 @@ __device__ __forceinline__ void zero_bytes(u8* p, u64 n) {
 // One CTA per chunk (16384 values). All threads write the chunk's slices of the
 // index stream and of the lo plane (packed 32-bit stores) and copy the chunk's
 // rANS block (states, model, words) that k_chunk_stats already produced.
-__global__ void __launch_bounds__(kCThreads) k_encode(Plan p, const u32* I, const u16* V, const u64* counts,
+__global__ void __launch_bounds__(kCThreads, 6) k_encode(Plan p, const u32* I, const u16* V, const u64* counts,
                                                      u8* enc) {
   __shared__ u32 s_t;
   const u32 tid = threadIdx.x;
