@@ -18,6 +18,7 @@ Prints ONE JSON line on rank 0. `--impl reference` times the CPU oracle instead.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -44,7 +45,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--workload", default="qwen3-30b-a3b",
-                   help="qwen3-30b-a3b | qwen3-4b | 1m | 30b-slice (first 6 layers, for ncu)")
+                   help="qwen3-30b-a3b | qwen3-4b | qwen3-235b-a22b | 1m | 30b-slice (first 6 layers, for ncu)")
     p.add_argument("--rho", type=float, default=0.01, help="update density (1 - sparsity)")
     p.add_argument("--mask", choices=["U", "R", "E"], default="U")
     p.add_argument("--codec", choices=["compressed", "raw"], default="compressed")
@@ -77,6 +78,15 @@ def parse():
                    help="f3 per-parameter routing (P:389): records whose FULL copy is smaller go FULL")
     p.add_argument("--groups", type=int, default=0,
                    help="tensor groups per Trainer, pipelined through transfer/apply (0: 1 for ring, 4 otherwise)")
+    p.add_argument("--model-shards", type=int, default=0,
+                   help="--topology sharded: split the model into K shards (0: N/2); Trainer t syncs shard t to "
+                        "Rollout t + N/2, so fewer GPUs than 2K run the first N/2 shard pairs of the K-way split "
+                        "(config 5: Qwen3-235B in 4 shards)")
+    p.add_argument("--stream-gb", type=float, default=0.0,
+                   help="Trainer streaming (config 5, SURVEY 8(d)): the Trainer holds only its snapshot; each "
+                        "step generates the new weights one tensor group of <= this many GB at a time into a "
+                        "scratch buffer, which that group's extract reads (the generator runs inside the timed "
+                        "step and is reported as its own phase, stream_generate)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--latency-steps", type=int, default=5, help="barrier-separated syncs for per-update latency")
@@ -100,6 +110,16 @@ def manifest_for(name: str) -> synth.Manifest:
 
 
 MASKS = {"U": synth.MASK_U, "R": synth.MASK_R, "E": synth.MASK_E}
+
+
+def stream_groups(numel, gb: float) -> int:
+    """Fewest contiguous tensor groups (transport.shard_ranges) whose largest holds <= gb GB of bf16."""
+    from paper_2605_07330_b200.transport import shard_ranges
+    lim = gb * 1e9 / 2
+    G = max(1, int(np.ceil(sum(numel) / lim)))
+    while G < len(numel) and max(sum(numel[lo:hi]) for lo, hi in shard_ranges(numel, G)) > lim:
+        G += 1
+    return G
 
 
 def measured_peaks():
@@ -248,7 +268,17 @@ class Rank:
         self.is_trainer = topo == "ring" or d.rank < half
         self.is_rollout = topo == "ring" or d.rank >= half
         sharded_model = topo in ("fanout", "sharded")
-        self.shards = transport.shard_ranges(manifest.numel, half) if sharded_model else None
+        n_shards = args.model_shards or half
+        if args.model_shards and (topo != "sharded" or n_shards < half):
+            raise SystemExit("--model-shards K needs --topology sharded and K >= N/2")
+        self.stream = args.stream_gb > 0
+        if self.stream and (topo != "sharded" or args.commit != "scatter" or args.dtype != "bf16"
+                            or args.tracking != "snapshot"):
+            raise SystemExit("--stream-gb runs with --topology sharded --commit scatter (bf16, snapshot tracking)")
+        self.shards = transport.shard_ranges(manifest.numel, n_shards) if sharded_model else None
+        if self.stream:   # the same group split on both ends of a shard pair
+            lo, hi = self.shards[d.rank % half]
+            self.G = stream_groups(manifest.numel[lo:hi], args.stream_gb)
         codec = ss.SYNC_CODEC_COMPRESSED if args.codec == "compressed" else ss.SYNC_CODEC_RAW
         self.dtype = {"bf16": synth.DTYPE_BF16, "fp16": synth.DTYPE_FP16, "fp8": synth.DTYPE_FP8}[args.dtype]
         adt = torch.uint8 if args.dtype == "fp8" else torch.int16   # arena element type
@@ -274,6 +304,8 @@ class Rank:
             cap = min(total, int(total * args.rho * 1.02) + (1 << 20))
             if self.tracking:
                 self._setup_tracking(mt, tid0, cap, rkw)
+            elif self.stream:
+                self._setup_stream(mt, tid0, cap, rkw)
             else:
                 self.X, self.Xv = sg.arena(mt, dev, dtype=adt)   # trainer snapshot (swaps with Y under swap)
                 self.Y, self.Yv = sg.arena(mt, dev, dtype=adt)   # trainer current weights
@@ -332,6 +364,49 @@ class Rank:
         self.N = self.mt.total if self.is_trainer else 0
         eb = 1 if args.dtype == "fp8" else 2
         self.S = eb * self.N   # bytes of weights this rank syncs per step (as the sender)
+
+    def _setup_stream(self, mt, tid0, cap, kw):
+        """Config 5: snapshot X resident, the new weights of one tensor group at a time in a scratch buffer.
+        Group g's 'current' views alias the scratch; FillNewPlan g regenerates them from X inside the step
+        (new = X with the U/R/E mask's bits flipped; after the commit the next step flips them back)."""
+        from paper_2605_07330_b200 import transport
+        from paper_2605_07330_b200.sync import GroupedSender
+        sg, dev, args = self.sg, self.d.dev, self.args
+        self.X, self.Xv = sg.arena(mt, dev)
+        sg.fill_old(self.Xv, mt, self.seed, tid0=tid0)
+        ranges = transport.shard_ranges(mt.numel, self.G)
+        biggest = max(sum(mt.numel[lo:hi]) for lo, hi in ranges)
+        self.Y = torch.empty(biggest, dtype=torch.int16, device=dev)
+        self.Yv = []
+        for lo, hi in ranges:
+            off = 0
+            for n in mt.numel[lo:hi]:
+                self.Yv.append(self.Y[off:off + n])
+                off += n
+        self.sender = GroupedSender(self.Xv, self.Yv, groups=self.G, max_changed=cap, **kw)
+        assert self.sender.ranges == ranges
+        # the update is a fixed set of bit flips (fill_new's mask and perturbation depend on the element, not on
+        # the step): found once per group with the batched generator, then every step rebuilds the group's new
+        # weights as a copy of its snapshot slice with those flips applied (new = X ^ d at I_d; after the commit
+        # the next step flips them back, as fill_new would)
+        self.flips = []
+        off = 0
+        for g, (lo, hi) in enumerate(ranges):
+            n = sum(mt.numel[lo:hi])
+            sg.FillNewPlan(self.Xv[lo:hi], self.Yv[lo:hi], mt.slice(lo, hi), self.seed, args.rho, MASKS[args.mask],
+                           tid0=tid0 + lo).run()
+            xs, ys = self.X[off:off + n], self.Y[:n]
+            idx = torch.nonzero(ys != xs).flatten()
+            self.flips.append((off, n, idx, ys[idx] ^ xs[idx]))
+            off += n
+        torch.cuda.synchronize()
+
+    def stream_generate(self, g: int):
+        """Group g's new weights into the scratch: its snapshot slice, with the update's flips applied."""
+        off, n, idx, d = self.flips[g]
+        ys = self.Y[:n]
+        ys.copy_(self.X[off:off + n])
+        ys[idx] = ys[idx] ^ d
 
     def _setup_tracking(self, mt, tid0, cap, kw):
         """f1 (Alg. 1): bf16 model weights W + two fp32 master versions M0 / M1 (the optimizer's outputs of
@@ -392,7 +467,11 @@ class Rank:
             rec(4 * g)
             if snd is not None:
                 p = snd.parts[g]
-                if self.tracking:
+                if self.stream:
+                    self.stream_generate(g)     # this group's new weights into the scratch (input generation)
+                    rec(4 * g + 1)
+                    p.ctx.sync_extract_batched(p.old_ptrs, p.new_ptrs, p.I, p.V, p.counts)
+                elif self.tracking:
                     # the optimizer-step epilogue (Alg. 1 l.5-7): the masters of this step are the other version
                     p.master_ptrs = self.master_tables[g][self.kstep % 2]
                     p.cast_track()
@@ -436,7 +515,7 @@ class Rank:
             if a.commit == "swap":
                 self.X, self.Y, self.Xv, self.Yv = self.Y, self.X, self.Yv, self.Xv
         rec(4 * G + 1)
-        if snd is not None and (a.commit == "scatter" or self.loop_snapshot) and toggle:
+        if snd is not None and (a.commit == "scatter" or self.loop_snapshot) and toggle and not self.stream:
             # snapshot == current now: the synthetic "optimizer step" flips the changed bits again so the
             # next sync has a fresh update of the same density (write-only scatter, input generation)
             for p in snd.parts:
@@ -558,6 +637,13 @@ def run_ours(args):
                   "sample": f"records of the first {min(cpu['k'], n0)} tensors vs the oracle"}
         del cpu["olds"], cpu["news"]
 
+    # the setup's objects (manifests, views, pointer tables) go to the permanent generation and the cyclic
+    # collector stays off through warm-up and the timed syncs: a full collection over tens of thousands of
+    # tensor views stalls a rank's host thread for ~10^2 ms at random steps (as serving processes do, the
+    # collector runs again once the measurement is over)
+    gc.collect()
+    gc.freeze()
+    gc.disable()
     # ---- warmup (also sizes every buffer)
     for _ in range(args.warmup):
         r.step()
@@ -601,7 +687,7 @@ def run_ours(args):
     clk = clocks.stop()
     step_ms = [e[0].elapsed_time(e[r.n_events() - 2]) for e in evs]
     launches = ss.launch_count() - launches0 + (K * r.G if (args.commit == "scatter" or r.loop_snapshot)
-                                                and r.sender is not None else 0)
+                                                and r.sender is not None and not r.stream else 0)
     launches = int(d.sum(launches))   # + the toggle kernels under --commit scatter
     ms_local = t_start.elapsed_time(t_end) if flush is None else float(np.sum(step_ms))
     ms = d.max(ms_local)
@@ -632,6 +718,7 @@ def run_ours(args):
                 "syncs": len(lat), "what": "one sync after a barrier, max over ranks (extract start -> last "
                                            "apply/commit)"} if lat else None)
 
+    gc.enable()
     # ---- f1: the plain CastAndCopy the tracking replaces (torch's fp32 -> bf16 copy kernel, a library kernel
     #      timed only for comparison) over up to 2^29 elements of the masters, scaled to this rank's elements
     track_cmp = None
@@ -671,7 +758,10 @@ def run_ours(args):
 
     # ---- e2e through the public API with host buffers (H2D of the new weights, D2H of the result)
     e2e = None
-    if r.tracking and not args.no_e2e:
+    if r.stream and not args.no_e2e:
+        e2e = {"value": None, "unit": UNIT, "reason": "not measured under --stream-gb (the Trainer generates its "
+                                                      "new weights group by group on the device)"}
+    elif r.tracking and not args.no_e2e:
         e2e = {"value": None, "unit": UNIT, "reason": "not measured under --tracking cast (the inputs are fp32 "
                                                       "masters produced on the device by the optimizer)"}
     elif not args.no_e2e and args.e2e_steps > 0:
@@ -734,12 +824,14 @@ def run_ours(args):
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
                    "groups": r.G, "replica": args.replica, "tracking": args.tracking, "route": args.route,
                    "element_dtype": args.dtype, "escape": args.escape,
+                   "model_shards": (args.model_shards or d.world // 2) if args.topology == "sharded" else None,
+                   "stream_gb": args.stream_gb or None,
                    "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
                    "l2": ("inputs larger than L2 (2 x S per Trainer); no flush" if flush is None else
                           "inputs smaller than L2: 512 MB write between steps, excluded via per-step events")},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
                          zip(["extract", "compress_pack", "transfer_apply", "commit", "synthetic_update",
-                              "cast_track"], phases)},
+                              "stream_generate" if r.stream else "cast_track"], phases)},
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic if not (r.tracking or args.dtype == "fp8") else None,
@@ -757,6 +849,13 @@ def run_ours(args):
     }
     if track_cmp is not None:
         out["tracking_vs_plain_cast"] = track_cmp
+    if r.stream:
+        gen = float(phases[5])
+        out["stream"] = {"groups": r.G, "generate_ms_per_step": round(gen, 4),
+                         "ms_per_step_excl_generation": round(ms / K - gen, 4),
+                         "latency_excl_generation_ms": round(latency["median_ms"] - gen, 4) if latency else None,
+                         "what": "the input generator (new weights of each group into the scratch) runs inside "
+                                 "the timed step; these subtract its per-step time (max over ranks)"}
     if parity is not None:
         out["parity_sampled"] = parity
     if cpu is not None:

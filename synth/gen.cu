@@ -128,6 +128,45 @@ __global__ void __launch_bounds__(256) k_toggle(u16* const* ys, const u32* I, co
   }
 }
 
+// Batched form of k_fill_new for many tensors in one launch (bench streaming mode): one job per tensor with
+// the same parameters synth_fill_new takes, a host-built table of tiles (job, first element).
+struct FillJob {
+  const u16* old;
+  u16* nw;
+  u64 n, key_mask, thr, key_pert, key_row, thr_row, cols;
+  int mode, active;
+};
+
+__global__ void k_fill_new_jobs(const FillJob* jobs, const u32* tile_job, const u64* tile_off, u64 n_tiles,
+                                u64 tile_elems) {
+  for (u64 tl = blockIdx.x; tl < n_tiles; tl += gridDim.x) {
+    const FillJob j = jobs[tile_job[tl]];
+    const u64 e0 = tile_off[tl];
+    const u64 e1 = e0 + tile_elems < j.n ? e0 + tile_elems : j.n;
+    // 8 elements per thread and 16-byte accesses where the job's pointers allow (arena views always do)
+    const bool vec = ((((uintptr_t)j.old) | ((uintptr_t)j.nw)) & 15u) == 0;
+    const u64 v_end = vec ? e0 + ((e1 - e0) & ~7ull) : e0;
+    for (u64 i0 = e0 + 8 * threadIdx.x; i0 < v_end; i0 += 8 * blockDim.x) {
+      const uint4 o4 = *reinterpret_cast<const uint4*>(j.old + i0);
+      u32 w[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const u64 i = i0 + k;
+        bool m = j.active && (mix(j.key_mask ^ i) >> 32) < j.thr;
+        if (j.mode == 1) m = m && ((mix(j.key_row ^ (i / j.cols)) >> 32) < j.thr_row);
+        if (m) w[k >> 1] ^= (u32)(1 + mix(j.key_pert ^ i) % 3) << (16 * (k & 1));
+      }
+      *reinterpret_cast<uint4*>(j.nw + i0) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    for (u64 i = v_end + threadIdx.x; i < e1; i += blockDim.x) {
+      bool m = j.active && (mix(j.key_mask ^ i) >> 32) < j.thr;
+      if (j.mode == 1) m = m && ((mix(j.key_row ^ (i / j.cols)) >> 32) < j.thr_row);
+      const u16 o = j.old[i];
+      j.nw[i] = m ? (u16)(o ^ (u16)(1 + mix(j.key_pert ^ i) % 3)) : o;
+    }
+  }
+}
+
 extern "C" {
 
 int synth_fill_old(void* out, u64 n, int norm, u64 key_val, const void* table, void* stream) {
@@ -163,6 +202,15 @@ int synth_fill_new8(const void* old, void* nw, u64 n, int mode, int active, u64 
   int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
   k_fill_new8<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)old, (uint8_t*)nw, n, mode, active, key_mask,
                                                        thr, key_pert, key_row, thr_row, cols ? cols : 1);
+  return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+int synth_fill_new_jobs(const void* jobs, const void* tile_job, const void* tile_off, u64 n_tiles, u64 tile_elems,
+                        void* stream) {
+  if (!n_tiles) return 0;
+  const int grid = (int)(n_tiles < 148 * 16 ? n_tiles : 148 * 16);
+  k_fill_new_jobs<<<grid, 512, 0, (cudaStream_t)stream>>>((const FillJob*)jobs, (const u32*)tile_job,
+                                                          (const u64*)tile_off, n_tiles, tile_elems);
   return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 

@@ -36,6 +36,8 @@ def lib():
         L.synth_toggle.argtypes = [P, P, P, P, u32, P, P]
         L.synth_fill_old8.argtypes = [P, u64, i32, u64, P, P]
         L.synth_fill_new8.argtypes = [P, P, u64, i32, i32, u64, u64, u64, u64, u64, u64, P]
+        L.synth_fill_new_jobs.argtypes = [P, P, P, u64, u64, P]
+        L.synth_fill_new_jobs.restype = ctypes.c_int
         for f in (L.synth_fill_old, L.synth_fill_new, L.synth_toggle, L.synth_fill_old8, L.synth_fill_new8):
             f.restype = i32
         _lib = L
@@ -93,6 +95,45 @@ def fill_new(old_views, new_views, manifest: Manifest, seed: int, rho: float, ma
         rc = f(ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(n.data_ptr()), o.numel(), mode,
                                   active, key(S_MASK, seed, tid), thr, key(S_PERT, seed, tid), key_row, thr_row,
                                   cols, _s())
+        assert rc == 0
+
+
+class FillNewPlan:
+    """fill_new over many tensors in ONE launch (bench streaming mode): the per-tensor parameters of
+    fill_new in a device job table, tiles of 1 Mi elements; bit-identical to calling fill_new per tensor."""
+    TILE = 1 << 20
+
+    def __init__(self, old_views, new_views, manifest: Manifest, seed: int, rho: float, mask: int = 0,
+                 tid0: int = 0):
+        assert all(o.element_size() == 2 for o in old_views)
+        jobs, tj, to = [], [], []
+        for k, (o, n, t) in enumerate(zip(old_views, new_views, manifest.tensors)):
+            tid = tid0 + k
+            mode, active, thr = 0, 1, threshold(rho)
+            key_row, thr_row, cols = 0, 0, 1
+            if mask == MASK_R and len(t.shape) == 2:
+                mode, thr = 1, threshold(min(1.0, rho / ROW_Q))
+                key_row, thr_row, cols = key(S_ROW, seed, tid), threshold(ROW_Q), t.cols
+            elif mask == MASK_E and t.expert >= 0:
+                e = np.array([t.expert], np.uint64)
+                active = int((h(S_EXP, seed, t.layer, e) >> np.uint64(32))[0] < np.uint64(threshold(EXPERT_F)))
+                thr = threshold(min(1.0, rho / EXPERT_F))
+            # FillJob: 2 pointers, 7 u64, 2 int32 (80 bytes)
+            jobs.append([o.data_ptr(), n.data_ptr(), o.numel(), key(S_MASK, seed, tid), thr, key(S_PERT, seed, tid),
+                         key_row, thr_row, cols, (active << 32) | mode])
+            for e0 in range(0, o.numel(), self.TILE):
+                tj.append(len(jobs) - 1)
+                to.append(e0)
+        dev = old_views[0].device
+        a = np.array(jobs, dtype=np.uint64).reshape(-1, 10) if jobs else np.zeros((0, 10), np.uint64)
+        self.jobs = torch.from_numpy(a.view(np.int64).copy()).to(dev)
+        self.tile_job = torch.tensor(tj or [0], dtype=torch.int32, device=dev)
+        self.tile_off = torch.tensor(to or [0], dtype=torch.int64, device=dev)
+        self.n_tiles = len(tj)
+
+    def run(self):
+        rc = lib().synth_fill_new_jobs(ctypes.c_void_p(self.jobs.data_ptr()), ctypes.c_void_p(self.tile_job.data_ptr()),
+                                       ctypes.c_void_p(self.tile_off.data_ptr()), self.n_tiles, self.TILE, _s())
         assert rc == 0
 
 

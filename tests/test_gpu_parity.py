@@ -94,6 +94,20 @@ def test_generator_twins_agree():
             assert (host16(a) == b).all()
         for a, b in zip(new, news):
             assert (host16(a) == b).all()
+        # the batched generator of the bench's streaming mode writes the same new weights (tensors larger
+        # than its 1 Mi-element tile included)
+        _, new2 = sg.arena(m, DEV)
+        sg.FillNewPlan(old, new2, m, seed=7, rho=0.05, mask=mask, tid0=11).run()
+        for a, b in zip(new2, news):
+            assert (host16(a) == b).all()
+    big = synth.Manifest("b", [synth.Tensor("w", (1100, 1000)), synth.Tensor("t", (8,))])
+    _, old = sg.arena(big, DEV)
+    _, new = sg.arena(big, DEV)
+    sg.fill_old(old, big, seed=3)
+    sg.FillNewPlan(old, new, big, seed=3, rho=0.01).run()
+    _, news = synth.generate(big, seed=3, rho=0.01)
+    for a, b in zip(new, news):
+        assert (host16(a) == b).all()
 
 
 # ----------------------------------------------------------------------------- whole path

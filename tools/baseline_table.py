@@ -22,6 +22,7 @@ ROWS = [
     ("30B 90% U, 2T→2R fanout", "fanout4_r10_U_b256", ""),
     ("30B 99.9% U, 2T→2R fanout", "fanout4_r001_U_b256", ""),
     ("30B 99% U, 2T→2R sharded", "sharded4_r01", ""),
+    ("235B 99% U, 2 of the 4 shard pairs of 4T→4R, Trainer streaming (config 5)", "sharded4_235b_stream", "stream"),
     ("30B 99% R, 2T→2R, 16 MB buckets (config 4)", "fanout4_r01_R_b16", "clustered"),
     ("30B 99% R, 2T→2R, 1 GB buckets (config 4)", "fanout4_r01_R_b1024", "clustered"),
     ("30B 99% E, 2T→2R, 256 MB (config 4)", "fanout4_r01_E_b256", "clustered"),
@@ -69,7 +70,13 @@ def main():
             fsec = 1 - (1 - p["rho_measured"]) ** per
             da = "%.0f%%" % ((pc + 64 * fsec * n_el / per) / ta / 1e9 / P * 100)
         lat = (d.get("latency_per_update") or {}).get("median_ms")
-        out.append(f"| {name} | {d['n_gpus']} | {d['value']:.0f} | {xc} | {da} | {lat:.2f} | "
+        lat_s = f"{lat:.2f}"
+        if kind == "stream":   # the input generator runs inside the step: report the sync alone
+            s = d["stream"]
+            lat_s = (f"{s['latency_excl_generation_ms']:.2f} (sync; + {s['generate_ms_per_step']:.0f} ms of input "
+                     f"generation per step)")
+            xc = "%.0f%%" % ((2 * s_tr + pc) / ((ph["extract"] + ph["compress_pack"]) / 1e3) / 1e9 / P * 100)
+        out.append(f"| {name} | {d['n_gpus']} | {d['value']:.0f} | {xc} | {da} | {lat_s} | "
                    f"{p['x_raw_eq1']} / {p['x_comp']} / {p['alpha']} | {d['bit_exact_replica']} | "
                    f"`profiles/r1_sweep/{key}.json` |")
     tab = "\n".join(out) + "\n"

@@ -56,6 +56,9 @@ SETS = {
         ("fanout4_r01_E_b1024", 4, ["--topology", "fanout", "--mask", "E", "--bucket-mb", "1024"]),
         ("fanout4_r01_cast", 4, ["--topology", "fanout", "--tracking", "cast"]),
         ("pair4_4b_r01", 4, ["--topology", "pair", "--workload", "qwen3-4b"]),
+        # config 5 on half the box: 2 of the 4 shard pairs of Qwen3-235B, Trainer new weights streamed
+        ("sharded4_235b_stream", 4, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--model-shards",
+                                     "4", "--stream-gb", "5", "--commit", "scatter", "--steps", "5"]),
     ],
     "n2": [
         ("ring2_r01", 2, ["--topology", "ring"]),
