@@ -34,3 +34,21 @@ def test_product_path_has_no_cpu_fallback():
     new = old.clone()
     with pytest.raises(Exception):
         ss.sync_extract(old, new)            # CPU tensors: the binding refuses, nothing runs on the host
+
+
+def test_stream_groups_fit_the_scratch():
+    """Config 5's streaming split: the fewest contiguous groups whose largest fits the scratch; a tensor larger
+    than the scratch ends up alone (the scratch is then sized to it)."""
+    sys.path.insert(0, ROOT)
+    import synth
+    from bench import stream_groups
+    from paper_2605_07330_b200.transport import shard_ranges
+    m = synth.qwen3_manifest("qwen3-235b-a22b")
+    lo, hi = shard_ranges(m.numel, 4)[0]
+    numel = m.numel[lo:hi]
+    G = stream_groups(numel, 5)
+    assert max(sum(numel[a:b]) for a, b in shard_ranges(numel, G)) * 2 <= 5e9
+    assert G == 1 or max(sum(numel[a:b]) for a, b in shard_ranges(numel, G - 1)) * 2 > 5e9
+    assert stream_groups([10, 10, 10], 1e-7) == 1          # 60 bytes fit a 100-byte scratch
+    assert stream_groups([10, 10, 10], 4e-8) == 2          # 40-byte scratch: 20 + 10 elements
+    assert stream_groups([100, 1, 1], 1e-7) == 3           # a 200-byte tensor can only go alone
