@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(256, kMinB) k_decode(DecodeBatch bb, u32 n_ten
         } else if (esc) {
           // parse the 32 elements of this step: lane l reads word wptr + l, shifted by one word for every
           // escape (two-word element) among the lanes before it; one ballot per escape in the step
-          u32 pos = wptr + lane, dv = 0;
+          u32 pos = wptr + lane, dv = 0, n_esc = 0;
           bool done = !act;
           while (true) {
             const bool in = !done && pos < wend;
@@ -461,6 +461,7 @@ __global__ void __launch_bounds__(256, kMinB) k_decode(DecodeBatch bb, u32 n_ten
               break;
             }
             const u32 e = __ffs(m) - 1;
+            ++n_esc;                      // every round resolves exactly one escape (two words)
             if (in && lane < e) {
               dv = w;
               done = true;
@@ -473,14 +474,8 @@ __global__ void __launch_bounds__(256, kMinB) k_decode(DecodeBatch bb, u32 n_ten
               pos += 1;
             }
           }
-          const u32 end = act ? pos + (dv > 32767u ? 2u : 1u) : 0u;
-          u32 mx = end;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const u32 y = __shfl_xor_sync(0xffffffffu, mx, o);
-            mx = y > mx ? y : mx;
-          }
-          wptr = mx > wptr ? mx : wptr;
+          // the step consumed one word per active element plus one per escape
+          wptr += __popc(__ballot_sync(0xffffffffu, act)) + n_esc;
           idx = carry + warp_incl_scan(dv);
           carry = __shfl_sync(0xffffffffu, idx, 31);
         } else {
