@@ -548,3 +548,60 @@ def test_config1_one_million_end_to_end():
     assert (host16(rol_d[0]) == news[0]).all()
     x_comp = 2 * (1 << 20) / sum(len(g) for g in got)
     assert 55 < x_comp < 65                      # ≈ 60x at ρ = 1% (Eq. 4, α ≈ 0.67)
+
+
+# ----------------------------------------------------------------------------- maximum tensor size
+NMAX = (1 << 31) - 1   # largest numel the format allows (DESIGN C2: tensor-local u32 index < 2^31)
+
+
+@pytest.mark.parametrize("mode", ["abs32", "delta16e", "delta16"])
+def test_max_numel_tensor_bit_exact(mode):
+    """One tensor of 2^31 - 1 elements with changes at both ends and between: extract is the definition (the
+    changed positions are the input), the buckets equal the oracle's byte for byte and the replica is
+    bit-identical. abs32 / delta16e: 3000 scattered changes (gaps ~ 2^31 / 3000 > 32767: ABS32, or DELTA16E
+    with an escape pair per gap); delta16: every 30000th element (71.6K changes, 5 chunks whose base
+    indices run up to 2^31 - 1)."""
+    rng = np.random.default_rng(31)
+    escape = mode == "delta16e"
+    if mode == "delta16":
+        pos = np.concatenate([np.arange(0, NMAX, 30000), [NMAX - 1]]).astype(np.int64)
+    else:
+        pos = np.unique(np.concatenate([rng.integers(0, NMAX, 3000), [0, 1, NMAX - 2, NMAX - 1]])).astype(np.int64)
+    val = rng.integers(1, 65536, pos.size, dtype=np.uint16)
+    old_h = np.zeros(NMAX, np.uint16)
+    new_h = old_h.copy()
+    new_h[pos] = val                      # old is all zero and val != 0: every listed position changes
+    old = torch.zeros(NMAX, dtype=torch.int16, device=DEV)
+    new = torch.from_numpy(new_h.view(np.int16)).to(DEV)
+    cap = 1 << 17
+    I, V, cnt, ws = ss.sync_extract(old, new, I=torch.empty(cap, dtype=torch.int32, device=DEV),
+                                    V=torch.empty(cap, dtype=torch.int16, device=DEV))
+    torch.cuda.synchronize()
+    assert ss.sync_extract_status(ws) == ss.SYNC_OK
+    c = int(cnt.item())
+    assert c == pos.size
+    assert (I[:c].cpu().numpy().view(np.uint32) == pos.astype(np.uint32)).all()
+    assert (host16(V[:c]) == val).all()
+    ref = oracle.sync_pack([old_h], [new_h], limit=64 << 20, crc=True, escape=escape)
+    assert ref.stats[mode] == 1
+    rol = old.clone()
+    snd = ss.SparseSyncSender([old], [new], bucket_limit=64 << 20, crc=True, escape=escape, max_changed=cap)
+    rcv = ss.SparseSyncReceiver([rol], bucket_limit=64 << 20, crc=True)
+    bl = snd.sync()
+    assert [snd.bucket(b).cpu().numpy().tobytes() for b in range(len(bl))] == \
+        [ref.bucket(b) for b in range(ref.n_buckets)]
+    for b in range(len(bl)):
+        rcv.apply(snd.bucket(b))
+    torch.cuda.synchronize()
+    snd.check()
+    rcv.check()
+    assert torch.equal(rol, new)
+
+
+def test_numel_2_31_is_rejected():
+    big = torch.zeros(1 << 31, dtype=torch.int16, device=DEV)
+    small = torch.empty(16, dtype=torch.int32, device=DEV)
+    with pytest.raises(ss.SyncError):
+        ss.sync_extract(big, big, I=small, V=small.view(torch.int16)[:16])
+    with pytest.raises(ss.SyncError):
+        ss.SparseSyncSender([big], [big], max_changed=16)
