@@ -787,6 +787,33 @@ def run_ours(args):
         roof_bytes = int(6 * n_el + 32 * f_sec * n_el / 16 + 8 * f_word * n_el / 32)
         achieved = roof_bytes / (cast_ms_local / 1e3) / 1e9
     peak = peaks.get("hbm_gbs", 6650.0)
+    # per-phase HBM fractions: one rank's algorithmic bytes per phase ÷ the phase time, against
+    # the measured copy peak and the 8 TB/s HBM3e spec-sheet figure. extract: 2S + 6 nnz; compress_pack:
+    # 6 nnz read + payload written; transfer_apply: payload + the touched 32 B sectors read and written (sector
+    # model, expected count for the U mask: N/16 (1 - (1 - rho)^16), ncu-confirmed). Only where
+    # every rank does one whole model's work per phase (ring / pair, plain bf16 / fp16 snapshot path).
+    phase_hbm = None
+    try:
+        if args.topology in ("ring", "pair") and not r.tracking and not r.stream and args.dtype != "fp8" \
+                and args.codec == "compressed":
+            t3 = [float(v) for v in phases[:3]]
+            sec = r.N / 16 * (1 - (1 - args.rho) ** 16) if args.mask == "U" else None
+            byts = [local_alg_extract, 6 * nnz + payload, payload + 64 * sec if sec is not None else None]
+            phase_hbm = {"peak": peak, "spec_gbs": 8000.0,
+                         "model": "extract 2S+6nnz; compress 6nnz+payload; apply payload+64 B x touched sectors (U)"}
+            # north_star's two halves: extract+compress (sender) and decompress+apply (receiver)
+            names = ["extract", "compress_pack", "transfer_apply", "extract+compress"]
+            byts.append(byts[0] + byts[1])
+            t3.append(t3[0] + t3[1])
+            for name, b, t in zip(names, byts, t3):
+                if b is None or t <= 0:
+                    phase_hbm[name] = None
+                    continue
+                gbs = b / (t / 1e3) / 1e9
+                phase_hbm[name] = {"gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                                   "frac_spec": round(gbs / 8000.0, 4)}
+    except Exception as exc:   # reporting only; never fails the run
+        phase_hbm = {"error": str(exc)[:200]}
     # ncu dram bytes / algorithmic bytes of the profiled extract launch (profiles/extract_traffic.json,
     # from `ncu --set full` on the 30b-slice workload), applied to this launch's algorithmic bytes
     traffic, traffic_src = None, None
@@ -844,6 +871,7 @@ def run_ours(args):
                     "alpha": round(vbytes_t / max((1 if args.dtype == "fp8" else 2) * nnz_t, 1), 4),
                     "delta16_records": int(n16_t), "abs32_records": int(n32_t), "delta16e_records": int(n16e_t),
                     "paper_context": "paper: 32-54x raw, ~60-101x compressed on H100 clusters (P:22, P:380)"},
+        "phase_hbm": phase_hbm,
         "clocks": clk, "gpu_launches": int(launches), "bit_exact_replica": verify, "e2e": e2e,
         "latency_per_update": latency,
     }
