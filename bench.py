@@ -894,23 +894,44 @@ def run_ours(args):
     return out if d.rank == 0 else None
 
 
+def host_ram_available() -> int:
+    """Bytes this job may still allocate on the host: /proc/meminfo's MemAvailable, capped by the memory
+    cgroup's limit minus its usage (v2 memory.max/current, v1 limit_in_bytes/usage_in_bytes). A container can
+    see a large host in /proc/meminfo while its cgroup is far smaller; the OOM killer enforces the cgroup."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        return 0
+    for lim_f, use_f in (("/sys/fs/cgroup/memory.max", "/sys/fs/cgroup/memory.current"),
+                         ("/sys/fs/cgroup/memory/memory.limit_in_bytes",
+                          "/sys/fs/cgroup/memory/memory.usage_in_bytes")):
+        try:
+            lim = open(lim_f).read().strip()
+            use = int(open(use_f).read().strip())
+        except (OSError, ValueError):
+            continue
+        if lim.isdigit() and int(lim) < (1 << 60):
+            avail = min(avail, max(0, int(lim) - use))
+        break
+    return avail
+
+
 def run_e2e(args, d: Dist, r: Rank):
     """Same metric through the public API with HOST buffers: per step the new weights arrive from pinned host
     memory (H2D inside the timed region) and the per-tensor change counts go back to the host (D2H)."""
     hosts, counts_h = None, None
     # host RAM guard: every Trainer rank needs n_host x S of pinned inputs; refuse rather than risk the OOM killer
     n_need = (2 if args.commit == "swap" else 1) * r.S
-    try:
-        import psutil
-        avail = psutil.virtual_memory().available
-    except Exception:
-        avail = 0
+    avail = host_ram_available()
     n_trainers = d.world if args.topology == "ring" else d.world // 2   # pinned buffers live on one host
-    ok = int(d.sum(1.0 if (avail - 24e9) / max(1, n_trainers) > n_need or r.sender is None else 0.0)) == d.world
+    # pin at most half of what the host has free: at N = 4 on a 528 GB box, 4 x 122 GB passed a 24 GB margin
+    # and the OOM killer took every rank (page cache, CUDA contexts and NCCL buffers need the rest)
+    ok = int(d.sum(1.0 if 0.5 * avail / max(1, n_trainers) > n_need or r.sender is None else 0.0)) == d.world
     if not ok:
         return {"value": None, "unit": UNIT,
                 "reason": f"host RAM ({avail / 1e9:.0f} GB available) cannot hold {n_trainers} x "
-                          f"{n_need / 1e9:.0f} GB of pinned host inputs"}
+                          f"{n_need / 1e9:.0f} GB of pinned host inputs within half of it"}
     if r.sender is not None:
         # the inputs of consecutive steps: under --commit swap the versions alternate (v1, v0, v1, ...),
         # so keep both as host arrays; under --commit scatter the toggle regenerates them on the device
