@@ -925,13 +925,15 @@ def run_e2e(args, d: Dist, r: Rank):
     n_need = (2 if args.commit == "swap" else 1) * r.S
     avail = host_ram_available()
     n_trainers = d.world if args.topology == "ring" else d.world // 2   # pinned buffers live on one host
-    # pin at most half of what the host has free: at N = 4 on a 528 GB box, 4 x 122 GB passed a 24 GB margin
-    # and the OOM killer took every rank (page cache, CUDA contexts and NCCL buffers need the rest)
-    ok = int(d.sum(1.0 if 0.5 * avail / max(1, n_trainers) > n_need or r.sender is None else 0.0)) == d.world
+    # keep max(48 GB, 10%) of the free RAM plus 16 GB per rank (CUDA context, NCCL, page cache) unpinned: at N = 4
+    # on a 528 GB box, 4 x 122 GB passed a flat 24 GB margin and the OOM killer took every rank; a 209 GB box
+    # still pins the 122 GB of N = 1
+    spare = avail - max(48e9, 0.1 * avail) - 16e9 * max(1, n_trainers)
+    ok = int(d.sum(1.0 if spare >= n_trainers * n_need or r.sender is None else 0.0)) == d.world
     if not ok:
         return {"value": None, "unit": UNIT,
                 "reason": f"host RAM ({avail / 1e9:.0f} GB available) cannot hold {n_trainers} x "
-                          f"{n_need / 1e9:.0f} GB of pinned host inputs within half of it"}
+                          f"{n_need / 1e9:.0f} GB of pinned host inputs and its reserve"}
     if r.sender is not None:
         # the inputs of consecutive steps: under --commit swap the versions alternate (v1, v0, v1, ...),
         # so keep both as host arrays; under --commit scatter the toggle regenerates them on the device
