@@ -95,6 +95,8 @@ def parse():
     p.add_argument("--cpu-sample-elems", type=float, default=1.2e9)
     p.add_argument("--ref-sample-elems", type=float, default=4e8)
     p.add_argument("--no-verify", action="store_true")
+    p.add_argument("--no-full-parity", action="store_true",
+                   help="skip the every-record comparison with the oracle (N=1, rank 0, before the timed region)")
     p.add_argument("--out", default=None, help="also write the JSON line to this file")
     return p.parse_args()
 
@@ -130,31 +132,76 @@ def measured_peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / throttle-reason sampler during the timed region (B200_PROFILING.md clocks line): NVML polled
+    every 5 ms from a thread (a 10-step region lasts ~0.3 s; nvidia-smi -lms sees only a couple of samples),
+    nvidia-smi as the fallback."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
+        self.nv = None
+        self.samples = []   # (sm_mhz, reason bits)
+        self.running = False
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def start(self):
         try:
+            self.nv, self.h = self._nvml_handle()
+            self.max_mhz = float(self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.running = True
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
+        try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv, h = self.nv, self.h
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        while self.running:
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, [n for n, b in zip(self.NAMES, bits) if r & b]))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self) -> dict:
+        if self.nv is not None:
+            self.running = False
+            self.t.join(timeout=2)
+            sm = sorted(x[0] for x in self.samples)
+            reasons = sorted({n for _, rs in self.samples for n in rs})
+            return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                    "samples": len(sm), "source": "NVML, 5 ms poll"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -163,7 +210,6 @@ class Clocks:
         except Exception:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
@@ -173,12 +219,12 @@ class Clocks:
                 mx = float(f[2])
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
+            for n, v in zip(self.NAMES, f[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
 # ============================================================================= distributed plumbing
@@ -536,33 +582,69 @@ class Rank:
         cmp = sum(t(4 * g + 2, 4 * g + 3) for g in range(G))
         return [ext, cmp, t(0, 4 * G) - cast - ext - cmp, t(4 * G, 4 * G + 1), t(4 * G + 1, 4 * G + 2), cast]
 
-    def digests(self):
-        """(trainer snapshot digest, {source: rollout digest of that source's range}) for the bit-exact check."""
-        if self.loop_snapshot:   # the replica is the snapshot: after a sync without toggle it must equal Y
-            self.step(toggle=False)
-            torch.cuda.synchronize()
-            return chunked_digest(self.Y), {0: chunked_digest(self.X)}
-        mine_x = chunked_digest(self.X) if self.X is not None else None
-        mine_r = None
-        if self.R is not None:
-            mine_r = {}
-            for src, gr in self.receivers.items():
-                w = gr.parts[0].weights[0]
-                lo = (w.data_ptr() - self.R.data_ptr()) // self.R.element_size()
-                n = sum(sum(x.numel() for x in p.weights) for p in gr.parts)
-                mine_r[src] = chunked_digest(self.R[lo:lo + n])
-        return mine_x, mine_r
+    def replica_ranges(self):
+        """{source rank: this rank's replica slice holding that source Trainer's synced weights}."""
+        if self.R is None:
+            return {}
+        out = {}
+        for src, gr in self.receivers.items():
+            w = gr.parts[0].weights[0]
+            lo = (w.data_ptr() - self.R.data_ptr()) // self.R.element_size()
+            n = sum(sum(x.numel() for x in p.weights) for p in gr.parts)
+            out[src] = self.R[lo:lo + n]
+        return out
 
 
-def chunked_digest(t: torch.Tensor, chunk: int = 1 << 24) -> tuple:
-    """Order-sensitive digest of an int16 / uint8 tensor (verification only, outside the timed region)."""
-    a = b = 0
-    for s in range(0, t.numel(), chunk):
-        c = t[s:s + chunk].to(torch.int64) & 0xFFFF
-        w = (torch.arange(s, s + c.numel(), device=t.device, dtype=torch.int64) % 65521) + 1
-        a += int(c.sum().item())
-        b += int((c * w).sum().item()) % (1 << 61)
-    return a, b
+CMP_CHUNK = 1 << 28   # elements per exact-compare chunk (512 MB of int16)
+
+
+def equal_chunked(a: torch.Tensor, b: torch.Tensor) -> bool:
+    """torch.equal over chunks (a whole-arena torch.equal would materialise a bool tensor of N elements)."""
+    if a.numel() != b.numel():
+        return False
+    return all(torch.equal(a[s:s + CMP_CHUNK], b[s:s + CMP_CHUNK]) for s in range(0, a.numel(), CMP_CHUNK))
+
+
+def verify_exact(r, d) -> dict:
+    """Bit-exact check of every replica element against the Trainer's committed snapshot, outside the
+    timed region. N = 1: device-local chunked torch.equal. N > 1: every (source Trainer -> Rollout) pair streams
+    the snapshot in 512 MB chunks over NCCL to the Rollout, which compares them with its replica slice."""
+    if r.loop_snapshot:   # the replica is the snapshot: after a sync without toggle it must equal Y
+        r.step(toggle=False)
+        torch.cuda.synchronize()
+        return {"bit_exact": equal_chunked(r.X, r.Y), "elements": r.X.numel(), "method": "device torch.equal"}
+    mine = {src: t for src, t in r.replica_ranges().items()}
+    if d.world == 1:
+        ok = all(equal_chunked(t, r.X) for t in mine.values())
+        return {"bit_exact": bool(ok and mine), "elements": sum(t.numel() for t in mine.values()),
+                "method": "device torch.equal (replica vs snapshot, same GPU)"}
+    dist = d.dist
+    needs = [None] * d.world
+    dist.all_gather_object(needs, {src: t.numel() for src, t in mine.items()}, group=d.ctrl)
+    pairs = sorted((src, dst, n) for dst in range(d.world) for src, n in (needs[dst] or {}).items())
+    scratch = None
+    ok, elems = True, 0
+    for src, dst, n in pairs:          # every rank walks the same schedule: one pair at a time
+        if d.rank not in (src, dst):
+            continue
+        if d.rank == src and (r.X is None or r.X.numel() != n):
+            raise RuntimeError(f"rank {src}: snapshot size differs from the replica range of rank {dst}")
+        for s0 in range(0, n, CMP_CHUNK):
+            k = min(CMP_CHUNK, n - s0)
+            if d.rank == src:
+                dist.send(r.X[s0:s0 + k].contiguous(), dst)
+            else:
+                if scratch is None:
+                    scratch = torch.empty(CMP_CHUNK, dtype=r.R.dtype, device=d.dev)
+                dist.recv(scratch[:k], src)
+                ok = ok and torch.equal(scratch[:k], mine[src][s0:s0 + k])
+                elems += k
+    torch.cuda.synchronize()
+    flags = [None] * d.world
+    dist.all_gather_object(flags, (ok, elems), group=d.ctrl)
+    return {"bit_exact": all(f[0] for f in flags) and sum(f[1] for f in flags) > 0,
+            "elements": int(sum(f[1] for f in flags)),
+            "method": "snapshot streamed over NCCL in 512 MB chunks, torch.equal on the Rollout"}
 
 
 def cpu_baseline(args, manifest: synth.Manifest, seed: int, sample_elems: float, steps: int = 1):
@@ -611,6 +693,96 @@ def parse_records(bucket_bytes_list):
     return out
 
 
+def cpu_info() -> dict:
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0))}
+
+
+_FP = {}   # full-parity job state, inherited by the forked workers (copy-on-write)
+
+
+def _full_parity_job(job):
+    """One worker: regenerate tensors [lo, hi) with the CPU twin of the generator, run the oracle's sender on
+    them (extract + encode + pack) and its receiver (decode + apply into a replica and a snapshot copy), and
+    compare every record with the GPU's bytes. Returns (records, mismatches, bytes synced, oracle seconds)."""
+    import oracle
+    import synth.cpu as sc
+    lo, hi = job
+    c = _FP["cfg"]
+    sub = c["manifest"].slice(lo, hi)
+    olds, news = sc.generate(sub, seed=c["seed"], rho=c["rho"], mask=c["mask"], tid0=lo, dtype=c["dtype"])
+    R = [o.copy() for o in olds]
+    Sn = [o.copy() for o in olds]
+    t0 = time.perf_counter()
+    pk = oracle.sync_pack(olds, news, codec=c["codec"], limit=1 << 40, route=c["route"], dtype=c["dtype"],
+                          escape=c["escape"])
+    for b in range(pk.n_buckets):
+        assert oracle.bucket_apply(pk.bucket(b), R) == oracle.OK
+        assert oracle.bucket_apply(pk.bucket(b), Sn) == oracle.OK
+    secs = time.perf_counter() - t0
+    ora = parse_records([pk.bucket(b) for b in range(pk.n_buckets)])
+    gpu = _FP["gpu"]
+    bad = 0
+    for j, rec in ora.items():
+        g = gpu.get(lo + j)
+        # the oracle ran on the slice, so its tensor ids are local: the id field is compared via the mapping
+        if g is None or len(g) != len(rec) or g[4:] != rec[4:] or int.from_bytes(g[:4], "little") != lo + j:
+            bad += 1
+    # a GPU record for a tensor the oracle saw no change in
+    bad += sum(1 for t in range(lo, hi) if t in gpu and (t - lo) not in ora)
+    ok_apply = all(np.array_equal(r, n) and np.array_equal(x, n) for r, x, n in zip(R, Sn, news))
+    elem_b = 1 if c["dtype"] == synth.DTYPE_FP8 else 2
+    return len(ora), bad + (0 if ok_apply else 1), elem_b * 2 * sub.total, secs
+
+
+def full_parity(args, r, manifest: synth.Manifest, dtype: int) -> dict:
+    """Every record of the whole manifest vs the oracle (rank 0, N = 1, before any step changes X / Y): the GPU
+    sender runs once on the seeded state, its buckets come to the host, and a pool of workers (all host cores)
+    regenerates the inputs with the CPU twin and runs the oracle on element-balanced tensor ranges. Also the
+    oracle's all-cores throughput (sum of the workers' concurrent rates)."""
+    import multiprocessing as mp
+    from paper_2605_07330_b200.transport import shard_ranges
+    gpu = {}
+    for (glo, _), p in zip(r.sender.ranges, r.sender.parts):
+        p.sync()
+        bl = [p.bucket(b).cpu().numpy().tobytes() for b in range(len(p.bucket_list))]
+        for t, rec in parse_records(bl).items():   # ids are local to the group: make them global
+            gpu[glo + t] = rec if glo == 0 else (glo + t).to_bytes(4, "little") + rec[4:]
+    torch.cuda.synchronize()
+    codec = 1 if args.codec == "compressed" else 0
+    _FP["cfg"] = dict(manifest=manifest, seed=r.seed, rho=args.rho, mask=MASKS[args.mask], dtype=dtype,
+                      codec=codec, route=args.route, escape=args.escape)
+    _FP["gpu"] = gpu
+    ci = cpu_info()
+    workers = max(1, ci["affinity"])
+    # jobs of <= 0.25 G elements (memory: a worker holds old, new, replica and snapshot copies of its range)
+    jobs = shard_ranges(manifest.numel, max(workers, int(np.ceil(manifest.total / 2.5e8))))
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(workers) as pool:
+        res = pool.map(_full_parity_job, jobs, chunksize=1)
+    wall = time.perf_counter() - t0
+    _FP.clear()
+    recs = sum(x[0] for x in res)
+    bad = sum(x[1] for x in res)
+    rate = sum(x[2] / x[3] for x in res if x[3] > 0) / len(res) * workers   # mean job rate x concurrent workers
+    return {"parity_full": {"records_checked": recs, "gpu_records": len(gpu), "mismatches": bad,
+                            "bit_exact": bad == 0 and recs == len(gpu),
+                            "what": "every record of the manifest, GPU bytes vs the oracle's (plus the oracle's own "
+                                    "replica/snapshot round trip); inputs regenerated by the CPU twin",
+                            "wall_s": round(wall, 1), "workers": workers},
+            "cpu_all_cores": {"value": round(rate / 1e9, 4), "unit": UNIT, "cores": workers, "kind": "oracle",
+                              "sample": f"the whole workload ({manifest.total:,} elements), oracle extract+encode+"
+                                        f"pack+apply+commit in {len(jobs)} jobs over {workers} forked workers; "
+                                        "value = mean per-job rate x workers (concurrent)", **ci}}
+
+
 def run_ours(args):
     import paper_2605_07330_b200 as ss
     d = Dist(args.gpus, args.topology, args.transport)
@@ -618,24 +790,16 @@ def run_ours(args):
     manifest = manifest_for(args.workload)
     r = Rank(args, d, manifest)
 
-    # ---- sampled full-size parity + CPU baseline (rank 0, N = 1 only; before any step mutates X/Y)
+    # ---- full-size parity (every record vs the oracle) + CPU baselines (rank 0, N = 1 only; before any step
+    #      mutates X / Y)
     cpu = None
     parity = None
-    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline and not r.tracking:
+    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline and not r.tracking and not r.stream:
         cpu = cpu_baseline(args, manifest, r.seed, args.cpu_sample_elems)
-        # inputs: GPU twin == CPU twin on the sampled tensors
-        hv = (lambda x: x.cpu().numpy()) if r.X.element_size() == 1 else (lambda x: x.cpu().numpy().view(np.uint16))
-        gen_ok = all(np.array_equal(hv(r.Xv[k]), cpu["olds"][k]) and np.array_equal(hv(r.Yv[k]), cpu["news"][k])
-                     for k in range(min(cpu["k"], 64)))
-        p0 = r.sender.parts[0]   # group 0 starts at tensor 0: its record ids are the oracle's
-        p0.sync()
-        gpu_recs = parse_records([p0.bucket(b).cpu().numpy().tobytes() for b in range(len(p0.bucket_list))])
-        ora_recs = parse_records([cpu["pack"].bucket(b) for b in range(cpu["pack"].n_buckets)])
-        n0 = r.sender.ranges[0][1]
-        same = all(gpu_recs.get(t) == v for t, v in ora_recs.items() if t < n0)
-        parity = {"records_checked": sum(1 for t in ora_recs if t < n0), "bit_exact": bool(same and gen_ok),
-                  "sample": f"records of the first {min(cpu['k'], n0)} tensors vs the oracle"}
         del cpu["olds"], cpu["news"]
+        if not args.no_full_parity:
+            parity = full_parity(args, r, manifest, r.dtype)
+            torch.cuda.synchronize()
 
     # the setup's objects (manifests, views, pointer tables) go to the permanent generation and the cyclic
     # collector stays off through warm-up and the timed syncs: a full collection over tens of thousands of
@@ -718,6 +882,24 @@ def run_ours(args):
                 "syncs": len(lat), "what": "one sync after a barrier, max over ranks (extract start -> last "
                                            "apply/commit)"} if lat else None)
 
+    # ---- K6 in-place scatter commit (row a9) timed beside the pointer-swap commit of the headline: the same
+    #      launch the --commit scatter path makes, over the last sync's (I, V) into the snapshot (which already
+    #      holds those values under swap: idempotent, the same sectors move)
+    k6 = None
+    if r.sender is not None and args.commit == "swap" and not r.tracking and not r.stream:
+        reps = 5
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            for p in r.sender.parts:
+                p.ctx.sync_commit_snapshot_batched(p.old_ptrs, p.I, p.V, p.counts)
+        e1.record()
+        torch.cuda.synchronize()
+        k6_ms = e0.elapsed_time(e1) / reps
+        k6 = {"ms": round(k6_ms, 4), "what": "sync_commit_snapshot_batched (K6 scatter) per sync, 5 reps; the "
+                                             "headline's --commit swap exchanges pointer tables instead",
+              "step_ms_with_scatter_commit": round(ms / K + k6_ms, 4)}
+
     gc.enable()
     # ---- f1: the plain CastAndCopy the tracking replaces (torch's fp32 -> bf16 copy kernel, a library kernel
     #      timed only for comparison) over up to 2^29 elements of the masters, scaled to this rank's elements
@@ -743,18 +925,7 @@ def run_ours(args):
     # ---- verification: rollout replica == the Trainer's committed snapshot (bit-exact)
     verify = None
     if not args.no_verify:
-        mine = r.digests()
-        if d.world == 1:
-            verify = mine[0] == mine[1][0]
-        else:
-            g = [None] * d.world
-            d.dist.all_gather_object(g, mine, group=d.ctrl)
-            W, half = d.world, d.world // 2
-            verify = True
-            for i in range(W):
-                for src, dig in (g[i][1] or {}).items():
-                    verify = verify and dig == g[src][0]
-            verify = verify and sum(len(x[1] or {}) for x in g) > 0
+        verify = verify_exact(r, d)
 
     # ---- e2e through the public API with host buffers (H2D of the new weights, D2H of the result)
     e2e = None
@@ -775,7 +946,8 @@ def run_ours(args):
     achieved = local_alg_extract / (ext_ms_local / 1e3) / 1e9   # rank 0 (a Trainer), its own launch
     roof_kernel, roof_bytes = "k_extract (K1)", local_alg_extract
     if args.dtype == "fp8":
-        roof_kernel = "k_diff8 + tracked compaction (FP8 extract)"
+        roof_kernel = ("k_diff8 + tracked compaction (FP8 extract, SS_FP8_BITMAP)" if os.environ.get("SS_FP8_BITMAP")
+                       else "k_extract<kB=1> (K1 on 8-bit elements)")
     if r.tracking:
         # f1: the dominant kernel is the cast with tracking. Algorithmic bytes per launch: read the fp32 master
         # and the bf16 weights (6 B / element), write the 32 B sectors that changed and the bitmap words that
@@ -800,10 +972,12 @@ def run_ours(args):
             sec = r.N / 16 * (1 - (1 - args.rho) ** 16) if args.mask == "U" else None
             byts = [local_alg_extract, 6 * nnz + payload, payload + 64 * sec if sec is not None else None]
             phase_hbm = {"peak": peak, "spec_gbs": 8000.0,
-                         "model": "extract 2S+6nnz; compress 6nnz+payload; apply payload+64 B x touched sectors (U)"}
+                         "model": "SURVEY 8(d): extract+compress 2S + P_c (read old and new once, write the final "
+                                  "payload once); decompress+apply P_c + 64 B x touched 32 B sectors (U mask). Per "
+                                  "kernel: extract (K1) 2S + 6nnz (its I/V output); compress_pack 6nnz + P_c"}
             # north_star's two halves: extract+compress (sender) and decompress+apply (receiver)
             names = ["extract", "compress_pack", "transfer_apply", "extract+compress"]
-            byts.append(byts[0] + byts[1])
+            byts.append(2 * r.S + payload)
             t3.append(t3[0] + t3[1])
             for name, b, t in zip(names, byts, t3):
                 if b is None or t <= 0:
@@ -827,11 +1001,16 @@ def run_ours(args):
             traffic = None
     topo_txt = {
         "ring": "ring: rank r = Trainer of its model + Rollout replica of rank r-1 (N=1: loopback)",
-        "pair": "pair: ranks < N/2 Trainers of a whole model, rank t+N/2 = Rollout of Trainer t (NCCL P2P)",
+        "pair": "pair: ranks < N/2 Trainers of a whole model, rank t+N/2 = Rollout of Trainer t",
         "fanout": "fanout: N/2 Trainers own element-balanced shards of one model; each of the N/2 Rollouts holds "
-                  "the whole model and applies every Trainer's buckets (NCCL P2P fan-out, P:61)",
-        "sharded": "sharded: N/2 Trainers own shards of one model; Rollout t+N/2 holds shard t (NCCL P2P)",
+                  "the whole model and applies every Trainer's buckets (fan-out, P:61)",
+        "sharded": "sharded: N/2 Trainers own shards of one model; Rollout t+N/2 holds shard t",
     }[args.topology]
+    if d.world > 1:
+        topo_txt += {"nccl": "; data plane: NCCL P2P send/recv",
+                     "peer": "; data plane: NVLink peer memory (CUDA IPC), pulled by the copy engines",
+                     "peer-direct": "; data plane: NVLink peer memory, decoded in place by the decode kernel"}[
+            args.transport]
     strong = args.topology in ("fanout", "sharded")
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": d.world, "steps": K,
@@ -844,7 +1023,7 @@ def run_ours(args):
         "dtype": f"{'u8' if args.dtype == 'fp8' else 'u16'} ({args.dtype} bit patterns; integer/bit work only)",
         "data": "synthetic: random-init bf16 weights of the named architecture (N(0,0.02) quantile table), "
                 f"{args.mask}-mask sparse perturbations, seeded",
-        "config": {"workload": f"{manifest.name} bf16, {100 * (1 - args.rho):.1f}% sparsity, {args.mask} mask",
+        "config": {"workload": f"{manifest.name} {args.dtype}, {100 * (1 - args.rho):.1f}% sparsity, {args.mask} mask",
                    "topology_mode": args.topology,
                    "elements_per_trainer_rank": r.N, "model_elements": manifest.total,
                    "tensors": len(manifest.tensors),
@@ -872,8 +1051,10 @@ def run_ours(args):
                     "delta16_records": int(n16_t), "abs32_records": int(n32_t), "delta16e_records": int(n16e_t),
                     "paper_context": "paper: 32-54x raw, ~60-101x compressed on H100 clusters (P:22, P:380)"},
         "phase_hbm": phase_hbm,
-        "clocks": clk, "gpu_launches": int(launches), "bit_exact_replica": verify, "e2e": e2e,
+        "clocks": clk, "gpu_launches": int(launches), "bit_exact_replica": verify["bit_exact"] if verify else None,
+        "replica_check": verify, "e2e": e2e,
         "latency_per_update": latency,
+        "commit_scatter": k6,
     }
     if track_cmp is not None:
         out["tracking_vs_plain_cast"] = track_cmp
@@ -885,11 +1066,13 @@ def run_ours(args):
                          "what": "the input generator (new weights of each group into the scratch) runs inside "
                                  "the timed step; these subtract its per-step time (max over ranks)"}
     if parity is not None:
-        out["parity_sampled"] = parity
+        out["parity_full"] = parity["parity_full"]
     if cpu is not None:
         out["cpu_baseline"] = {"value": round(cpu["S"] / min(cpu["times"]) / 1e9, 4), "unit": UNIT, "cores": 1,
                                "kind": "oracle", "sample": cpu["sample"],
-                               "seconds": round(min(cpu["times"]), 3)}
+                               "seconds": round(min(cpu["times"]), 3), **cpu_info()}
+        if parity is not None:
+            out["cpu_baseline"]["all_cores"] = parity["cpu_all_cores"]
     d.close()
     return out if d.rank == 0 else None
 
@@ -939,9 +1122,12 @@ def run_e2e(args, d: Dist, r: Rank):
         # so keep both as host arrays; under --commit scatter the toggle regenerates them on the device
         n_host = 2 if args.commit == "swap" else 1
         try:
-            hosts = [torch.empty(r.Y.numel(), dtype=torch.int16, pin_memory=True) for _ in range(n_host)]
+            # the arena's own element type (uint8 under --dtype fp8): the pinned bytes are the S the guard counted
+            # and the H2D copy needs no cast (no device temporary)
+            hosts = [torch.empty_like(r.Y, device="cpu", pin_memory=True) for _ in range(n_host)]
         except Exception as e:
-            return {"value": None, "unit": UNIT, "reason": f"cannot pin {n_host * 2 * r.Y.numel() / 1e9:.0f} GB: {e}"}
+            return {"value": None, "unit": UNIT,
+                    "reason": f"cannot pin {n_host * r.Y.numel() * r.Y.element_size() / 1e9:.0f} GB: {e}"}
         hosts[0].copy_(r.Y)
         if n_host == 2:
             hosts[1].copy_(r.X)
@@ -963,9 +1149,10 @@ def run_e2e(args, d: Dist, r: Rank):
     ms = d.max(t0.elapsed_time(t1))
     total_S = d.sum(r.S)
     d2h = d.sum(sum(8 * p.counts.numel() for p in r.sender.parts) if r.sender is not None else 0)
+    h2d = d.sum(r.Y.numel() * r.Y.element_size() if hosts is not None else 0)   # counted from the copied tensor
     del hosts
     return {"value": round(total_S * K / (ms / 1e3) / 1e9, 3), "unit": UNIT,
-            "h2d_bytes_per_step": int(total_S), "d2h_bytes_per_step": int(d2h),
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "steps": K, "ms_per_step": round(ms / K, 3)}
 
 
@@ -983,7 +1170,7 @@ def run_reference(args):
     return {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus, "steps": K, "warmup": W,
             "ms_per_step": round(per * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u16 (bf16 bit patterns)", "data": "synthetic (same recipe as our arm)", "impl": "reference",
-            "config": {"workload": f"{manifest.name} bf16, {100 * (1 - args.rho):.1f}% sparsity, {args.mask} mask",
+            "config": {"workload": f"{manifest.name} {args.dtype}, {100 * (1 - args.rho):.1f}% sparsity, {args.mask} mask",
                        "codec": args.codec, "bucket_mb": args.bucket_mb},
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": cpu["sample"]},

@@ -161,12 +161,13 @@ int sync_compress(sync_ctx* ctx, const uint32_t* d_I, const uint16_t* d_V, const
                   uint8_t* d_enc, uint64_t enc_cap, sync_stream_t stream);
 
 /* ---- a5 bucket pack (Fig. workflow, C11) ----------------
- * BLOCKING until the record sizes of the preceding sync_compress are known:
- * runs the greedy bucketing on the host (the one host sync point of a sync),
- * then enqueues on `stream` the copy of every record into d_buckets plus the
- * headers, directories and (flag) CRC-32, and returns (the bucket bytes are
- * ready when `stream` reaches that point). Bucket b starts at h_offsets[b]
- * (256-aligned) and is h_sizes[b] bytes. *n_buckets = 0 when nothing changed. */
+ * Enqueues on `stream` the device bucket plan of the preceding sync_compress
+ * (greedy, DESIGN C11), the copy of every record into d_buckets, the headers,
+ * directories and (flag) CRC-32; then BLOCKS until the plan table is on the
+ * host (as sync_pack_result; the bucket bytes are ready when `stream` reaches
+ * that point). Bucket b starts at h_offsets[b] (256-aligned) and is
+ * h_sizes[b] bytes. *n_buckets = 0 when nothing changed. SYNC_ERR_CAPACITY as
+ * sync_compress_pack_async.                                                 */
 int sync_bucket_pack(sync_ctx* ctx, const uint8_t* d_enc, uint8_t* d_buckets, uint64_t buckets_cap,
                      uint32_t* n_buckets, uint64_t* h_offsets, uint64_t* h_sizes, uint32_t max_buckets,
                      sync_stream_t stream);
@@ -174,14 +175,32 @@ int sync_bucket_pack(sync_ctx* ctx, const uint8_t* d_enc, uint8_t* d_buckets, ui
 int sync_buckets_bound(sync_ctx* ctx, uint64_t* bytes, sync_stream_t stream);
 
 /* ---- a2-a5 fused: plan -> bucket plan -> encode in place -------------------
- * BLOCKING until the record sizes are known. Same bytes as sync_compress +
- * sync_bucket_pack, but every record is encoded straight into its bucket
- * position (no staging stream, no copy): plan + per-chunk model on the device,
- * greedy bucketing on the host from the record sizes (h_offsets / h_sizes are
- * final on return), then the encode kernel and the bucket headers/directories
- * (+ CRC) are enqueued on `stream`. If d_buckets is too small (or more than
- * max_buckets are needed) it returns SYNC_ERR_CAPACITY and *h_need (if not
- * NULL) holds the required buffer bytes; nothing is written.               */
+ * Same bytes as sync_compress + sync_bucket_pack, but every record is encoded
+ * straight into its bucket position (no staging stream, no copy). Everything
+ * runs on the device (bucketing and packing overlap the transfer):
+ * record plan + per-chunk model (K2), the greedy bucket plan (DESIGN C11,
+ * bucket.cu), the encode (K3), the bucket headers/directories (+ CRC, K4).
+ *
+ * sync_compress_pack_async: ENQUEUE-ONLY (never blocks; capturable in a CUDA
+ * graph). The bucket count / offsets / sizes land in the context's page-locked
+ * table once the bucket plan kernel has run; read them with sync_pack_result.
+ * If d_buckets is too small (buckets_cap) or more than max_buckets buckets are
+ * needed, SYNC_ERR_CAPACITY is latched in the device status word, nothing is
+ * encoded or written, and sync_pack_result reports it with the needed bytes.
+ *
+ * sync_pack_result: BLOCKS until the last enqueued bucket plan of this context
+ * is complete (an event right after the plan kernel: not the encode behind
+ * it), then copies n_buckets, h_offsets[0..n) / h_sizes[0..n) (host arrays of
+ * >= max_buckets entries) and *h_need (bytes of the bucket buffer the plan
+ * needs; may be NULL). Returns SYNC_ERR_CAPACITY (n_buckets = 0) if the plan
+ * did not fit, SYNC_ERR_ARG if nothing was enqueued.
+ *
+ * sync_compress_pack = sync_compress_pack_async + sync_pack_result (the host
+ * waits for the plan while the encode kernels run).                         */
+int sync_compress_pack_async(sync_ctx* ctx, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,
+                             uint8_t* d_buckets, uint64_t buckets_cap, uint32_t max_buckets, sync_stream_t stream);
+int sync_pack_result(sync_ctx* ctx, uint32_t* n_buckets, uint64_t* h_offsets, uint64_t* h_sizes,
+                     uint32_t max_buckets, uint64_t* h_need);
 int sync_compress_pack(sync_ctx* ctx, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,
                        uint8_t* d_buckets, uint64_t buckets_cap, uint32_t* n_buckets, uint64_t* h_offsets,
                        uint64_t* h_sizes, uint32_t max_buckets, uint64_t* h_need, sync_stream_t stream);
@@ -264,6 +283,12 @@ int sync_ctx_stats(sync_ctx* ctx, sync_stats* out, sync_stream_t stream);
 const char* sync_strerror(int status);
 /* Number of kernels the library launched since load (diagnostics). */
 uint64_t sync_launch_count(void);
+/* Process-wide cap on the CTAs of every kernel the library launches from now on (0 = no cap: the persistent
+ * kernels size their grid to the SM count x occupancy). For sharing the GPU with a concurrently running
+ * training step (as NCCL_MAX_CTAS does for collectives). Correctness never depends on how many CTAs are
+ * co-resident: K1 claims its tiles from a ticket, so any grid, and any number of resident CTAs, finishes
+ * (DESIGN.md §6 K1 forward progress). Returns SYNC_ERR_ARG for a negative value. Not stream-ordered.      */
+int sync_set_max_ctas(int max_ctas);
 
 #ifdef __cplusplus
 }

@@ -50,7 +50,7 @@ EXPORTS = [
     "sync_buckets_bound", "sync_compress_pack", "sync_bucket_unpack", "sync_decompress", "sync_decompress_apply", "sync_decompress_apply_batched", "sync_apply",
     "sync_commit_snapshot", "sync_commit_snapshot_batched", "sync_status", "sync_ctx_stats", "sync_strerror",
     "sync_launch_count", "sync_bitmap_words", "sync_cast_track_batched", "sync_extract_tracked",
-    "sync_set_current",
+    "sync_set_current", "sync_set_max_ctas", "sync_compress_pack_async", "sync_pack_result",
 ]
 # NVLink peer-memory plumbing (include/sparsesync_peer.h)
 PEER_EXPORTS = [
@@ -108,6 +108,8 @@ def lib() -> ctypes.CDLL:
             "sync_bucket_pack": [P, P, P, u64, P, P, P, u32, P],
             "sync_buckets_bound": [P, P, P],
             "sync_compress_pack": [P, P, P, P, P, u64, P, P, P, u32, P, P],
+            "sync_compress_pack_async": [P, P, P, P, P, u64, u32, P],
+            "sync_pack_result": [P, P, P, P, u32, P],
             "sync_bucket_unpack": [P, P, u64, P, u32, P, P],
             "sync_decompress": [P, P, u64, P, P, u64, P],
             "sync_decompress_apply": [P, P, u64, P, P],
@@ -139,6 +141,8 @@ def lib() -> ctypes.CDLL:
         L.sync_strerror.restype = ctypes.c_char_p
         L.sync_launch_count.argtypes = []
         L.sync_launch_count.restype = u64
+        L.sync_set_max_ctas.argtypes = [i32]
+        L.sync_set_max_ctas.restype = i32
         _lib = L
     return _lib
 
@@ -188,6 +192,11 @@ def ptr_table(tensors, device) -> torch.Tensor:
 
 def launch_count() -> int:
     return int(lib().sync_launch_count())
+
+
+def set_max_ctas(max_ctas: int) -> None:
+    """Cap the CTAs of every library kernel launched from now on (0 = no cap); see sync_set_max_ctas."""
+    _ck(lib().sync_set_max_ctas(int(max_ctas)), "sync_set_max_ctas")
 
 
 # ----------------------------------------------------------------------------- single-tensor calls
@@ -314,6 +323,25 @@ class SyncContext:
                                         self._max_buckets, ctypes.byref(need), _stream(stream))
         if code != SYNC_OK:
             err = SyncError(code, "sync_compress_pack")
+            err.need = need.value
+            raise err
+        return [(int(self._h_off[b]), int(self._h_size[b])) for b in range(nb.value)]
+
+    def sync_compress_pack_async(self, I: torch.Tensor, V: torch.Tensor, counts: torch.Tensor,
+                                 buckets: torch.Tensor, stream=None):
+        """Enqueue-only fused compress + pack (CUDA-graph capturable); read the plan with sync_pack_result."""
+        _ck(lib().sync_compress_pack_async(self._h, _ptr(I), _ptr(V), _dev_ptr(counts), _dev_ptr(buckets),
+                                           buckets.numel(), self._max_buckets, _stream(stream)),
+            "sync_compress_pack_async")
+
+    def sync_pack_result(self):
+        """Blocks until the last enqueued bucket plan is on the host; [(offset, size)] or SyncError (.need)."""
+        nb = ctypes.c_uint32()
+        need = ctypes.c_uint64()
+        code = lib().sync_pack_result(self._h, ctypes.byref(nb), self._h_off, self._h_size, self._max_buckets,
+                                      ctypes.byref(need))
+        if code != SYNC_OK:
+            err = SyncError(code, "sync_pack_result")
             err.need = need.value
             raise err
         return [(int(self._h_off[b]), int(self._h_size[b])) for b in range(nb.value)]

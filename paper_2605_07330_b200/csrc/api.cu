@@ -16,7 +16,17 @@ using namespace ss;
 
 namespace ss {
 static std::atomic<uint64_t> g_launches{0};
+static std::atomic<int> g_max_ctas{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < kMaxDevices ? dev : 0;
+}
+int clamp_ctas(int grid) {
+  const int m = g_max_ctas.load(std::memory_order_relaxed);
+  return (m > 0 && grid > m) ? m : grid;
+}
 }  // namespace ss
 
 namespace {
@@ -26,7 +36,7 @@ constexpr u64 kAlign = 256;
 struct Layout {
   u64 numel, tile_prefix, tile_tensor, misc, tile_state, stage_ring, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
   u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, rec_dst, totals, recs, bks, views, nviews, crc;
-  u64 bm_off, group_sum, chunk_esc, chunk_escoff, bitmap8, total;
+  u64 bm_off, group_sum, chunk_esc, chunk_escoff, bitmap8, rec_list, srec, crec, nxt, bstart, seg_off, total;
 };
 
 u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4 + 32; }  // + 32 bad flags
@@ -68,6 +78,12 @@ Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_change
   L.chunk_esc = take(4ull * max_chunks);                   // f4: escapes per chunk
   L.chunk_escoff = take(8ull * (max_chunks + 1));          // f4: their exclusive prefix
   L.bitmap8 = take(4ull * bm8_words);                      // FP8: change bitmap of the extract
+  L.rec_list = take(4ull * T);                             // device bucket plan (bucket.cu)
+  L.srec = take(8ull * (T + 1));
+  L.crec = take(8ull * (T + 1));
+  L.nxt = take(4ull * T);
+  L.bstart = take(4ull * (T + 1));
+  L.seg_off = take(8ull * (T + 1));
   L.total = o;
   return L;
 }
@@ -96,7 +112,11 @@ int check_manifest(const sync_manifest* m, const sync_config* c, Dims* d) {
   // largest possible record (one tensor fully changed): bounds a received bucket for the CRC scratch
   d->max_record = 6 * maxn + 20 * ((maxn + kChunk - 1) / kChunk) + 64;
   u64 mb = c->bucket_limit > d->max_record + 64 ? c->bucket_limit : d->max_record + 64;
-  d->crc_n = crc_slots(mb);
+  // CRC scratch: one received bucket (receiver), or the segments of every bucket of a sender plan: payload
+  // <= the encoded-stream bound + bucket headers/directories, + one partial segment per bucket
+  const u64 enc_bound = 6 * c->max_changed + 20 * d->max_chunks + 64ull * d->T + 64;
+  const u64 send_segs = (enc_bound + 64ull * (d->T + 1) + 8ull * d->T) / 65536 + d->T + 1;
+  d->crc_n = crc_slots(mb) > send_segs ? crc_slots(mb) : send_segs;
   return SYNC_OK;
 }
 
@@ -108,28 +128,6 @@ inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
   } while (0)
 
 }  // namespace
-
-// Page-locked host memory for the per-sync host<->device tables: the copies are truly asynchronous, and the
-// next call's read_plan() synchronises the stream before the host touches them again.
-template <class T>
-struct PinnedAlloc {
-  using value_type = T;
-  PinnedAlloc() = default;
-  template <class U>
-  PinnedAlloc(const PinnedAlloc<U>&) {}
-  T* allocate(size_t n) {
-    void* p = nullptr;
-    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
-    return static_cast<T*>(p);
-  }
-  void deallocate(T* p, size_t) { cudaFreeHost(p); }
-  template <class U>
-  bool operator==(const PinnedAlloc<U>&) const { return true; }
-  template <class U>
-  bool operator!=(const PinnedAlloc<U>&) const { return false; }
-};
-template <class T>
-using pvec = std::vector<T, PinnedAlloc<T>>;
 
 struct sync_ctx {
   Dims d;
@@ -146,10 +144,16 @@ struct sync_ctx {
   int grid;   // grid-stride kernels: CTAs of 256 threads
   const u64* plan_counts;
   bool plan_valid;
-  pvec<u64> h_rec_bytes, h_chunk_off, h_enc_off, h_totals, h_rec_dst;
-  pvec<u32> h_rec_mode;
-  pvec<RecordDesc> h_recs;
-  pvec<BucketDesc> h_bks;
+  // the device bucket plan's result table, written by k_bucket_plan straight into mapped page-locked host
+  // memory: {n_buckets, failed, need} + offsets[T + 1] + sizes[T + 1]; valid once pack_ev has completed
+  u64* h_pack;
+  u64* d_pack;
+  cudaEvent_t pack_ev;
+  bool pack_pending;
+  ~sync_ctx() {
+    if (h_pack) cudaFreeHost(h_pack);
+    if (pack_ev) cudaEventDestroy(pack_ev);
+  }
 };
 
 extern "C" {
@@ -217,19 +221,16 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
     return SYNC_ERR_CUDA;
   }
   x->misc = reinterpret_cast<u32*>(w + L.misc);
-  try {   // pinned host tables, sized once
-    x->h_rec_bytes.reserve(d.T);
-    x->h_rec_mode.reserve(d.T);
-    x->h_chunk_off.reserve(d.T + 1);
-    x->h_enc_off.reserve(d.T + 1);
-    x->h_totals.reserve(16);
-    x->h_rec_dst.reserve(d.T);
-    x->h_recs.reserve(d.T);
-    x->h_bks.reserve(d.T + 1);
-  } catch (...) {
+  x->h_pack = nullptr;
+  x->pack_ev = nullptr;
+  x->pack_pending = false;
+  if (cudaHostAlloc(&x->h_pack, 8ull * (4 + 2 * (d.T + 1)), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&x->d_pack, x->h_pack, 0) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->pack_ev, cudaEventDisableTiming) != cudaSuccess) {
     delete x;
     return SYNC_ERR_CUDA;
   }
+  memset(x->h_pack, 0, 8ull * (4 + 2 * (d.T + 1)));
   Plan& p = x->plan;
   p.n_tensors = d.T;
   p.cap = c->max_changed;
@@ -256,6 +257,9 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   p.word_scratch = reinterpret_cast<u16*>(w + L.word_scratch);
   p.totals = reinterpret_cast<u64*>(w + L.totals);
   p.status = x->misc + 1;
+  p.rec_list = reinterpret_cast<u32*>(w + L.rec_list);
+  p.srec = reinterpret_cast<u64*>(w + L.srec);
+  p.crec = reinterpret_cast<u64*>(w + L.crec);
   int dev = 0;
   cudaGetDevice(&dev);
   x->sm_count = 148;
@@ -295,7 +299,7 @@ int sync_extract(const uint16_t* d_old, const uint16_t* d_new, uint64_t n, uint3
   CK(cudaMemsetAsync(misc, 0, 4, s));  // tile counter (status is sticky until read)
   CK(cudaMemsetAsync(d_count, 0, 8, s));
   if (n_tiles) CK(cudaMemsetAsync(w + kAlign, 0, 8 * n_tiles, s));
-  launch_extract_single(d_old, d_new, n, d_I, d_V, cap, d_count, reinterpret_cast<u64*>(w + kAlign),
+  launch_extract_single(d_old, d_new, n, d_I, d_V, cap, d_count, reinterpret_cast<u64*>(w + kAlign), misc,
                         reinterpret_cast<u32*>(w + kAlign + pad_to(8 * n_tiles + 8, kAlign)), misc + 1,
                         s);
   CK(cudaGetLastError());
@@ -329,14 +333,14 @@ int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const u
     a.I = d_I;
     a.V = d_V;
     launch_extract8(a, reinterpret_cast<const uint8_t* const*>(d_old_ptrs),
-                    reinterpret_cast<const uint8_t* const*>(d_new_ptrs), 16 * x->sm_count, s);
+                    reinterpret_cast<const uint8_t* const*>(d_new_ptrs), clamp_ctas(16 * x->sm_count), s);
     CK(cudaGetLastError());
     return SYNC_OK;
   }
   if (x->d.n_tiles) CK(cudaMemsetAsync(x->ws + x->L.tile_state, 0, 8 * x->d.n_tiles, s));
   launch_extract_batched(d_old_ptrs, d_new_ptrs, reinterpret_cast<const u64*>(x->ws + x->L.tile_prefix),
                          reinterpret_cast<const u32*>(x->ws + x->L.tile_tensor), x->plan.numel, x->d.T, x->d.n_tiles, d_I, d_V, x->cfg.max_changed, d_counts,
-                         reinterpret_cast<u64*>(x->ws + x->L.tile_state),
+                         reinterpret_cast<u64*>(x->ws + x->L.tile_state), x->misc,
                          reinterpret_cast<u32*>(x->ws + x->L.stage_ring), x->misc + 1, s,
                          x->plan.dtype == SYNC_DTYPE_FP8 ? 1 : 2);
   CK(cudaGetLastError());
@@ -378,7 +382,7 @@ int sync_cast_track_batched(sync_ctx* x, const float* const* d_master_ptrs, uint
   if (!x || (x->d.T && (!d_master_ptrs || !d_weight_ptrs || !d_bitmap))) return SYNC_ERR_ARG;
   if (x->d.T && !aligned16(d_bitmap)) return SYNC_ERR_ALIGNMENT;
   if (x->plan.dtype != SYNC_DTYPE_BF16) return SYNC_ERR_DTYPE;   // the cast is round_BF16 (Alg. 1 l.5)
-  launch_cast_track(track_args(x, d_bitmap), d_master_ptrs, d_weight_ptrs, 8 * x->sm_count, (cudaStream_t)stream);
+  launch_cast_track(track_args(x, d_bitmap), d_master_ptrs, d_weight_ptrs, clamp_ctas(8 * x->sm_count), (cudaStream_t)stream);
   CK(cudaGetLastError());
   return SYNC_OK;
 }
@@ -392,7 +396,7 @@ int sync_extract_tracked(sync_ctx* x, uint16_t* const* d_weight_ptrs, uint32_t* 
   a.counts = d_counts;
   a.I = d_I;
   a.V = d_V;
-  launch_extract_tracked(a, d_weight_ptrs, clear, 16 * x->sm_count, (cudaStream_t)stream);
+  launch_extract_tracked(a, d_weight_ptrs, clear, clamp_ctas(16 * x->sm_count), (cudaStream_t)stream);
   CK(cudaGetLastError());
   return SYNC_OK;
 }
@@ -416,9 +420,9 @@ int sync_compress(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const u
   x->plan.enc_cap = enc_cap;
   launch_plan_scan(x->plan, d_counts, s);
   // CTA-per-chunk kernels of 128 threads: 2x the grid of the 256-thread kernels (~9 resident per SM)
-  if (x->cfg.codec == SYNC_CODEC_COMPRESSED) launch_chunk_stats(x->plan, d_I, d_V, d_counts, 2 * x->grid, s);
+  if (x->cfg.codec == SYNC_CODEC_COMPRESSED) launch_chunk_stats(x->plan, d_I, d_V, d_counts, clamp_ctas(2 * x->grid), s);
   launch_plan_sizes(x->plan, d_counts, s);
-  launch_encode(x->plan, d_I, d_V, d_counts, d_enc, 2 * x->grid, s);
+  launch_encode(x->plan, d_I, d_V, d_counts, d_enc, clamp_ctas(2 * x->grid), s);
   CK(cudaGetLastError());
   x->plan_counts = d_counts;
   x->plan_valid = true;
@@ -426,157 +430,134 @@ int sync_compress(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const u
 }
 
 // ------------------------------------------------------------------------ pack
-static int read_plan(sync_ctx* x, cudaStream_t s) {
-  const u32 T = x->d.T;
-  x->h_rec_bytes.resize(T);
-  x->h_rec_mode.resize(T);
-  x->h_chunk_off.resize(T + 1);
-  x->h_enc_off.resize(T + 1);
-  x->h_totals.resize(16);
-  if (T) {
-    CK(cudaMemcpyAsync(x->h_rec_bytes.data(), x->plan.rec_bytes, 8ull * T, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(x->h_rec_mode.data(), x->plan.rec_mode, 4ull * T, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(x->h_chunk_off.data(), x->plan.chunk_off, 8ull * (T + 1), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(x->h_enc_off.data(), x->plan.enc_off, 8ull * (T + 1), cudaMemcpyDeviceToHost, s));
-  }
-  CK(cudaMemcpyAsync(x->h_totals.data(), x->plan.totals, 8 * 16, cudaMemcpyDeviceToHost, s));
+static int read_totals(sync_ctx* x, u64* t, cudaStream_t s) {
+  CK(cudaMemcpyAsync(t, x->plan.totals, 8 * 16, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return SYNC_OK;
 }
 
 int sync_buckets_bound(sync_ctx* x, uint64_t* bytes, sync_stream_t stream) {
   if (!x || !bytes || !x->plan_valid) return SYNC_ERR_ARG;
-  int st = read_plan(x, (cudaStream_t)stream);
+  u64 t[16];
+  int st = read_totals(x, t, (cudaStream_t)stream);
   if (st) return st;
-  u64 nr = x->h_totals[kTotRecords];
-  *bytes = x->h_totals[kTotEnc] + 8 * nr + (nr + 1) * (32 + 16 + kBucketAlign);
+  u64 nr = t[kTotRecords];
+  *bytes = t[kTotEnc] + 8 * nr + (nr + 1) * (32 + 16 + kBucketAlign);
   return SYNC_OK;
 }
 
-// Greedy bucket plan (DESIGN C11) from the record sizes read back by read_plan():
-// fills x->h_recs / x->h_bks and the caller's offsets/sizes. Host-side bookkeeping only.
-static int plan_buckets(sync_ctx* x, uint64_t buckets_cap, uint32_t max_buckets, uint64_t* h_offsets,
-                        uint64_t* h_sizes, uint32_t* n_buckets, uint64_t* h_need) {
-  const u32 T = x->d.T;
-  const u64 L = x->cfg.bucket_limit;
-  x->h_recs.clear();
-  x->h_bks.clear();
-  // size(bucket) = 32 + pad16(8 n) + Σ record_bytes; a record never splits; an oversized record sits alone
-  u64 base = 0;
-  BucketDesc cur{};
-  u64 cur_sum = 0;
-  auto close = [&]() {
-    if (cur.n_records == 0) return;
-    cur.bytes = 32 + pad_to(8ull * cur.n_records, 16) + cur_sum;
-    cur.base = pad_to(base, kBucketAlign);
-    base = cur.base + cur.bytes;
-    cur.seq = (u32)x->h_bks.size();
-    x->h_bks.push_back(cur);
-    cur = BucketDesc{};
-    cur_sum = 0;
-  };
-  for (u32 t = 0; t < T; ++t) {
-    const u64 rb = x->h_rec_bytes[t];
-    if (!rb) continue;
-    if (cur.n_records && 32 + pad_to(8ull * (cur.n_records + 1), 16) + cur_sum + rb > L) close();
-    if (cur.n_records == 0) cur.first_record = (u32)x->h_recs.size();
-    RecordDesc r{};
-    r.src = x->h_enc_off[t];
-    r.bytes = (u32)rb;
-    r.tensor = t;
-    r.first_chunk = cur.n_chunks;
-    r.dst = cur_sum;  // provisional: offset within the record area
-    x->h_recs.push_back(r);
-    cur.n_records++;
-    // chunks of a record on the wire = ceil(nnz field / C); a FULL record's nnz field is numel
-    cur.n_chunks += x->h_rec_mode[t] == kModeFull ? (u32)((x->numel[t] + kChunk - 1) / kChunk)
-                                                  : (u32)(x->h_chunk_off[t + 1] - x->h_chunk_off[t]);
-    cur_sum += rb;
+// Enqueue the device bucket plan (bucket.cu) and the bucket assembly after it. fused: the records are encoded
+// straight into their bucket positions (k_encode after the plan); else d_enc holds the contiguous encoded
+// stream of sync_compress and k_pack_copy moves it. pack_ev completes when the plan table is in host memory,
+// ahead of the encode/copy kernels behind it.
+static int enqueue_pack(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,
+                        const uint8_t* d_enc, uint8_t* d_buckets, uint64_t buckets_cap, uint32_t max_buckets,
+                        cudaStream_t s) {
+  const Layout& L = x->L;
+  u8* w = x->ws;
+  u64* d_dst = reinterpret_cast<u64*>(w + L.rec_dst);
+  BucketPlan b{};
+  b.rec_list = x->plan.rec_list;
+  b.srec = x->plan.srec;
+  b.crec = x->plan.crec;
+  b.enc_off = x->plan.enc_off;
+  b.nxt = reinterpret_cast<u32*>(w + L.nxt);
+  b.bstart = reinterpret_cast<u32*>(w + L.bstart);
+  b.seg_off = reinterpret_cast<u64*>(w + L.seg_off);
+  b.recs = reinterpret_cast<RecordDesc*>(w + L.recs);
+  b.bks = reinterpret_cast<BucketDesc*>(w + L.bks);
+  b.rec_dst = d_enc ? nullptr : d_dst;
+  b.totals = x->plan.totals;
+  b.status = x->plan.status;
+  b.limit = x->cfg.bucket_limit;
+  b.cap_bytes = buckets_cap;
+  b.max_buckets = max_buckets;
+  b.out_hdr = x->d_pack;
+  b.out_off = x->d_pack + 4;
+  b.out_size = x->d_pack + 4 + (x->d.T + 1);
+  launch_bucket_plan(b, x->d.T, x->sm_count, s);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(s, &cap));
+  if (cap == cudaStreamCaptureStatusActive) CK(cudaEventRecordWithFlags(x->pack_ev, s, cudaEventRecordExternal));
+  else CK(cudaEventRecord(x->pack_ev, s));
+  x->pack_pending = true;
+  if (!d_enc) {   // fused: encode every record into its bucket position
+    x->plan.rec_dst = d_dst;
+    launch_encode(x->plan, d_I, d_V, d_counts, d_buckets, clamp_ctas(2 * x->grid), s);
+    x->plan.rec_dst = x->plan.enc_off;
   }
-  close();
-  const u32 nb = (u32)x->h_bks.size();
-  if (h_need) *h_need = base;
-  if (nb > max_buckets || base > buckets_cap) return SYNC_ERR_CAPACITY;
-  for (u32 b = 0; b < nb; ++b) {
-    const BucketDesc& bk = x->h_bks[b];
-    const u64 rec0 = 32 + pad_to(8ull * bk.n_records, 16);
-    for (u32 q = 0; q < bk.n_records; ++q) {
-      RecordDesc& r = x->h_recs[bk.first_record + q];
-      r.dir_offset = (u32)(rec0 + r.dst);
-      r.dst = bk.base + rec0 + r.dst;
-    }
-    if (h_offsets) h_offsets[b] = bk.base;
-    if (h_sizes) h_sizes[b] = bk.bytes;
-  }
-  *n_buckets = nb;
-  return SYNC_OK;
-}
-
-static int finish_buckets(sync_ctx* x, uint8_t* d_buckets, const uint8_t* d_enc, cudaStream_t s) {
-  const u32 nb = (u32)x->h_bks.size();
-  RecordDesc* d_recs = reinterpret_cast<RecordDesc*>(x->ws + x->L.recs);
-  BucketDesc* d_bks = reinterpret_cast<BucketDesc*>(x->ws + x->L.bks);
-  CK(cudaMemcpyAsync(d_recs, x->h_recs.data(), sizeof(RecordDesc) * x->h_recs.size(), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(d_bks, x->h_bks.data(), sizeof(BucketDesc) * nb, cudaMemcpyHostToDevice, s));
-  launch_pack(d_enc, d_buckets, d_recs, (u32)x->h_recs.size(), d_bks, nb, d_enc ? x->h_totals[kTotEnc] : 0,
-              x->cfg.flags, x->grid, s);
-  if (x->cfg.flags & SYNC_FLAG_CRC) {
-    for (u32 b = 0; b < nb; ++b)
-      if (crc_slots(x->h_bks[b].bytes) > x->d.crc_n) return SYNC_ERR_CAPACITY;
-    crc_fill(d_buckets, x->h_bks.data(), nb, reinterpret_cast<u32*>(x->ws + x->L.crc), s);
-  }
+  const u32 T1 = x->d.T ? x->d.T : 1u;
+  const u32 mb = max_buckets < T1 ? max_buckets : T1;
+  launch_pack(d_enc, d_buckets, b.recs, b.bks, b.totals, mb, x->cfg.flags, clamp_ctas(x->grid), s);
+  if (x->cfg.flags & SYNC_FLAG_CRC)
+    crc_fill(d_buckets, b.bks, b.seg_off, b.totals, mb, reinterpret_cast<u32*>(w + L.crc), clamp_ctas(x->grid), s);
   CK(cudaGetLastError());
-  // no host wait: the H2D sources are pinned ctx tables, rewritten only after the next read_plan() sync
+  return SYNC_OK;
+}
+
+int sync_pack_result(sync_ctx* x, uint32_t* n_buckets, uint64_t* h_offsets, uint64_t* h_sizes,
+                     uint32_t max_buckets, uint64_t* h_need) {
+  if (!x || !n_buckets) return SYNC_ERR_ARG;
+  *n_buckets = 0;
+  if (h_need) *h_need = 0;
+  if (!x->pack_pending) return SYNC_ERR_ARG;
+  CK(cudaEventSynchronize(x->pack_ev));
+  const volatile u64* hp = x->h_pack;
+  const u64 nb = hp[0], failed = hp[1];
+  if (h_need) *h_need = hp[2];
+  if (failed) return SYNC_ERR_CAPACITY;   // latched on the device too; nothing was encoded or packed
+  if (nb > max_buckets) return SYNC_ERR_CAPACITY;
+  const u64* off = x->h_pack + 4;
+  const u64* sz = x->h_pack + 4 + (x->d.T + 1);
+  for (u64 b = 0; b < nb; ++b) {
+    if (h_offsets) h_offsets[b] = off[b];
+    if (h_sizes) h_sizes[b] = sz[b];
+  }
+  *n_buckets = (u32)nb;
   return SYNC_OK;
 }
 
 int sync_bucket_pack(sync_ctx* x, const uint8_t* d_enc, uint8_t* d_buckets, uint64_t buckets_cap,
                      uint32_t* n_buckets, uint64_t* h_offsets, uint64_t* h_sizes, uint32_t max_buckets,
                      sync_stream_t stream) {
-  if (!x || !n_buckets || !x->plan_valid) return SYNC_ERR_ARG;
+  if (!x || !n_buckets || !x->plan_valid || !d_enc) return SYNC_ERR_ARG;
   if (!aligned16(d_buckets) || !aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
-  cudaStream_t s = (cudaStream_t)stream;
   *n_buckets = 0;
-  int st = read_plan(x, s);
+  int st = enqueue_pack(x, nullptr, nullptr, nullptr, d_enc, d_buckets, buckets_cap, max_buckets,
+                        (cudaStream_t)stream);
   if (st) return st;
-  if (x->h_totals[kTotOverflow]) return SYNC_ERR_CAPACITY;
-  st = plan_buckets(x, buckets_cap, max_buckets, h_offsets, h_sizes, n_buckets, nullptr);
-  if (st || *n_buckets == 0) return st;
-  return finish_buckets(x, d_buckets, d_enc, s);
+  return sync_pack_result(x, n_buckets, h_offsets, h_sizes, max_buckets, nullptr);
+}
+
+int sync_compress_pack_async(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,
+                             uint8_t* d_buckets, uint64_t buckets_cap, uint32_t max_buckets, sync_stream_t stream) {
+  if (!x || (x->d.T && !d_counts)) return SYNC_ERR_ARG;
+  if (x->plan.route && !x->plan.cur) return SYNC_ERR_ARG;   // SYNC_FLAG_ROUTE needs sync_set_current
+  if (!aligned16(d_buckets)) return SYNC_ERR_ALIGNMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  // plan (record sizes) exactly as sync_compress, without the encode
+  x->plan.enc_cap = ~0ull;
+  x->plan.rec_dst = x->plan.enc_off;
+  launch_plan_scan(x->plan, d_counts, s);
+  if (x->cfg.codec == SYNC_CODEC_COMPRESSED)
+    launch_chunk_stats(x->plan, d_I, d_V, d_counts, clamp_ctas(2 * x->grid), s);
+  launch_plan_sizes(x->plan, d_counts, s);
+  CK(cudaGetLastError());
+  x->plan_counts = d_counts;
+  x->plan_valid = true;
+  return enqueue_pack(x, d_I, d_V, d_counts, nullptr, d_buckets, buckets_cap, max_buckets, s);
 }
 
 int sync_compress_pack(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,
                        uint8_t* d_buckets, uint64_t buckets_cap, uint32_t* n_buckets, uint64_t* h_offsets,
                        uint64_t* h_sizes, uint32_t max_buckets, uint64_t* h_need, sync_stream_t stream) {
-  if (!x || !n_buckets || (x->d.T && !d_counts)) return SYNC_ERR_ARG;
-  if (x->plan.route && !x->plan.cur) return SYNC_ERR_ARG;   // SYNC_FLAG_ROUTE needs sync_set_current
-  if (!aligned16(d_buckets)) return SYNC_ERR_ALIGNMENT;
-  cudaStream_t s = (cudaStream_t)stream;
+  if (!n_buckets) return SYNC_ERR_ARG;
   *n_buckets = 0;
   if (h_need) *h_need = 0;
-  // plan (record sizes) exactly as sync_compress, without the encode
-  x->plan.enc_cap = ~0ull;
-  x->plan.rec_dst = x->plan.enc_off;
-  launch_plan_scan(x->plan, d_counts, s);
-  if (x->cfg.codec == SYNC_CODEC_COMPRESSED) launch_chunk_stats(x->plan, d_I, d_V, d_counts, 2 * x->grid, s);
-  launch_plan_sizes(x->plan, d_counts, s);
-  CK(cudaGetLastError());
-  x->plan_counts = d_counts;
-  x->plan_valid = true;
-  int st = read_plan(x, s);
+  int st = sync_compress_pack_async(x, d_I, d_V, d_counts, d_buckets, buckets_cap, max_buckets, stream);
   if (st) return st;
-  if (x->h_totals[kTotOverflow]) return SYNC_ERR_CAPACITY;
-  st = plan_buckets(x, buckets_cap, max_buckets, h_offsets, h_sizes, n_buckets, h_need);
-  if (st || *n_buckets == 0) return st;
-  // each record is encoded straight into its bucket position (no staging copy)
-  x->h_rec_dst.assign(x->d.T, 0);
-  for (const RecordDesc& r : x->h_recs) x->h_rec_dst[r.tensor] = r.dst;
-  u64* d_dst = reinterpret_cast<u64*>(x->ws + x->L.rec_dst);
-  CK(cudaMemcpyAsync(d_dst, x->h_rec_dst.data(), 8ull * x->d.T, cudaMemcpyHostToDevice, s));
-  x->plan.rec_dst = d_dst;
-  launch_encode(x->plan, d_I, d_V, d_counts, d_buckets, 2 * x->grid, s);
-  x->plan.rec_dst = x->plan.enc_off;
-  return finish_buckets(x, d_buckets, nullptr, s);
+  // the host waits for the plan table only: the encode / pack kernels queued behind it keep the GPU busy
+  return sync_pack_result(x, n_buckets, h_offsets, h_sizes, max_buckets, h_need);
 }
 
 // ------------------------------------------------------------------------ receive
@@ -622,7 +603,7 @@ int sync_decompress(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, uint32
   u32* nv = reinterpret_cast<u32*>(x->ws + x->L.nviews);
   launch_unpack(d_bucket, bytes, x->d.T, x->plan.numel, views, x->d.T, nv, x->plan.status, x->plan.dtype, s);
   launch_decode(&d_bucket, &bytes, 1, x->d.T, x->plan.numel, nullptr, views, d_I, d_V, d_cap, x->plan.status, bad,
-                x->plan.dtype, x->grid, decode_is_dense(&bytes, 1, x->total_elems), s);
+                x->plan.dtype, clamp_ctas(x->grid), decode_is_dense(&bytes, 1, x->total_elems), s);
   CK(cudaGetLastError());
   return SYNC_OK;
 }
@@ -636,7 +617,7 @@ int sync_decompress_apply(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, 
   int st = maybe_crc_check(x, &d_bucket, &bytes, 1, s, &bad);
   if (st) return st;
   launch_decode(&d_bucket, &bytes, 1, x->d.T, x->plan.numel, d_weight_ptrs, nullptr, nullptr, nullptr, 0,
-                x->plan.status, bad, x->plan.dtype, x->grid, decode_is_dense(&bytes, 1, x->total_elems), s);
+                x->plan.status, bad, x->plan.dtype, clamp_ctas(x->grid), decode_is_dense(&bytes, 1, x->total_elems), s);
   CK(cudaGetLastError());
   return SYNC_OK;
 }
@@ -654,7 +635,7 @@ int sync_decompress_apply_batched(sync_ctx* x, const uint8_t* const* h_buckets, 
     int st = maybe_crc_check(x, h_buckets + b0, h_bytes + b0, n, s, &bad);
     if (st) return st;
     launch_decode(h_buckets + b0, h_bytes + b0, n, x->d.T, x->plan.numel, d_weight_ptrs, nullptr, nullptr,
-                  nullptr, 0, x->plan.status, bad, x->plan.dtype, x->grid, dense, s);
+                  nullptr, 0, x->plan.status, bad, x->plan.dtype, clamp_ctas(x->grid), dense, s);
   }
   CK(cudaGetLastError());
   return SYNC_OK;
@@ -685,7 +666,7 @@ int sync_commit_snapshot_batched(sync_ctx* x, uint16_t* const* d_snapshot_ptrs, 
     launch_plan_scan(x->plan, d_counts, s);
     x->plan_valid = false;
   }
-  launch_commit_batched(x->plan, d_snapshot_ptrs, d_I, d_V, x->grid, s);
+  launch_commit_batched(x->plan, d_snapshot_ptrs, d_I, d_V, clamp_ctas(x->grid), s);
   CK(cudaGetLastError());
   return SYNC_OK;
 }
@@ -740,5 +721,11 @@ const char* sync_strerror(int status) {
 }
 
 uint64_t sync_launch_count(void) { return g_launches.load(); }
+
+int sync_set_max_ctas(int max_ctas) {
+  if (max_ctas < 0) return SYNC_ERR_ARG;
+  g_max_ctas.store(max_ctas, std::memory_order_relaxed);
+  return SYNC_OK;
+}
 
 }  // extern "C"

@@ -23,6 +23,7 @@ constexpr u32 kLow = 1u << 16;              // rANS lower bound
 constexpr u32 kMagic = 0x424C5253u;         // "SRLB"
 constexpr u32 kVersion = 1;
 constexpr u64 kBucketAlign = 256;
+constexpr u64 kCrcSegBytes = 65536;         // CRC-32 segment (one CTA of k_crc_seg)
 // rANS block head kept by the stats pass: 32 lane states, nwords, nsym, <= 256 entries
 constexpr u32 kRhdrWords = 34 + 256;
 

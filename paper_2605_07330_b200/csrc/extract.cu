@@ -8,23 +8,29 @@
 // density). Persistent, warp-specialised kernel (DESIGN §6 K1). A tile (the
 // look-back unit) is 32768 elements of one tensor, streamed as four 8192-
 // element sub-tiles (16 KB of old + 16 KB of new each):
-//   * scheduler warp: CTA c owns tiles c, c+G, c+2G, ...; resolves tile ->
-//     tensor / pointers a few tiles ahead (tile table + one round of loads);
+//   * scheduler warp: claims the CTA's next tile from a global ticket
+//     (atomicAdd), so tiles are taken in increasing order by CTAs that are
+//     already running; resolves tile -> tensor / pointers a few tiles ahead
+//     (tile table + one round of loads);
 //   * copier warp: TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx)
 //     of each sub-tile into one of kStages shared-memory stages;
 //   * 8 consumer warps: per sub-tile, an 8-bit change mask per 128-bit vector,
 //     one block scan, append (local index | value << 16) to the
 //     tile's staging slot (a per-CTA ring of kSlots slots in global memory,
 //     L2-resident); at the end of the tile publish its aggregate at once;
-//   * writer warps: per tile, the global offset from its own previous tile's
-//     prefix plus the counts published in between (the only wait on other
-//     CTAs), then the coalesced write of (I, V).
+//   * writer warps: per tile, the global offset from the CTA's own previous
+//     tile's prefix plus the counts published in between (the only wait on
+//     other CTAs), then the coalesced write of (I, V).
 //     The ring gives the writer kSlots tiles of slack, so the look-back
 //     latency never stalls the stream.
 //   * tiles denser than a slot (> 12.5%) take a slow path: the writer re-reads
 //     the tile from global and writes directly.
-// All CTAs are resident and each counts its tiles in increasing order, so
-// every count a writer waits for is eventually published.
+// Forward progress without co-residency: a writer of tile j waits only for
+// counts of tiles < j, all claimed (the ticket is monotonic) by CTAs that are
+// running. By induction on the smallest unpublished tile m: its CTA's earlier
+// tiles are < m, so their writers' windows are complete, the ring drains and
+// m gets counted. Any number of resident CTAs (MPS, green contexts, a kernel
+// spinning on another stream) therefore finishes the launch.
 #include <cstdio>
 #include <type_traits>
 #include <cstdlib>
@@ -56,6 +62,7 @@ struct ExtractArgs {
   u64 cap;
   u64* counts;                 // [T]
   u64* tile_state;             // [n_tiles]
+  u32* ticket;                 // next unclaimed tile (zeroed before the launch)
   u32* stage_ring;             // [grid][kSlots][kSlotCap]
   u32* status;
   unsigned long long* prof;    // debug cycle counters (SS_XPROF=1), else null
@@ -87,6 +94,7 @@ struct StagedTile {            // consumers -> writer, one per ring slot
   u64 tile;                    // ~0 = no more tiles
   u64 tile_base;               // first element of the tile within its tensor
   u64 tile_end;
+  u64 prev;                    // the CTA's previous tile (~0 = none): the writer's window starts after it
   const u16* po;
   const u16* pn;
   u32 t;
@@ -99,14 +107,15 @@ __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" 
 
 // ---------------------------------------------------------------- cross-CTA prefix
 // Tile states: bit 63 = published, [62:0] = the tile's change count. Consumers
-// publish a tile's count as soon as it is counted. With the static round-robin
-// assignment (tile j = c + k*G), the writer of CTA c already knows the inclusive
-// prefix of its own previous tile j-G, so
-//     excl(j) = incl(j-G) + sum_{i = j-G+1}^{j-1} count(i)
-// needs only the G-1 counts in between — published by consumers, never by other
-// writers, so no chain of look-backs forms. One L2 round trip reads the whole
-// window (32 lanes x kLB contiguous states); entries not yet published are
-// re-polled alone, with a short back-off.
+// publish a tile's count as soon as it is counted. The writer of CTA c already
+// knows the inclusive prefix of c's previous tile p (claimed earlier from the
+// ticket), so
+//     excl(j) = incl(p) + sum_{i = p+1}^{j-1} count(i)
+// needs only the counts in between (about G-1 of them when all CTAs run) —
+// published by consumers, never by other writers, so no chain of look-backs
+// forms. A CTA's first tile sums from tile 0. One L2 round trip reads 32 x kLB
+// contiguous states; entries not yet published are re-polled alone, with a
+// short back-off.
 constexpr int kLB = 16;  // window 512 >= G - 1 for G <= 513 CTAs
 constexpr u64 kPublished = 1ull << 63;
 
@@ -237,7 +246,9 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
     for (u32 k = 0;; ++k) {
       const u32 q = k % kXQueue;
       if (k >= (u32)kXQueue) mbar_wait(&qempty[q], ((k / kXQueue) - 1) & 1);
-      const u64 tile = (u64)blockIdx.x + (u64)k * gridDim.x;
+      u32 tk = 0;
+      if (lane == 0) tk = atomicAdd(a.ticket, 1u);
+      const u64 tile = __shfl_sync(0xffffffffu, tk, 0);
       if (tile >= a.n_tiles) {
         if (lane == 0) {
           jobs[q].tile = ~0ull;
@@ -344,7 +355,6 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
     // (through shared memory).
     const u32 w = warp - (kXConsumers / 32 + 2);
     long long p_w = 0, p_lb = 0, p_wr = 0, n_t = 0;
-    const u64 G = gridDim.x;
     for (u32 k = w;; k += kWriters) {
       const u32 b = k % kSlots;
       long long c0 = clock64();
@@ -353,10 +363,11 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       p_w += c1 - c0;
       const StagedTile m = meta[b];
       if (m.tile == ~0ull) break;
-      const u64 win = window_sum(a.tile_state, m.tile < G ? 0ull : m.tile - G + 1, m.tile);
+      const bool first = m.prev == ~0ull;
+      const u64 win = window_sum(a.tile_state, first ? 0ull : m.prev + 1, m.tile);
       // wait for the inclusive prefix of this CTA's previous tile (k - 1)
       while (*(volatile u32*)s_done != k) __nanosleep(32);
-      const u64 prefix = (m.tile < G ? 0ull : *(volatile u64*)s_incl) + win;
+      const u64 prefix = (first ? 0ull : *(volatile u64*)s_incl) + win;
       __syncwarp();
       if (lane == 0) {
         *(volatile u64*)s_incl = prefix + m.count;
@@ -453,6 +464,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
 
   // -------------------------------------------------------------- consumer warps
   u32 tile_cnt = 0, tseq = 0, b = 0;
+  u64 prev_tile = ~0ull;
   bool overflow = false;
   long long p_full = 0, p_se = 0, n_s = 0;
   const long long c_start = clock64();
@@ -575,6 +587,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       m.tile = si.tile;
       m.tile_base = si.base - (u64)si.sub * kSubE;
       m.tile_end = si.base + si.n_valid;
+      m.prev = prev_tile;
       m.po = si.po;
       m.pn = si.pn;
       m.t = si.t;
@@ -584,6 +597,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       meta[b] = m;
       mbar_arrive(&sfull[b]);
     }
+    prev_tile = si.tile;
     ++tseq;
   }
   if (a.prof && tid == 0) {
@@ -603,19 +617,20 @@ static size_t extract_smem() {
 template <bool kSingle, int kStages, int kWriters, int kB = 2>
 static void launch_k(const ExtractArgs& a, cudaStream_t s) {
   constexpr int kXBlock = xblock(kWriters);
-  static int grid_cap = 0;
+  static int grid_cap[kMaxDevices] = {};   // per device: the attribute is a per-device setting
   const size_t sm = extract_smem<kStages>();
-  if (!grid_cap) {
+  const int dev = current_device();
+  if (!grid_cap[dev]) {
     cudaFuncSetAttribute(k_extract<kSingle, kStages, kWriters, kB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    int dev = 0, n_sm = 148, per = 1;
-    cudaGetDevice(&dev);
+    int n_sm = 148, per = 1;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_extract<kSingle, kStages, kWriters, kB>, kXBlock, sm);
-    grid_cap = n_sm * (per > 0 ? per : 1);
-    if (grid_cap > (int)kMaxExtractCtas) grid_cap = (int)kMaxExtractCtas;
+    int cap = n_sm * (per > 0 ? per : 1);
+    grid_cap[dev] = cap > (int)kMaxExtractCtas ? (int)kMaxExtractCtas : cap;
   }
-  u64 grid = a.n_tiles < (u64)grid_cap ? a.n_tiles : (u64)grid_cap;
+  const u64 cap = (u64)clamp_ctas(grid_cap[dev]);
+  u64 grid = a.n_tiles < cap ? a.n_tiles : cap;
   static unsigned long long* prof = nullptr;
   static int want_prof = -1;
   if (want_prof < 0) want_prof = getenv("SS_XPROF") ? 1 : 0;
@@ -664,8 +679,8 @@ static void launch(const ExtractArgs& a, cudaStream_t s) {
 
 void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, const u64* tile_prefix,
                             const u32* tile_tensor, const u64* numel, u32 n_tensors, u64 n_tiles, u32* I, u16* V,
-                            u64 cap, u64* counts, u64* tile_state, u32* stage_ring, u32* status, cudaStream_t s,
-                            int elem_bytes) {
+                            u64 cap, u64* counts, u64* tile_state, u32* ticket, u32* stage_ring, u32* status,
+                            cudaStream_t s, int elem_bytes) {
   if (n_tiles == 0) return;
   ExtractArgs a{};
   a.old_ptrs = d_old;
@@ -680,6 +695,7 @@ void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, co
   a.cap = cap;
   a.counts = counts;
   a.tile_state = tile_state;
+  a.ticket = ticket;
   a.stage_ring = stage_ring;
   a.status = status;
   if (elem_bytes == 1) launch_k<false, 3, 3, 1>(a, s);   // FP8: the same pipeline on 8-bit elements
@@ -687,7 +703,7 @@ void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, co
 }
 
 void launch_extract_single(const u16* d_old, const u16* d_new, u64 n, u32* I, u16* V, u64 cap, u64* count,
-                           u64* tile_state, u32* stage_ring, u32* status, cudaStream_t s) {
+                           u64* tile_state, u32* ticket, u32* stage_ring, u32* status, cudaStream_t s) {
   u64 n_tiles = (n + kTile - 1) / kTile;
   if (n_tiles == 0) return;
   ExtractArgs a{};
@@ -701,6 +717,7 @@ void launch_extract_single(const u16* d_old, const u16* d_new, u64 n, u32* I, u1
   a.cap = cap;
   a.counts = count;
   a.tile_state = tile_state;
+  a.ticket = ticket;
   a.stage_ring = stage_ring;
   a.status = status;
   launch<true>(a, s);

@@ -8,6 +8,11 @@
 namespace ss {
 
 void count_launch();
+// Launch sizing (api.cu). Per-device caches are indexed by the current device (< kMaxDevices).
+constexpr int kMaxDevices = 64;
+int current_device();
+// grid of a persistent / grid-stride kernel after the process-wide sync_set_max_ctas() limit
+int clamp_ctas(int grid);
 
 // Device views of the workspace (all arrays live in the caller's workspace).
 struct Plan {
@@ -38,23 +43,28 @@ struct Plan {
   uint32_t* chunk_esc;           // [max_chunks] index gaps > 32767 in the chunk (f4)
   uint64_t* chunk_escoff;        // [max_chunks+1] exclusive prefix of chunk_esc
   const uint16_t* const* cur;    // f3: current weights (FULL records), device pointer table
+  uint32_t* rec_list;            // [T] tensor of record k (records = tensors with a change, manifest order)
+  uint64_t* srec;                // [T+1] exclusive prefix of the record bytes over records
+  uint64_t* crec;                // [T+1] exclusive prefix of the on-wire chunk counts over records
 };
 
 enum TotalsIdx {
   kTotNnz = 0, kTotChunks = 1, kTotRecords = 2, kTotEnc = 3, kTotDelta16 = 4, kTotAbs32 = 5,
   kTotRansChunks = 6, kTotOverflow = 7, kTotIndexBytes = 8, kTotValueBytes = 9, kTotFull = 10,
-  kTotDelta16E = 11
+  kTotDelta16E = 11, kTotBuckets = 12, kTotBucketBytes = 13, kTotSegs = 14
 };
 constexpr uint32_t kModeFull = 2;     // record idx_mode of a FULL record (f3)
 constexpr uint32_t kModeDelta16E = 3;  // record idx_mode of an escape-coded DELTA16 record (f4)
 
 void launch_extract_batched(const uint16_t* const* d_old, const uint16_t* const* d_new, const uint64_t* tile_prefix,
-                            const uint32_t* tile_tensor, const uint64_t* numel, uint32_t n_tensors, uint64_t n_tiles, uint32_t* I, uint16_t* V,
-                            uint64_t cap, uint64_t* counts, uint64_t* tile_state, uint32_t* stage_ring,
-                            uint32_t* status, cudaStream_t s, int elem_bytes = 2);   // 1: FP8
+                            const uint32_t* tile_tensor, const uint64_t* numel, uint32_t n_tensors, uint64_t n_tiles,
+                            uint32_t* I, uint16_t* V, uint64_t cap, uint64_t* counts, uint64_t* tile_state,
+                            uint32_t* ticket, uint32_t* stage_ring, uint32_t* status, cudaStream_t s,
+                            int elem_bytes = 2);   // 1: FP8
+// ticket: a zeroed device u32 (the tile claim counter)
 void launch_extract_single(const uint16_t* d_old, const uint16_t* d_new, uint64_t n, uint32_t* I, uint16_t* V,
-                           uint64_t cap, uint64_t* count, uint64_t* tile_state, uint32_t* stage_ring,
-                           uint32_t* status, cudaStream_t s);
+                           uint64_t cap, uint64_t* count, uint64_t* tile_state, uint32_t* ticket,
+                           uint32_t* stage_ring, uint32_t* status, cudaStream_t s);
 
 // plan.cu
 void launch_plan_scan(const Plan& p, const uint64_t* counts, cudaStream_t s);
@@ -67,7 +77,7 @@ void launch_encode(const Plan& p, const uint32_t* I, const uint16_t* V, const ui
                    int grid, cudaStream_t s);
 
 // pack.cu
-struct BucketDesc {              // host-computed bucket plan (uploaded)
+struct BucketDesc {              // one bucket of the device plan (bucket.cu)
   uint64_t base;                 // byte offset of the bucket in the caller's buffer
   uint64_t bytes;
   uint32_t n_records;
@@ -83,10 +93,35 @@ struct RecordDesc {              // one per record, manifest order
   uint32_t first_chunk;          // within its bucket
   uint32_t tensor;
 };
-void launch_pack(const uint8_t* enc, uint8_t* buckets, const RecordDesc* recs, uint32_t n_records,
-                 const BucketDesc* bks, uint32_t n_buckets, uint64_t enc_total, uint32_t flags, int grid,
-                 cudaStream_t s);
-void crc_fill(uint8_t* buckets, const BucketDesc* h_bks, uint32_t n_buckets, uint32_t* scratch, cudaStream_t s);
+// bucket.cu: the greedy bucket plan on the device (DESIGN C11)
+struct BucketPlan {
+  const uint32_t* rec_list;      // Plan::rec_list / srec / crec (from k_plan_sizes)
+  const uint64_t* srec;
+  const uint64_t* crec;
+  const uint64_t* enc_off;       // [T] record t's offset in the contiguous encoded stream (unfused path)
+  uint32_t* nxt;                 // [T] scratch
+  uint32_t* bstart;              // [T+1] first record of each bucket (+ sentinel)
+  uint64_t* seg_off;             // [T+1] first CRC segment of each bucket
+  RecordDesc* recs;              // [T]
+  BucketDesc* bks;               // [T]
+  uint64_t* rec_dst;             // [T] where k_encode writes record t (fused path), or null
+  uint64_t* totals;
+  uint32_t* status;
+  uint64_t limit;                // L
+  uint64_t cap_bytes;            // the caller's bucket buffer
+  uint32_t max_buckets;          // the caller's table
+  uint64_t* out_hdr;             // mapped pinned host: {n_buckets, failed, need}
+  uint64_t* out_off;             // mapped pinned host: [T+1] bucket offsets
+  uint64_t* out_size;            // mapped pinned host: [T+1] bucket sizes
+};
+void launch_bucket_plan(const BucketPlan& b, uint32_t n_tensors, int sm_count, cudaStream_t s);
+
+// bucket headers + directories for the device plan (counts read from totals); enc != null: also copy the
+// contiguous encoded stream into the bucket positions (unfused path)
+void launch_pack(const uint8_t* enc, uint8_t* buckets, const RecordDesc* recs, const BucketDesc* bks,
+                 const uint64_t* totals, uint32_t max_buckets, uint32_t flags, int grid, cudaStream_t s);
+void crc_fill(uint8_t* buckets, const BucketDesc* bks, const uint64_t* seg_off, const uint64_t* totals,
+              uint32_t max_buckets, uint32_t* scratch, int grid, cudaStream_t s);
 
 // decode.cu
 // CRC-32 of one bucket vs its header: mismatch latches SYNC_ERR_CRC and sets *bad_flag (device u32).

@@ -331,12 +331,13 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
     __syncthreads();
   }
   const u64 rans = block_sum64(rans_local, s_w2);
-  // 2. record sizes and offsets
-  u64 carry_enc = 0, n16 = 0, n32 = 0, ib_tot = 0, vb_tot = 0, nfull = 0, n16e = 0;
+  // 2. record sizes and offsets; the record table (compacted: tensors with a change, in manifest order) with
+  //    the byte and on-wire chunk prefixes the device bucket planner walks (bucket.cu)
+  u64 carry_enc = 0, n16 = 0, n32 = 0, ib_tot = 0, vb_tot = 0, nfull = 0, n16e = 0, carry_r = 0, carry_c = 0;
   for (u32 b = 0; b < T; b += (u32)kRound) {
     const u32 t0 = b + threadIdx.x * kPer;
-    u64 bytes[kPer];
-    u64 sum = 0;
+    u64 bytes[kPer], wch[kPer];
+    u64 sum = 0, rsum = 0, csum = 0;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
       const u32 t = t0 + k;
@@ -384,18 +385,37 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* 
         p.rec_bytes[t] = by;
       }
       bytes[k] = by;
+      // chunks of a record on the wire = ceil(nnz field / C); a FULL record's nnz field is numel
+      wch[k] = !by ? 0 : mode == kModeFull ? (p.numel[t] + kChunk - 1) / kChunk : p.chunk_off[t + 1] - p.chunk_off[t];
       sum += by;
+      rsum += by ? 1 : 0;
+      csum += wch[k];
     }
-    u64 e;
+    u64 e, re, ce;
     const u64 tot = block_excl_scan64(sum, &e, s_w);
-    u64 run = carry_enc + e;
+    const u64 rtot = block_excl_scan64(rsum, &re, s_w2);
+    const u64 ctot = block_excl_scan64(csum, &ce, s_w);
+    u64 run = carry_enc + e, rrun = carry_r + re, crun = carry_c + ce;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
       const u32 t = t0 + k;
       if (t < T) p.enc_off[t] = run;
+      if (bytes[k]) {
+        p.rec_list[rrun] = t;
+        p.srec[rrun] = run;
+        p.crec[rrun] = crun;
+        rrun++;
+      }
       run += bytes[k];
+      crun += wch[k];
     }
     carry_enc += tot;
+    carry_r += rtot;
+    carry_c += ctot;
+  }
+  if (threadIdx.x == 0) {
+    p.srec[carry_r] = carry_enc;
+    p.crec[carry_r] = carry_c;
   }
   n16 = block_sum64(n16, s_w);
   n32 = block_sum64(n32, s_w2);

@@ -347,18 +347,18 @@ __global__ void __launch_bounds__(kTT) k_track_write(TrackArgs a, u16* const* W,
 
 void launch_cast_track(const TrackArgs& a, const float* const* master, u16* const* W, int grid, cudaStream_t s) {
   if (!a.n_tiles) return;
-  static int cap = 0;
+  static int cap[kMaxDevices] = {};   // per device: the attribute is a per-device setting
   const size_t sm = cast_smem();
-  if (!cap) {
+  const int dev = current_device();
+  if (!cap[dev]) {
     cudaFuncSetAttribute(k_cast_track, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    int dev = 0, n_sm = 148, per = 1;
-    cudaGetDevice(&dev);
+    int n_sm = 148, per = 1;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cast_track, kCBlock, sm);
-    cap = n_sm * (per > 0 ? per : 1);
+    cap[dev] = n_sm * (per > 0 ? per : 1);
   }
-  (void)grid;
-  const u64 g = a.n_tiles < (u64)cap ? a.n_tiles : (u64)cap;   // persistent: every CTA resident
+  const u64 lim = (u64)(grid < cap[dev] ? grid : cap[dev]);   // grid: the caller's (clamped) CTA budget
+  const u64 g = a.n_tiles < lim ? a.n_tiles : lim;   // persistent, no cross-CTA waits
   k_cast_track<<<(unsigned)g, kCBlock, sm, s>>>(a, master, W);
   count_launch();
 }
