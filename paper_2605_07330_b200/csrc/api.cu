@@ -257,6 +257,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   p.word_scratch = reinterpret_cast<u16*>(w + L.word_scratch);
   p.totals = reinterpret_cast<u64*>(w + L.totals);
   p.status = x->misc + 1;
+  p.work = reinterpret_cast<u64*>(x->misc + 16);   // misc words 16..19
   p.rec_list = reinterpret_cast<u32*>(w + L.rec_list);
   p.srec = reinterpret_cast<u64*>(w + L.srec);
   p.crec = reinterpret_cast<u64*>(w + L.crec);

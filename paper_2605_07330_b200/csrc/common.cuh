@@ -187,12 +187,9 @@ __device__ __forceinline__ u32 warp_normalize(WarpModel& m, u32 n) {
       u32 t = __shfl_xor_sync(0xffffffffu, best, o);
       best = t > best ? t : best;
     }
-    u32 bs = 255u - (best & 0xFFu);
-    if (bs / 8 == lane) {
+    const u32 bs = 255u - (best & 0xFFu);
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if ((u32)k == bs % 8) f[k] += kM - sum;
-    }
+    for (int k = 0; k < 8; ++k) f[k] += (lane * 8 + (u32)k == bs) ? kM - sum : 0u;   // registers, no local
     sum = kM;
   }
   while (sum > kM) {
@@ -210,12 +207,9 @@ __device__ __forceinline__ u32 warp_normalize(WarpModel& m, u32 n) {
       u32 t = __shfl_xor_sync(0xffffffffu, best, o);
       best = t > best ? t : best;
     }
-    u32 bs = 255u - (best & 0xFFu);
-    if (bs / 8 == lane) {
+    const u32 bs = 255u - (best & 0xFFu);
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if ((u32)k == bs % 8) f[k] -= 1;
-    }
+    for (int k = 0; k < 8; ++k) f[k] -= (lane * 8 + (u32)k == bs) ? 1u : 0u;
     sum -= 1;
   }
   // exclusive prefix over symbols (lane-major, 8 per lane)

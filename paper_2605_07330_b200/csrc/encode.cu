@@ -18,18 +18,23 @@ __device__ __forceinline__ void zero_bytes(u8* p, u64 n) {
   for (u64 q = threadIdx.x; q < n; q += blockDim.x) p[q] = 0;
 }
 
-// One CTA per chunk (16384 values). All threads write the chunk's slices of the
+// One CTA per chunk (16384 values; persistent CTAs claim chunks from a counter). All threads write the chunk's slices of the
 // index stream and of the lo plane (packed 32-bit stores) and copy the chunk's
 // rANS block (states, model, words) that k_chunk_stats already produced.
 __global__ void __launch_bounds__(kCThreads, 6) k_encode(Plan p, const u32* I, const u16* V, const u64* counts,
                                                      u8* enc) {
   __shared__ u32 s_t;
+  __shared__ u64 s_g;
   const u32 tid = threadIdx.x;
   const u64 n_chunks = p.totals[kTotChunks];
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
   const bool e8 = p.dtype == SYNC_DTYPE_FP8;   // FP8: one value plane (the byte), no lo plane
-  for (u64 g = blockIdx.x; g < n_chunks; g += gridDim.x) {
+  for (;;) {
     __syncthreads();
+    if (tid == 0) s_g = atomicAdd(reinterpret_cast<unsigned long long*>(p.work + 1), 1ull);   // next chunk
+    __syncthreads();
+    const u64 g = s_g;
+    if (g >= n_chunks) break;
     const ChunkPos c = locate_chunk(p, counts, g, s_t, I, V);
     const u32 t = c.t;
     const u64 nnz = c.nnz, k = c.k, p0 = c.p0;
@@ -258,7 +263,15 @@ __global__ void __launch_bounds__(kCThreads, 6) k_encode(Plan p, const u32* I, c
 
 void launch_encode(const Plan& p, const u32* I, const u16* V, const u64* counts, u8* enc, int grid,
                    cudaStream_t s) {
-  k_encode<<<grid, kCThreads, 0, s>>>(p, I, V, counts, enc);
+  static int cap[kMaxDevices] = {};   // persistent: the resident CTAs claim chunks from a counter
+  const int dev = current_device();
+  if (!cap[dev]) {
+    int n_sm = 148, per = 1;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_encode, kCThreads, 0);
+    cap[dev] = n_sm * (per > 0 ? per : 1);
+  }
+  k_encode<<<grid < cap[dev] ? grid : cap[dev], kCThreads, 0, s>>>(p, I, V, counts, enc);
   count_launch();
 }
 

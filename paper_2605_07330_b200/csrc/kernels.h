@@ -46,6 +46,7 @@ struct Plan {
   uint32_t* rec_list;            // [T] tensor of record k (records = tensors with a change, manifest order)
   uint64_t* srec;                // [T+1] exclusive prefix of the record bytes over records
   uint64_t* crec;                // [T+1] exclusive prefix of the on-wire chunk counts over records
+  uint64_t* work;                // [2] chunk claim counters (k_chunk_stats, k_encode), zeroed by k_plan_scan
 };
 
 enum TotalsIdx {

@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_scan(Plan p, const u64* c
     bool over = carry_nnz > p.cap || carry_ch > p.max_chunks;
     if (over) latch(p.status, SYNC_ERR_CAPACITY);
     for (int k = 0; k < 16; ++k) p.totals[k] = 0;
+    p.work[0] = 0;   // chunk counters of k_chunk_stats / k_encode
+    p.work[1] = 0;
     p.totals[kTotNnz] = carry_nnz;
     p.totals[kTotChunks] = over ? 0 : carry_ch;
     p.totals[kTotRecords] = carry_rec;
@@ -91,78 +93,81 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_scan(Plan p, const u64* c
 
 __device__ unsigned long long g_cprof[8];  // debug cycle counters (SS_CPROF=1)
 
-// One warp per chunk: the warp builds its chunk's histogram + max first difference (8
-// loads in flight per lane, per-warp shared histogram), normalises the model, then runs
-// the rANS encode pass reading V from L2 with the next 8 steps prefetched into registers
-// (words to the chunk's scratch in emission order; final states + model to chunk_rhdr).
-// No hi plane in shared memory: ~32 independent rANS chains per SM (a CTA-per-chunk
-// variant with the hi plane staged in shared memory measured 1.2-1.7x slower).
+// One warp per chunk: the warp builds its chunk's histogram + max first difference, normalises the model,
+// then runs the rANS encode pass reading V from L2 with the next 8 steps prefetched into registers (words to
+// the chunk's scratch in emission order; final states + model to chunk_rhdr). No hi plane in shared memory:
+// ~32 independent rANS chains per SM (a CTA-per-chunk variant with the hi plane staged in shared memory
+// measured 1.2-1.7x slower). Persistent grid (the resident CTAs); each warp claims its next chunk from a
+// counter, so no CTA waits for its slowest warp and there is no tail of partial waves.
+// Histogram / gap pass: lane l owns the 8 consecutive values of an 8-aligned group (one 16-byte load of V,
+// two of I); the gap into the group comes from lane l-1's last index (one shuffle), the warp's carry from
+// the previous round.
 constexpr int kWPF = 8;
 __global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
   __shared__ WarpModel s_m[8];
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpModel& m = s_m[warp];
   const u64 n_chunks = p.totals[kTotChunks];
-  const u64 nwarps = (u64)gridDim.x * 8;
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
   // the coded value plane: the hi byte of a 16-bit element, the whole byte of an FP8 one (V's low half)
   const u32 sh = p.dtype == SYNC_DTYPE_FP8 ? 0u : 8u;
-  for (u64 g = (u64)blockIdx.x * 8 + warp; g < n_chunks; g += nwarps) {
+  for (;;) {
+    u64 g = 0;
+    if (lane == 0) g = atomicAdd(reinterpret_cast<unsigned long long*>(p.work), 1ull);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if (g >= n_chunks) break;
     const long long t0 = clock64();
     const u64* co = p.chunk_off;
     const u32 t = warp_upper_search(p.n_tensors, g, [&](u32 i) { return co[i]; });
     const u64 nnz = counts[t];
     const u64 p0 = (g - co[t]) * kChunk;
     const u32 nk = (u32)((nnz - p0) < kChunk ? (nnz - p0) : kChunk);
-    const u32* Ic = I + p.rec_off[t] + p0;
-    const u16* Vc = V + p.rec_off[t] + p0;
+    const u64 gs = p.rec_off[t] + p0, ge = gs + nk;   // the chunk's values in I / V
+    const u16* Vc = V + gs;
     const long long t1 = clock64();
-    // ---- histogram + max first difference; the next block's loads are issued before the current
-    //      block is consumed, and the element before each 32-group comes from the previous group
     for (u32 sym = lane; sym < 256; sym += 32) m.hist[sym] = 0;
     __syncwarp();
+    // I of the element before the chunk (Δ_0 = I_0 when the chunk starts its record)
+    u32 carry0 = (lane == 0 && p0) ? I[gs - 1] : 0u;
+    carry0 = __shfl_sync(0xffffffffu, carry0, 0);
+    u32 carry = carry0;
     u32 gmax = 0, nesc = 0;
-    u32 carry = (lane == 0 && p0) ? Ic[-1] : 0u;   // I of the element before the chunk (Δ_0 = I_0 if none)
-    carry = __shfl_sync(0xffffffffu, carry, 0);
-    u32 hv[kWPF], cur[kWPF], hn[kWPF], cn[kWPF];
-    // the coded byte of V[q] is byte 2q + vb of the V array (vb = 1: the hi byte of a 16-bit element)
-    const u8* Vb = reinterpret_cast<const u8*>(Vc) + (sh ? 1 : 0);
-    auto load = [&](u32 b0, u32* h, u32* c) {
-      if (b0 + 32 * kWPF <= nk) {   // whole block inside the chunk: plain loads at constant offsets
-        const u8* vp = Vb + 2 * (b0 + lane);
-        const u32* ip = Ic + b0 + lane;
+    for (u64 e0 = gs & ~7ull; e0 < ge; e0 += 256) {
+      const u64 e = e0 + 8ull * lane;
+      u32 iv[8], hv[8];
+      if (e < ge && e + 8 <= p.cap) {   // a whole 8-group inside the I / V arrays (values outside the chunk
+                                        // are loaded and masked below)
+        const uint4 va = *reinterpret_cast<const uint4*>(V + e);
+        const uint4 ia = *reinterpret_cast<const uint4*>(I + e);
+        const uint4 ib = *reinterpret_cast<const uint4*>(I + e + 4);
+        const u32 vw[4] = {va.x, va.y, va.z, va.w};
 #pragma unroll
-        for (int u = 0; u < kWPF; ++u) {
-          h[u] = vp[64 * u];
-          c[u] = ip[32 * u];
+        for (int k = 0; k < 4; ++k) {
+          hv[2 * k] = (vw[k] >> sh) & 0xFFu;
+          hv[2 * k + 1] = (vw[k] >> (16 + sh)) & 0xFFu;
         }
-        return;
-      }
+        iv[0] = ia.x; iv[1] = ia.y; iv[2] = ia.z; iv[3] = ia.w;
+        iv[4] = ib.x; iv[5] = ib.y; iv[6] = ib.z; iv[7] = ib.w;
+      } else {
 #pragma unroll
-      for (int u = 0; u < kWPF; ++u) {
-        const u32 q = b0 + u * 32 + lane;
-        h[u] = q < nk ? (u32)Vb[2 * q] : 0x100u;
-        c[u] = q < nk ? Ic[q] : 0u;
+        for (int k = 0; k < 8; ++k) {
+          const bool in = e + k >= gs && e + k < ge;
+          iv[k] = in ? I[e + k] : 0u;
+          hv[k] = in ? ((u32)V[e + k] >> sh) & 0xFFu : 0u;
+        }
       }
-    };
-    load(0, hn, cn);
-    for (u32 b0 = 0; b0 < nk; b0 += 32 * kWPF) {
+      u32 prev = __shfl_up_sync(0xffffffffu, iv[7], 1);
+      if (lane == 0) prev = carry;
+      carry = __shfl_sync(0xffffffffu, iv[7], 31);
 #pragma unroll
-      for (int u = 0; u < kWPF; ++u) {
-        hv[u] = hn[u];
-        cur[u] = cn[u];
-      }
-      if (b0 + 32 * kWPF < nk) load(b0 + 32 * kWPF, hn, cn);
-#pragma unroll
-      for (int u = 0; u < kWPF; ++u) {
-        const u32 q = b0 + u * 32 + lane;
-        if (hv[u] < 256) atomicAdd(&m.hist[hv[u]], 1u);
-        u32 prev = __shfl_up_sync(0xffffffffu, cur[u], 1);
-        if (lane == 0) prev = carry;
-        carry = __shfl_sync(0xffffffffu, cur[u], 31);
-        const u32 d = q < nk ? cur[u] - prev : 0u;
-        gmax = d > gmax ? d : gmax;
-        nesc += d > 32767u ? 1u : 0u;
+      for (int k = 0; k < 8; ++k) {
+        const u64 q = e + k;
+        if (q >= gs && q < ge) {
+          atomicAdd(&m.hist[hv[k]], 1u);
+          const u32 d = iv[k] - (q == gs ? carry0 : (k ? iv[k - 1] : prev));
+          gmax = d > gmax ? d : gmax;
+          nesc += d > 32767u ? 1u : 0u;
+        }
       }
     }
 #pragma unroll
@@ -186,7 +191,8 @@ __global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, co
     const u32 G = (nk + 31) / 32;
     const u32 lt = (1u << lane) - 1u;
     const u32 wcap = nk / 2;
-    u16* ws = p.word_scratch + chunk_words_base(p.rec_off[t] + p0, g);
+    u16* ws = p.word_scratch + chunk_words_base(gs, g);
+    const u8* Vb = reinterpret_cast<const u8*>(Vc) + (sh ? 1 : 0);   // byte 2q + vb: the coded byte of V[q]
     asm volatile("" : "+l"(ws));   // keep the 64-bit base in registers (no per-step rematerialisation)
     const uint2* const fr = m.fr;
     u32 nxt[kWPF];
@@ -455,7 +461,15 @@ void launch_chunk_stats(const Plan& p, const u32* I, const u16* V, const u64* co
     unsigned long long z[8] = {0};
     cudaMemcpyToSymbolAsync(g_cprof, z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
   }
-  k_chunk_stats<<<grid, 256, 0, s>>>(q, I, V, counts);
+  static int cap[kMaxDevices] = {};   // persistent: the resident CTAs (the warps claim chunks)
+  const int dev = current_device();
+  if (!cap[dev]) {
+    int n_sm = 148, per = 1;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chunk_stats, 256, 0);
+    cap[dev] = n_sm * (per > 0 ? per : 1);
+  }
+  k_chunk_stats<<<grid < cap[dev] ? grid : cap[dev], 256, 0, s>>>(q, I, V, counts);
   if (want) {
     unsigned long long h[8];
     cudaMemcpyFromSymbolAsync(h, g_cprof, sizeof(h), 0, cudaMemcpyDeviceToHost, s);

@@ -165,18 +165,82 @@ class PairLink(_Link):
 
 class FanoutLink(_Link):
     """T Trainers (shards) -> R Rollouts (full replicas): every Trainer sends each bucket to every Rollout;
-    a Rollout applies Trainer t's buckets with the receiver of t's shard."""
+    a Rollout applies Trainer t's buckets with the receiver of t's shard.
 
-    def __init__(self, rank, world, device, trainers: list[int], rollouts: list[int], ctrl=None, group=None):
+    mode "p2p": one NCCL send per (bucket, Rollout) — R copies leave the Trainer.
+    mode "broadcast": one NCCL broadcast per bucket in the group {t} + Rollouts (NCCL pipelines it through
+    the group, or multicasts it over NVSwitch with NVLS), so each bucket leaves the Trainer once. The groups
+    are created here: every rank must construct the link (torch.distributed.new_group is collective)."""
+
+    def __init__(self, rank, world, device, trainers: list[int], rollouts: list[int], ctrl=None, group=None,
+                 mode: str = "p2p"):
         super().__init__(rank, world, device, ctrl, group)
         self.trainers, self.rollouts = list(trainers), list(rollouts)
+        if mode not in ("p2p", "broadcast"):
+            raise ValueError(f"FanoutLink mode {mode!r}")
+        self.mode = mode
+        self.bgroups = {}
+        if mode == "broadcast":
+            for t in self.trainers:
+                self.bgroups[t] = dist.new_group(sorted([t] + self.rollouts))
 
     def send(self, send_buf, blist, tag: int = 0):
+        if self.mode == "broadcast":
+            return self._bcast(send_buf, blist, {}, tag)
         return self._run(send_buf, blist, self.rollouts, [], {}, tag)
 
     def receive(self, apply_fns: dict, tag: int = 0):
         """apply_fns: {trainer rank: fn(bucket)}."""
+        if self.mode == "broadcast":
+            return self._bcast(None, [], apply_fns, tag)
         return self._run(None, [], [], self.trainers, apply_fns, tag)
+
+    def _bcast(self, send_buf, blist, apply_fns, tag: int = 0):
+        trainer = self.rank in self.trainers
+        dsts = self.rollouts if trainer else []
+        srcs = [] if trainer else self.trainers
+        incoming = _manifest_exchange(blist, dsts, srcs, self.ctrl)
+        self.last_in = incoming
+        self.fence(tag)
+        bufs, keys = {}, {}
+        for i, s in enumerate(srcs):
+            keys[s], bufs[s] = self._buf(s, tag, i == 0, max((o + z for o, z in incoming[s]), default=0))
+        cur = torch.cuda.current_stream(self.device) if self.cuda else None
+        if self.cuda:
+            self.comm.wait_stream(cur)
+            for s in srcs:
+                ev = self.free.get(keys[s])
+                if ev is not None:
+                    self.comm.wait_event(ev)
+        # every group member walks (bucket b, trainer t) in the same order
+        order = []
+        nb = len(blist) if trainer else max([len(v) for v in incoming.values()] or [0])
+        for b in range(nb):
+            for t in self.trainers:
+                if trainer and t == self.rank:
+                    order.append((t, b, send_buf[blist[b][0]:blist[b][0] + blist[b][1]]))
+                elif not trainer and b < len(incoming[t]):
+                    o, z = incoming[t][b]
+                    order.append((t, b, bufs[t][o:o + z]))
+        ctx = torch.cuda.stream(self.comm) if self.cuda else _Null()
+        works = []
+        with ctx:
+            for t, b, view in order:
+                works.append(dist.broadcast(view, src=t, group=self.bgroups[t], async_op=True))
+        for (t, b, view), w in zip(order, works):
+            if trainer and self.cuda:
+                self.pending_sends.setdefault(tag, []).append(w)
+                continue
+            w.wait()
+            if not trainer and apply_fns.get(t) is not None:
+                apply_fns[t](view)
+        if self.cuda:
+            for s in srcs:
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                self.free[keys[s]] = ev
+        self.seq[tag] = self.seq.get(tag, 0) + 1
+        return incoming
 
 
 def shard_ranges(numel: list[int], parts: int) -> list[tuple[int, int]]:

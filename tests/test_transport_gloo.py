@@ -79,12 +79,18 @@ def _model4(seed):
     return synth.generate(m, seed=seed, rho=0.05)
 
 
-SHARDS = [(0, 2), (2, 4)]
+def _shards(half):
+    from paper_2605_07330_b200.transport import shard_ranges
+    import synth
+    m = synth.Manifest("m4", [synth.Tensor("a", (64, 300)), synth.Tensor("n", (32,), synth.KIND_NORM),
+                              synth.Tensor("b", (50_000,)), synth.Tensor("c", (128, 129))])
+    return shard_ranges(m.numel, half)
 
 
 def _worker4(rank, world, port, mode, q):
-    """ranks 0, 1: Trainers of shards 0, 1 of one model; ranks 2, 3: Rollouts (full replica for fanout,
-    shard rank-2 for sharded pairs)."""
+    """ranks < world/2: Trainers of element-balanced shards of one model; ranks >= world/2: Rollouts (full
+    replica for fanout / fanout_bcast, shard rank - world/2 for sharded pairs). World 4: 2T -> 2R; world 8:
+    4T -> 4R (configs 4 and 5 of BASELINE.json)."""
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -92,35 +98,42 @@ def _worker4(rank, world, port, mode, q):
     try:
         import oracle
         from paper_2605_07330_b200.transport import FanoutLink, PairLink
+        half = world // 2
+        shards = _shards(half)
+        trainers, rollouts = list(range(half)), list(range(half, world))
         olds, news = _model4(seed=7)
-        if rank < 2:
-            lo, hi = SHARDS[rank]
+        link = None
+        if mode in ("fanout", "fanout_bcast"):   # every rank builds the link (broadcast groups are collective)
+            link = FanoutLink(rank, world, "cpu", trainers=trainers, rollouts=rollouts,
+                              mode="broadcast" if mode == "fanout_bcast" else "p2p")
+        if rank < half:
+            lo, hi = shards[rank]
             pk = oracle.sync_pack(olds[lo:hi], news[lo:hi], limit=2 << 10)
             send_buf = torch.from_numpy(pk.buf.copy())
             blist = [(int(o), int(s)) for o, s in zip(pk.offsets, pk.sizes)]
-            if mode == "fanout":
-                FanoutLink(rank, world, "cpu", trainers=[0, 1], rollouts=[2, 3]).send(send_buf, blist)
+            if link is not None:
+                link.send(send_buf, blist)
             else:
-                PairLink(rank, world, "cpu", trainer=rank, rollout=rank + 2).send(send_buf, blist)
-            ok = len(blist) > 1
+                PairLink(rank, world, "cpu", trainer=rank, rollout=rank + half).send(send_buf, blist)
+            ok = len(blist) >= 1
         else:
             W = [o.copy() for o in olds]
 
             def fn(t):
-                lo, hi = SHARDS[t]
+                lo, hi = shards[t]
                 view = W[lo:hi]   # the shard's records carry shard-local tensor ids
 
                 def apply(bk):
                     assert oracle.bucket_apply(bk.numpy().tobytes(), view) == oracle.OK
                 return apply
 
-            if mode == "fanout":
-                FanoutLink(rank, world, "cpu", trainers=[0, 1], rollouts=[2, 3]).receive({0: fn(0), 1: fn(1)})
+            if link is not None:
+                link.receive({t: fn(t) for t in trainers})
                 ok = all((w == n).all() for w, n in zip(W, news))
             else:
-                t = rank - 2
+                t = rank - half
                 PairLink(rank, world, "cpu", trainer=t, rollout=rank).receive(fn(t))
-                lo, hi = SHARDS[t]
+                lo, hi = shards[t]
                 ok = all((w == n).all() for w, n in zip(W[lo:hi], news[lo:hi]))
                 ok = ok and all((w == o).all() for k, (w, o) in enumerate(zip(W, olds)) if not lo <= k < hi)
         q.put((rank, bool(ok)))
@@ -128,18 +141,21 @@ def _worker4(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["fanout", "sharded_pairs"])
-def test_world4_gloo(mode):
+@pytest.mark.parametrize("world", [4, 8])
+@pytest.mark.parametrize("mode", ["fanout", "fanout_bcast", "sharded_pairs"])
+def test_fanout_and_pairs_gloo(world, mode):
+    """2T->2R and 4T->4R (the 8-GPU topology of configs 4/5): replica fan-out by per-destination sends and
+    by broadcast, and sharded Trainer -> Rollout pairs; every Rollout's weights == the oracle's new weights."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker4, args=(r, 4, port, mode, q)) for r in range(4)]
+    ps = [ctx.Process(target=_worker4, args=(r, world, port, mode, q)) for r in range(world)]
     for p in ps:
         p.start()
     for p in ps:
-        p.join(180)
-    res = dict(q.get(timeout=10) for _ in range(4))
-    assert res == {r: True for r in range(4)}
+        p.join(240)
+    res = dict(q.get(timeout=10) for _ in range(world))
+    assert res == {r: True for r in range(world)}
     assert all(p.exitcode == 0 for p in ps)
 
 
@@ -165,13 +181,20 @@ def test_shard_ranges():
     sys.path.insert(0, ROOT)
     import synth
     from paper_2605_07330_b200.transport import shard_ranges
-    m = synth.qwen3_manifest("qwen3-30b-a3b")
-    for T in (1, 2, 4, 8):
-        r = shard_ranges(m.numel, T)
-        assert r[0][0] == 0 and r[-1][1] == len(m.numel)
-        assert all(a < b for a, b in r) and all(r[i][1] == r[i + 1][0] for i in range(T - 1))
-        sizes = [sum(m.numel[a:b]) for a, b in r]
-        assert max(sizes) - min(sizes) <= 2 * max(m.numel)
+    for name in ("qwen3-30b-a3b", "qwen3-235b-a22b"):
+        m = synth.qwen3_manifest(name)
+        for T in (1, 2, 4, 8):
+            r = shard_ranges(m.numel, T)
+            assert r[0][0] == 0 and r[-1][1] == len(m.numel)
+            assert all(a < b for a, b in r) and all(r[i][1] == r[i + 1][0] for i in range(T - 1))
+            sizes = [sum(m.numel[a:b]) for a, b in r]
+            assert max(sizes) - min(sizes) <= 2 * max(m.numel)
+    # config 5: Qwen3-235B in 4 shards, one per Trainer of the 4T -> 4R box: each shard (old + new during the
+    # sync) must leave room on a 180 GB B200 for the streamed groups (SURVEY 8(d) memory check)
+    m = synth.qwen3_manifest("qwen3-235b-a22b")
+    r4 = shard_ranges(m.numel, 4)
+    per = [2 * sum(m.numel[a:b]) for a, b in r4]          # bf16 bytes of each shard
+    assert all(1.14e11 < x < 1.21e11 for x in per), per   # 117.5 GB each, balanced to ~3%
     rng = random.Random(0)
     for _ in range(300):
         n = rng.randint(1, 12)
