@@ -36,7 +36,7 @@ constexpr u64 kAlign = 256;
 struct Layout {
   u64 numel, tile_prefix, tile_tensor, misc, tile_state, stage_ring, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
   u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, rec_dst, totals, recs, bks, views, nviews, crc;
-  u64 bm_off, group_sum, chunk_esc, chunk_escoff, bitmap8, rec_list, srec, crec, nxt, bstart, seg_off, total;
+  u64 bm_off, group_sum, chunk_esc, chunk_escoff, bitmap8, rec_list, srec, crec, nxt, bstart, seg_off, gscan, total;
 };
 
 u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4 + 32; }  // + 32 bad flags
@@ -84,6 +84,7 @@ Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_change
   L.nxt = take(4ull * T);
   L.bstart = take(4ull * (T + 1));
   L.seg_off = take(8ull * (T + 1));
+  L.gscan = take(32ull * (2 * ((T + 1023) / 1024 + 1) + (max_chunks + 1023) / 1024 + 1));   // scan.cuh states
   L.total = o;
   return L;
 }
@@ -216,6 +217,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
     }
   }
   if (cudaMemsetAsync(w + L.misc, 0, 4 * 64, s) != cudaSuccess ||
+      cudaMemsetAsync(w + L.gscan, 0, L.seg_off < L.gscan ? L.total - L.gscan : 0, s) != cudaSuccess ||
       cudaMemsetAsync(w + L.totals, 0, 8 * 16, s) != cudaSuccess) {
     delete x;
     return SYNC_ERR_CUDA;
@@ -258,6 +260,11 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   p.totals = reinterpret_cast<u64*>(w + L.totals);
   p.status = x->misc + 1;
   p.work = reinterpret_cast<u64*>(x->misc + 16);   // misc words 16..19
+  p.tickets = x->misc + 24;                         // misc words 24..26 (zeroed at creation, never reset)
+  p.gscan = reinterpret_cast<u64*>(w + L.gscan);
+  p.gscan_T = (d.T + 1023) / 1024 + 1;
+  p.gscan_C = (u32)((d.max_chunks + 1023) / 1024);
+  p.epoch = 0;
   p.rec_list = reinterpret_cast<u32*>(w + L.rec_list);
   p.srec = reinterpret_cast<u64*>(w + L.srec);
   p.crec = reinterpret_cast<u64*>(w + L.crec);
@@ -419,6 +426,7 @@ int sync_compress(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const u
   if (!aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
   x->plan.enc_cap = enc_cap;
+  x->plan.epoch++;   // the grid scans' publication flag (scan.cuh)
   launch_plan_scan(x->plan, d_counts, s);
   // CTA-per-chunk kernels of 128 threads: 2x the grid of the 256-thread kernels (~9 resident per SM)
   if (x->cfg.codec == SYNC_CODEC_COMPRESSED) launch_chunk_stats(x->plan, d_I, d_V, d_counts, clamp_ctas(2 * x->grid), s);
@@ -539,6 +547,7 @@ int sync_compress_pack_async(sync_ctx* x, const uint32_t* d_I, const uint16_t* d
   // plan (record sizes) exactly as sync_compress, without the encode
   x->plan.enc_cap = ~0ull;
   x->plan.rec_dst = x->plan.enc_off;
+  x->plan.epoch++;   // the grid scans' publication flag (scan.cuh)
   launch_plan_scan(x->plan, d_counts, s);
   if (x->cfg.codec == SYNC_CODEC_COMPRESSED)
     launch_chunk_stats(x->plan, d_I, d_V, d_counts, clamp_ctas(2 * x->grid), s);
@@ -664,7 +673,8 @@ int sync_commit_snapshot_batched(sync_ctx* x, uint16_t* const* d_snapshot_ptrs, 
   if (x->d.T == 0) return SYNC_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (!(x->plan_valid && x->plan_counts == d_counts)) {
-    launch_plan_scan(x->plan, d_counts, s);
+    x->plan.epoch++;   // the grid scans' publication flag (scan.cuh)
+  launch_plan_scan(x->plan, d_counts, s);
     x->plan_valid = false;
   }
   launch_commit_batched(x->plan, d_snapshot_ptrs, d_I, d_V, clamp_ctas(x->grid), s);

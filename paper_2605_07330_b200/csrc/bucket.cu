@@ -6,11 +6,13 @@
 //  * k_bucket_next (grid)   nxt[i] = one past the last record of a bucket that starts at record i:
 //                           the largest j with 32 + pad16(8 (j - i)) + srec[j] - srec[i] <= L (at least
 //                           i + 1). The size is increasing in j, so a binary search finds it.
-//  * k_bucket_plan (1 CTA)  walks the chain 0 -> nxt[0] -> ... (one step per bucket, nxt staged in shared
-//                           memory), then in parallel: bucket sizes, 256-aligned bases, record directory
-//                           entries and destinations, CRC segment offsets; capacity checks (bytes, bucket
-//                           count) latch SYNC_ERR_CAPACITY and leave nothing to encode. The bucket count,
-//                           offsets and sizes go to the context's mapped pinned table (no copy, no host sync).
+//  * k_bucket_plan (1 CTA)  walks the chain 0 -> nxt[0] -> ... (one step per bucket; nxt staged in shared
+//                           memory first when many buckets are expected), then in parallel: bucket sizes,
+//                           256-aligned bases, CRC segment offsets; capacity checks (bytes, bucket count)
+//                           latch SYNC_ERR_CAPACITY and leave nothing to encode. The bucket count, offsets
+//                           and sizes go to the context's mapped pinned table (no copy, no host sync).
+//  * k_bucket_records (grid) per record: its bucket (binary search over the starts), destination and
+//                           directory entry.
 // The host never sees a record size: sync_compress_pack is enqueue-only up to reading the final table.
 #include "common.cuh"
 #include "kernels.h"
@@ -67,9 +69,14 @@ __global__ void __launch_bounds__(kBThreads) k_bucket_plan(BucketPlan b, u32 sme
     s_fail = over ? 1u : 0u;
     s_need = 0;
   }
-  const bool in_smem = R <= smem_nxt;
-  if (!over && in_smem)
+  // stage nxt in shared memory only when the walk is long (expected buckets = payload / L): a short walk
+  // reads the few entries it needs from L2 directly
+  const u64 est = R ? b.srec[R] / (b.limit ? b.limit : 1) + 1 : 0;
+  const bool in_smem = !over && est > 64 && R <= smem_nxt;
+  if (in_smem) {
+#pragma unroll 8
     for (u64 i = tid; i < R; i += kBThreads) s_nxt[i] = b.nxt[i];
+  }
   __syncthreads();
   // ---- 1. bucket starts: one step per bucket along the greedy chain
   if (tid == 0) {
@@ -141,10 +148,15 @@ __global__ void __launch_bounds__(kBThreads) k_bucket_plan(BucketPlan b, u32 sme
     }
     __threadfence_system();
   }
-  if (fail) return;
-  // ---- 3. records: bucket by binary search over the starts, destination, directory entry
-  for (u64 k = tid; k < R; k += kBThreads) {
-    u32 lo = 0, hi = nb - 1;   // last bucket whose start <= k
+}
+
+// per record: its bucket (the last start <= k), destination, directory entry
+__global__ void __launch_bounds__(256) k_bucket_records(BucketPlan b) {
+  const u64 R = b.totals[kTotRecords];
+  if (b.totals[kTotOverflow]) return;
+  const u32 nb = (u32)b.totals[kTotBuckets];
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < R; k += (u64)gridDim.x * blockDim.x) {
+    u32 lo = 0, hi = nb - 1;
     while (lo < hi) {
       const u32 mid = (lo + hi + 1) / 2;
       if (b.bstart[mid] <= k) lo = mid;
@@ -183,6 +195,8 @@ void launch_bucket_plan(const BucketPlan& b, u32 n_tensors, int sm_count, cudaSt
     attr[dev] = true;
   }
   k_bucket_plan<<<1, kBThreads, 4 * (size_t)n_sm, s>>>(b, n_sm);
+  count_launch();
+  k_bucket_records<<<g < gmax ? g : gmax, 256, 0, s>>>(b);
   count_launch();
 }
 

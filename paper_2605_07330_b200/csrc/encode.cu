@@ -163,46 +163,35 @@ __global__ void __launch_bounds__(kCThreads, 6) k_encode(Plan p, const u32* I, c
         __syncthreads();
       }
     } else {
-      constexpr int kG = 4;
+      // thread tid owns positions q = q0 + u * kCThreads + tid (u < kU): every load / store instruction of a
+      // warp covers 32 consecutive values (coalesced), kU values per thread in flight; Δ from the value of
+      // lane l - 1 (a shuffle), lane 0 loads its predecessor (Δ_0 = I_0 at a record's first value)
+      constexpr int kU = 8;
+      const u32 lane = tid & 31;
+      const u32* Ic = Ir + p0;
+      u16* D16 = reinterpret_cast<u16*>(rec + 16) + p0;
+      u32* A32 = reinterpret_cast<u32*>(rec + 16) + p0;
       u8* L = rec + lo_off + p0;
-      for (u32 q0 = 4 * tid; q0 < nk; q0 += 4 * kCThreads * kG) {
-        u32 iv[kG][5];
-        u16 vv[kG][4];
+      const u32 first_prev = p0 ? Ic[-1] : 0u;
+      for (u32 q0 = 0; q0 < nk; q0 += kCThreads * kU) {
+        u32 iv[kU], pv[kU], vv[kU];
 #pragma unroll
-        for (int j = 0; j < kG; ++j) {
-          const u32 q = q0 + 4 * kCThreads * j;
-          const u64 pp = p0 + q;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            iv[j][e + 1] = (q + e < nk) ? Ir[pp + e] : 0u;
-            vv[j][e] = (q + e < nk) ? Vc[q + e] : (u16)0;
-          }
-          iv[j][0] = (q < nk && pp) ? Ir[pp - 1] : 0u;
+        for (int u = 0; u < kU; ++u) {
+          const u32 q = q0 + u * kCThreads + tid;
+          const bool in = q < nk;
+          iv[u] = in ? Ic[q] : 0u;
+          vv[u] = in ? (u32)Vc[q] : 0u;
+          pv[u] = (lane == 0 && in && mode == 0) ? (q ? Ic[q - 1] : first_prev) : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < kG; ++j) {
-          const u32 q = q0 + 4 * kCThreads * j;
-          if (q >= nk) continue;
-          if (q + 4 <= nk) {
-            if (mode == 0) {
-              const uint2 d = make_uint2((iv[j][1] - iv[j][0]) | ((iv[j][2] - iv[j][1]) << 16),
-                                         (iv[j][3] - iv[j][2]) | ((iv[j][4] - iv[j][3]) << 16));
-              *reinterpret_cast<uint2*>(reinterpret_cast<u16*>(rec + 16) + p0 + q) = d;
-            } else {
-              *reinterpret_cast<uint4*>(reinterpret_cast<u32*>(rec + 16) + p0 + q) =
-                  make_uint4(iv[j][1], iv[j][2], iv[j][3], iv[j][4]);
-            }
-            if (!e8)
-              *reinterpret_cast<u32*>(L + q) = (u32)(vv[j][0] & 0xFFu) | ((u32)(vv[j][1] & 0xFFu) << 8) |
-                                               ((u32)(vv[j][2] & 0xFFu) << 16) | ((u32)(vv[j][3] & 0xFFu) << 24);
-          } else {
-            for (u32 e = 0; q + e < nk; ++e) {  // chunk tail: reload (keeps the arrays in registers)
-              const u64 pe = p0 + q + e;
-              const u32 cur = Ir[pe], prev = pe ? Ir[pe - 1] : 0u;
-              if (mode == 0) reinterpret_cast<u16*>(rec + 16)[pe] = (u16)(cur - prev);
-              else reinterpret_cast<u32*>(rec + 16)[pe] = cur;
-              if (!e8) L[q + e] = (u8)(Vc[q + e] & 0xFFu);
-            }
+        for (int u = 0; u < kU; ++u) {
+          const u32 q = q0 + u * kCThreads + tid;
+          u32 prev = __shfl_up_sync(0xffffffffu, iv[u], 1);
+          if (lane == 0) prev = pv[u];
+          if (q < nk) {
+            if (mode == 0) D16[q] = (u16)(iv[u] - prev);
+            else A32[q] = iv[u];
+            if (!e8) L[q] = (u8)(vv[u] & 0xFFu);
           }
         }
       }

@@ -47,6 +47,11 @@ struct Plan {
   uint64_t* srec;                // [T+1] exclusive prefix of the record bytes over records
   uint64_t* crec;                // [T+1] exclusive prefix of the on-wire chunk counts over records
   uint64_t* work;                // [2] chunk claim counters (k_chunk_stats, k_encode), zeroed by k_plan_scan
+  uint32_t* tickets;             // [3] CTA tickets of the grid scans (scan.cuh); never reset
+  uint64_t* gscan;               // GScanState [gscan_T + gscan_C + gscan_T]: plan_scan, plan_chunks, plan_records
+  uint32_t gscan_T;              // CTAs of the per-tensor scans = ceil(T / 1024)
+  uint32_t gscan_C;              // CTAs of the per-chunk scan = ceil(max_chunks / 1024)
+  uint64_t epoch;                // this plan's number (>= 1): the scans' publication flag
 };
 
 enum TotalsIdx {

@@ -1,92 +1,61 @@
 // plan.cu — K2: record plan for the §3.3 encodings (rows a2 + sizing of a3/a4).
 //
 // From the per-tensor counts of K1:
-//  * k_plan_scan   (1 CTA)   value offsets, chunk offsets, totals (manifest order)
+//  * k_plan_scan   (grid)    value offsets, chunk offsets, totals (manifest order)
 //  * k_chunk_stats (grid)    per chunk: max index gap (-> DELTA16/ABS32, P:360,
 //                            DESIGN C4), hi-byte histogram, normalised rANS model
 //                            and the rANS encode pass -> exact hi block size and
 //                            RAW/RANS decision (never-expand); words, states
 //                            and model kept in scratch for k_encode
-//  * k_plan_sizes  (1 CTA)   chunk hi-offset prefix, record sizes,
-//                            record byte offsets, statistics
+//  * k_plan_chunks (grid)    chunk hi-offset / escape prefixes
+//  * k_plan_records (grid)   record sizes and modes, record byte offsets, the compacted
+//                            record table for the bucket planner, statistics
+// The scans are grid-wide (scan.cuh: one item per thread, CTA totals published with the plan's epoch):
+// single-CTA versions took 40 + 117 us of latency per sync on the 30B manifest.
 #include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
 #include "chunk.cuh"
+#include "scan.cuh"
 
 namespace ss {
 
-constexpr int kScanThreads = 1024;
+#define G_STATE(p, off) (reinterpret_cast<GScanState*>((p).gscan) + (off))
+#define G_OFF_CHUNKS(p) ((p).gscan_T)
+#define G_OFF_RECORDS(p) ((p).gscan_T + (p).gscan_C)
 
-// Block-wide exclusive scan of a u64 (1024 threads); returns the block total.
-__device__ __forceinline__ u64 block_excl_scan64(u64 v, u64* excl, u64* s_w) {
-  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  u64 inc = warp_incl_scan64(v);
-  if (lane == 31) s_w[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    u64 w = s_w[lane];
-    u64 wi = warp_incl_scan64(w);
-    s_w[lane] = wi - w;
-    if (lane == 31) s_w[32] = wi;
-  }
-  __syncthreads();
-  *excl = s_w[warp] + inc - v;
-  u64 total = s_w[32];
-  __syncthreads();
-  return total;
-}
-
-constexpr int kPerScan = 8;   // tensors per thread per round (one block scan pair per 8192 tensors)
-__global__ void __launch_bounds__(kScanThreads) k_plan_scan(Plan p, const u64* counts) {
-  __shared__ u64 s_w[33];
-  __shared__ u64 s_w2[33];
-  u64 carry_nnz = 0, carry_ch = 0, carry_rec = 0;
+// one tensor per thread: (nnz, chunks, record flag) -> rec_off, chunk_off; the last CTA writes the totals
+__global__ void __launch_bounds__(kGScan) k_plan_scan(Plan p, const u64* counts) {
+  __shared__ u64 s_w[3 * 33];
+  __shared__ u32 s_j;
   const u32 T = p.n_tensors;
-  constexpr u32 kRound = kScanThreads * kPerScan;
-  for (u32 b = 0; b < T; b += kRound) {
-    const u32 t0 = b + threadIdx.x * kPerScan;
-    u64 c[kPerScan];
-    u64 s1 = 0, s2 = 0;
-#pragma unroll
-    for (int k = 0; k < kPerScan; ++k) {
-      const u32 t = t0 + k;
-      c[k] = t < T ? counts[t] : 0;
-      s1 += c[k];
-      s2 += (((c[k] + kChunk - 1) / kChunk) << 32) | (c[k] ? 1u : 0u);   // chunks (< 2^32 total) | record flag
-    }
-    u64 e1, e2;
-    const u64 tot1 = block_excl_scan64(s1, &e1, s_w);
-    const u64 tot2 = block_excl_scan64(s2, &e2, s_w2);
-    u64 r1 = carry_nnz + e1, r2 = carry_ch + (e2 >> 32);
-#pragma unroll
-    for (int k = 0; k < kPerScan; ++k) {
-      const u32 t = t0 + k;
-      if (t < T) {
-        p.rec_off[t] = r1;
-        p.chunk_off[t] = r2;
-        p.maxgap[t] = 0;
-      }
-      r1 += c[k];
-      r2 += (c[k] + kChunk - 1) / kChunk;
-    }
-    carry_nnz += tot1;
-    carry_ch += tot2 >> 32;
-    carry_rec += tot2 & 0xFFFFFFFFull;
+  const u32 G = T ? (T + kGScan - 1) / kGScan : 1;
+  const u32 j = gscan_rank(p.tickets + 0, G, &s_j);
+  const u32 t = j * kGScan + threadIdx.x;
+  const u64 c = t < T ? counts[t] : 0;
+  const u64 v[3] = {c, (c + kChunk - 1) / kChunk, c ? 1ull : 0ull};
+  u64 ex[3], tot[3], pre[3];
+  block_scan3(v, ex, tot, s_w);
+  gscan_publish_and_prefix(G_STATE(p, 0), j, p.epoch, tot, pre, s_w);
+  if (t < T) {
+    p.rec_off[t] = pre[0] + ex[0];
+    p.chunk_off[t] = pre[1] + ex[1];
+    p.maxgap[t] = 0;
   }
-  if (threadIdx.x == 0) {
-    p.rec_off[T] = carry_nnz;
-    p.chunk_off[T] = carry_ch;
-    bool over = carry_nnz > p.cap || carry_ch > p.max_chunks;
+  if (j + 1 == G && threadIdx.x == 0) {
+    const u64 nnz = pre[0] + tot[0], ch = pre[1] + tot[1], rec = pre[2] + tot[2];
+    p.rec_off[T] = nnz;
+    p.chunk_off[T] = ch;
+    const bool over = nnz > p.cap || ch > p.max_chunks;
     if (over) latch(p.status, SYNC_ERR_CAPACITY);
     for (int k = 0; k < 16; ++k) p.totals[k] = 0;
     p.work[0] = 0;   // chunk counters of k_chunk_stats / k_encode
     p.work[1] = 0;
-    p.totals[kTotNnz] = carry_nnz;
-    p.totals[kTotChunks] = over ? 0 : carry_ch;
-    p.totals[kTotRecords] = carry_rec;
+    p.totals[kTotNnz] = nnz;
+    p.totals[kTotChunks] = over ? 0 : ch;
+    p.totals[kTotRecords] = rec;
     p.totals[kTotOverflow] = over ? 1 : 0;
   }
 }
@@ -103,6 +72,7 @@ __device__ unsigned long long g_cprof[8];  // debug cycle counters (SS_CPROF=1)
 // two of I); the gap into the group comes from lane l-1's last index (one shuffle), the warp's carry from
 // the previous round.
 constexpr int kWPF = 8;
+template <bool kEsc>   // f4: also count the gaps > 32767 per chunk (escape words)
 __global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
   __shared__ WarpModel s_m[8];
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -132,41 +102,64 @@ __global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, co
     carry0 = __shfl_sync(0xffffffffu, carry0, 0);
     u32 carry = carry0;
     u32 gmax = 0, nesc = 0;
-    for (u64 e0 = gs & ~7ull; e0 < ge; e0 += 256) {
-      const u64 e = e0 + 8ull * lane;
-      u32 iv[8], hv[8];
-      if (e < ge && e + 8 <= p.cap) {   // a whole 8-group inside the I / V arrays (values outside the chunk
-                                        // are loaded and masked below)
-        const uint4 va = *reinterpret_cast<const uint4*>(V + e);
-        const uint4 ia = *reinterpret_cast<const uint4*>(I + e);
-        const uint4 ib = *reinterpret_cast<const uint4*>(I + e + 4);
-        const u32 vw[4] = {va.x, va.y, va.z, va.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          hv[2 * k] = (vw[k] >> sh) & 0xFFu;
-          hv[2 * k + 1] = (vw[k] >> (16 + sh)) & 0xFFu;
-        }
-        iv[0] = ia.x; iv[1] = ia.y; iv[2] = ia.z; iv[3] = ia.w;
-        iv[4] = ib.x; iv[5] = ib.y; iv[6] = ib.z; iv[7] = ib.w;
-      } else {
+    // one round = 256 values (8 per lane); the next round's 16-byte loads are issued before this round is
+    // consumed. Groups wholly inside the chunk (all but its first and last) take the unmasked path.
+    auto load = [&](u64 e, uint4& va, uint4& ia, uint4& ib) {
+      if (e < ge && e + 8 <= p.cap) {   // a whole 8-group inside the I / V arrays
+        va = *reinterpret_cast<const uint4*>(V + e);
+        ia = *reinterpret_cast<const uint4*>(I + e);
+        ib = *reinterpret_cast<const uint4*>(I + e + 4);
+      } else {                           // the arrays' tail: element loads (masked below)
+        u32 h[8], x[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const bool in = e + k >= gs && e + k < ge;
-          iv[k] = in ? I[e + k] : 0u;
-          hv[k] = in ? ((u32)V[e + k] >> sh) & 0xFFu : 0u;
+          const bool in = e + k < ge;
+          x[k] = in ? I[e + k] : 0u;
+          h[k] = in ? (u32)V[e + k] : 0u;
         }
+        va = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+        ia = make_uint4(x[0], x[1], x[2], x[3]);
+        ib = make_uint4(x[4], x[5], x[6], x[7]);
       }
+    };
+    uint4 nva, nia, nib;
+    const u64 eb = gs & ~7ull;
+    load(eb + 8ull * lane, nva, nia, nib);
+    for (u64 e0 = eb; e0 < ge; e0 += 256) {
+      const u64 e = e0 + 8ull * lane;
+      const uint4 va = nva, ia = nia, ib = nib;
+      if (e0 + 256 < ge) load(e + 256, nva, nia, nib);
+      const u32 vw[4] = {va.x, va.y, va.z, va.w};
+      u32 hv[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        hv[2 * k] = (vw[k] >> sh) & 0xFFu;
+        hv[2 * k + 1] = (vw[k] >> (16 + sh)) & 0xFFu;
+      }
+      const u32 iv[8] = {ia.x, ia.y, ia.z, ia.w, ib.x, ib.y, ib.z, ib.w};
       u32 prev = __shfl_up_sync(0xffffffffu, iv[7], 1);
       if (lane == 0) prev = carry;
       carry = __shfl_sync(0xffffffffu, iv[7], 31);
+      if (e >= gs && e + 8 <= ge) {
+        // whole group inside the chunk; if it starts the chunk it is lane 0's of the first round, whose
+        // prev is carry0
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const u64 q = e + k;
-        if (q >= gs && q < ge) {
+        for (int k = 0; k < 8; ++k) {
           atomicAdd(&m.hist[hv[k]], 1u);
-          const u32 d = iv[k] - (q == gs ? carry0 : (k ? iv[k - 1] : prev));
+          const u32 d = iv[k] - (k ? iv[k - 1] : prev);
           gmax = d > gmax ? d : gmax;
-          nesc += d > 32767u ? 1u : 0u;
+          if (kEsc) nesc += d > 32767u ? 1u : 0u;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const u64 q = e + k;
+          if (q >= gs && q < ge) {
+            atomicAdd(&m.hist[hv[k]], 1u);
+            const u32 d = iv[k] - (q == gs ? carry0 : (k ? iv[k - 1] : prev));
+            gmax = d > gmax ? d : gmax;
+            if (kEsc) nesc += d > 32767u ? 1u : 0u;
+          }
         }
       }
     }
@@ -178,7 +171,7 @@ __global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, co
     if (lane == 0 && gmax) atomicMax(&p.maxgap[t], gmax);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nesc += __shfl_xor_sync(0xffffffffu, nesc, o);
-    if (lane == 0) p.chunk_esc[g] = nesc;   // f4: gaps that need an escape word
+    if (kEsc && lane == 0) p.chunk_esc[g] = nesc;   // f4: gaps that need an escape word
     __syncwarp();
     const long long t2 = clock64();
     if (!comp) continue;
@@ -271,184 +264,132 @@ __global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, co
   }
 }
 
-// Block-wide sum of a u64 (1024 threads); every thread gets the total.
-__device__ __forceinline__ u64 block_sum64(u64 v, u64* s_w) {
-  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) s_w[warp] = v;
-  __syncthreads();
-  u64 t = s_w[lane];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  __syncthreads();
-  return t;
+// one chunk per thread: exclusive prefixes of the padded hi block sizes and of the escape counts; RANS chunks
+__global__ void __launch_bounds__(kGScan) k_plan_chunks(Plan p, u32 G) {
+  __shared__ u64 s_w[3 * 33];
+  __shared__ u32 s_j;
+  const u32 j = gscan_rank(p.tickets + 1, G, &s_j);
+  const u64 n_chunks = p.totals[kTotChunks];
+  const u64 g = (u64)j * kGScan + threadIdx.x;
+  const bool in = g < n_chunks;
+  const u64 v[3] = {in ? pad_to(p.chunk_hi[g], 4) : 0, (in && p.escape) ? p.chunk_esc[g] : 0,
+                    in ? p.chunk_mode[g] : 0};
+  u64 ex[3], tot[3], pre[3];
+  block_scan3(v, ex, tot, s_w);
+  gscan_publish_and_prefix(G_STATE(p, G_OFF_CHUNKS(p)), j, p.epoch, tot, pre, s_w);
+  if (in) {
+    p.chunk_hioff[g] = pre[0] + ex[0];
+    p.chunk_escoff[g] = pre[1] + ex[1];
+  }
+  if (j + 1 == G && threadIdx.x == 0) {
+    p.chunk_hioff[n_chunks] = pre[0] + tot[0];
+    p.chunk_escoff[n_chunks] = pre[1] + tot[1];
+    p.totals[kTotRansChunks] = pre[2] + tot[2];
+  }
 }
 
-// Single CTA; every thread owns kPer consecutive items per round, so a round covers 8192 chunks or tensors
-// with one block scan (30B: 3 rounds over the chunks, 3 over the tensors).
-constexpr int kPer = 8;
-__global__ void __launch_bounds__(kScanThreads) k_plan_sizes(Plan p, const u64* counts) {
-  __shared__ u64 s_w[33];
-  __shared__ u64 s_w2[33];
+// one tensor per thread: record mode and size (C4, C19, §3.6), the byte offset of each record
+// in the contiguous stream (enc_off), and the record table (compacted: tensors with a change, manifest order)
+// with its byte and on-wire chunk prefixes for the bucket planner (bucket.cu); statistics by atomics
+__global__ void __launch_bounds__(kGScan) k_plan_records(Plan p, const u64* counts) {
+  __shared__ u64 s_w[3 * 33];
+  __shared__ u64 s_st[6];
+  __shared__ u32 s_j;
   const u32 T = p.n_tensors;
+  const u32 G = T ? (T + kGScan - 1) / kGScan : 1;
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
   const bool e8 = p.dtype == SYNC_DTYPE_FP8;
-  const u64 n_chunks = p.totals[kTotChunks];
   const bool over = p.totals[kTotOverflow] != 0;
-  constexpr u64 kRound = (u64)kScanThreads * kPer;
-  // 1. exclusive prefix of padded hi block sizes over all chunks (+ RANS chunk count)
-  u64 carry = 0, rans_local = 0, ecarry = 0;
-  if (comp) {
-    for (u64 b = 0; b < n_chunks; b += kRound) {
-      const u64 g0 = b + (u64)threadIdx.x * kPer;
-      u64 v[kPer], es[kPer];
-      u64 sum = 0, esum = 0;
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const u64 g = g0 + k;
-        v[k] = g < n_chunks ? pad_to(p.chunk_hi[g], 4) : 0;
-        es[k] = (p.escape && g < n_chunks) ? p.chunk_esc[g] : 0;
-        rans_local += g < n_chunks ? p.chunk_mode[g] : 0;
-        sum += v[k];
-        esum += es[k];
-      }
-      u64 e, ee;
-      const u64 tot = block_excl_scan64(sum, &e, s_w);
-      const u64 etot = block_excl_scan64(esum, &ee, s_w2);
-      u64 run = carry + e, erun = ecarry + ee;
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const u64 g = g0 + k;
-        if (g < n_chunks) {
-          p.chunk_hioff[g] = run;
-          p.chunk_escoff[g] = erun;
+  const u32 j = gscan_rank(p.tickets + 2, G, &s_j);
+  if (threadIdx.x < 6) s_st[threadIdx.x] = 0;
+  const u32 t = j * kGScan + threadIdx.x;
+  const u64 c = (t < T && !over) ? counts[t] : 0;
+  u64 by = 0, ib = 0, wch = 0;
+  u32 mode = 1;
+  if (c) {
+    const u64 ch0 = p.chunk_off[t], ch1 = p.chunk_off[t + 1];
+    const u64 numel = p.numel[t];
+    if (comp) {
+      const u32 mg = p.maxgap[t];
+      const u64 hi = p.chunk_hioff[ch1] - p.chunk_hioff[ch0];
+      mode = mg <= 32767u ? 0u : 1u;
+      u64 table = 0;
+      if (mode && p.escape) {   // f4: escapes < nnz -> DELTA16E beats ABS32
+        const u64 ne = p.chunk_escoff[ch1] - p.chunk_escoff[ch0];
+        if (ne < c) {
+          mode = kModeDelta16E;
+          table = 4 * (ch1 - ch0 + 1);
+          ib = pad_to(2 * (c + ne), 4);
         }
-        run += v[k];
-        erun += es[k];
       }
-      carry += tot;
-      ecarry += etot;
+      if (mode != kModeDelta16E) ib = pad_to((mode ? 4 : 2) * c, 4);
+      by = pad_to(16 + table + ib + (e8 ? 0 : pad_to(c, 4)) + 16 * (ch1 - ch0) + hi, 16);   // FP8: no lo plane
+    } else {
+      ib = 4 * c;
+      by = pad_to(16 + (e8 ? 5 : 6) * c, 16);
     }
-    if (threadIdx.x == 0) {
-      p.chunk_hioff[n_chunks] = carry;
-      p.chunk_escoff[n_chunks] = ecarry;
+    const u64 full = pad_to(16 + (e8 ? 1 : 2) * numel, 16);   // f3 routing (DESIGN C19)
+    if (p.route && full < by) {
+      mode = kModeFull;
+      by = full;
+      ib = 0;
     }
-    __syncthreads();
+    // chunks of a record on the wire = ceil(nnz field / C); a FULL record's nnz field is numel
+    wch = mode == kModeFull ? (numel + kChunk - 1) / kChunk : ch1 - ch0;
   }
-  const u64 rans = block_sum64(rans_local, s_w2);
-  // 2. record sizes and offsets; the record table (compacted: tensors with a change, in manifest order) with
-  //    the byte and on-wire chunk prefixes the device bucket planner walks (bucket.cu)
-  u64 carry_enc = 0, n16 = 0, n32 = 0, ib_tot = 0, vb_tot = 0, nfull = 0, n16e = 0, carry_r = 0, carry_c = 0;
-  for (u32 b = 0; b < T; b += (u32)kRound) {
-    const u32 t0 = b + threadIdx.x * kPer;
-    u64 bytes[kPer], wch[kPer];
-    u64 sum = 0, rsum = 0, csum = 0;
+  if (t < T) {
+    p.rec_mode[t] = mode;
+    p.rec_bytes[t] = by;
+  }
+  __syncthreads();   // s_st zeroed
+  {                  // statistics: record kinds, index / value bytes (warp sums, then one shared atomic per warp)
+    const int kind = !by ? -1 : mode == kModeFull ? 3 : mode == kModeDelta16E ? 2 : mode ? 1 : 0;
+    u64 st[6] = {kind == 0, kind == 1, kind == 2, kind == 3, by ? ib : 0, by ? by - 16 - ib : 0};
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const u32 t = t0 + k;
-      const u64 c = (t < T && !over) ? counts[t] : 0;
-      u64 by = 0, ib = 0;
-      u32 mode = 1;
-      if (c) {
-        if (comp) {
-          const u64 ch0 = p.chunk_off[t], ch1 = p.chunk_off[t + 1];
-          mode = p.maxgap[t] <= 32767u ? 0u : 1u;
-          u64 table = 0;
-          if (mode && p.escape) {   // f4: escapes < nnz -> DELTA16E beats ABS32
-            const u64 ne = p.chunk_escoff[ch1] - p.chunk_escoff[ch0];
-            if (ne < c) {
-              mode = kModeDelta16E;
-              table = 4 * (ch1 - ch0 + 1);
-              ib = pad_to(2 * (c + ne), 4);
-            }
-          }
-          if (mode != kModeDelta16E) ib = pad_to((mode ? 4 : 2) * c, 4);
-          const u64 hi = p.chunk_hioff[ch1] - p.chunk_hioff[ch0];
-          by = pad_to(16 + table + ib + (e8 ? 0 : pad_to(c, 4)) + 16 * (ch1 - ch0) + hi, 16);   // FP8: no lo plane
-        } else {
-          ib = 4 * c;
-          by = pad_to(16 + (e8 ? 5 : 6) * c, 16);
-        }
-        const u64 full = pad_to(16 + (e8 ? 1 : 2) * p.numel[t], 16);   // f3 routing (DESIGN C19)
-        if (p.route && full < by) {
-          mode = kModeFull;
-          by = full;
-          ib = 0;
-          nfull++;
-        } else if (mode == kModeDelta16E) {
-          n16e++;
-        } else if (mode) {
-          n32++;
-        } else {
-          n16++;
-        }
-        ib_tot += ib;
-        vb_tot += by - 16 - ib;
-      }
-      if (t < T) {
-        p.rec_mode[t] = mode;
-        p.rec_bytes[t] = by;
-      }
-      bytes[k] = by;
-      // chunks of a record on the wire = ceil(nnz field / C); a FULL record's nnz field is numel
-      wch[k] = !by ? 0 : mode == kModeFull ? (p.numel[t] + kChunk - 1) / kChunk : p.chunk_off[t + 1] - p.chunk_off[t];
-      sum += by;
-      rsum += by ? 1 : 0;
-      csum += wch[k];
+    for (int k = 0; k < 6; ++k) {
+      st[k] = warp_sum64(st[k]);
+      if ((threadIdx.x & 31) == 0 && st[k]) atomicAdd(reinterpret_cast<unsigned long long*>(&s_st[k]), st[k]);
     }
-    u64 e, re, ce;
-    const u64 tot = block_excl_scan64(sum, &e, s_w);
-    const u64 rtot = block_excl_scan64(rsum, &re, s_w2);
-    const u64 ctot = block_excl_scan64(csum, &ce, s_w);
-    u64 run = carry_enc + e, rrun = carry_r + re, crun = carry_c + ce;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const u32 t = t0 + k;
-      if (t < T) p.enc_off[t] = run;
-      if (bytes[k]) {
-        p.rec_list[rrun] = t;
-        p.srec[rrun] = run;
-        p.crec[rrun] = crun;
-        rrun++;
-      }
-      run += bytes[k];
-      crun += wch[k];
-    }
-    carry_enc += tot;
-    carry_r += rtot;
-    carry_c += ctot;
+  }
+  const u64 v[3] = {by, by ? 1ull : 0ull, wch};
+  u64 ex[3], tot[3], pre[3];
+  block_scan3(v, ex, tot, s_w);
+  gscan_publish_and_prefix(G_STATE(p, G_OFF_RECORDS(p)), j, p.epoch, tot, pre, s_w);
+  const u64 off = pre[0] + ex[0];
+  if (t < T) p.enc_off[t] = off;
+  if (by) {
+    const u64 r = pre[1] + ex[1];
+    p.rec_list[r] = t;
+    p.srec[r] = off;
+    p.crec[r] = pre[2] + ex[2];
   }
   if (threadIdx.x == 0) {
-    p.srec[carry_r] = carry_enc;
-    p.crec[carry_r] = carry_c;
-  }
-  n16 = block_sum64(n16, s_w);
-  n32 = block_sum64(n32, s_w2);
-  ib_tot = block_sum64(ib_tot, s_w);
-  vb_tot = block_sum64(vb_tot, s_w2);
-  nfull = block_sum64(nfull, s_w);
-  n16e = block_sum64(n16e, s_w2);
-  if (threadIdx.x == 0) {
-    p.enc_off[T] = carry_enc;
-    if (carry_enc > p.enc_cap) {
-      latch(p.status, SYNC_ERR_CAPACITY);
-      p.totals[kTotOverflow] = 1;
-      p.totals[kTotChunks] = 0;   // nothing gets encoded
+    // codec RAW: every record counts as ABS32 (u32 indices)
+    const u64 n16 = s_st[0], n32 = s_st[1], n16e = s_st[2], nfull = s_st[3];
+    if (n16 && comp) atomicAdd(reinterpret_cast<unsigned long long*>(&p.totals[kTotDelta16]), n16);
+    if (n32 + (comp ? 0 : n16)) atomicAdd(reinterpret_cast<unsigned long long*>(&p.totals[kTotAbs32]), n32 + (comp ? 0 : n16));
+    if (n16e) atomicAdd(reinterpret_cast<unsigned long long*>(&p.totals[kTotDelta16E]), n16e);
+    if (nfull) atomicAdd(reinterpret_cast<unsigned long long*>(&p.totals[kTotFull]), nfull);
+    if (s_st[4]) atomicAdd(reinterpret_cast<unsigned long long*>(&p.totals[kTotIndexBytes]), (unsigned long long)s_st[4]);
+    if (s_st[5]) atomicAdd(reinterpret_cast<unsigned long long*>(&p.totals[kTotValueBytes]), (unsigned long long)s_st[5]);
+    if (j + 1 == G) {
+      const u64 enc = pre[0] + tot[0], R = pre[1] + tot[1];
+      p.enc_off[T] = enc;
+      p.srec[R] = enc;
+      p.crec[R] = pre[2] + tot[2];
+      p.totals[kTotEnc] = enc;
+      if (enc > p.enc_cap) {
+        latch(p.status, SYNC_ERR_CAPACITY);
+        p.totals[kTotOverflow] = 1;
+        p.totals[kTotChunks] = 0;   // nothing gets encoded
+      }
     }
-    p.totals[kTotEnc] = carry_enc;
-    p.totals[kTotDelta16] = comp ? n16 : 0;
-    p.totals[kTotAbs32] = comp ? n32 : n16 + n32;
-    p.totals[kTotRansChunks] = rans;
-    p.totals[kTotIndexBytes] = ib_tot;
-    p.totals[kTotValueBytes] = vb_tot;
-    p.totals[kTotFull] = nfull;
-    p.totals[kTotDelta16E] = n16e;
   }
 }
 
 void launch_plan_scan(const Plan& p, const u64* counts, cudaStream_t s) {
-  k_plan_scan<<<1, kScanThreads, 0, s>>>(p, counts);
+  const u32 T = p.n_tensors ? p.n_tensors : 1;
+  k_plan_scan<<<(T + kGScan - 1) / kGScan, kGScan, 0, s>>>(p, counts);
   count_launch();
 }
 
@@ -466,10 +407,12 @@ void launch_chunk_stats(const Plan& p, const u32* I, const u16* V, const u64* co
   if (!cap[dev]) {
     int n_sm = 148, per = 1;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chunk_stats, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chunk_stats<false>, 256, 0);
     cap[dev] = n_sm * (per > 0 ? per : 1);
   }
-  k_chunk_stats<<<grid < cap[dev] ? grid : cap[dev], 256, 0, s>>>(q, I, V, counts);
+  const int g = grid < cap[dev] ? grid : cap[dev];
+  if (p.escape) k_chunk_stats<true><<<g, 256, 0, s>>>(q, I, V, counts);
+  else k_chunk_stats<false><<<g, 256, 0, s>>>(q, I, V, counts);
   if (want) {
     unsigned long long h[8];
     cudaMemcpyFromSymbolAsync(h, g_cprof, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
@@ -482,7 +425,12 @@ void launch_chunk_stats(const Plan& p, const u32* I, const u16* V, const u64* co
 }
 
 void launch_plan_sizes(const Plan& p, const u64* counts, cudaStream_t s) {
-  k_plan_sizes<<<1, kScanThreads, 0, s>>>(p, counts);
+  if (p.codec == SYNC_CODEC_COMPRESSED) {
+    k_plan_chunks<<<p.gscan_C, kGScan, 0, s>>>(p, p.gscan_C);
+    count_launch();
+  }
+  const u32 T = p.n_tensors ? p.n_tensors : 1;
+  k_plan_records<<<(T + kGScan - 1) / kGScan, kGScan, 0, s>>>(p, counts);
   count_launch();
 }
 
