@@ -59,8 +59,9 @@ def parse():
                         "t + N/2 holds shard t (SURVEY 8(e) sharded Rollout)")
     p.add_argument("--commit", choices=["swap", "scatter"], default="swap",
                    help="snapshot commit: pointer swap of double-buffered trainer weights, or in-place scatter")
-    p.add_argument("--transport", choices=["nccl", "peer", "peer-direct"], default="peer",
-                   help="bucket data plane: NCCL P2P, NVLink peer memory pulled by the copy engines, or decoded "
+    p.add_argument("--transport", choices=["nccl", "nccl-bcast", "peer", "peer-direct"], default="peer",
+                   help="bucket data plane: NCCL P2P, NCCL broadcast (fanout: one broadcast per bucket to the "
+                        "Trainer's group of Rollouts), NVLink peer memory pulled by the copy engines, or decoded "
                         "in place from peer memory by the decode kernel")
     p.add_argument("--replica", choices=["separate", "snapshot"], default="separate",
                    help="N=1 only. separate: a third arena is the Rollout replica; snapshot: the decode+apply "
@@ -247,7 +248,7 @@ class Dist:
             # bring up the NCCL communicator (and, for the NCCL data plane, the P2P channels the topology
             # uses) before the weight arenas take the HBM
             dist.barrier(device_ids=[self.local])
-            if transport == "nccl":
+            if transport in ("nccl", "nccl-bcast"):
                 x = torch.zeros(1 << 20, dtype=torch.uint8, device=self.dev)
                 y = torch.empty_like(x)
                 W, half = self.world, self.world // 2
@@ -387,7 +388,7 @@ class Rank:
                 self.receivers[src] = GroupedReceiver(self.Rv[lo:hi], groups=self.G, **kw)
         torch.cuda.synchronize()
         self.link = None
-        if W > 1 and args.transport != "nccl":
+        if W > 1 and args.transport not in ("nccl", "nccl-bcast"):
             if topo == "ring":
                 dsts, srcs = [(d.rank + 1) % W], [(d.rank - 1) % W]
             elif topo == "fanout":
@@ -401,7 +402,8 @@ class Rank:
                 self.link = transport.RingLink(d.rank, W, dev, d.ctrl)
             elif topo == "fanout":
                 self.link = transport.FanoutLink(d.rank, W, dev, trainers=list(range(half)),
-                                                 rollouts=list(range(half, W)), ctrl=d.ctrl)
+                                                 rollouts=list(range(half, W)), ctrl=d.ctrl,
+                                                 mode="broadcast" if args.transport == "nccl-bcast" else "p2p")
             else:
                 t = d.rank if self.is_trainer else d.rank - half
                 self.link = transport.PairLink(d.rank, W, dev, trainer=t, rollout=t + half, ctrl=d.ctrl)
@@ -1008,6 +1010,7 @@ def run_ours(args):
     }[args.topology]
     if d.world > 1:
         topo_txt += {"nccl": "; data plane: NCCL P2P send/recv",
+                     "nccl-bcast": "; data plane: NCCL broadcast per bucket (fanout) / P2P send/recv",
                      "peer": "; data plane: NVLink peer memory (CUDA IPC), pulled by the copy engines",
                      "peer-direct": "; data plane: NVLink peer memory, decoded in place by the decode kernel"}[
             args.transport]

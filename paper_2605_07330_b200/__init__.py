@@ -18,7 +18,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsparsesync.so")
+# SS_LIB: another build of the same library (dev A/B runs on one box); the default is the in-tree build
+LIB_PATH = os.environ.get("SS_LIB") or os.path.join(_HERE, "libsparsesync.so")
 
 SYNC_OK = 0
 SYNC_ERR_ARG = -1
@@ -252,7 +253,8 @@ class SyncContext:
 
     def __init__(self, numel, bucket_limit: int = 256 << 20, max_changed: int | None = None,
                  codec: int = SYNC_CODEC_COMPRESSED, crc: bool = False, device=None, route: bool = False,
-                 dtype: int = SYNC_DTYPE_BF16, escape: bool = False):
+                 dtype: int = SYNC_DTYPE_BF16, escape: bool = False, workspace: torch.Tensor | None = None):
+        """workspace: optional caller-owned uint8 device tensor of >= workspace_size bytes (else allocated)."""
         self.numel = [int(n) for n in numel]
         self.device = torch.device(device or "cuda")
         self.T = len(self.numel)
@@ -266,7 +268,12 @@ class SyncContext:
         need = ctypes.c_size_t()
         _ck(lib().sync_workspace_size(ctypes.byref(self._m), ctypes.byref(self._c), ctypes.byref(need)),
             "sync_workspace_size")
-        self.workspace = torch.zeros(need.value, dtype=torch.uint8, device=self.device)
+        if workspace is not None:
+            if workspace.dtype != torch.uint8 or workspace.numel() < need.value:
+                raise SyncError(SYNC_ERR_WORKSPACE if workspace.numel() < need.value else -1, "workspace")
+            self.workspace = workspace
+        else:
+            self.workspace = torch.zeros(need.value, dtype=torch.uint8, device=self.device)
         eb = ctypes.c_uint64()
         _ck(lib().sync_enc_bound(ctypes.byref(self._m), ctypes.byref(self._c), ctypes.byref(eb)), "sync_enc_bound")
         self.enc_bound = eb.value

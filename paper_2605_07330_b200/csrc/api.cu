@@ -36,7 +36,7 @@ constexpr u64 kAlign = 256;
 struct Layout {
   u64 numel, tile_prefix, tile_tensor, misc, tile_state, stage_ring, rec_off, chunk_off, maxgap, rec_mode, rec_bytes, enc_off;
   u64 chunk_hi, chunk_mode, chunk_hioff, chunk_rhdr, word_scratch, rec_dst, totals, recs, bks, views, nviews, crc;
-  u64 bm_off, group_sum, chunk_esc, chunk_escoff, bitmap8, rec_list, srec, crec, nxt, bstart, seg_off, gscan, total;
+  u64 bm_off, group_sum, chunk_esc, chunk_escoff, chunk_t, bitmap8, rec_list, srec, crec, nxt, bstart, seg_off, gscan, total;
 };
 
 u64 crc_slots(u64 max_bucket_bytes) { return max_bucket_bytes / 4096 + 4 + 32; }  // + 32 bad flags
@@ -77,6 +77,7 @@ Layout make_layout(u32 T, u64 n_tiles, u64 max_chunks, u64 crc_n, u64 max_change
   L.group_sum = take(8ull * (n_tiles / 1024 + 2));       // f1: tile-offset scan groups
   L.chunk_esc = take(4ull * max_chunks);                   // f4: escapes per chunk
   L.chunk_escoff = take(8ull * (max_chunks + 1));          // f4: their exclusive prefix
+  L.chunk_t = take(4ull * max_chunks);                     // tensor of each chunk
   L.bitmap8 = take(4ull * bm8_words);                      // FP8: change bitmap of the extract
   L.rec_list = take(4ull * T);                             // device bucket plan (bucket.cu)
   L.srec = take(8ull * (T + 1));
@@ -242,6 +243,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   p.escape = (c->flags & SYNC_FLAG_ESCAPE) ? 1 : 0;
   p.chunk_esc = reinterpret_cast<u32*>(w + L.chunk_esc);
   p.chunk_escoff = reinterpret_cast<u64*>(w + L.chunk_escoff);
+  p.chunk_t = reinterpret_cast<u32*>(w + L.chunk_t);
   p.cur = nullptr;
   p.max_chunks = d.max_chunks;
   p.numel = reinterpret_cast<const u64*>(w + L.numel);

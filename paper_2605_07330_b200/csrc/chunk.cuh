@@ -23,6 +23,19 @@ struct ChunkPos {
 // n_k / 2 words, so consecutive chunks never overlap.
 __device__ __forceinline__ u64 chunk_words_base(u64 vpos, u64 g) { return vpos / 2 + g; }
 
+__device__ __forceinline__ ChunkPos chunk_at(const Plan& p, const u64* counts, u64 g, u32 t, const u32* I,
+                                             const u16* V) {
+  ChunkPos c;
+  c.t = t;
+  c.nnz = counts[t];
+  c.k = g - p.chunk_off[t];
+  c.p0 = c.k * kChunk;
+  c.nk = (u32)((c.nnz - c.p0) < kChunk ? (c.nnz - c.p0) : kChunk);
+  c.Ir = I + p.rec_off[t];
+  c.Vc = V + p.rec_off[t] + c.p0;
+  return c;
+}
+
 // Locate chunk g (warp 0 searches the chunk offsets) — all threads get the same.
 __device__ __forceinline__ ChunkPos locate_chunk(const Plan& p, const u64* counts, u64 g, u32& s_t,
                                                  const u32* I, const u16* V) {

@@ -24,18 +24,21 @@ __device__ __forceinline__ void zero_bytes(u8* p, u64 n) {
 __global__ void __launch_bounds__(kCThreads, 6) k_encode(Plan p, const u32* I, const u16* V, const u64* counts,
                                                      u8* enc) {
   __shared__ u32 s_t;
-  __shared__ u64 s_g;
+  __shared__ u64 s_g[2];
   const u32 tid = threadIdx.x;
   const u64 n_chunks = p.totals[kTotChunks];
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
   const bool e8 = p.dtype == SYNC_DTYPE_FP8;   // FP8: one value plane (the byte), no lo plane
-  for (;;) {
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(p.work + 1);
+  if (tid == 0) s_g[0] = atomicAdd(ctr, 1ull);
+  for (u32 it = 0;; ++it) {
     __syncthreads();
-    if (tid == 0) s_g = atomicAdd(reinterpret_cast<unsigned long long*>(p.work + 1), 1ull);   // next chunk
-    __syncthreads();
-    const u64 g = s_g;
+    const u64 g = s_g[it & 1];
     if (g >= n_chunks) break;
-    const ChunkPos c = locate_chunk(p, counts, g, s_t, I, V);
+    if (tid == 0) s_g[(it + 1) & 1] = atomicAdd(ctr, 1ull);   // claim the next chunk now: its latency hides
+                                                                // behind this chunk's work
+    // the compressed codec's stats pass recorded each chunk's tensor (no search)
+    const ChunkPos c = comp ? chunk_at(p, counts, g, p.chunk_t[g], I, V) : locate_chunk(p, counts, g, s_t, I, V);
     const u32 t = c.t;
     const u64 nnz = c.nnz, k = c.k, p0 = c.p0;
     const u32 nk = c.nk;

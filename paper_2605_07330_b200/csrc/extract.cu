@@ -43,7 +43,10 @@ namespace ss {
 
 constexpr int kXConsumers = kXThreads;            // 256 consumer threads (8 warps)
 constexpr int xblock(int writers) { return kXConsumers + 64 + 32 * writers; }  // + copier, scheduler, writers
-constexpr int kXQueue = 4;                        // tiles resolved ahead by the scheduler
+#ifndef SS_XQUEUE
+#define SS_XQUEUE 4
+#endif
+constexpr int kXQueue = SS_XQUEUE;                // tiles claimed + resolved ahead by the scheduler
 constexpr u32 kStageBytes = (u32)kSub * 2 * 2;    // old + new, 16 KB each
 
 struct ExtractArgs {
@@ -354,6 +357,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
     // the cheap inclusive-prefix hand-off between consecutive tiles is serial
     // (through shared memory).
     const u32 w = warp - (kXConsumers / 32 + 2);
+    const u64 keep = policy_evict_last();
     long long p_w = 0, p_lb = 0, p_wr = 0, n_t = 0;
     for (u32 k = w;; k += kWriters) {
       const u32 b = k % kSlots;
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
 #pragma unroll
         for (int c = 0; c < kE; ++c) {
           const u32 q = c * 32 + lane;
-          nx[c] = q < m.count ? stg[q] : 0u;
+          nx[c] = q < m.count ? ld_hint(stg + q, keep) : 0u;
         }
         for (u32 q0 = 0; q0 < m.count; q0 += 32 * kE) {
           u32 ev[kE];
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
 #pragma unroll
             for (int c = 0; c < kE; ++c) {
               const u32 q = q0 + 32 * kE + c * 32 + lane;
-              nx[c] = q < m.count ? stg[q] : 0u;
+              nx[c] = q < m.count ? ld_hint(stg + q, keep) : 0u;
             }
           }
 #pragma unroll
@@ -407,9 +411,9 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
             const u32 q = q0 + c * 32 + lane;
             if (q < m.count) {
               const u64 pos = prefix + q;
-              if (room || pos < a.cap) {
-                a.I[pos] = (u32)(m.tile_base + (ev[c] & 0xFFFFu));
-                a.V[pos] = (u16)(ev[c] >> 16);
+              if (room || pos < a.cap) {   // streaming stores: the output is not re-read by this kernel
+                __stcs(a.I + pos, (u32)(m.tile_base + (ev[c] & 0xFFFFu)));
+                __stcs(a.V + pos, (u16)(ev[c] >> 16));
               } else {
                 latch(a.status, SYNC_ERR_CAPACITY);
               }
@@ -463,6 +467,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
   }
 
   // -------------------------------------------------------------- consumer warps
+  const u64 keep = policy_evict_last();   // the staging ring: written here, read back by the writers
   u32 tile_cnt = 0, tseq = 0, b = 0;
   u64 prev_tile = ~0ull;
   bool overflow = false;
@@ -555,7 +560,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
           const int bb = (kB == 1 ? __ffsll((long long)mk) : __ffs((int)mk)) - 1;
           mk &= mk - 1;
           const u32 val = kB == 1 ? (u32)sn8[kPerT * tid + bb] : (u32)sn16[kPerT * tid + bb];
-          *sp++ = __byte_perm(local + (u32)bb, val, 0x5410);
+          st_hint(sp++, __byte_perm(local + (u32)bb, val, 0x5410), keep);
         }
       }
       while (mk) {
@@ -569,7 +574,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
           if (kPerT * tid + bb + 1 <= si.bulk) val = sn16[kPerT * tid + bb];
           else val = si.pn[si.base + kPerT * tid + bb];
         }
-        stg[pos++] = (local + bb) | ((u32)val << 16);
+        st_hint(stg + pos++, (local + bb) | ((u32)val << 16), keep);
       }
     } else {
       overflow = true;

@@ -41,6 +41,7 @@ struct Plan {
   uint32_t dtype;                // record dtype tag (SYNC_DTYPE_*)
   int escape;                    // f4: SYNC_FLAG_ESCAPE
   uint32_t* chunk_esc;           // [max_chunks] index gaps > 32767 in the chunk (f4)
+  uint32_t* chunk_t;             // [max_chunks] tensor of each chunk (k_chunk_stats -> k_encode)
   uint64_t* chunk_escoff;        // [max_chunks+1] exclusive prefix of chunk_esc
   const uint16_t* const* cur;    // f3: current weights (FULL records), device pointer table
   uint32_t* rec_list;            // [T] tensor of record k (records = tensors with a change, manifest order)

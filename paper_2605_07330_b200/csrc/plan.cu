@@ -89,11 +89,11 @@ __global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, co
     const long long t0 = clock64();
     const u64* co = p.chunk_off;
     const u32 t = warp_upper_search(p.n_tensors, g, [&](u32 i) { return co[i]; });
+    if (lane == 0) p.chunk_t[g] = t;   // for k_encode
     const u64 nnz = counts[t];
     const u64 p0 = (g - co[t]) * kChunk;
     const u32 nk = (u32)((nnz - p0) < kChunk ? (nnz - p0) : kChunk);
     const u64 gs = p.rec_off[t] + p0, ge = gs + nk;   // the chunk's values in I / V
-    const u16* Vc = V + gs;
     const long long t1 = clock64();
     for (u32 sym = lane; sym < 256; sym += 32) m.hist[sym] = 0;
     __syncwarp();
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, co
     const u32 lt = (1u << lane) - 1u;
     const u32 wcap = nk / 2;
     u16* ws = p.word_scratch + chunk_words_base(gs, g);
-    const u8* Vb = reinterpret_cast<const u8*>(Vc) + (sh ? 1 : 0);   // byte 2q + vb: the coded byte of V[q]
+    const u8* Vb = reinterpret_cast<const u8*>(V + gs) + (sh ? 1 : 0);   // byte 2q + vb: the coded byte of V[q]
     asm volatile("" : "+l"(ws));   // keep the 64-bit base in registers (no per-step rematerialisation)
     const uint2* const fr = m.fr;
     u32 nxt[kWPF];

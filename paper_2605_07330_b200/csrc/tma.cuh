@@ -39,4 +39,19 @@ __device__ __forceinline__ u64 policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ u64 policy_evict_last() {
+  u64 p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 32-bit global store / load with an L2 eviction-priority hint (the extract's staging ring stays L2-resident
+// while the weights stream through with evict_first)
+__device__ __forceinline__ void st_hint(u32* p, u32 v, u64 pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ u32 ld_hint(const u32* p, u64 pol) {
+  u32 v;
+  asm volatile("ld.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol) : "memory");
+  return v;
+}
 }  // namespace ss
