@@ -88,6 +88,8 @@ def parse():
                         "step generates the new weights one tensor group of <= this many GB at a time into a "
                         "scratch buffer, which that group's extract reads (the generator runs inside the timed "
                         "step and is reported as its own phase, stream_generate)")
+    p.add_argument("--no-overlap-commit", action="store_true",
+                   help="--stream-gb: commit the snapshot after the group loop instead of per group on a side stream")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--latency-steps", type=int, default=5, help="barrier-separated syncs for per-update latency")
@@ -319,6 +321,7 @@ class Rank:
         if args.model_shards and (topo != "sharded" or n_shards < half):
             raise SystemExit("--model-shards K needs --topology sharded and K >= N/2")
         self.stream = args.stream_gb > 0
+        self.overlap_commit = False
         if self.stream and (topo != "sharded" or args.commit != "scatter" or args.dtype != "bf16"
                             or args.tracking != "snapshot"):
             raise SystemExit("--stream-gb runs with --topology sharded --commit scatter (bf16, snapshot tracking)")
@@ -433,6 +436,8 @@ class Rank:
                 off += n
         self.sender = GroupedSender(self.Xv, self.Yv, groups=self.G, max_changed=cap, **kw)
         assert self.sender.ranges == ranges
+        self.overlap_commit = not args.no_overlap_commit
+        self.commit_stream = torch.cuda.Stream(device=dev)
         # the update is a fixed set of bit flips (fill_new's mask and perturbation depend on the element, not on
         # the step): found once per group with the batched generator, then every step rebuilds the group's new
         # weights as a copy of its snapshot slice with those flips applied (new = X ^ d at I_d; after the commit
@@ -544,6 +549,14 @@ class Rank:
                                recv_buf=p.I.view(torch.uint8) if ring_swap else None)
                 else:
                     L.send(p.buckets, blist, tag=g)
+                if self.overlap_commit:
+                    # config 5: group g's snapshot scatter runs on a side stream while group g+1 is generated
+                    # and extracted (disjoint tensors); its buckets stay in the bucket buffer until the Rollout
+                    # has consumed them, so the delta is still retained for a retry
+                    ev_c = torch.cuda.Event()
+                    ev_c.record()
+                    self.commit_stream.wait_event(ev_c)
+                    p.commit(stream=self.commit_stream, mode="scatter")
             else:
                 rec(4 * g + 1)
                 rec(4 * g + 2)
@@ -558,6 +571,8 @@ class Rank:
         rec(4 * G)
         if self.loop_snapshot or self.tracking:
             pass                        # committed by the decode+apply (loopback) / nothing to commit (f1)
+        elif self.overlap_commit:
+            torch.cuda.current_stream().wait_stream(self.commit_stream)   # the per-group commits are done
         elif snd is not None:
             snd.commit(mode=a.commit)
             if a.commit == "swap":

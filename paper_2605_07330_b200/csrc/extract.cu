@@ -43,10 +43,7 @@ namespace ss {
 
 constexpr int kXConsumers = kXThreads;            // 256 consumer threads (8 warps)
 constexpr int xblock(int writers) { return kXConsumers + 64 + 32 * writers; }  // + copier, scheduler, writers
-#ifndef SS_XQUEUE
-#define SS_XQUEUE 4
-#endif
-constexpr int kXQueue = SS_XQUEUE;                // tiles claimed + resolved ahead by the scheduler
+constexpr int kXQueue = 4;                        // tiles claimed + resolved ahead by the scheduler
 constexpr u32 kStageBytes = (u32)kSub * 2 * 2;    // old + new, 16 KB each
 
 struct ExtractArgs {
