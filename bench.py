@@ -648,13 +648,15 @@ def verify_exact(r, d) -> dict:
             raise RuntimeError(f"rank {src}: snapshot size differs from the replica range of rank {dst}")
         for s0 in range(0, n, CMP_CHUNK):
             k = min(CMP_CHUNK, n - s0)
+            # NCCL has no int16: the chunks travel as bytes
             if d.rank == src:
-                dist.send(r.X[s0:s0 + k].contiguous(), dst)
+                dist.send(r.X[s0:s0 + k].contiguous().view(torch.uint8), dst)
             else:
+                es = r.R.element_size()
                 if scratch is None:
-                    scratch = torch.empty(CMP_CHUNK, dtype=r.R.dtype, device=d.dev)
-                dist.recv(scratch[:k], src)
-                ok = ok and torch.equal(scratch[:k], mine[src][s0:s0 + k])
+                    scratch = torch.empty(CMP_CHUNK * es, dtype=torch.uint8, device=d.dev)
+                dist.recv(scratch[:k * es], src)
+                ok = ok and torch.equal(scratch[:k * es], mine[src][s0:s0 + k].view(torch.uint8))
                 elems += k
     torch.cuda.synchronize()
     flags = [None] * d.world
