@@ -905,7 +905,11 @@ def run_ours(args):
     #      launch the --commit scatter path makes, over the last sync's (I, V) into the snapshot (which already
     #      holds those values under swap: idempotent, the same sectors move)
     k6 = None
-    if r.sender is not None and args.commit == "swap" and not r.tracking and not r.stream:
+    ring_recv_into_I = args.topology == "ring" and d.world > 1 and not r.tracking   # I holds the peer's buckets
+    if ring_recv_into_I:
+        k6 = {"ms": None, "what": "not measured: under --topology ring at N > 1 the last sync received the peer's "
+                                  "buckets into the (dead) I array, so there is no (I, V) left to scatter"}
+    if r.sender is not None and args.commit == "swap" and not r.tracking and not r.stream and not ring_recv_into_I:
         reps = 5
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -1198,11 +1202,20 @@ def run_reference(args):
 
 
 def main():
+    # the JSON line is the only thing on stdout: libraries that print to fd 1 (NCCL's version banner) go to
+    # stderr instead
+    out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    sys.stdout = sys.stderr
+    _main(out)
+
+
+def _main(stdout):
     args = parse()
     out = run_reference(args) if args.impl == "reference" else run_ours(args)
     if out is not None:
         line = json.dumps(out)
-        print(line, flush=True)
+        print(line, file=stdout, flush=True)
         if args.out:
             with open(args.out, "w") as f:
                 f.write(line + "\n")
