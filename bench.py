@@ -322,9 +322,13 @@ class Rank:
             raise SystemExit("--model-shards K needs --topology sharded and K >= N/2")
         self.stream = args.stream_gb > 0
         self.overlap_commit = False
-        if self.stream and (topo != "sharded" or args.commit != "scatter" or args.dtype != "bf16"
-                            or args.tracking != "snapshot"):
-            raise SystemExit("--stream-gb runs with --topology sharded --commit scatter (bf16, snapshot tracking)")
+        # config 5 with the paper's own hook (f1): the Trainer holds only its weights W and the change bitmap; the
+        # optimizer step that produces each update (the fp32 masters of each group, cast into W with tracking)
+        # runs before every timed sync, outside it
+        self.track_stream = self.stream and args.tracking == "cast"
+        if self.stream and (topo != "sharded" or args.dtype != "bf16"
+                            or (args.commit != "scatter" and not self.track_stream)):
+            raise SystemExit("--stream-gb runs with --topology sharded (bf16) and --commit scatter or --tracking cast")
         self.shards = transport.shard_ranges(manifest.numel, n_shards) if sharded_model else None
         if self.stream:   # the same group split on both ends of a shard pair
             lo, hi = self.shards[d.rank % half]
@@ -352,7 +356,9 @@ class Rank:
             self.mt = mt
             total = mt.total
             cap = min(total, int(total * args.rho * 1.02) + (1 << 20))
-            if self.tracking:
+            if self.track_stream:
+                self._setup_tracking_stream(mt, tid0, cap, rkw)
+            elif self.tracking:
                 self._setup_tracking(mt, tid0, cap, rkw)
             elif self.stream:
                 self._setup_stream(mt, tid0, cap, rkw)
@@ -498,6 +504,51 @@ class Rank:
         self.master_tables = [[ptr_table(self.Mv[v][lo:hi], dev) for v in range(2)]
                               for lo, hi in self.sender.ranges]
 
+    def _setup_tracking_stream(self, mt, tid0, cap, kw):
+        """Config 5 under f1 (Alg. 1): W (this Trainer's shard of the bf16 weights) resident, a change bitmap, and
+        one fp32 master scratch of the largest tensor group: the optimizer step of each group writes the group's
+        masters there and casts them into W with tracking (prepare_update, untimed); the sync (timed) gathers
+        the tracked set (no snapshot exists, so nothing is streamed and there is no commit)."""
+        from paper_2605_07330_b200 import transport
+        from paper_2605_07330_b200.sync import GroupedSender
+        sg, dev, args = self.sg, self.d.dev, self.args
+        self.tid0 = tid0
+        self.W, self.Wv = sg.arena(mt, dev)
+        sg.fill_old(self.Wv, mt, self.seed, tid0=tid0)
+        ranges = transport.shard_ranges(mt.numel, self.G)
+        biggest = max(sum(mt.numel[lo:hi]) for lo, hi in ranges)
+        self.Mst = torch.empty(biggest, dtype=torch.float32, device=dev)   # masters of one group
+        self.Tst = torch.empty(biggest, dtype=torch.int16, device=dev)     # the group's target bf16 values
+        self.Mv, self.Tv = [], []
+        for lo, hi in ranges:
+            off = 0
+            for n in mt.numel[lo:hi]:
+                self.Mv.append(self.Mst[off:off + n])
+                self.Tv.append(self.Tst[off:off + n])
+                off += n
+        self.sender = GroupedSender(None, self.Wv, groups=self.G, max_changed=cap, master=self.Mv, **kw)
+        assert self.sender.ranges == ranges
+        self.X = self.W          # what a Rollout must match
+        self.version = 0         # W holds version 0 (the old values)
+
+    def prepare_update(self):
+        """f1 streaming (config 5): the optimizer step between syncs, per group — the group's next weights
+        (alternately the new and the old version of the synthetic update) as fp32 masters, then Alg. 1's
+        CastAndCopy with tracking into W. Not part of the sync; bench.py times the syncs only."""
+        if not self.track_stream or self.sender is None:
+            return
+        sg, a = self.sg, self.args
+        self.version ^= 1
+        for g, (lo, hi) in enumerate(self.sender.ranges):
+            m = self.mt.slice(lo, hi)
+            tv = self.Tv[lo:hi]
+            sg.fill_old(tv, m, self.seed, tid0=self.tid0 + lo)
+            if self.version:
+                sg.fill_new(tv, tv, m, self.seed, a.rho, MASKS[a.mask], tid0=self.tid0 + lo)
+            n = sum(m.numel)
+            self.Mst[:n].copy_(self.Tst[:n].view(torch.bfloat16))   # exact: round_BF16(master) == the target
+            self.sender.parts[g].cast_track()
+
     def receivers_all(self):
         return [p for g in self.receivers.values() for p in g.parts]
 
@@ -520,10 +571,13 @@ class Rank:
             rec(4 * g)
             if snd is not None:
                 p = snd.parts[g]
-                if self.stream:
+                if self.stream and not self.track_stream:
                     self.stream_generate(g)     # this group's new weights into the scratch (input generation)
                     rec(4 * g + 1)
                     p.ctx.sync_extract_batched(p.old_ptrs, p.new_ptrs, p.I, p.V, p.counts)
+                elif self.track_stream:
+                    rec(4 * g + 1)
+                    p.extract()                 # I = the tracked set, V = W[I] (the cast ran in prepare_update)
                 elif self.tracking:
                     # the optimizer-step epilogue (Alg. 1 l.5-7): the masters of this step are the other version
                     p.master_ptrs = self.master_tables[g][self.kstep % 2]
@@ -829,6 +883,7 @@ def run_ours(args):
     gc.disable()
     # ---- warmup (also sizes every buffer)
     for _ in range(args.warmup):
+        r.prepare_update()
         r.step()
     torch.cuda.synchronize()
     nnz = payload = nb = raw_payload = vbytes = n16 = n32 = n16e = 0
@@ -864,6 +919,9 @@ def run_ours(args):
     for k in range(K):
         if flush is not None:
             flush.fill_(k & 0xFF)
+        if r.track_stream:   # config 5 under f1: the optimizer step that makes the update runs between syncs
+            r.prepare_update()
+            d.barrier()
         r.step(evs[k])
     t_end.record()
     d.barrier()
@@ -872,7 +930,9 @@ def run_ours(args):
     launches = ss.launch_count() - launches0 + (K * r.G if (args.commit == "scatter" or r.loop_snapshot)
                                                 and r.sender is not None and not r.stream else 0)
     launches = int(d.sum(launches))   # + the toggle kernels under --commit scatter
-    ms_local = t_start.elapsed_time(t_end) if flush is None else float(np.sum(step_ms))
+    # syncs separated by untimed work (an L2 flush, or config 5's optimizer step): the sum of the syncs' own
+    # event intervals
+    ms_local = t_start.elapsed_time(t_end) if flush is None and not r.track_stream else float(np.sum(step_ms))
     ms = d.max(ms_local)
     sm_med, sm_best = d.max(float(np.median(step_ms))), d.max(float(min(step_ms)))
     phases = np.mean([r.phase_ms(e) for e in evs], axis=0)
@@ -890,6 +950,7 @@ def run_ours(args):
     #      (start -> this rank's last kernel of the sync: commit on a Trainer, apply on a Rollout)
     lat = []
     for _ in range(args.latency_steps):
+        r.prepare_update()
         d.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -971,7 +1032,16 @@ def run_ours(args):
     if args.dtype == "fp8":
         roof_kernel = ("k_diff8 + tracked compaction (FP8 extract, SS_FP8_BITMAP)" if os.environ.get("SS_FP8_BITMAP")
                        else "k_extract<kB=1> (K1 on 8-bit elements)")
-    if r.tracking:
+    if r.track_stream:
+        # config 5 under f1: the sync's dominant kernels gather the tracked set: read the bitmap (N/8 B), clear the
+        # words that had a bit, read the 32 B sectors holding a change, write I and V (6 B per change)
+        n_el = r.N
+        f_sec = 1 - (1 - args.rho) ** 16
+        f_word = 1 - (1 - args.rho) ** 32
+        roof_kernel = "k_track_count + k_track_write (f1 gather of the tracked set, Alg. 2 l.4-5)"
+        roof_bytes = int(n_el / 8 + 4 * f_word * n_el / 32 + 32 * f_sec * n_el / 16 + 6 * nnz)
+        achieved = roof_bytes / (max(ext_ms_local, 1e-9) / 1e3) / 1e9
+    elif r.tracking:
         # f1: the dominant kernel is the cast with tracking. Algorithmic bytes per launch: read the fp32 master
         # and the bf16 weights (6 B / element), write the 32 B sectors that changed and the bitmap words that
         # gained a bit (read + write)
@@ -1061,7 +1131,7 @@ def run_ours(args):
                           "inputs smaller than L2: 512 MB write between steps, excluded via per-step events")},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
                          zip(["extract", "compress_pack", "transfer_apply", "commit", "synthetic_update",
-                              "stream_generate" if r.stream else "cast_track"], phases)},
+                              "stream_generate" if r.stream and not r.track_stream else "cast_track"], phases)},
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic if not (r.tracking or args.dtype == "fp8") else None,
@@ -1082,7 +1152,13 @@ def run_ours(args):
     }
     if track_cmp is not None:
         out["tracking_vs_plain_cast"] = track_cmp
-    if r.stream:
+    if r.track_stream:
+        out["stream"] = {"groups": r.G, "mode": "f1 tracking (Alg. 1): W + change bitmap on the Trainer, no snapshot",
+                         "what": "each update's optimizer step (per group: fp32 masters cast into W with tracking) "
+                                 "runs between the timed syncs; ms_per_step and latency_per_update are the syncs "
+                                 "alone (gather of the tracked set, compress, send, Rollout apply), measured "
+                                 "directly with CUDA events (max over ranks)"}
+    elif r.stream:
         gen = float(phases[5])
         out["stream"] = {"groups": r.G, "generate_ms_per_step": round(gen, 4),
                          "ms_per_step_excl_generation": round(ms / K - gen, 4),

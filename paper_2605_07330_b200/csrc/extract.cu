@@ -657,8 +657,9 @@ static void launch_k(const ExtractArgs& a, cudaStream_t s) {
   }
 }
 
-// 3 stages (two CTAs per SM) and 3 writer warps by default (3 writers: +5% at 10% density, equal at 1%);
-// SS_XWRITERS=2|4 and (with 2 writers) SS_XSTAGES=2|4 select other instantiations for experiments.
+// 3 stages (two CTAs per SM) and 4 writer warps by default (round 2, with ticketed tiles, same-box A/B: 4 writers
+// beat 3 by 0.4% at 1% density and 1.6% at 10%; round 1's static schedule had preferred 3); SS_XWRITERS=2|3 and
+// (with 2 writers) SS_XSTAGES=2|4 select other instantiations for experiments.
 template <bool kSingle>
 static void launch(const ExtractArgs& a, cudaStream_t s) {
   static int stages = 0, writers = 0;
@@ -666,16 +667,16 @@ static void launch(const ExtractArgs& a, cudaStream_t s) {
     const char* e = getenv("SS_XSTAGES");
     stages = e ? atoi(e) : 3;
     const char* w = getenv("SS_XWRITERS");
-    writers = w ? atoi(w) : 3;
+    writers = w ? atoi(w) : 4;
   }
   if (writers == 2) {
     if (stages == 2) launch_k<kSingle, 2, 2>(a, s);
     else if (stages == 4) launch_k<kSingle, 4, 2>(a, s);
     else launch_k<kSingle, 3, 2>(a, s);
-  } else if (writers == 4) {
-    launch_k<kSingle, 3, 4>(a, s);
-  } else {
+  } else if (writers == 3) {
     launch_k<kSingle, 3, 3>(a, s);
+  } else {
+    launch_k<kSingle, 3, 4>(a, s);
   }
 }
 
@@ -700,7 +701,7 @@ void launch_extract_batched(const u16* const* d_old, const u16* const* d_new, co
   a.ticket = ticket;
   a.stage_ring = stage_ring;
   a.status = status;
-  if (elem_bytes == 1) launch_k<false, 3, 3, 1>(a, s);   // FP8: the same pipeline on 8-bit elements
+  if (elem_bytes == 1) launch_k<false, 3, 4, 1>(a, s);   // FP8: the same pipeline on 8-bit elements
   else launch<false>(a, s);
 }
 

@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -122,6 +123,69 @@ __global__ void k_scatter_evict(u16* W, const u32* I, u64 count) {  // stores wi
   }
 }
 
+// read-only stream (the roofline of a read-dominated kernel such as K1): 16-byte loads, 4 in flight per thread,
+// XOR-reduced so the loads are not dead
+__global__ void k_read_stream(const uint4* p, u64 n16, u32* sink) {
+  u32 acc = 0;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const uint4 a = __ldcs(p + i), b = __ldcs(p + i + stride), c = __ldcs(p + i + 2 * stride),
+                d = __ldcs(p + i + 3 * stride);
+    acc ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w ^ d.x ^ d.y ^ d.z ^ d.w;
+  }
+  for (; i < n16; i += stride) {
+    const uint4 a = __ldcs(p + i);
+    acc ^= a.x ^ a.y ^ a.z ^ a.w;
+  }
+  if (acc == 0x12345678u) *sink = acc;
+}
+
+// full 32 B sector RMW: the thread of a sector's first change loads the sector (two 16-byte loads), merges
+// every change of that sector and stores the whole sector, so the L2 never sees a partial-sector write
+template <int kU>
+__global__ void k_scatter_sector(u16* W, const u32* I, u64 count) {
+  const u64 per = 16384;
+  for (u64 c0 = (u64)blockIdx.x * per; c0 < count; c0 += (u64)gridDim.x * per) {
+    const u64 end = c0 + per < count ? c0 + per : count;
+    for (u64 k0 = c0 + threadIdx.x; k0 < end; k0 += blockDim.x * kU) {
+      u32 idx[kU], prv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const u64 k = k0 + u * blockDim.x;
+        idx[u] = k < end ? I[k] : 0xFFFFFFFFu;
+        prv[u] = (k < end && k > 0) ? I[k - 1] : 0xFFFFFFFFu;
+      }
+      uint4 a[kU], b[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const bool first = idx[u] != 0xFFFFFFFFu && (prv[u] == 0xFFFFFFFFu || (prv[u] >> 4) != (idx[u] >> 4));
+        if (first) {
+          const uint4* sp = reinterpret_cast<const uint4*>(W + ((u64)(idx[u] >> 4) << 4));
+          a[u] = sp[0];
+          b[u] = sp[1];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const bool first = idx[u] != 0xFFFFFFFFu && (prv[u] == 0xFFFFFFFFu || (prv[u] >> 4) != (idx[u] >> 4));
+        if (!first) continue;
+        u16 v[16];
+        memcpy(v, &a[u], 16);
+        memcpy(v + 8, &b[u], 16);
+        const u32 sec = idx[u] >> 4;
+        for (u64 j = k0 + u * blockDim.x; j < count && (I[j] >> 4) == sec; ++j) v[I[j] & 15] = (u16)I[j];
+        uint4* dp = reinterpret_cast<uint4*>(W + ((u64)sec << 4));
+        uint4 x, y;
+        memcpy(&x, v, 16);
+        memcpy(&y, v + 8, 16);
+        dp[0] = x;
+        dp[1] = y;
+      }
+    }
+  }
+}
+
 // full 128 B line RMW per touched line (warp-cooperative: lane = 4-byte word of the line)
 __global__ void k_scatter_line(u16* W, const u32* I, u64 count) {
   const u64 warps = (u64)gridDim.x * (blockDim.x / 32);
@@ -220,8 +284,25 @@ int main(int argc, char** argv) {
   run("contig-warp8 g=8x", [&] { k_scatter_contig<8><<<nsm * 8, 256>>>(W, I, count); });
   run("contig-warp8 g=32x", [&] { k_scatter_contig<8><<<nsm * 32, 256>>>(W, I, count); });
   run("evict_first g=8x", [&] { k_scatter_evict<8><<<nsm * 8, 256>>>(W, I, count); });
+  run("sector-rmw8 g=8x", [&] { k_scatter_sector<8><<<nsm * 8, 256>>>(W, I, count); });
+  run("sector-rmw4 g=16x", [&] { k_scatter_sector<4><<<nsm * 16, 256>>>(W, I, count); });
   run("line-rmw g=8x", [&] { k_scatter_line<<<nsm * 8, 256>>>(W, I, count); });
   run("line-rmw g=32x", [&] { k_scatter_line<<<nsm * 32, 256>>>(W, I, count); });
+  {  // read-only stream over W (2n bytes)
+    u32* sink;
+    cudaMalloc(&sink, 4);
+    for (int g : {nsm * 4, nsm * 8}) {
+      k_read_stream<<<g, 512>>>(reinterpret_cast<const uint4*>(W), n * 2 / 16, sink);
+      cudaEventRecord(e0);
+      for (int r = 0; r < 5; ++r) k_read_stream<<<g, 512>>>(reinterpret_cast<const uint4*>(W), n * 2 / 16, sink);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= 5;
+      printf("%-28s %8.3f ms  %7.1f GB/s (read only, grid %d)\n", "read stream", ms, 2.0 * n / ms / 1e6, g);
+    }
+  }
   // reference: dense copy of W (read + write)
   u16* W2;
   if (cudaMalloc(&W2, n * 2) == cudaSuccess) {
