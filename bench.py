@@ -988,7 +988,7 @@ def run_ours(args):
     # ---- f1: the plain CastAndCopy the tracking replaces (torch's fp32 -> bf16 copy kernel, a library kernel
     #      timed only for comparison) over up to 2^29 elements of the masters, scaled to this rank's elements
     track_cmp = None
-    if r.tracking and r.sender is not None:
+    if r.tracking and r.sender is not None and not r.track_stream:
         n_el = r.N
         k = min(n_el, 1 << 29)
         src = r.M[0][:k]

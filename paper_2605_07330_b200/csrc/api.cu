@@ -266,7 +266,7 @@ int sync_ctx_create(sync_ctx** out, const sync_manifest* m, const sync_config* c
   p.gscan = reinterpret_cast<u64*>(w + L.gscan);
   p.gscan_T = (d.T + 1023) / 1024 + 1;
   p.gscan_C = (u32)((d.max_chunks + 1023) / 1024);
-  p.epoch = 0;
+  p.epochs = x->misc + 28;                          // misc words 28..30 (zeroed at creation)
   p.rec_list = reinterpret_cast<u32*>(w + L.rec_list);
   p.srec = reinterpret_cast<u64*>(w + L.srec);
   p.crec = reinterpret_cast<u64*>(w + L.crec);
@@ -428,7 +428,6 @@ int sync_compress(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const u
   if (!aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
   x->plan.enc_cap = enc_cap;
-  x->plan.epoch++;   // the grid scans' publication flag (scan.cuh)
   launch_plan_scan(x->plan, d_counts, s);
   // CTA-per-chunk kernels of 128 threads: 2x the grid of the 256-thread kernels (~9 resident per SM)
   if (x->cfg.codec == SYNC_CODEC_COMPRESSED) launch_chunk_stats(x->plan, d_I, d_V, d_counts, clamp_ctas(2 * x->grid), s);
@@ -549,7 +548,6 @@ int sync_compress_pack_async(sync_ctx* x, const uint32_t* d_I, const uint16_t* d
   // plan (record sizes) exactly as sync_compress, without the encode
   x->plan.enc_cap = ~0ull;
   x->plan.rec_dst = x->plan.enc_off;
-  x->plan.epoch++;   // the grid scans' publication flag (scan.cuh)
   launch_plan_scan(x->plan, d_counts, s);
   if (x->cfg.codec == SYNC_CODEC_COMPRESSED)
     launch_chunk_stats(x->plan, d_I, d_V, d_counts, clamp_ctas(2 * x->grid), s);
@@ -675,8 +673,7 @@ int sync_commit_snapshot_batched(sync_ctx* x, uint16_t* const* d_snapshot_ptrs, 
   if (x->d.T == 0) return SYNC_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (!(x->plan_valid && x->plan_counts == d_counts)) {
-    x->plan.epoch++;   // the grid scans' publication flag (scan.cuh)
-  launch_plan_scan(x->plan, d_counts, s);
+    launch_plan_scan(x->plan, d_counts, s);
     x->plan_valid = false;
   }
   launch_commit_batched(x->plan, d_snapshot_ptrs, d_I, d_V, clamp_ctas(x->grid), s);

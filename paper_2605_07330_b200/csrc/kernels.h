@@ -52,7 +52,7 @@ struct Plan {
   uint64_t* gscan;               // GScanState [gscan_T + gscan_C + gscan_T]: plan_scan, plan_chunks, plan_records
   uint32_t gscan_T;              // CTAs of the per-tensor scans = ceil(T / 1024)
   uint32_t gscan_C;              // CTAs of the per-chunk scan = ceil(max_chunks / 1024)
-  uint64_t epoch;                // this plan's number (>= 1): the scans' publication flag
+  uint32_t* epochs;              // [3] device epoch counters of the three grid scans (scan.cuh)
 };
 
 enum TotalsIdx {

@@ -10,7 +10,7 @@
 //  * k_plan_chunks (grid)    chunk hi-offset / escape prefixes
 //  * k_plan_records (grid)   record sizes and modes, record byte offsets, the compacted
 //                            record table for the bucket planner, statistics
-// The scans are grid-wide (scan.cuh: one item per thread, CTA totals published with the plan's epoch):
+// The scans are grid-wide (scan.cuh: one item per thread, CTA totals published with the scan's epoch):
 // single-CTA versions took 40 + 117 us of latency per sync on the 30B manifest.
 #include <cstdio>
 #include <cstdlib>
@@ -32,13 +32,16 @@ __global__ void __launch_bounds__(kGScan) k_plan_scan(Plan p, const u64* counts)
   __shared__ u32 s_j;
   const u32 T = p.n_tensors;
   const u32 G = T ? (T + kGScan - 1) / kGScan : 1;
+  __shared__ u64 s_e;
   const u32 j = gscan_rank(p.tickets + 0, G, &s_j);
+  const u64 epoch = gscan_epoch(p.epochs + 0, &s_e);
   const u32 t = j * kGScan + threadIdx.x;
   const u64 c = t < T ? counts[t] : 0;
   const u64 v[3] = {c, (c + kChunk - 1) / kChunk, c ? 1ull : 0ull};
   u64 ex[3], tot[3], pre[3];
   block_scan3(v, ex, tot, s_w);
-  gscan_publish_and_prefix(G_STATE(p, 0), j, p.epoch, tot, pre, s_w);
+  gscan_publish_and_prefix(G_STATE(p, 0), j, epoch, tot, pre, s_w);
+  if (j + 1 == G) gscan_advance(p.epochs + 0, epoch);
   if (t < T) {
     p.rec_off[t] = pre[0] + ex[0];
     p.chunk_off[t] = pre[1] + ex[1];
@@ -268,7 +271,9 @@ __global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, co
 __global__ void __launch_bounds__(kGScan) k_plan_chunks(Plan p, u32 G) {
   __shared__ u64 s_w[3 * 33];
   __shared__ u32 s_j;
+  __shared__ u64 s_e;
   const u32 j = gscan_rank(p.tickets + 1, G, &s_j);
+  const u64 epoch = gscan_epoch(p.epochs + 1, &s_e);
   const u64 n_chunks = p.totals[kTotChunks];
   const u64 g = (u64)j * kGScan + threadIdx.x;
   const bool in = g < n_chunks;
@@ -276,7 +281,8 @@ __global__ void __launch_bounds__(kGScan) k_plan_chunks(Plan p, u32 G) {
                     in ? p.chunk_mode[g] : 0};
   u64 ex[3], tot[3], pre[3];
   block_scan3(v, ex, tot, s_w);
-  gscan_publish_and_prefix(G_STATE(p, G_OFF_CHUNKS(p)), j, p.epoch, tot, pre, s_w);
+  gscan_publish_and_prefix(G_STATE(p, G_OFF_CHUNKS(p)), j, epoch, tot, pre, s_w);
+  if (j + 1 == G) gscan_advance(p.epochs + 1, epoch);
   if (in) {
     p.chunk_hioff[g] = pre[0] + ex[0];
     p.chunk_escoff[g] = pre[1] + ex[1];
@@ -300,7 +306,9 @@ __global__ void __launch_bounds__(kGScan) k_plan_records(Plan p, const u64* coun
   const bool comp = p.codec == SYNC_CODEC_COMPRESSED;
   const bool e8 = p.dtype == SYNC_DTYPE_FP8;
   const bool over = p.totals[kTotOverflow] != 0;
+  __shared__ u64 s_e;
   const u32 j = gscan_rank(p.tickets + 2, G, &s_j);
+  const u64 epoch = gscan_epoch(p.epochs + 2, &s_e);
   if (threadIdx.x < 6) s_st[threadIdx.x] = 0;
   const u32 t = j * kGScan + threadIdx.x;
   const u64 c = (t < T && !over) ? counts[t] : 0;
@@ -354,7 +362,8 @@ __global__ void __launch_bounds__(kGScan) k_plan_records(Plan p, const u64* coun
   const u64 v[3] = {by, by ? 1ull : 0ull, wch};
   u64 ex[3], tot[3], pre[3];
   block_scan3(v, ex, tot, s_w);
-  gscan_publish_and_prefix(G_STATE(p, G_OFF_RECORDS(p)), j, p.epoch, tot, pre, s_w);
+  gscan_publish_and_prefix(G_STATE(p, G_OFF_RECORDS(p)), j, epoch, tot, pre, s_w);
+  if (j + 1 == G) gscan_advance(p.epochs + 2, epoch);
   const u64 off = pre[0] + ex[0];
   if (t < T) p.enc_off[t] = off;
   if (by) {

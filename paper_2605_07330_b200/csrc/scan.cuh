@@ -6,8 +6,10 @@
 // the totals of CTAs 0..j-1 (every one read directly — aggregates only, no chain of inclusive prefixes, so
 // the wait is one round of loads once they have published). Tickets count up forever: a kernel with a fixed
 // grid G uses ticket mod G, and every launch consumes exactly G tickets. The state words are never reset:
-// a CTA publishes (values, epoch) and a reader accepts only the current epoch (epochs start at 1 on a zeroed
-// workspace and increase by one per plan).
+// a CTA publishes (values, epoch) and a reader accepts only the current epoch. The epoch lives in device
+// memory (one counter per scan): every CTA reads it at its start, and the last CTA advances it once it has
+// seen every other CTA's totals (so all of them have read the old value) — no host bookkeeping, so a plan
+// captured in a CUDA graph stays correct on every replay.
 #pragma once
 #include "common.cuh"
 
@@ -43,6 +45,17 @@ __device__ __forceinline__ void block_scan3(const u64 (&v)[3], u64 (&ex)[3], u64
     tot[k] = s_w[k * 33 + 32];
   }
   __syncthreads();
+}
+
+// This launch's epoch (block-uniform): the counter's value + 1 (a zeroed workspace starts at epoch 1).
+__device__ __forceinline__ u64 gscan_epoch(const u32* ctr, u64* s_e) {
+  if (threadIdx.x == 0) *s_e = (u64)*(volatile const u32*)ctr + 1;
+  __syncthreads();
+  return *s_e;
+}
+// The last CTA, after gscan_publish_and_prefix: advance the counter to this launch's epoch.
+__device__ __forceinline__ void gscan_advance(u32* ctr, u64 epoch) {
+  if (threadIdx.x == 0) *(volatile u32*)ctr = (u32)epoch;
 }
 
 // This CTA's rank in ticket order (block-uniform).

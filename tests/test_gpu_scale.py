@@ -270,3 +270,43 @@ def test_extract_finishes_while_half_the_sms_are_held():
 def ctypes_stream(s):
     import ctypes
     return ctypes.c_void_p(s.cuda_stream)
+
+
+# ----------------------------------------------------------------------------- enqueue-only sender
+def test_sender_captured_in_a_cuda_graph_matches_oracle():
+    """sync_extract_batched + sync_compress_pack_async are enqueue-only (the bucket plan runs on the device and
+    lands in mapped host memory): the whole sender is captured once in a CUDA graph and replayed; after each
+    replay sync_pack_result returns the plan and the buckets equal the oracle's bytes."""
+    m = synth.Manifest("cg", [synth.Tensor("a", (700, 512)), synth.Tensor("n", (64,), synth.KIND_NORM),
+                              synth.Tensor("b", (300_001 // 8 * 8,)), synth.Tensor("c", (24,))])
+    olds, news = synth.generate(m, seed=17, rho=0.02)
+    L = 64 << 10
+    ref = oracle.sync_pack(olds, news, limit=L, crc=True)
+    old_d = [to_dev(o) for o in olds]
+    new_d = [to_dev(n) for n in news]
+    cap = sum(o.size for o in olds)
+    ctx = ss.SyncContext(m.numel, bucket_limit=L, max_changed=cap, crc=True, device=DEV)
+    op, np_ = ss.ptr_table(old_d, DEV), ss.ptr_table(new_d, DEV)
+    I = torch.empty(cap, dtype=torch.int32, device=DEV)
+    V = torch.empty(cap, dtype=torch.int16, device=DEV)
+    counts = torch.zeros(len(olds), dtype=torch.int64, device=DEV)
+    buckets = torch.zeros(4 * cap + (1 << 20), dtype=torch.uint8, device=DEV)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):        # warm-up outside the capture (first-use attributes, constant uploads)
+        ctx.sync_extract_batched(op, np_, I, V, counts, stream=s)
+        ctx.sync_compress_pack_async(I, V, counts, buckets, stream=s)
+    s.synchronize()
+    first = ctx.sync_pack_result()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ctx.sync_extract_batched(op, np_, I, V, counts, stream=s)
+        ctx.sync_compress_pack_async(I, V, counts, buckets, stream=s)
+    for _ in range(3):
+        buckets.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        bl = ctx.sync_pack_result()
+        assert bl == first
+        got = [buckets[o:o + z].cpu().numpy().tobytes() for o, z in bl]
+        assert got == [ref.bucket(b) for b in range(ref.n_buckets)]
+    ctx.check()
