@@ -1092,6 +1092,13 @@ def run_ours(args):
             traffic_src = f"ncu --set full dram__bytes_read+write / algorithmic = {ratio:.4f} (30b-slice launch)"
         except Exception:
             traffic = None
+    read_ceiling = None   # tools/scatter_bench read-only stream (profiles/r2/read_ceiling.json)
+    rc_f = os.path.join(ROOT, "profiles", "r2", "read_ceiling.json")
+    if os.path.exists(rc_f):
+        try:
+            read_ceiling = float(json.load(open(rc_f))["read_stream_gbs"])
+        except Exception:
+            read_ceiling = None
     topo_txt = {
         "ring": "ring: rank r = Trainer of its model + Rollout replica of rank r-1 (N=1: loopback)",
         "pair": "pair: ranks < N/2 Trainers of a whole model, rank t+N/2 = Rollout of Trainer t",
@@ -1137,7 +1144,11 @@ def run_ours(args):
                      "traffic": traffic if not (r.tracking or args.dtype == "fp8") else None,
                      "bytes_per_launch": roof_bytes,
                      "traffic_source": traffic_src if not (r.tracking or args.dtype == "fp8") else None,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                     "read_ceiling_gbs": read_ceiling,
+                     "frac_of_read_ceiling": round(achieved / read_ceiling, 4) if read_ceiling else None,
+                     "read_ceiling_source": "profiles/r2/read_ceiling.json: a read-only 16-byte-load stream on B200 "
+                                            "(K1 is 99.7% reads at rho = 1%)" if read_ceiling else None},
         "payload": {"nnz": int(nnz_t), "rho_measured": round(nnz_t / max(d.sum(r.N), 1), 6), "buckets": int(nb_t),
                     "bytes": int(payload_t), "x_comp": round(total_S / max(payload_t, 1), 2),
                     "x_raw_eq1": round(total_S / max(raw_t, 1), 2),
