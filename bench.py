@@ -88,6 +88,9 @@ def parse():
                         "step generates the new weights one tensor group of <= this many GB at a time into a "
                         "scratch buffer, which that group's extract reads (the generator runs inside the timed "
                         "step and is reported as its own phase, stream_generate)")
+    p.add_argument("--overlap-apply", action="store_true",
+                   help="N=1: decode + apply each group on a second stream while the next group is extracted "
+                        "(use with --groups > 1)")
     p.add_argument("--no-overlap-commit", action="store_true",
                    help="--stream-gb: commit the snapshot after the group loop instead of per group on a side stream")
     p.add_argument("--seed", type=int, default=0)
@@ -322,6 +325,7 @@ class Rank:
             raise SystemExit("--model-shards K needs --topology sharded and K >= N/2")
         self.stream = args.stream_gb > 0
         self.overlap_commit = False
+        self.apply_stream = torch.cuda.Stream(device=d.dev) if (args.overlap_apply and W == 1) else None
         # config 5 with the paper's own hook (f1): the Trainer holds only its weights W and the change bitmap; the
         # optimizer step that produces each update (the fp32 masters of each group, cast into W with tracking)
         # runs before every timed sync, outside it
@@ -592,7 +596,15 @@ class Rank:
                     L.fence(g)            # the previous sync's sends of group g have left its bucket buffer
                 blist = p.compress_pack()  # fused K2-K4 (blocking: host bucket plan)
                 rec(4 * g + 3)
-                if L is None:             # N = 1: the ring closes on itself
+                if L is None and self.apply_stream is not None:
+                    # N = 1, --overlap-apply: group g's decode + apply runs on its own stream while group g+1 is
+                    # extracted (the scatter is bound by DRAM access efficiency, the extract by bandwidth)
+                    ev_a = torch.cuda.Event()
+                    ev_a.record()
+                    self.apply_stream.wait_event(ev_a)
+                    with torch.cuda.stream(self.apply_stream):
+                        self.receivers[0].parts[g].apply_many([p.bucket(b) for b in range(len(blist))])
+                elif L is None:           # N = 1: the ring closes on itself
                     self.receivers[0].parts[g].apply_many([p.bucket(b) for b in range(len(blist))])
                 elif ring:
                     # under --commit swap group g's I array is dead until the next extract of group g:
@@ -622,6 +634,8 @@ class Rank:
                 else:
                     src = next(iter(self.receivers))
                     L.receive(self.receivers[src].parts[g].apply, tag=g)
+        if self.apply_stream is not None:
+            torch.cuda.current_stream().wait_stream(self.apply_stream)
         rec(4 * G)
         if self.loop_snapshot or self.tracking:
             pass                        # committed by the decode+apply (loopback) / nothing to commit (f1)

@@ -631,7 +631,10 @@ static void launch_k(const ExtractArgs& a, cudaStream_t s) {
     int cap = n_sm * (per > 0 ? per : 1);
     grid_cap[dev] = cap > (int)kMaxExtractCtas ? (int)kMaxExtractCtas : cap;
   }
-  const u64 cap = (u64)clamp_ctas(grid_cap[dev]);
+  static int env_cap = -1;   // SS_XCTAS: a K1-only grid cap (dev experiments: leave SMs to concurrent kernels)
+  if (env_cap < 0) env_cap = getenv("SS_XCTAS") ? atoi(getenv("SS_XCTAS")) : 0;
+  u64 cap = (u64)clamp_ctas(grid_cap[dev]);
+  if (env_cap > 0 && (u64)env_cap < cap) cap = (u64)env_cap;
   u64 grid = a.n_tiles < cap ? a.n_tiles : cap;
   static unsigned long long* prof = nullptr;
   static int want_prof = -1;
