@@ -88,10 +88,24 @@ __global__ void __launch_bounds__(kCThreads, 6) k_encode(Plan p, const u32* I, c
     if (!comp) {
       u32* Io = reinterpret_cast<u32*>(rec + 16) + p0;
       u8* Vb = rec + 16 + 4 * nnz;
-      for (u32 q = tid; q < nk; q += kCThreads) {
-        Io[q] = Ir[p0 + q];
-        if (e8) Vb[p0 + q] = (u8)Vc[q];
-        else reinterpret_cast<u16*>(Vb)[p0 + q] = Vc[q];
+      constexpr int kR = 8;   // coalesced, 8 values per thread in flight (one at a time was latency-bound)
+      for (u32 q0 = 0; q0 < nk; q0 += kCThreads * kR) {
+        u32 iv[kR], vv[kR];
+#pragma unroll
+        for (int u = 0; u < kR; ++u) {
+          const u32 q = q0 + u * kCThreads + tid;
+          iv[u] = q < nk ? Ir[p0 + q] : 0u;
+          vv[u] = q < nk ? (u32)Vc[q] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kR; ++u) {
+          const u32 q = q0 + u * kCThreads + tid;
+          if (q < nk) {
+            Io[q] = iv[u];
+            if (e8) Vb[p0 + q] = (u8)vv[u];
+            else reinterpret_cast<u16*>(Vb)[p0 + q] = (u16)vv[u];
+          }
+        }
       }
       const u64 used = 16 + (e8 ? 5 : 6) * nnz;
       if (last) zero_bytes(rec + used, rb - used);

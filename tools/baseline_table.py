@@ -1,9 +1,15 @@
-"""Regenerate BASELINE.md §4's table from the committed sweep JSONs (dev tool)."""
+"""Regenerate BASELINE.md §4's table from the committed sweep JSONs (dev tool).
+usage: python tools/baseline_table.py [sweep dir under profiles/, default r2_sweep]"""
 import json
 import os
+import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-P = 6554.6
+SWEEP = sys.argv[1] if len(sys.argv) > 1 else "r2_sweep"
+try:
+    P = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+except Exception:
+    P = 6537.6
 ROWS = [
     ("1M bf16, 99% U (config 1)", "one_1m_r01", "tiny"),
     ("Qwen3-4B 99% U, 1 GPU loopback", "one_4b_r01", ""),
@@ -23,6 +29,10 @@ ROWS = [
     ("30B 99.9% U, 2T→2R fanout", "fanout4_r001_U_b256", ""),
     ("30B 99% U, 2T→2R sharded", "sharded4_r01", ""),
     ("235B 99% U, 2 of the 4 shard pairs of 4T→4R, Trainer streaming (config 5)", "sharded4_235b_stream", "stream"),
+    ("235B 99% U, 2 of the 4 shard pairs of 4T→4R, f1 tracking, optimizer outside the sync (config 5)",
+     "sharded4_235b_f1", "f1"),
+    ("30B 99% U, 2T→2R fanout, NCCL sends", "fanout4_r01_U_b256_nccl", ""),
+    ("30B 99% U, 2T→2R fanout, NCCL broadcast", "fanout4_r01_U_b256_bcast", ""),
     ("30B 99% R, 2T→2R, 16 MB buckets (config 4)", "fanout4_r01_R_b16", "clustered"),
     ("30B 99% R, 2T→2R, 1 GB buckets (config 4)", "fanout4_r01_R_b1024", "clustered"),
     ("30B 99% E, 2T→2R, 256 MB (config 4)", "fanout4_r01_E_b256", "clustered"),
@@ -40,10 +50,11 @@ def main():
            "(sector model) | Per-update latency (ms) | X_raw / X_comp / α | Bit-exact | JSON |",
            "|---|---|---|---|---|---|---|---|---|"]
     for name, key, kind in ROWS:
-        f = os.path.join(ROOT, "profiles", "r1_sweep", key + ".json")
+        f = os.path.join(ROOT, "profiles", SWEEP, key + ".json")
         if not os.path.exists(f):
             continue
-        d = json.load(open(f))
+        txt = open(f).read()
+        d = json.loads(txt[txt.index("{"):])
         ph, p, c = d["ms_per_phase"], d["payload"], d["config"]
         topo = c["topology_mode"]
         ntr = d["n_gpus"] if topo == "ring" else max(1, d["n_gpus"] // 2)
@@ -71,14 +82,14 @@ def main():
             da = "%.0f%%" % ((pc + 64 * fsec * n_el / per) / ta / 1e9 / P * 100)
         lat = (d.get("latency_per_update") or {}).get("median_ms")
         lat_s = f"{lat:.2f}"
-        if kind == "stream":   # the input generator runs inside the step: report the sync alone
+        if kind == "stream" and "latency_excl_generation_ms" in d.get("stream", {}):   # sync alone
             s = d["stream"]
             lat_s = (f"{s['latency_excl_generation_ms']:.2f} (sync; + {s['generate_ms_per_step']:.0f} ms of input "
                      f"generation per step)")
             xc = "%.0f%%" % ((2 * s_tr + pc) / ((ph["extract"] + ph["compress_pack"]) / 1e3) / 1e9 / P * 100)
         out.append(f"| {name} | {d['n_gpus']} | {d['value']:.0f} | {xc} | {da} | {lat_s} | "
                    f"{p['x_raw_eq1']} / {p['x_comp']} / {p['alpha']} | {d['bit_exact_replica']} | "
-                   f"`profiles/r1_sweep/{key}.json` |")
+                   f"`profiles/{SWEEP}/{key}.json` |")
     tab = "\n".join(out) + "\n"
     path = os.path.join(ROOT, "BASELINE.md")
     b = open(path).read()

@@ -33,6 +33,10 @@ SETS = {
         ("fanout8_r01_E_b64", 8, ["--topology", "fanout", "--mask", "E", "--bucket-mb", "64"]),
         ("fanout8_r01_E_b256", 8, ["--topology", "fanout", "--mask", "E"]),
         ("fanout8_r01_E_b1024", 8, ["--topology", "fanout", "--mask", "E", "--bucket-mb", "1024"]),
+        ("sharded8_235b_f1", 8, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--stream-gb", "5",
+                                 "--tracking", "cast", "--steps", "5"]),
+        ("sharded8_235b_stream", 8, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--stream-gb", "5",
+                                     "--commit", "scatter", "--steps", "5"]),
     ],
     # configs 3 / 4 at N=4 (gpurun offers 1, 2 or 4 GPUs of a box: 2T->2R stands in for 4T->4R)
     "n4": [
@@ -59,6 +63,12 @@ SETS = {
         # config 5 on half the box: 2 of the 4 shard pairs of Qwen3-235B, Trainer new weights streamed
         ("sharded4_235b_stream", 4, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--model-shards",
                                      "4", "--stream-gb", "5", "--commit", "scatter", "--steps", "5"]),
+        # config 5 with the paper's own hook (f1): W + bitmap, the optimizer step outside the timed sync
+        ("sharded4_235b_f1", 4, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--model-shards", "4",
+                                 "--stream-gb", "5", "--tracking", "cast", "--steps", "5"]),
+        # fan-out data planes: peer memory (default), NCCL per-destination sends, NCCL broadcast
+        ("fanout4_r01_U_b256_nccl", 4, ["--topology", "fanout", "--transport", "nccl"]),
+        ("fanout4_r01_U_b256_bcast", 4, ["--topology", "fanout", "--transport", "nccl-bcast"]),
     ],
     "n2": [
         ("ring2_r01", 2, ["--topology", "ring"]),
@@ -68,6 +78,8 @@ SETS = {
         ("pair2_r01", 2, ["--topology", "pair"]),
         ("pair2_r10", 2, ["--topology", "pair", "--rho", "0.1"]),
         ("pair2_r001", 2, ["--topology", "pair", "--rho", "0.001"]),
+        ("sharded2_235b_f1", 2, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--model-shards", "4",
+                                 "--stream-gb", "5", "--tracking", "cast", "--steps", "5"]),
     ],
     "n1": [
         ("one_r01", 1, []),
