@@ -949,6 +949,7 @@ def run_ours(args):
     ms_local = t_start.elapsed_time(t_end) if flush is None and not r.track_stream else float(np.sum(step_ms))
     ms = d.max(ms_local)
     sm_med, sm_best = d.max(float(np.median(step_ms))), d.max(float(min(step_ms)))
+    step_all = [round(d.max(float(x)), 3) for x in step_ms]   # per step, max over ranks
     phases = np.mean([r.phase_ms(e) for e in evs], axis=0)
     ext_ms_local = phases[0]
     cast_ms_local = phases[5]
@@ -1130,7 +1131,7 @@ def run_ours(args):
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": d.world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
-        "ms_per_step_stats": {"median": round(sm_med, 4), "best": round(sm_best, 4),
+        "ms_per_step_stats": {"median": round(sm_med, 4), "best": round(sm_best, 4), "all": step_all,
                               "what": "per-step CUDA events, max over ranks"},
         "higher_is_better": True,
         "scaling": "strong" if strong else "weak",
