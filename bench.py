@@ -88,6 +88,9 @@ def parse():
                         "step generates the new weights one tensor group of <= this many GB at a time into a "
                         "scratch buffer, which that group's extract reads (the generator runs inside the timed "
                         "step and is reported as its own phase, stream_generate)")
+    p.add_argument("--graph", action="store_true",
+                   help="N=1: capture each sync (extract, compress+pack, decode+apply from the device bucket table) "
+                        "as a CUDA graph and replay it (no host in the loop; the phase split is not measured)")
     p.add_argument("--overlap-apply", action="store_true",
                    help="N=1: decode + apply each group on a second stream while the next group is extracted "
                         "(use with --groups > 1)")
@@ -325,6 +328,10 @@ class Rank:
             raise SystemExit("--model-shards K needs --topology sharded and K >= N/2")
         self.stream = args.stream_gb > 0
         self.overlap_commit = False
+        self.graphs = None
+        if args.graph and (W != 1 or topo != "ring" or args.commit != "swap" or args.tracking != "snapshot"
+                           or args.crc or (args.groups not in (0, 1)) or args.replica != "separate"):
+            raise SystemExit("--graph: N = 1 loopback, one group, --commit swap, snapshot tracking, no CRC")
         self.apply_stream = torch.cuda.Stream(device=d.dev) if (args.overlap_apply and W == 1) else None
         # config 5 with the paper's own hook (f1): the Trainer holds only its weights W and the change bitmap; the
         # optimizer step that produces each update (the fp32 masters of each group, cast into W with tracking)
@@ -553,6 +560,28 @@ class Rank:
             self.Mst[:n].copy_(self.Tst[:n].view(torch.bfloat16))   # exact: round_BF16(master) == the target
             self.sender.parts[g].cast_track()
 
+    def capture_graphs(self):
+        """--graph (N = 1 loopback, one group, --commit swap): capture the sync in both directions."""
+        snd, rcv = self.sender, self.receivers[0]
+        p, rp = snd.parts[0], rcv.parts[0]
+        A, B = p.old_ptrs, p.new_ptrs
+        table = p.ctx.sync_pack_table()
+        rp_ptrs = rp.weight_ptrs
+        self._graph_keep = (rp_ptrs, table)
+        s = torch.cuda.Stream(device=self.d.dev)
+        s.wait_stream(torch.cuda.current_stream())
+        graphs = []
+        dense = self.args.rho >= 0.03
+        for old, new in ((A, B), (B, A)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                p.ctx.sync_extract_batched(old, new, p.I, p.V, p.counts, stream=s)
+                p.ctx.sync_compress_pack_async(p.I, p.V, p.counts, p.buckets, stream=s)
+                rp.ctx.sync_decompress_apply_table(p.buckets, table, 64, rp_ptrs, dense=dense, stream=s)
+            graphs.append(g)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graphs, self.graph_tables = graphs, (A, B)
+
     def receivers_all(self):
         return [p for g in self.receivers.values() for p in g.parts]
 
@@ -571,6 +600,19 @@ class Rank:
         peer = isinstance(L, T.PeerLink)
         ring_swap = ring and a.commit == "swap" and not self.tracking
         self.kstep += 1
+        if self.graphs is not None:
+            # --graph: the whole sync (extract, compress + pack, decode + apply from the device bucket table) is
+            # one CUDA graph per direction of the double-buffered commit; the commit is the pointer swap
+            p = snd.parts[0]
+            for i in range(4 * G):
+                rec(i)
+            self.graphs[0 if p.old_ptrs is self.graph_tables[0] else 1].replay()
+            rec(4 * G)
+            snd.commit(mode="swap")
+            self.X, self.Y, self.Xv, self.Yv = self.Y, self.X, self.Yv, self.Xv
+            rec(4 * G + 1)
+            rec(4 * G + 2)
+            return
         for g in range(G):
             rec(4 * g)
             if snd is not None:
@@ -900,6 +942,11 @@ def run_ours(args):
         r.prepare_update()
         r.step()
     torch.cuda.synchronize()
+    if args.graph:
+        r.capture_graphs()
+        for _ in range(2):   # one replay per direction before the timed region
+            r.step()
+        torch.cuda.synchronize()
     nnz = payload = nb = raw_payload = vbytes = n16 = n32 = n16e = 0
     if r.sender is not None:   # rank 0 is always a Trainer
         st = [p.ctx.sync_status() for p in r.sender.parts]
@@ -1042,7 +1089,8 @@ def run_ours(args):
     nnz_t, payload_t, raw_t = d.sum(nnz), d.sum(payload), d.sum(raw_payload)
     vbytes_t, n16_t, n32_t, nb_t = d.sum(vbytes), d.sum(n16), d.sum(n32), d.sum(nb)
     n16e_t = d.sum(n16e)
-    achieved = local_alg_extract / (ext_ms_local / 1e3) / 1e9   # rank 0 (a Trainer), its own launch
+    # rank 0 (a Trainer), its own launch (under --graph the phases are inside one graph: no per-kernel time)
+    achieved = local_alg_extract / (ext_ms_local / 1e3) / 1e9 if ext_ms_local > 0 else 0.0
     roof_kernel, roof_bytes = "k_extract (K1)", local_alg_extract
     if args.dtype == "fp8":
         roof_kernel = ("k_diff8 + tracked compaction (FP8 extract, SS_FP8_BITMAP)" if os.environ.get("SS_FP8_BITMAP")
@@ -1145,7 +1193,7 @@ def run_ours(args):
                    "tensors": len(manifest.tensors),
                    "codec": args.codec, "bucket_mb": args.bucket_mb, "crc": args.crc, "commit": args.commit,
                    "groups": r.G, "replica": args.replica, "tracking": args.tracking, "route": args.route,
-                   "element_dtype": args.dtype, "escape": args.escape,
+                   "element_dtype": args.dtype, "escape": args.escape, "cuda_graph": bool(args.graph),
                    "model_shards": (args.model_shards or d.world // 2) if args.topology == "sharded" else None,
                    "stream_gb": args.stream_gb or None,
                    "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,

@@ -28,6 +28,13 @@ struct DecodeBatch {            // passed by value (kernel parameter)
   const u8* bk[kDecodeBatch];
   u64 bytes[kDecodeBatch];
   u32 n;
+  // table mode (t_hdr != null): the buckets b0 .. b0 + 31 of a device bucket table (a sender's plan: t_hdr[0]
+  // buckets at t_base + t_off[b], t_size[b] bytes) instead of the host-filled arrays above
+  const u64* t_hdr;
+  const u64* t_off;
+  const u64* t_size;
+  const u8* t_base;
+  u32 t_b0;
 };
 
 __device__ __forceinline__ int read_bucket_header(const u8* bk, u64 avail, BucketHdr* h) {
@@ -174,13 +181,33 @@ __global__ void __launch_bounds__(256, kMinB) k_decode(DecodeBatch bb, u32 n_ten
   __shared__ DecodeModel s_dm[8];
   __shared__ BucketHdr s_h[kDecodeBatch];
   __shared__ u64 s_pre[kDecodeBatch + 1];
+  __shared__ const u8* s_bk[kDecodeBatch];
+  __shared__ u32 s_n;
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   DecodeModel& dm = s_dm[warp];
   const bool e8 = dtype == SYNC_DTYPE_FP8;   // FP8: one value plane (the byte), no lo plane, byte stores
-  if (threadIdx.x < bb.n) {   // headers; a bucket with a bad header or failed CRC contributes no chunks
+  u64 my_bytes = 0;
+  if (bb.t_hdr) {             // table mode: this launch's slice of the device bucket table
+    const u64 nt = *(volatile const u64*)bb.t_hdr;
+    const u32 n = nt > bb.t_b0 ? (u32)(nt - bb.t_b0 < kDecodeBatch ? nt - bb.t_b0 : kDecodeBatch) : 0u;
+    if (threadIdx.x == 0) s_n = n;
+    if (threadIdx.x < n) {
+      s_bk[threadIdx.x] = bb.t_base + bb.t_off[bb.t_b0 + threadIdx.x];
+      my_bytes = bb.t_size[bb.t_b0 + threadIdx.x];
+    }
+  } else {
+    if (threadIdx.x == 0) s_n = bb.n;
+    if (threadIdx.x < bb.n) {
+      s_bk[threadIdx.x] = bb.bk[threadIdx.x];
+      my_bytes = bb.bytes[threadIdx.x];
+    }
+  }
+  __syncthreads();
+  const u32 nb = s_n;
+  if (threadIdx.x < nb) {   // headers; a bucket with a bad header or failed CRC contributes no chunks
     const u32 i = threadIdx.x;
     BucketHdr h;
-    int herr = read_bucket_header(bb.bk[i], bb.bytes[i], &h);
+    int herr = read_bucket_header(s_bk[i], my_bytes, &h);
     if (herr != SYNC_OK) {
       if (blockIdx.x == 0) latch(status, herr);
       h.n_chunks = 0;
@@ -192,19 +219,19 @@ __global__ void __launch_bounds__(256, kMinB) k_decode(DecodeBatch bb, u32 n_ten
   __syncthreads();
   if (threadIdx.x == 0) {
     u64 acc = 0;
-    for (u32 i = 0; i < bb.n; ++i) {
+    for (u32 i = 0; i < nb; ++i) {
       s_pre[i] = acc;
       acc += s_h[i].n_chunks;
     }
-    s_pre[bb.n] = acc;
+    s_pre[nb] = acc;
   }
   __syncthreads();
-  const u64 total = s_pre[bb.n];
+  const u64 total = s_pre[nb];
   const u64 nwarps = (u64)gridDim.x * (blockDim.x >> 5);
   for (u64 gg = (u64)blockIdx.x * (blockDim.x >> 5) + warp; gg < total; gg += nwarps) {
     // bucket of global chunk gg: the last i with s_pre[i] <= gg (kDecodeBatch <= 32: one ballot)
-    const u32 bi = 31 - __clz(__ballot_sync(0xffffffffu, lane < bb.n && s_pre[lane] <= gg));
-    const u8* bk = bb.bk[bi];
+    const u32 bi = 31 - __clz(__ballot_sync(0xffffffffu, lane < nb && s_pre[lane] <= gg));
+    const u8* bk = s_bk[bi];
     const BucketHdr h = s_h[bi];
     const u64 g = gg - s_pre[bi];
     const u32* dir = reinterpret_cast<const u32*>(bk + 32);
@@ -529,7 +556,7 @@ void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u3
                    u16* const* weights, const sync_record_view* views, u32* I_out, u16* V_out, u64 out_cap,
                    u32* status, const u32* crc_bad, u32 dtype, int grid, bool dense, cudaStream_t s) {
   for (u32 b0 = 0; b0 < n_buckets; b0 += kDecodeBatch) {
-    DecodeBatch bb;
+    DecodeBatch bb{};
     bb.n = n_buckets - b0 < kDecodeBatch ? n_buckets - b0 : kDecodeBatch;
     for (u32 i = 0; i < bb.n; ++i) {
       bb.bk[i] = buckets[b0 + i];
@@ -542,6 +569,24 @@ void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u3
       run_decode<3, 4>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad, dtype, grid, s);
     else
       run_decode<1, 8>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad, dtype, grid, s);
+    count_launch();
+  }
+}
+
+void launch_decode_table(const u64* t_hdr, const u64* t_off, const u64* t_size, const u8* base, u32 max_buckets,
+                         u32 n_tensors, const u64* numel, u16* const* weights, u32* status, u32 dtype, int grid,
+                         bool dense, cudaStream_t s) {
+  for (u32 b0 = 0; b0 < max_buckets; b0 += kDecodeBatch) {   // a launch past the table's count decodes nothing
+    DecodeBatch bb{};
+    bb.t_hdr = t_hdr;
+    bb.t_off = t_off;
+    bb.t_size = t_size;
+    bb.t_base = base;
+    bb.t_b0 = b0;
+    if (dense)
+      run_decode<3, 4>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status, nullptr, dtype, grid, s);
+    else
+      run_decode<1, 8>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status, nullptr, dtype, grid, s);
     count_launch();
   }
 }

@@ -310,3 +310,93 @@ def test_sender_captured_in_a_cuda_graph_matches_oracle():
         got = [buckets[o:o + z].cpu().numpy().tobytes() for o, z in bl]
         assert got == [ref.bucket(b) for b in range(ref.n_buckets)]
     ctx.check()
+
+
+def test_bucket_plan_long_chain_and_global_walk():
+    """The device bucket plan with more records than its shared-memory staging holds (> 51,200: the chain of
+    bucket starts is walked from global memory) and tiny buckets (one bucket per few records: ~20K buckets,
+    the per-bucket scans past one round of 1024): bucket bytes == the oracle's; too small a bucket table
+    returns SYNC_ERR_CAPACITY and writes nothing."""
+    T = 53_000
+    m = synth.Manifest("chain", [synth.Tensor(f"t{k}", (16,)) for k in range(T)])
+    olds, news = synth.generate(m, seed=29, rho=0.3)
+    for k in range(0, T, 7):
+        news[k] = olds[k] ^ np.uint16(1)          # every tensor has a change (few enough for 16 elements)
+    for k in range(T):
+        if (olds[k] == news[k]).all():
+            news[k] = olds[k].copy()
+            news[k][3] ^= np.uint16(2)
+    L = 1024
+    ref = oracle.sync_pack(olds, news, limit=L)
+    assert ref.stats["n_records"] == T and ref.n_buckets > 8192
+    old_d = [to_dev(o) for o in olds]
+    new_d = [to_dev(n) for n in news]
+    snd = ss.SparseSyncSender(old_d, new_d, bucket_limit=L, max_changed=16 * T)
+    bl = snd.sync()
+    assert len(bl) == ref.n_buckets
+    for b in (0, 1, len(bl) // 2, len(bl) - 1):
+        assert snd.bucket(b).cpu().numpy().tobytes() == ref.bucket(b)
+    got = b"".join(snd.bucket(b).cpu().numpy().tobytes() for b in range(len(bl)))
+    assert got == b"".join(ref.bucket(b) for b in range(ref.n_buckets))
+    # a bucket table smaller than the plan: SYNC_ERR_CAPACITY, nothing encoded
+    import ctypes
+    ctx = snd.ctx
+    n = ctypes.c_uint32()
+    need = ctypes.c_uint64()
+    code = ss.lib().sync_compress_pack(ctx._h, ss._ptr(snd.I), ss._ptr(snd.V), ss._dev_ptr(snd.counts),
+                                       ss._dev_ptr(snd.buckets), snd.buckets.numel(), ctypes.byref(n), ctx._h_off,
+                                       ctx._h_size, 100, ctypes.byref(need), ss._stream(None))
+    assert code == ss.SYNC_ERR_CAPACITY and n.value == 0
+    assert ss.lib().sync_status(ctx._h, ss._stream(None)) == ss.SYNC_ERR_CAPACITY
+
+
+def test_whole_loopback_sync_in_cuda_graphs():
+    """Sender and receiver with no host in the loop: extract + sync_compress_pack_async + the decode over the
+    sender's device bucket table (sync_decompress_apply_table), captured as two CUDA graphs (v0 -> v1 and
+    v1 -> v0, the double-buffered commit) and replayed alternately: after every replay the replica equals the
+    version just synced, and the v0 -> v1 buckets equal the oracle's."""
+    m = synth.Manifest("g2", [synth.Tensor("a", (700, 512)), synth.Tensor("n", (64,), synth.KIND_NORM),
+                              synth.Tensor("b", (300_000,)), synth.Tensor("c", (24,))])
+    olds, news = synth.generate(m, seed=41, rho=0.02)
+    L = 64 << 10
+    ref = oracle.sync_pack(olds, news, limit=L)
+    X = [to_dev(o) for o in olds]
+    Y = [to_dev(n) for n in news]
+    R = [to_dev(o) for o in olds]
+    cap = sum(o.size for o in olds)
+    tx = ss.SyncContext(m.numel, bucket_limit=L, max_changed=cap, device=DEV)
+    rx = ss.SyncContext(m.numel, bucket_limit=L, max_changed=cap, device=DEV)
+    A, B = ss.ptr_table(X, DEV), ss.ptr_table(Y, DEV)
+    Rp = ss.ptr_table(R, DEV)
+    I = torch.empty(cap, dtype=torch.int32, device=DEV)
+    V = torch.empty(cap, dtype=torch.int16, device=DEV)
+    counts = torch.zeros(len(olds), dtype=torch.int64, device=DEV)
+    buckets = torch.zeros(4 * cap + (1 << 20), dtype=torch.uint8, device=DEV)
+    table = tx.sync_pack_table()
+    s = torch.cuda.Stream()
+
+    def sync(old, new):
+        tx.sync_extract_batched(old, new, I, V, counts, stream=s)
+        tx.sync_compress_pack_async(I, V, counts, buckets, stream=s)
+        rx.sync_decompress_apply_table(buckets, table, 64, Rp, stream=s)
+
+    with torch.cuda.stream(s):    # warm-up (first-use attributes) with the identity update
+        sync(A, A)
+    s.synchronize()
+    graphs = []
+    for old, new in ((A, B), (B, A)):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            sync(old, new)
+        graphs.append(g)
+    for k in range(4):
+        graphs[k % 2].replay()
+        torch.cuda.synchronize()
+        want = news if k % 2 == 0 else olds
+        assert all((host(r) == w).all() for r, w in zip(R, want)), f"replica after replay {k}"
+        if k == 0:
+            bl = tx.sync_pack_result()
+            assert [buckets[o:o + z].cpu().numpy().tobytes() for o, z in bl] == \
+                [ref.bucket(b) for b in range(ref.n_buckets)]
+    tx.check()
+    rx.check()
