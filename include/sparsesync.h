@@ -206,21 +206,22 @@ int sync_compress_pack(sync_ctx* ctx, const uint32_t* d_I, const uint16_t* d_V, 
                        uint64_t* h_sizes, uint32_t max_buckets, uint64_t* h_need, sync_stream_t stream);
 
 /* ---- device-side bucket table (no host in the loop) ------------------------
- * sync_pack_table: device pointers to the context's bucket table, which every
- * bucket plan rewrites (stream-ordered): *d_hdr[0] = bucket count (0 after a
- * capacity failure), d_off[b] / d_size[b] = bucket b's offset in the bucket
- * buffer and its bytes. Valid for the life of the context (page-locked host
- * memory mapped into the device address space).
+ * sync_pack_table: device pointers to the context's bucket table (device memory
+ * in its workspace), which every bucket plan rewrites (stream-ordered):
+ * d_hdr[0] = bucket count (0 after a capacity failure), d_off[b * stride] /
+ * d_size[b * stride] = bucket b's offset in the bucket buffer and its bytes.
+ * Valid for the life of the context.
  * sync_decompress_apply_table: K5 over the buckets such a table lists (same
  * GPU or a peer that can read it): d_base = the bucket buffer; it launches
  * ceil(max_buckets / 32) decode kernels, each taking its slice of the table,
  * so the whole sender + receiver can be captured in one CUDA graph. flags bit
  * 0 = the dense launch variant (payload >= ~0.1 B per weight). Not with
  * SYNC_FLAG_CRC (SYNC_ERR_ARG): the CRC pass needs host sizes. Asynchronous. */
-int sync_pack_table(sync_ctx* ctx, const uint64_t** d_hdr, const uint64_t** d_off, const uint64_t** d_size);
+int sync_pack_table(sync_ctx* ctx, const uint64_t** d_hdr, const uint64_t** d_off, const uint64_t** d_size,
+                    uint32_t* stride);
 int sync_decompress_apply_table(sync_ctx* ctx, const uint8_t* d_base, const uint64_t* d_hdr, const uint64_t* d_off,
-                                const uint64_t* d_size, uint32_t max_buckets, uint16_t* const* d_weight_ptrs,
-                                uint32_t flags, sync_stream_t stream);
+                                const uint64_t* d_size, uint32_t stride, uint32_t max_buckets,
+                                uint16_t* const* d_weight_ptrs, uint32_t flags, sync_stream_t stream);
 
 /* ---- a7 unpack / decompress (Alg. 3 l.5; "exact inverse") ---
  * sync_bucket_unpack validates one bucket in device memory (magic, version,

@@ -112,8 +112,8 @@ def lib() -> ctypes.CDLL:
             "sync_compress_pack": [P, P, P, P, P, u64, P, P, P, u32, P, P],
             "sync_compress_pack_async": [P, P, P, P, P, u64, u32, P],
             "sync_pack_result": [P, P, P, P, u32, P],
-            "sync_pack_table": [P, P, P, P],
-            "sync_decompress_apply_table": [P, P, P, P, P, u32, P, u32, P],
+            "sync_pack_table": [P, P, P, P, P],
+            "sync_decompress_apply_table": [P, P, P, P, P, u32, u32, P, u32, P],
             "sync_bucket_unpack": [P, P, u64, P, u32, P, P],
             "sync_decompress": [P, P, u64, P, P, u64, P],
             "sync_decompress_apply": [P, P, u64, P, P],
@@ -359,15 +359,17 @@ class SyncContext:
     def sync_pack_table(self):
         """Device pointers (hdr, offsets, sizes) of this context's bucket table (see include/sparsesync.h)."""
         h, o, z = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
-        _ck(lib().sync_pack_table(self._h, ctypes.byref(h), ctypes.byref(o), ctypes.byref(z)), "sync_pack_table")
-        return h.value, o.value, z.value
+        st = ctypes.c_uint32()
+        _ck(lib().sync_pack_table(self._h, ctypes.byref(h), ctypes.byref(o), ctypes.byref(z), ctypes.byref(st)),
+            "sync_pack_table")
+        return h.value, o.value, z.value, st.value
 
     def sync_decompress_apply_table(self, buckets: torch.Tensor, table, max_buckets: int, weight_ptrs: torch.Tensor,
                                     dense: bool = False, stream=None):
         """K5 over a sender's device bucket table (graph-capturable; no host knowledge of the bucket count)."""
-        h, o, z = table
+        h, o, z, st = table
         _ck(lib().sync_decompress_apply_table(self._h, _dev_ptr(buckets), ctypes.c_void_p(h), ctypes.c_void_p(o),
-                                              ctypes.c_void_p(z), int(max_buckets), _dev_ptr(weight_ptrs),
+                                              ctypes.c_void_p(z), int(st), int(max_buckets), _dev_ptr(weight_ptrs),
                                               1 if dense else 0, _stream(stream)), "sync_decompress_apply_table")
 
     def sync_commit_snapshot_batched(self, snap_ptrs: torch.Tensor, I: torch.Tensor, V: torch.Tensor,

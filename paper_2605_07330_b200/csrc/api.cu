@@ -651,21 +651,26 @@ int sync_decompress_apply_batched(sync_ctx* x, const uint8_t* const* h_buckets, 
   return SYNC_OK;
 }
 
-int sync_pack_table(sync_ctx* x, const uint64_t** d_hdr, const uint64_t** d_off, const uint64_t** d_size) {
-  if (!x || !d_hdr || !d_off || !d_size) return SYNC_ERR_ARG;
-  *d_hdr = x->d_pack;
-  *d_off = x->d_pack + 4;
-  *d_size = x->d_pack + 4 + (x->d.T + 1);
+int sync_pack_table(sync_ctx* x, const uint64_t** d_hdr, const uint64_t** d_off, const uint64_t** d_size,
+                    uint32_t* stride) {
+  if (!x || !d_hdr || !d_off || !d_size || !stride) return SYNC_ERR_ARG;
+  // the plan's device-resident copy (workspace): the count in the totals, the bucket descriptors' base / bytes
+  // (the mapped host table would cost every decode CTA a round trip to host memory)
+  const BucketDesc* bks = reinterpret_cast<const BucketDesc*>(x->ws + x->L.bks);
+  *d_hdr = x->plan.totals + kTotBuckets;
+  *d_off = &bks[0].base;
+  *d_size = &bks[0].bytes;
+  *stride = sizeof(BucketDesc) / 8;
   return SYNC_OK;
 }
 
 int sync_decompress_apply_table(sync_ctx* x, const uint8_t* d_base, const uint64_t* d_hdr, const uint64_t* d_off,
-                                const uint64_t* d_size, uint32_t max_buckets, uint16_t* const* d_weight_ptrs,
-                                uint32_t flags, sync_stream_t stream) {
-  if (!x || !d_base || !d_hdr || !d_off || !d_size || !d_weight_ptrs) return SYNC_ERR_ARG;
+                                const uint64_t* d_size, uint32_t stride, uint32_t max_buckets,
+                                uint16_t* const* d_weight_ptrs, uint32_t flags, sync_stream_t stream) {
+  if (!x || !d_base || !d_hdr || !d_off || !d_size || !d_weight_ptrs || !stride) return SYNC_ERR_ARG;
   if (x->cfg.flags & SYNC_FLAG_CRC) return SYNC_ERR_ARG;   // table mode has no host sizes for the CRC pass
   if (!aligned16(d_base)) return SYNC_ERR_ALIGNMENT;
-  launch_decode_table(d_hdr, d_off, d_size, d_base, max_buckets, x->d.T, x->plan.numel, d_weight_ptrs,
+  launch_decode_table(d_hdr, d_off, d_size, stride, d_base, max_buckets, x->d.T, x->plan.numel, d_weight_ptrs,
                       x->plan.status, x->plan.dtype, clamp_ctas(x->grid), (flags & 1u) != 0,
                       (cudaStream_t)stream);
   CK(cudaGetLastError());

@@ -35,6 +35,7 @@ struct DecodeBatch {            // passed by value (kernel parameter)
   const u64* t_size;
   const u8* t_base;
   u32 t_b0;
+  u32 t_stride;                  // u64 words between consecutive entries of t_off / t_size
 };
 
 __device__ __forceinline__ int read_bucket_header(const u8* bk, u64 avail, BucketHdr* h) {
@@ -192,8 +193,8 @@ __global__ void __launch_bounds__(256, kMinB) k_decode(DecodeBatch bb, u32 n_ten
     const u32 n = nt > bb.t_b0 ? (u32)(nt - bb.t_b0 < kDecodeBatch ? nt - bb.t_b0 : kDecodeBatch) : 0u;
     if (threadIdx.x == 0) s_n = n;
     if (threadIdx.x < n) {
-      s_bk[threadIdx.x] = bb.t_base + bb.t_off[bb.t_b0 + threadIdx.x];
-      my_bytes = bb.t_size[bb.t_b0 + threadIdx.x];
+      s_bk[threadIdx.x] = bb.t_base + bb.t_off[(u64)(bb.t_b0 + threadIdx.x) * bb.t_stride];
+      my_bytes = bb.t_size[(u64)(bb.t_b0 + threadIdx.x) * bb.t_stride];
     }
   } else {
     if (threadIdx.x == 0) s_n = bb.n;
@@ -573,9 +574,9 @@ void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u3
   }
 }
 
-void launch_decode_table(const u64* t_hdr, const u64* t_off, const u64* t_size, const u8* base, u32 max_buckets,
-                         u32 n_tensors, const u64* numel, u16* const* weights, u32* status, u32 dtype, int grid,
-                         bool dense, cudaStream_t s) {
+void launch_decode_table(const u64* t_hdr, const u64* t_off, const u64* t_size, u32 stride, const u8* base,
+                         u32 max_buckets, u32 n_tensors, const u64* numel, u16* const* weights, u32* status,
+                         u32 dtype, int grid, bool dense, cudaStream_t s) {
   for (u32 b0 = 0; b0 < max_buckets; b0 += kDecodeBatch) {   // a launch past the table's count decodes nothing
     DecodeBatch bb{};
     bb.t_hdr = t_hdr;
@@ -583,6 +584,7 @@ void launch_decode_table(const u64* t_hdr, const u64* t_off, const u64* t_size, 
     bb.t_size = t_size;
     bb.t_base = base;
     bb.t_b0 = b0;
+    bb.t_stride = stride;
     if (dense)
       run_decode<3, 4>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status, nullptr, dtype, grid, s);
     else

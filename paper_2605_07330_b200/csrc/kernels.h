@@ -143,10 +143,11 @@ void launch_decode(const uint8_t* const* buckets, const uint64_t* bytes, uint32_
                    const uint64_t* numel, uint16_t* const* weights, const sync_record_view* views, uint32_t* I_out,
                    uint16_t* V_out, uint64_t out_cap, uint32_t* status, const uint32_t* crc_bad, uint32_t dtype,
                    int grid, bool dense, cudaStream_t s);
-// the same, from a device bucket table (a sender context's plan table: t_hdr[0] buckets, offsets / sizes);
+// the same, from a device bucket table (a sender context's plan: t_hdr[0] buckets, offsets / sizes every
+// `stride` u64 words);
 // ceil(max_buckets / 32) launches, each decoding its slice of the table (no host knowledge of the count)
-void launch_decode_table(const uint64_t* t_hdr, const uint64_t* t_off, const uint64_t* t_size, const uint8_t* base,
-                         uint32_t max_buckets, uint32_t n_tensors, const uint64_t* numel, uint16_t* const* weights,
+void launch_decode_table(const uint64_t* t_hdr, const uint64_t* t_off, const uint64_t* t_size, uint32_t stride,
+                         const uint8_t* base, uint32_t max_buckets, uint32_t n_tensors, const uint64_t* numel, uint16_t* const* weights,
                          uint32_t* status, uint32_t dtype, int grid, bool dense, cudaStream_t s);
 // a decode call is "dense" when its buckets carry >= 0.1 byte per model element (rho >~ 3%)
 inline bool decode_is_dense(const uint64_t* bytes, uint32_t n, uint64_t model_elems) {

@@ -314,8 +314,8 @@ def test_sender_captured_in_a_cuda_graph_matches_oracle():
 
 def test_bucket_plan_long_chain_and_global_walk():
     """The device bucket plan with more records than its shared-memory staging holds (> 51,200: the chain of
-    bucket starts is walked from global memory) and tiny buckets (one bucket per few records: ~20K buckets,
-    the per-bucket scans past one round of 1024): bucket bytes == the oracle's; too small a bucket table
+    bucket starts is walked from global memory) and tiny buckets (~3,900 buckets of ~14 records: the
+    per-bucket scans past their first rounds of 1024): bucket bytes == the oracle's; too small a bucket table
     returns SYNC_ERR_CAPACITY and writes nothing."""
     T = 53_000
     m = synth.Manifest("chain", [synth.Tensor(f"t{k}", (16,)) for k in range(T)])
@@ -328,7 +328,7 @@ def test_bucket_plan_long_chain_and_global_walk():
             news[k][3] ^= np.uint16(2)
     L = 1024
     ref = oracle.sync_pack(olds, news, limit=L)
-    assert ref.stats["n_records"] == T and ref.n_buckets > 8192
+    assert ref.stats["n_records"] == T and ref.n_buckets > 2048   # > 51,200 records; several bucket-scan rounds
     old_d = [to_dev(o) for o in olds]
     new_d = [to_dev(n) for n in news]
     snd = ss.SparseSyncSender(old_d, new_d, bucket_limit=L, max_changed=16 * T)
