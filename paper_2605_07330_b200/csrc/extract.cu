@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
     // (through shared memory).
     const u32 w = warp - (kXConsumers / 32 + 2);
     const u64 keep = policy_evict_last();
-    long long p_w = 0, p_lb = 0, p_wr = 0, n_t = 0;
+    long long p_w = 0, p_lb = 0, p_wr = 0, n_t = 0, p_win = 0, p_span = 0;
     for (u32 k = w;; k += kWriters) {
       const u32 b = k % kSlots;
       long long c0 = clock64();
@@ -366,6 +366,9 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       if (m.tile == ~0ull) break;
       const bool first = m.prev == ~0ull;
       const u64 win = window_sum(a.tile_state, first ? 0ull : m.prev + 1, m.tile);
+      const long long c1b = clock64();
+      p_win += c1b - c1;
+      p_span += first ? 0 : (long long)(m.tile - m.prev - 1);
       // wait for the inclusive prefix of this CTA's previous tile (k - 1)
       while (*(volatile u32*)s_done != k) __nanosleep(32);
       const u64 prefix = (first ? 0ull : *(volatile u64*)s_incl) + win;
@@ -459,6 +462,8 @@ __global__ void __launch_bounds__(xblock(kWriters), 2) k_extract(ExtractArgs a) 
       atomicAdd(&a.prof[4], (unsigned long long)p_lb);
       atomicAdd(&a.prof[5], (unsigned long long)p_wr);
       atomicAdd(&a.prof[8], (unsigned long long)n_t);
+      atomicAdd(&a.prof[10], (unsigned long long)p_win);
+      atomicAdd(&a.prof[11], (unsigned long long)p_span);
     }
     return;
   }
@@ -654,9 +659,11 @@ static void launch_k(const ExtractArgs& a, cudaStream_t s) {
     const double G = (double)grid;
     fprintf(stderr,
             "[xprof] grid %llu tiles/cta %.1f subs/cta %.1f | per CTA kcycles: consumer total %.1f wait_full %.1f "
-            "wait_slot %.1f | copier wait_empty %.1f | writer wait %.1f lookback %.1f write %.1f\n",
+            "wait_slot %.1f | copier wait_empty %.1f | writer wait %.1f lookback %.1f (window %.1f, mean window "
+            "%.0f tiles) write %.1f\n",
             (unsigned long long)grid, h[8] / G, h[9] / G, h[6] / G / 1e3, h[0] / G / 1e3, h[1] / G / 1e3,
-            h[2] / G / 1e3, h[3] / G / 1e3, h[4] / G / 1e3, h[5] / G / 1e3);
+            h[2] / G / 1e3, h[3] / G / 1e3, h[4] / G / 1e3, h[10] / G / 1e3, h[8] ? (double)h[11] / h[8] : 0.0,
+            h[5] / G / 1e3);
   }
 }
 

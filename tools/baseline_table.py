@@ -31,6 +31,7 @@ ROWS = [
     ("235B 99% U, 2 of the 4 shard pairs of 4T→4R, Trainer streaming (config 5)", "sharded4_235b_stream", "stream"),
     ("235B 99% U, 2 of the 4 shard pairs of 4T→4R, f1 tracking, optimizer outside the sync (config 5)",
      "sharded4_235b_f1", "f1"),
+    ("235B 99% U, 1 of the 4 shard pairs, f1 tracking (config 5)", "sharded2_235b_f1", "f1"),
     ("30B 99% U, 2T→2R fanout, NCCL sends", "fanout4_r01_U_b256_nccl", ""),
     ("30B 99% U, 2T→2R fanout, NCCL broadcast", "fanout4_r01_U_b256_bcast", ""),
     ("30B 99% R, 2T→2R, 16 MB buckets (config 4)", "fanout4_r01_R_b16", "clustered"),
