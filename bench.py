@@ -88,6 +88,9 @@ def parse():
                         "step generates the new weights one tensor group of <= this many GB at a time into a "
                         "scratch buffer, which that group's extract reads (the generator runs inside the timed "
                         "step and is reported as its own phase, stream_generate)")
+    p.add_argument("--decode-pipeline", action="store_true",
+                   help="N=1: extract all groups, then compress group g while group g-1 is decoded on a second stream "
+                        "(use with --groups > 1)")
     p.add_argument("--graph", action="store_true",
                    help="N=1: capture each sync (extract, compress+pack, decode+apply from the device bucket table) "
                         "as a CUDA graph and replay it (no host in the loop; the phase split is not measured)")
@@ -332,7 +335,12 @@ class Rank:
         if args.graph and (W != 1 or topo != "ring" or args.commit != "swap" or args.tracking != "snapshot"
                            or args.crc or (args.groups not in (0, 1)) or args.replica != "separate"):
             raise SystemExit("--graph: N = 1 loopback, one group, --commit swap, snapshot tracking, no CRC")
-        self.apply_stream = torch.cuda.Stream(device=d.dev) if (args.overlap_apply and W == 1) else None
+        self.decode_pipeline = bool(args.decode_pipeline)
+        if self.decode_pipeline and (W != 1 or topo != "ring" or args.commit != "swap" or args.tracking != "snapshot"
+                                     or args.replica != "separate"):
+            raise SystemExit("--decode-pipeline: N = 1 loopback, --commit swap, snapshot tracking")
+        self.apply_stream = (torch.cuda.Stream(device=d.dev)
+                             if ((args.overlap_apply or args.decode_pipeline) and W == 1) else None)
         # config 5 with the paper's own hook (f1): the Trainer holds only its weights W and the change bitmap; the
         # optimizer step that produces each update (the fp32 masters of each group, cast into W with tracking)
         # runs before every timed sync, outside it
@@ -600,6 +608,31 @@ class Rank:
         peer = isinstance(L, T.PeerLink)
         ring_swap = ring and a.commit == "swap" and not self.tracking
         self.kstep += 1
+        if self.decode_pipeline:
+            # --decode-pipeline (N = 1): extract every group first, then compress group g while group g-1 is decoded
+            # on a second stream (the compress is issue-bound, the decode bound by DRAM access efficiency)
+            for g in range(G):
+                p = snd.parts[g]
+                rec(4 * g)
+                rec(4 * g + 1)
+                p.ctx.sync_extract_batched(p.old_ptrs, p.new_ptrs, p.I, p.V, p.counts)
+                rec(4 * g + 2)
+            for g in range(G):
+                p = snd.parts[g]
+                blist = p.compress_pack()
+                rec(4 * g + 3)
+                ev_a = torch.cuda.Event()
+                ev_a.record()
+                self.apply_stream.wait_event(ev_a)
+                with torch.cuda.stream(self.apply_stream):
+                    self.receivers[0].parts[g].apply_many([p.bucket(b) for b in range(len(blist))])
+            torch.cuda.current_stream().wait_stream(self.apply_stream)
+            rec(4 * G)
+            snd.commit(mode="swap")
+            self.X, self.Y, self.Xv, self.Yv = self.Y, self.X, self.Yv, self.Xv
+            rec(4 * G + 1)
+            rec(4 * G + 2)
+            return
         if self.graphs is not None:
             # --graph: the whole sync (extract, compress + pack, decode + apply from the device bucket table) is
             # one CUDA graph per direction of the double-buffered commit; the commit is the pointer swap
