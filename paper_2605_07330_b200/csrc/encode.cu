@@ -12,16 +12,101 @@
 #include "kernels.h"
 #include "chunk.cuh"
 
+// k_encode is bound by load latency (ncu: long-scoreboard stalls, DRAM at ~55% of peak with 24 warps per SM):
+// the vectorised rounds below with 2 rounds in flight per thread at 8 CTAs (32 warps) per SM beat 4 rounds at
+// 6 CTAs by 5% (rho = 1%) / 4-7% (rho = 10%) and the one-value-per-thread loop alone by 5% / 7% (same-box A/B,
+// round 2; 10 or 12 CTAs spill). Dev overrides for A/B builds: -DSS_ENC_KV, -DSS_ENC_MINB.
+#ifndef SS_ENC_KV
+#define SS_ENC_KV 2
+#endif
+#ifndef SS_ENC_MINB
+#define SS_ENC_MINB 8
+#endif
+
 namespace ss {
 
 __device__ __forceinline__ void zero_bytes(u8* p, u64 n) {
   for (u64 q = threadIdx.x; q < n; q += blockDim.x) p[q] = 0;
 }
 
+// Vectorised index stream + lo plane (compressed codec, DELTA16 / ABS32): lane l of warp w owns the 4 values
+// q = 512 r + 128 w + 4 l .. + 3 of round r — one 16-byte load of I and one 8-byte load of V per 4 values (twice
+// the bytes in flight per register of the one-value-per-thread loop), one 8-byte DELTA16 / 16-byte ABS32 store
+// and one 4-byte lo store. The chunk's first value sits at global position cs, D = cs mod 4 (uniform): lanes load
+// the aligned quads at cs - D + ... and shift by D with the next lane's quad (a shuffle; lane 31 loads the quad
+// after its own). Processes the whole rounds (512 values) of [0, nk); returns how many values it did.
+template <int D>
+__device__ __forceinline__ u32 encode_vec(const u32* I, const u16* V, u64 cs, u32 nk, u64 cap, bool first_rec,
+                                          u32 mode, bool e8, u16* D16, u32* A32, u8* L) {
+  constexpr int kV = SS_ENC_KV;   // rounds in flight per thread
+  const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  u32 nr = nk / 512;
+  while (nr && cs + (u64)nr * 512 + 4 > cap) --nr;   // keep every quad load inside the arrays
+  const u64 ab = cs - D;                              // 4-aligned
+  for (u32 r0 = 0; r0 < nr; r0 += kV) {
+    uint4 qi[kV], ni[kV];
+    uint2 qv[kV], nv[kV];
+    u32 pred[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const u32 qb = (r0 + u) * 512 + 128 * warp;     // the warp's first value of this round
+      qi[u] = make_uint4(0, 0, 0, 0);
+      qv[u] = make_uint2(0, 0);
+      ni[u] = make_uint4(0, 0, 0, 0);
+      nv[u] = make_uint2(0, 0);
+      pred[u] = 0;
+      if (r0 + u < nr) {
+        const u64 a = ab + qb + 4 * lane;
+        qi[u] = *reinterpret_cast<const uint4*>(I + a);
+        qv[u] = *reinterpret_cast<const uint2*>(V + a);
+        if (D && lane == 31) {
+          ni[u] = *reinterpret_cast<const uint4*>(I + a + 4);
+          nv[u] = *reinterpret_cast<const uint2*>(V + a + 4);
+        }
+        if (lane == 0 && (mode == 0) && !(first_rec && qb == 0)) pred[u] = I[cs + qb - 1];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      if (r0 + u >= nr) break;
+      const u32 q = (r0 + u) * 512 + 128 * warp + 4 * lane;
+      u32 wi[8] = {qi[u].x, qi[u].y, qi[u].z, qi[u].w, 0, 0, 0, 0};
+      u32 wv[4] = {qv[u].x, qv[u].y, 0, 0};
+      if (D) {
+        const uint4 n4 = make_uint4(__shfl_down_sync(0xffffffffu, qi[u].x, 1), __shfl_down_sync(0xffffffffu, qi[u].y, 1),
+                                    __shfl_down_sync(0xffffffffu, qi[u].z, 1), __shfl_down_sync(0xffffffffu, qi[u].w, 1));
+        const uint2 n2 = make_uint2(__shfl_down_sync(0xffffffffu, qv[u].x, 1), __shfl_down_sync(0xffffffffu, qv[u].y, 1));
+        const bool l31 = lane == 31;
+        wi[4] = l31 ? ni[u].x : n4.x;
+        wi[5] = l31 ? ni[u].y : n4.y;
+        wi[6] = l31 ? ni[u].z : n4.z;
+        wi[7] = l31 ? ni[u].w : n4.w;
+        wv[2] = l31 ? nv[u].x : n2.x;
+        wv[3] = l31 ? nv[u].y : n2.y;
+      }
+      const u32 i0 = wi[D], i1 = wi[D + 1], i2 = wi[D + 2], i3 = wi[D + 3];
+      // 16-bit values D .. D+3 of the 8-element window wv (element j = half j & 1 of word j >> 1)
+      const u32 e0 = wv[D >> 1] >> (16 * (D & 1)), e1 = wv[(D + 1) >> 1] >> (16 * ((D + 1) & 1));
+      const u32 e2 = wv[(D + 2) >> 1] >> (16 * ((D + 2) & 1)), e3 = wv[(D + 3) >> 1] >> (16 * ((D + 3) & 1));
+      if (mode == 0) {
+        u32 prev = __shfl_up_sync(0xffffffffu, i3, 1);
+        if (lane == 0) prev = pred[u];
+        *reinterpret_cast<uint2*>(D16 + q) = make_uint2(__byte_perm(i0 - prev, i1 - i0, 0x5410),
+                                                        __byte_perm(i2 - i1, i3 - i2, 0x5410));
+      } else {
+        *reinterpret_cast<uint4*>(A32 + q) = make_uint4(i0, i1, i2, i3);
+      }
+      if (!e8)
+        *reinterpret_cast<u32*>(L + q) = (e0 & 0xFFu) | ((e1 & 0xFFu) << 8) | ((e2 & 0xFFu) << 16) | ((e3 & 0xFFu) << 24);
+    }
+  }
+  return nr * 512;
+}
+
 // One CTA per chunk (16384 values; persistent CTAs claim chunks from a counter). All threads write the chunk's slices of the
 // index stream and of the lo plane (packed 32-bit stores) and copy the chunk's
 // rANS block (states, model, words) that k_chunk_stats already produced.
-__global__ void __launch_bounds__(kCThreads, 6) k_encode(Plan p, const u32* I, const u16* V, const u64* counts,
+__global__ void __launch_bounds__(kCThreads, SS_ENC_MINB) k_encode(Plan p, const u32* I, const u16* V, const u64* counts,
                                                      u8* enc) {
   __shared__ u32 s_t;
   __shared__ u64 s_g[2];
@@ -183,14 +268,24 @@ __global__ void __launch_bounds__(kCThreads, 6) k_encode(Plan p, const u32* I, c
       // thread tid owns positions q = q0 + u * kCThreads + tid (u < kU): every load / store instruction of a
       // warp covers 32 consecutive values (coalesced), kU values per thread in flight; Δ from the value of
       // lane l - 1 (a shuffle), lane 0 loads its predecessor (Δ_0 = I_0 at a record's first value)
-      constexpr int kU = 8;   // (same-box A/B: 8 CTAs/SM at 64 registers with 4 or 6 in flight were 9% slower)
+      constexpr int kU = 8;   // the remainder after the vectorised rounds (and unaligned I / V): one value per thread
       const u32 lane = tid & 31;
       const u32* Ic = Ir + p0;
       u16* D16 = reinterpret_cast<u16*>(rec + 16) + p0;
       u32* A32 = reinterpret_cast<u32*>(rec + 16) + p0;
       u8* L = rec + lo_off + p0;
       const u32 first_prev = p0 ? Ic[-1] : 0u;
-      for (u32 q0 = 0; q0 < nk; q0 += kCThreads * kU) {
+      u32 qv = 0;   // values done by the vectorised rounds
+      const u64 cs = (u64)(Ic - I);
+      if (kCThreads == 128 && !(((uintptr_t)I) & 15u) && !(((uintptr_t)V) & 7u) && (u64)(Vc - V) == cs) {
+        switch ((u32)(cs & 3u)) {
+          case 0: qv = encode_vec<0>(I, V, cs, nk, p.cap, p0 == 0, mode, e8, D16, A32, L); break;
+          case 1: qv = encode_vec<1>(I, V, cs, nk, p.cap, p0 == 0, mode, e8, D16, A32, L); break;
+          case 2: qv = encode_vec<2>(I, V, cs, nk, p.cap, p0 == 0, mode, e8, D16, A32, L); break;
+          default: qv = encode_vec<3>(I, V, cs, nk, p.cap, p0 == 0, mode, e8, D16, A32, L); break;
+        }
+      }
+      for (u32 q0 = qv; q0 < nk; q0 += kCThreads * kU) {
         u32 iv[kU], pv[kU], vv[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {

@@ -20,6 +20,12 @@
 #include "chunk.cuh"
 #include "scan.cuh"
 
+// k_chunk_stats CTAs per SM (dev override -DSS_CS_MINB): 4 at 64 registers; same-box A/B round 2: 3 (78
+// registers) +5%, 5 or 6 (spilling) +4% / +30%
+#ifndef SS_CS_MINB
+#define SS_CS_MINB 4
+#endif
+
 namespace ss {
 
 #define G_STATE(p, off) (reinterpret_cast<GScanState*>((p).gscan) + (off))
@@ -76,7 +82,7 @@ __device__ unsigned long long g_cprof[8];  // debug cycle counters (SS_CPROF=1)
 // the previous round.
 constexpr int kWPF = 8;
 template <bool kEsc>   // f4: also count the gaps > 32767 per chunk (escape words)
-__global__ void __launch_bounds__(256, 4) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
+__global__ void __launch_bounds__(256, SS_CS_MINB) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
   __shared__ WarpModel s_m[8];
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpModel& m = s_m[warp];
