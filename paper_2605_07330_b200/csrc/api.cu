@@ -9,10 +9,21 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
 using namespace ss;
+
+namespace {
+// NVTX range around each enqueueing entry point (named after it), so a trace (nsys, or ncu --nvtx
+// --nvtx-include) attributes the kernels to the ABI call that launched them; a no-op without a tool attached
+struct ApiRange {
+  explicit ApiRange(const char* name) { nvtxRangePushA(name); }
+  ~ApiRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace ss {
 static std::atomic<uint64_t> g_launches{0};
@@ -297,6 +308,7 @@ int sync_extract_workspace_size(uint64_t n, size_t* bytes) {
 
 int sync_extract(const uint16_t* d_old, const uint16_t* d_new, uint64_t n, uint32_t* d_I, uint16_t* d_V,
                  uint64_t cap, uint64_t* d_count, void* d_workspace, size_t workspace_bytes, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_extract");
   size_t need;
   if (sync_extract_workspace_size(n, &need)) return SYNC_ERR_ARG;
   if (!d_count || !d_workspace || (n && (!d_old || !d_new))) return SYNC_ERR_ARG;
@@ -331,6 +343,7 @@ static TrackArgs track_args(sync_ctx* x, uint32_t* d_bitmap);
 
 int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const uint16_t* const* d_new_ptrs,
                          uint32_t* d_I, uint16_t* d_V, uint64_t* d_counts, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_extract_batched");
   if (!x || (x->d.T && (!d_old_ptrs || !d_new_ptrs || !d_counts))) return SYNC_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   x->plan_valid = false;
@@ -389,6 +402,7 @@ int sync_bitmap_words(sync_ctx* x, uint64_t* words) {
 
 int sync_cast_track_batched(sync_ctx* x, const float* const* d_master_ptrs, uint16_t* const* d_weight_ptrs,
                             uint32_t* d_bitmap, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_cast_track_batched");
   if (!x || (x->d.T && (!d_master_ptrs || !d_weight_ptrs || !d_bitmap))) return SYNC_ERR_ARG;
   if (x->d.T && !aligned16(d_bitmap)) return SYNC_ERR_ALIGNMENT;
   if (x->plan.dtype != SYNC_DTYPE_BF16) return SYNC_ERR_DTYPE;   // the cast is round_BF16 (Alg. 1 l.5)
@@ -399,6 +413,7 @@ int sync_cast_track_batched(sync_ctx* x, const float* const* d_master_ptrs, uint
 
 int sync_extract_tracked(sync_ctx* x, uint16_t* const* d_weight_ptrs, uint32_t* d_bitmap, uint32_t* d_I,
                          uint16_t* d_V, uint64_t* d_counts, int clear, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_extract_tracked");
   if (!x || (x->d.T && (!d_weight_ptrs || !d_bitmap || !d_counts))) return SYNC_ERR_ARG;
   x->plan_valid = false;
   if (x->d.T == 0) return SYNC_OK;
@@ -423,6 +438,7 @@ int sync_enc_bound(const sync_manifest* m, const sync_config* c, uint64_t* bytes
 
 int sync_compress(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts, uint8_t* d_enc,
                   uint64_t enc_cap, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_compress");
   if (!x || (x->d.T && (!d_counts || !d_enc))) return SYNC_ERR_ARG;
   if (x->plan.route && !x->plan.cur) return SYNC_ERR_ARG;   // SYNC_FLAG_ROUTE needs sync_set_current
   if (!aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
@@ -530,6 +546,7 @@ int sync_pack_result(sync_ctx* x, uint32_t* n_buckets, uint64_t* h_offsets, uint
 int sync_bucket_pack(sync_ctx* x, const uint8_t* d_enc, uint8_t* d_buckets, uint64_t buckets_cap,
                      uint32_t* n_buckets, uint64_t* h_offsets, uint64_t* h_sizes, uint32_t max_buckets,
                      sync_stream_t stream) {
+  ApiRange nvtx_range("sync_bucket_pack");
   if (!x || !n_buckets || !x->plan_valid || !d_enc) return SYNC_ERR_ARG;
   if (!aligned16(d_buckets) || !aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
   *n_buckets = 0;
@@ -541,6 +558,7 @@ int sync_bucket_pack(sync_ctx* x, const uint8_t* d_enc, uint8_t* d_buckets, uint
 
 int sync_compress_pack_async(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,
                              uint8_t* d_buckets, uint64_t buckets_cap, uint32_t max_buckets, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_compress_pack_async");
   if (!x || (x->d.T && !d_counts)) return SYNC_ERR_ARG;
   if (x->plan.route && !x->plan.cur) return SYNC_ERR_ARG;   // SYNC_FLAG_ROUTE needs sync_set_current
   if (!aligned16(d_buckets)) return SYNC_ERR_ALIGNMENT;
@@ -561,6 +579,7 @@ int sync_compress_pack_async(sync_ctx* x, const uint32_t* d_I, const uint16_t* d
 int sync_compress_pack(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const uint64_t* d_counts,
                        uint8_t* d_buckets, uint64_t buckets_cap, uint32_t* n_buckets, uint64_t* h_offsets,
                        uint64_t* h_sizes, uint32_t max_buckets, uint64_t* h_need, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_compress_pack");
   if (!n_buckets) return SYNC_ERR_ARG;
   *n_buckets = 0;
   if (h_need) *h_need = 0;
@@ -589,6 +608,7 @@ static int maybe_crc_check(sync_ctx* x, const uint8_t* const* d_buckets, const u
 
 int sync_bucket_unpack(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, sync_record_view* d_views,
                        uint32_t max_views, uint32_t* d_n_records, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_bucket_unpack");
   if (!x || !d_bucket || !d_views || !d_n_records) return SYNC_ERR_ARG;
   if (!aligned16(d_bucket)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
@@ -603,6 +623,7 @@ int sync_bucket_unpack(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, syn
 
 int sync_decompress(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, uint32_t* d_I, uint16_t* d_V,
                     uint64_t d_cap, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_decompress");
   if (!x || !d_bucket) return SYNC_ERR_ARG;
   if (!aligned16(d_bucket)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
@@ -620,6 +641,7 @@ int sync_decompress(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, uint32
 
 int sync_decompress_apply(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, uint16_t* const* d_weight_ptrs,
                           sync_stream_t stream) {
+  ApiRange nvtx_range("sync_decompress_apply");
   if (!x || !d_bucket || !d_weight_ptrs) return SYNC_ERR_ARG;
   if (!aligned16(d_bucket)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
@@ -634,6 +656,7 @@ int sync_decompress_apply(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, 
 
 int sync_decompress_apply_batched(sync_ctx* x, const uint8_t* const* h_buckets, const uint64_t* h_bytes,
                                   uint32_t n_buckets, uint16_t* const* d_weight_ptrs, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_decompress_apply_batched");
   if (!x || !d_weight_ptrs || (n_buckets && (!h_buckets || !h_bytes))) return SYNC_ERR_ARG;
   for (u32 i = 0; i < n_buckets; ++i)
     if (!h_buckets[i] || !aligned16(h_buckets[i])) return h_buckets[i] ? SYNC_ERR_ALIGNMENT : SYNC_ERR_ARG;
@@ -667,6 +690,7 @@ int sync_pack_table(sync_ctx* x, const uint64_t** d_hdr, const uint64_t** d_off,
 int sync_decompress_apply_table(sync_ctx* x, const uint8_t* d_base, const uint64_t* d_hdr, const uint64_t* d_off,
                                 const uint64_t* d_size, uint32_t stride, uint32_t max_buckets,
                                 uint16_t* const* d_weight_ptrs, uint32_t flags, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_decompress_apply_table");
   if (!x || !d_base || !d_hdr || !d_off || !d_size || !d_weight_ptrs || !stride) return SYNC_ERR_ARG;
   if (x->cfg.flags & SYNC_FLAG_CRC) return SYNC_ERR_ARG;   // table mode has no host sizes for the CRC pass
   if (!aligned16(d_base)) return SYNC_ERR_ALIGNMENT;
@@ -680,6 +704,7 @@ int sync_decompress_apply_table(sync_ctx* x, const uint8_t* d_base, const uint64
 // ------------------------------------------------------------------------ apply / commit
 int sync_apply(uint16_t* d_W, const uint32_t* d_I, const uint16_t* d_V, uint64_t count, uint64_t numel,
                uint32_t* d_status, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_apply");
   if (count && (!d_W || !d_I || !d_V)) return SYNC_ERR_ARG;
   if (numel >= (1ull << 31)) return SYNC_ERR_ARG;
   if (!aligned16(d_W) || !aligned16(d_I) || !aligned16(d_V)) return SYNC_ERR_ALIGNMENT;
@@ -690,11 +715,13 @@ int sync_apply(uint16_t* d_W, const uint32_t* d_I, const uint16_t* d_V, uint64_t
 
 int sync_commit_snapshot(uint16_t* d_snapshot, const uint32_t* d_I, const uint16_t* d_V, uint64_t count,
                          uint64_t numel, uint32_t* d_status, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_commit_snapshot");
   return sync_apply(d_snapshot, d_I, d_V, count, numel, d_status, stream);
 }
 
 int sync_commit_snapshot_batched(sync_ctx* x, uint16_t* const* d_snapshot_ptrs, const uint32_t* d_I,
                                  const uint16_t* d_V, const uint64_t* d_counts, sync_stream_t stream) {
+  ApiRange nvtx_range("sync_commit_snapshot_batched");
   if (!x || (x->d.T && (!d_snapshot_ptrs || !d_counts))) return SYNC_ERR_ARG;
   if (x->d.T == 0) return SYNC_OK;
   cudaStream_t s = (cudaStream_t)stream;
