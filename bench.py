@@ -1178,14 +1178,16 @@ def run_ours(args):
     except Exception as exc:   # reporting only; never fails the run
         phase_hbm = {"error": str(exc)[:200]}
     # ncu dram bytes / algorithmic bytes of the profiled extract launch (profiles/extract_traffic.json,
-    # from `ncu --set full` on the 30b-slice workload), applied to this launch's algorithmic bytes
+    # from `ncu --set full` of the headline workload's K1 launch), applied to this launch's algorithmic bytes
     traffic, traffic_src = None, None
     tf = os.path.join(ROOT, "profiles", "extract_traffic.json")
     if os.path.exists(tf):
         try:
-            ratio = json.load(open(tf))["ratio"]
+            tj = json.load(open(tf))
+            ratio = tj["ratio"]
             traffic = int(round(ratio * local_alg_extract))
-            traffic_src = f"ncu --set full dram__bytes_read+write / algorithmic = {ratio:.4f} (30b-slice launch)"
+            traffic_src = (f"ncu --set full dram__bytes_read+write / algorithmic = {ratio:.4f} "
+                           f"({tj.get('workload', '30b-slice launch')})")
         except Exception:
             traffic = None
     read_ceiling = None   # tools/scatter_bench read-only stream (profiles/r2/read_ceiling.json)
