@@ -1020,13 +1020,18 @@ def run_ours(args):
     t_end.record()
     d.barrier()
     clk = clocks.stop()
-    step_ms = [e[0].elapsed_time(e[r.n_events() - 2]) for e in evs]
+    # a step is the sync: its first event to the commit end; the synthetic update that follows under
+    # --replica snapshot / --commit scatter (input generation for the next step) is not part of it
+    toggles = (args.commit == "scatter" or r.loop_snapshot) and r.sender is not None and not r.stream
+    i_end = r.n_events() - 3                       # commit end
+    step_ms = [e[0].elapsed_time(e[i_end]) for e in evs]
     launches = ss.launch_count() - launches0 + (K * r.G if (args.commit == "scatter" or r.loop_snapshot)
                                                 and r.sender is not None and not r.stream else 0)
     launches = int(d.sum(launches))   # + the toggle kernels under --commit scatter
     # syncs separated by untimed work (an L2 flush, or config 5's optimizer step): the sum of the syncs' own
     # event intervals
-    ms_local = t_start.elapsed_time(t_end) if flush is None and not r.track_stream else float(np.sum(step_ms))
+    ms_local = (t_start.elapsed_time(t_end) if flush is None and not r.track_stream and not toggles
+                else float(np.sum(step_ms)))
     ms = d.max(ms_local)
     sm_med, sm_best = d.max(float(np.median(step_ms))), d.max(float(min(step_ms)))
     step_all = [round(d.max(float(x)), 3) for x in step_ms]   # per step, max over ranks
@@ -1047,12 +1052,10 @@ def run_ours(args):
     for _ in range(args.latency_steps):
         r.prepare_update()
         d.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        r.step()
-        e1.record()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(r.n_events())]
+        r.step(ev)   # start -> commit end: the synthetic update after it is not part of the sync
         torch.cuda.synchronize()
-        lat.append(d.max(e0.elapsed_time(e1)))
+        lat.append(d.max(ev[0].elapsed_time(ev[i_end])))
     latency = ({"median_ms": round(float(np.median(lat)), 4), "best_ms": round(float(min(lat)), 4),
                 "syncs": len(lat), "what": "one sync after a barrier, max over ranks (extract start -> last "
                                            "apply/commit)"} if lat else None)
@@ -1233,7 +1236,11 @@ def run_ours(args):
                    "stream_gb": args.stream_gb or None,
                    "transport": args.transport if d.world > 1 else "loopback", "topology": topo_txt,
                    "l2": ("inputs larger than L2 (2 x S per Trainer); no flush" if flush is None else
-                          "inputs smaller than L2: 512 MB write between steps, excluded via per-step events")},
+                          "inputs smaller than L2: 512 MB write between steps, excluded via per-step events"),
+                   "step_timing": ("sum of each sync's own CUDA-event interval (start -> commit end): the synthetic "
+                                   "update between syncs (input generation) is outside it"
+                                   if toggles or flush is not None or r.track_stream else
+                                   "one CUDA-event interval around the K steps")},
         "ms_per_phase": {n: round(float(v), 4) for n, v in
                          zip(["extract", "compress_pack", "transfer_apply", "commit", "synthetic_update",
                               "stream_generate" if r.stream and not r.track_stream else "cast_track"], phases)},
