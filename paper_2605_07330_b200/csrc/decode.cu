@@ -16,6 +16,20 @@
 #include "common.cuh"
 #include "kernels.h"
 
+// decode launch variants (CTAs per SM, prefetch depth) for dense / sparse calls; dev overrides for A/B builds
+#ifndef SS_DEC_DMINB
+#define SS_DEC_DMINB 3
+#endif
+#ifndef SS_DEC_DPF
+#define SS_DEC_DPF 4
+#endif
+#ifndef SS_DEC_SMINB
+#define SS_DEC_SMINB 1
+#endif
+#ifndef SS_DEC_SPF
+#define SS_DEC_SPF 8
+#endif
+
 namespace ss {
 
 struct BucketHdr {
@@ -567,9 +581,11 @@ void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u3
     // dense syncs are decode-bound: the 3-CTA / 4-deep variant keeps more chunks in flight; sparse ones are
     // scatter-bound and keep the 8-deep load pipeline
     if (dense)
-      run_decode<3, 4>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad, dtype, grid, s);
+      run_decode<SS_DEC_DMINB, SS_DEC_DPF>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad,
+                                           dtype, grid, s);
     else
-      run_decode<1, 8>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad, dtype, grid, s);
+      run_decode<SS_DEC_SMINB, SS_DEC_SPF>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad,
+                                           dtype, grid, s);
     count_launch();
   }
 }
@@ -586,9 +602,11 @@ void launch_decode_table(const u64* t_hdr, const u64* t_off, const u64* t_size, 
     bb.t_b0 = b0;
     bb.t_stride = stride;
     if (dense)
-      run_decode<3, 4>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status, nullptr, dtype, grid, s);
+      run_decode<SS_DEC_DMINB, SS_DEC_DPF>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status,
+                                           nullptr, dtype, grid, s);
     else
-      run_decode<1, 8>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status, nullptr, dtype, grid, s);
+      run_decode<SS_DEC_SMINB, SS_DEC_SPF>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status,
+                                           nullptr, dtype, grid, s);
     count_launch();
   }
 }

@@ -16,7 +16,7 @@ ROWS = [
     ("Qwen3-4B 99% U, 1T→1R (config 2)", "pair2_4b_r01", ""),
     ("30B 99% U, 1 GPU (headline)", "one_r01", ""),
     ("30B 99.9% U, 1 GPU", "one_r001", ""),
-    ("30B 90% U, 1 GPU (snapshot loopback + toggle)", "one_r10_snap", ""),
+    ("30B 90% U, 1 GPU (snapshot loopback; the toggle between syncs untimed)", "one_r10_snap", ""),
     ("30B 99% U, ring 2 GPUs", "ring2_r01", ""),
     ("30B 99.9% U, ring 2 GPUs", "ring2_r001", ""),
     ("30B 99% U, 1T→1R", "pair2_r01", ""),
