@@ -16,12 +16,14 @@
 #include "common.cuh"
 #include "kernels.h"
 
-// decode launch variants (CTAs per SM, prefetch depth) for dense / sparse calls; dev overrides for A/B builds
+// decode launch variants (CTAs per SM, prefetch depth) for dense / sparse calls; dev overrides for A/B builds.
+// Dense (decode-bound): 4 CTAs / 3-deep beat 3 / 4-deep by 13% at rho = 10% (BF16 and FP8; 4 / 2-deep -9%,
+// 4 / 4-deep spills); sparse (scatter-bound): 2 CTAs at 124 registers / 8-deep, more CTAs lose 1-3% (round 2)
 #ifndef SS_DEC_DMINB
-#define SS_DEC_DMINB 3
+#define SS_DEC_DMINB 4
 #endif
 #ifndef SS_DEC_DPF
-#define SS_DEC_DPF 4
+#define SS_DEC_DPF 3
 #endif
 #ifndef SS_DEC_SMINB
 #define SS_DEC_SMINB 1
@@ -578,7 +580,7 @@ void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u3
       bb.bytes[i] = bytes[b0 + i];
     }
     const u32* bad = crc_bad ? crc_bad + b0 : nullptr;
-    // dense syncs are decode-bound: the 3-CTA / 4-deep variant keeps more chunks in flight; sparse ones are
+    // dense syncs are decode-bound: the 4-CTA / 3-deep variant keeps more chunks in flight; sparse ones are
     // scatter-bound and keep the 8-deep load pipeline
     if (dense)
       run_decode<SS_DEC_DMINB, SS_DEC_DPF>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad,
