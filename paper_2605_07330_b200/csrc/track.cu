@@ -296,10 +296,17 @@ __global__ void k_track_counts(TrackArgs a) {
 }
 
 // Thread i owns words 4i..4i+3 of the tile (one 16-byte load): one block scan per tile gives each thread its
-// first output position, and its set bits are written in ascending element order.
+// first output position. A tile with at most kTW set bits (rho <= 25%) lists its tile-local indices in shared
+// memory (each thread its own set bits, ascending, at its scan position), then all threads gather
+// V = W[tile base + local] for consecutive list entries with kTG loads in flight per thread and store I / V
+// coalesced — the gather is a random 32-byte-sector read, so it needs many loads in flight (a thread walking
+// its own bits issued one dependent load at a time). Denser tiles take that per-thread walk.
+constexpr u32 kTW = 8192;   // list capacity per tile (u16 local indices: 16 KB of shared memory)
+constexpr int kTG = 4;      // gathers in flight per thread
 template <bool k8>   // k8: 8-bit elements (FP8): V = the byte, zero-extended
 __global__ void __launch_bounds__(kTT) k_track_write(TrackArgs a, u16* const* W, int clear) {
   __shared__ u64 s[33];
+  __shared__ u16 s_idx[kTW];
   const bool fits = tile_offset(a, a.n_tiles) <= a.cap;   // on overflow the set is kept for a retry
   for (u64 tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
     const u32 t = a.tile_tensor[tile];
@@ -319,15 +326,49 @@ __global__ void __launch_bounds__(kTT) k_track_write(TrackArgs a, u16* const* W,
     }
     const u32 c = __popc(wv[0]) + __popc(wv[1]) + __popc(wv[2]) + __popc(wv[3]);
     u64 ex;
-    const u64 tot = block_excl64((u64)c, &ex, s);
+    const u64 tot = block_excl64((u64)c, &ex, s);   // ends with a barrier: s_idx is free again
     if (tot == 0) continue;
-    u64 pos = tile_offset(a, tile) + ex;
+    const u64 pos0 = tile_offset(a, tile);
     if (c && clear && fits) {
       if (v16) *reinterpret_cast<uint4*>(bm + w0) = make_uint4(0, 0, 0, 0);
       else
         for (u32 j = 0; j < 4; ++j)
           if (w0 + j < nw) bm[w0 + j] = 0;
     }
+    if (tot <= kTW) {
+      u32 q = (u32)ex;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        u32 bits = wv[j];
+        while (bits) {
+          const u32 b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          s_idx[q++] = (u16)(32u * (w0 + j) + b);
+        }
+      }
+      __syncthreads();
+      const u32 n = (u32)tot;
+      for (u32 e0 = 0; e0 < n; e0 += kTT * kTG) {
+        u32 li[kTG];
+        u16 v[kTG];
+#pragma unroll
+        for (int u = 0; u < kTG; ++u) {
+          const u32 e = e0 + u * kTT + threadIdx.x;
+          li[u] = e < n ? (u32)s_idx[e] : 0u;
+          v[u] = e < n ? (k8 ? (u16)reinterpret_cast<const uint8_t*>(Wt)[base + li[u]] : Wt[base + li[u]]) : (u16)0;
+        }
+#pragma unroll
+        for (int u = 0; u < kTG; ++u) {
+          const u32 e = e0 + u * kTT + threadIdx.x;
+          if (e < n && pos0 + e < a.cap) {
+            a.I[pos0 + e] = (u32)(base + li[u]);
+            a.V[pos0 + e] = v[u];
+          }
+        }
+      }
+      continue;   // the next tile's block scan starts with a barrier before s_idx is rewritten
+    }
+    u64 pos = pos0 + ex;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       u32 bits = wv[j];
