@@ -646,6 +646,12 @@ class Rank:
             rec(4 * G + 1)
             rec(4 * G + 2)
             return
+        # a Trainer sending over peer memory (pair / fanout / sharded, G groups) enqueues each group's extract
+        # and compress + pack without waiting for its bucket plan (it runs on the device) and marks the group's
+        # buckets ready in stream order; group g-1's manifest goes out once group g is queued behind it — so the
+        # GPU runs the groups back to back while the Rollouts consume them
+        deferred = ([] if (snd is not None and peer and not ring and not self.overlap_commit
+                           and os.environ.get("SS_BENCH_DEFER", "1") != "0") else None)
         for g in range(G):
             rec(4 * g)
             if snd is not None:
@@ -669,6 +675,14 @@ class Rank:
                 rec(4 * g + 2)
                 if L is not None:
                     L.fence(g)            # the previous sync's sends of group g have left its bucket buffer
+                if deferred is not None:
+                    p.compress_pack_async()   # fused K2-K4, enqueue-only (device bucket plan)
+                    L.mark_ready(g)
+                    rec(4 * g + 3)
+                    deferred.append(g)
+                    if len(deferred) > 1:     # group g is queued behind g-1: send g-1's manifest now
+                        self._send_deferred(snd, L, deferred.pop(0))
+                    continue
                 blist = p.compress_pack()  # fused K2-K4 (blocking: host bucket plan)
                 rec(4 * g + 3)
                 if L is None and self.apply_stream is not None:
@@ -709,6 +723,8 @@ class Rank:
                 else:
                     src = next(iter(self.receivers))
                     L.receive(self.receivers[src].parts[g].apply, tag=g)
+        for g in deferred or []:
+            self._send_deferred(snd, L, g)
         if self.apply_stream is not None:
             torch.cuda.current_stream().wait_stream(self.apply_stream)
         rec(4 * G)
@@ -730,6 +746,12 @@ class Rank:
         # every step, so every step syncs a genuine update (v0 -> v1, then v1 -> v0) with no generator work;
         # under --tracking cast the two fp32 master versions alternate the same way
         rec(4 * G + 2)
+
+    @staticmethod
+    def _send_deferred(snd, L, g):
+        p = snd.parts[g]
+        blist = p.pack_result()        # group g's plan (blocks until it is on the host)
+        L.send(p.buckets, blist, tag=g, marked=not p.redone)
 
     def phase_ms(self, ev):
         """extract (+ cast_track under --tracking cast), compress_pack (summed over groups), transfer_apply (the

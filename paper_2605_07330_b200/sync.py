@@ -131,6 +131,39 @@ class SparseSyncSender:
                     self.buckets = torch.empty(int(e.need * 1.05) + 4096, dtype=torch.uint8, device=self.device)
         raise SyncError(SYNC_ERR_CAPACITY, "sync_compress_pack: could not size the buffers")
 
+    def compress_pack_async(self, stream=None):
+        """Enqueue-only fused K2-K4 (sync_compress_pack_async: the bucket plan runs on the device, the host does
+        not wait); collect the bucket list with pack_result(). Lets a caller enqueue several groups' syncs back
+        to back and read their plans afterwards."""
+        if self.buckets.numel() == 0:
+            self.buckets = torch.empty(int(3.5 * self.cap) + 64 * len(self.numel) + 4096, dtype=torch.uint8,
+                                       device=self.device)
+        self.ctx.sync_compress_pack_async(self.I, self.V, self.counts, self.buckets, stream)
+
+    def pack_result(self, stream=None):
+        """The bucket list of the last compress_pack_async (blocks until its plan is on the host). On a capacity
+        error the buffers are grown and the group is re-done synchronously (compress_pack), so the returned
+        list is always complete; .redone tells the caller that the buckets were rewritten after the enqueue."""
+        self.redone = False
+        try:
+            self.bucket_list = self.ctx.sync_pack_result()
+            return self.bucket_list
+        except SyncError as e:
+            if e.code != SYNC_ERR_CAPACITY:
+                raise
+            self.ctx.sync_status(stream)
+            stats = self.ctx.stats(stream)
+            if stats["nnz"] > self.cap:
+                self._alloc(min(sum(self.numel), int(stats["nnz"] * 1.1) + 65536))
+                self._reextract(stream)
+            elif getattr(e, "need", 0) > self.buckets.numel():
+                self.buckets = torch.empty(int(e.need * 1.05) + 4096, dtype=torch.uint8, device=self.device)
+            self.redone = True
+            return self.compress_pack(stream)
+
+    def _reextract(self, stream=None):
+        self.ctx.sync_extract_batched(self.old_ptrs, self.new_ptrs, self.I, self.V, self.counts, stream)
+
     def sync(self, stream=None, fused: bool = True):
         """extract + compress + pack; returns the bucket list. Call commit() once the buckets were delivered."""
         if fused:
@@ -170,6 +203,9 @@ class TrackedSender(SparseSyncSender):
 
     def extract(self, stream=None, clear: bool = True):
         self.ctx.sync_extract_tracked(self.weight_ptrs, self.bitmap, self.I, self.V, self.counts, clear, stream)
+
+    def _reextract(self, stream=None):
+        self.extract(stream)   # on overflow the set was kept (nothing cleared)
 
     def compress_pack(self, stream=None):
         if self.buckets.numel() == 0:

@@ -377,7 +377,14 @@ class PeerLink:
                 self.peer_consumed[key] = _open_event(_t2h(ack_t[1:9]))
             _wait(self._stream(), self.peer_consumed[key])
 
-    def send(self, send_buf: torch.Tensor, blist, tag: int = 0):
+    def mark_ready(self, tag: int = 0):
+        """Record group `tag`'s "ready" event on the stream now (right after its encode was enqueued), for a
+        caller that enqueues several groups before it sends their manifests (send(..., marked=True))."""
+        if tag not in self.ready:
+            self.ready[tag] = _PeerEvent()
+        self.ready[tag].record(self._stream())
+
+    def send(self, send_buf: torch.Tensor, blist, tag: int = 0, marked: bool = False):
         import ctypes
         self.fence(tag)   # normally already done by the caller before it rewrote the buffer
         seq = self.seq.get(tag, 0)
@@ -389,9 +396,8 @@ class PeerLink:
                  "sync_peer_mem_export")
             ex = (send_buf.data_ptr(), send_buf.numel(), (ex[2] + 1) if ex else 1, h.raw, off.value)
             self.exported[tag] = ex
-        if tag not in self.ready:
-            self.ready[tag] = _PeerEvent()
-        self.ready[tag].record(self._stream())
+        if not marked:
+            self.mark_ready(tag)
         hdr = torch.zeros(_HDR, dtype=torch.int64)
         hdr[0], hdr[1], hdr[2], hdr[3] = seq, len(blist), ex[2], ex[4]
         hdr[5:13] = _h2t(ex[3])

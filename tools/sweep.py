@@ -33,7 +33,7 @@ SETS = {
         ("fanout8_r01_E_b64", 8, ["--topology", "fanout", "--mask", "E", "--bucket-mb", "64"]),
         ("fanout8_r01_E_b256", 8, ["--topology", "fanout", "--mask", "E"]),
         ("fanout8_r01_E_b1024", 8, ["--topology", "fanout", "--mask", "E", "--bucket-mb", "1024"]),
-        ("sharded8_235b_f1", 8, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--stream-gb", "5",
+        ("sharded8_235b_f1", 8, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--stream-gb", "10",
                                  "--tracking", "cast", "--steps", "5"]),
         ("sharded8_235b_stream", 8, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--stream-gb", "5",
                                      "--commit", "scatter", "--steps", "5"]),
@@ -65,7 +65,7 @@ SETS = {
                                      "4", "--stream-gb", "5", "--commit", "scatter", "--steps", "5"]),
         # config 5 with the paper's own hook (f1): W + bitmap, the optimizer step outside the timed sync
         ("sharded4_235b_f1", 4, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--model-shards", "4",
-                                 "--stream-gb", "5", "--tracking", "cast", "--steps", "5"]),
+                                 "--stream-gb", "10", "--tracking", "cast", "--steps", "5"]),
         # fan-out data planes: peer memory (default), NCCL per-destination sends, NCCL broadcast
         ("fanout4_r01_U_b256_nccl", 4, ["--topology", "fanout", "--transport", "nccl"]),
         ("fanout4_r01_U_b256_bcast", 4, ["--topology", "fanout", "--transport", "nccl-bcast"]),
