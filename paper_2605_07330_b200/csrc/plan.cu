@@ -80,7 +80,10 @@ __device__ unsigned long long g_cprof[8];  // debug cycle counters (SS_CPROF=1)
 // Histogram / gap pass: lane l owns the 8 consecutive values of an 8-aligned group (one 16-byte load of V,
 // two of I); the gap into the group comes from lane l-1's last index (one shuffle), the warp's carry from
 // the previous round.
-constexpr int kWPF = 8;
+#ifndef SS_WPF
+#define SS_WPF 8
+#endif
+constexpr int kWPF = SS_WPF;   // rANS steps per prefetched block of coded bytes (dev override -DSS_WPF)
 template <bool kEsc>   // f4: also count the gaps > 32767 per chunk (escape words)
 __global__ void __launch_bounds__(256, SS_CS_MINB) k_chunk_stats(Plan p, const u32* I, const u16* V, const u64* counts) {
   __shared__ WarpModel s_m[8];

@@ -79,7 +79,7 @@ SETS = {
         ("pair2_r10", 2, ["--topology", "pair", "--rho", "0.1"]),
         ("pair2_r001", 2, ["--topology", "pair", "--rho", "0.001"]),
         ("sharded2_235b_f1", 2, ["--workload", "qwen3-235b-a22b", "--topology", "sharded", "--model-shards", "4",
-                                 "--stream-gb", "5", "--tracking", "cast", "--steps", "5"]),
+                                 "--stream-gb", "10", "--tracking", "cast", "--steps", "5"]),
     ],
     "n1": [
         ("one_r01", 1, []),
