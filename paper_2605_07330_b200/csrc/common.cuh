@@ -141,7 +141,6 @@ __device__ __forceinline__ u32 div_by(u32 x, u32 f, u32 rcp, u32* rem) {
 struct WarpModel {
   u32 hist[256];
   u16 freq[256];
-  u16 cum[256];
   // per symbol {freq | cum << 16, rcp_of(freq)}: one 64-bit load per step in the encode loop; entry 256 is a
   // no-op symbol (freq 4096, cum 0) for the padding positions past a chunk's end: it never emits and
   // x + q * (4096 - 4096) + 0 leaves the state unchanged
@@ -222,7 +221,6 @@ __device__ __forceinline__ u32 warp_normalize(WarpModel& m, u32 n) {
   for (int k = 0; k < 8; ++k) {
     u32 s = lane * 8 + k;
     m.freq[s] = (u16)f[k];
-    m.cum[s] = (u16)run;
     m.fr[s] = make_uint2(f[k] | (run << 16), f[k] ? rcp_of(f[k]) : 0u);
     run += f[k];
   }
