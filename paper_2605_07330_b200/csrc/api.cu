@@ -313,6 +313,7 @@ int sync_extract(const uint16_t* d_old, const uint16_t* d_new, uint64_t n, uint3
   if (sync_extract_workspace_size(n, &need)) return SYNC_ERR_ARG;
   if (!d_count || !d_workspace || (n && (!d_old || !d_new))) return SYNC_ERR_ARG;
   if (workspace_bytes < need) return SYNC_ERR_WORKSPACE;
+  if (!aligned16(d_I) || !aligned16(d_V)) return SYNC_ERR_ALIGNMENT;   // the header's I / V contract
   if (!aligned16(d_workspace)) return SYNC_ERR_ALIGNMENT;
   cudaStream_t s = (cudaStream_t)stream;
   u8* w = static_cast<u8*>(d_workspace);
@@ -345,6 +346,7 @@ int sync_extract_batched(sync_ctx* x, const uint16_t* const* d_old_ptrs, const u
                          uint32_t* d_I, uint16_t* d_V, uint64_t* d_counts, sync_stream_t stream) {
   ApiRange nvtx_range("sync_extract_batched");
   if (!x || (x->d.T && (!d_old_ptrs || !d_new_ptrs || !d_counts))) return SYNC_ERR_ARG;
+  if (!aligned16(d_I) || !aligned16(d_V)) return SYNC_ERR_ALIGNMENT;   // the header's I / V contract
   cudaStream_t s = (cudaStream_t)stream;
   x->plan_valid = false;
   if (x->d.T == 0) return SYNC_OK;
@@ -415,6 +417,7 @@ int sync_extract_tracked(sync_ctx* x, uint16_t* const* d_weight_ptrs, uint32_t* 
                          uint16_t* d_V, uint64_t* d_counts, int clear, sync_stream_t stream) {
   ApiRange nvtx_range("sync_extract_tracked");
   if (!x || (x->d.T && (!d_weight_ptrs || !d_bitmap || !d_counts))) return SYNC_ERR_ARG;
+  if (!aligned16(d_I) || !aligned16(d_V)) return SYNC_ERR_ALIGNMENT;   // the header's I / V contract
   x->plan_valid = false;
   if (x->d.T == 0) return SYNC_OK;
   TrackArgs a = track_args(x, d_bitmap);
@@ -442,6 +445,7 @@ int sync_compress(sync_ctx* x, const uint32_t* d_I, const uint16_t* d_V, const u
   if (!x || (x->d.T && (!d_counts || !d_enc))) return SYNC_ERR_ARG;
   if (x->plan.route && !x->plan.cur) return SYNC_ERR_ARG;   // SYNC_FLAG_ROUTE needs sync_set_current
   if (!aligned16(d_enc)) return SYNC_ERR_ALIGNMENT;
+  if (!aligned16(d_I) || !aligned16(d_V)) return SYNC_ERR_ALIGNMENT;   // the header's I / V contract
   cudaStream_t s = (cudaStream_t)stream;
   x->plan.enc_cap = enc_cap;
   launch_plan_scan(x->plan, d_counts, s);
@@ -562,6 +566,7 @@ int sync_compress_pack_async(sync_ctx* x, const uint32_t* d_I, const uint16_t* d
   if (!x || (x->d.T && !d_counts)) return SYNC_ERR_ARG;
   if (x->plan.route && !x->plan.cur) return SYNC_ERR_ARG;   // SYNC_FLAG_ROUTE needs sync_set_current
   if (!aligned16(d_buckets)) return SYNC_ERR_ALIGNMENT;
+  if (!aligned16(d_I) || !aligned16(d_V)) return SYNC_ERR_ALIGNMENT;   // the header's I / V contract
   cudaStream_t s = (cudaStream_t)stream;
   // plan (record sizes) exactly as sync_compress, without the encode
   x->plan.enc_cap = ~0ull;
@@ -626,6 +631,7 @@ int sync_decompress(sync_ctx* x, const uint8_t* d_bucket, uint64_t bytes, uint32
   ApiRange nvtx_range("sync_decompress");
   if (!x || !d_bucket) return SYNC_ERR_ARG;
   if (!aligned16(d_bucket)) return SYNC_ERR_ALIGNMENT;
+  if (!aligned16(d_I) || !aligned16(d_V)) return SYNC_ERR_ALIGNMENT;   // the header's I / V contract
   cudaStream_t s = (cudaStream_t)stream;
   const u32* bad;
   int st = maybe_crc_check(x, &d_bucket, &bytes, 1, s, &bad);
@@ -723,6 +729,7 @@ int sync_commit_snapshot_batched(sync_ctx* x, uint16_t* const* d_snapshot_ptrs, 
                                  const uint16_t* d_V, const uint64_t* d_counts, sync_stream_t stream) {
   ApiRange nvtx_range("sync_commit_snapshot_batched");
   if (!x || (x->d.T && (!d_snapshot_ptrs || !d_counts))) return SYNC_ERR_ARG;
+  if (!aligned16(d_I) || !aligned16(d_V)) return SYNC_ERR_ALIGNMENT;   // the header's I / V contract
   if (x->d.T == 0) return SYNC_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (!(x->plan_valid && x->plan_counts == d_counts)) {

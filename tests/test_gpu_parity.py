@@ -605,3 +605,32 @@ def test_numel_2_31_is_rejected():
         ss.sync_extract(big, big, I=small, V=small.view(torch.int16)[:16])
     with pytest.raises(ss.SyncError):
         ss.SparseSyncSender([big], [big], max_changed=16)
+
+
+@pytest.mark.parametrize("off", [0, 8, 1, 3])
+@pytest.mark.parametrize("rho,mask", [(0.01, synth.MASK_U), (0.3, synth.MASK_U), (0.02, synth.MASK_R)])
+def test_iv_views_alignment_contract(off, rho, mask):
+    """I / V must be 16-byte aligned (include/sparsesync.h; k_chunk_stats and k_encode use 16- / 8-byte vector
+    loads of them): views at a 16-byte multiple give the oracle's bytes (ABS32 records under the R mask, dense
+    chunks at 30%); any other offset is refused with SYNC_ERR_ALIGNMENT before a kernel runs."""
+    m = mixed_manifest()
+    olds, news = synth.generate(m, seed=5, rho=rho, mask=mask)
+    old_d = [to_dev(o) for o in olds]
+    new_d = [to_dev(n) for n in news]
+    snd = ss.SparseSyncSender(old_d, new_d, bucket_limit=64 << 10)
+    cap = snd.cap
+    bi = torch.empty(cap + 8, dtype=torch.int32, device=DEV)
+    bv = torch.empty(cap + 8, dtype=torch.int16, device=DEV)
+    snd.I, snd.V = bi[off:off + cap], bv[off:off + cap]
+    if off % 8:
+        with pytest.raises(ss.SyncError) as e:
+            snd.sync(fused=True)
+        assert e.value.code == ss.SYNC_ERR_ALIGNMENT
+        return
+    ref = oracle.sync_pack(olds, news, codec=ss.SYNC_CODEC_COMPRESSED, limit=64 << 10, crc=False)
+    bl = snd.sync(fused=True)
+    torch.cuda.synchronize()
+    snd.check()
+    assert len(bl) == ref.n_buckets
+    for b in range(ref.n_buckets):
+        assert snd.bucket(b).cpu().numpy().tobytes() == ref.bucket(b), f"off={off}: bucket {b} bytes differ"
