@@ -100,9 +100,11 @@ def test_peer_ring_world2(mode, groups):
     assert all(p.exitcode == 0 for p in ps)
 
 
-def _worker_fanout(rank, world, port, q):
+def _worker_fanout(rank, world, port, q, deferred=False):
     """ranks 0, 1: Trainers of shards 0, 1 of one model (2 groups each); ranks 2, 3: full-replica Rollouts
-    (fanout). Every process on cuda:(rank % device count)."""
+    (fanout). Every process on cuda:(rank % device count). deferred: the Trainers enqueue each group's
+    compress + pack without waiting for its plan (compress_pack_async), mark its buckets ready in stream order
+    and send group g-1's manifest once group g is queued (bench.py's sender)."""
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -130,11 +132,24 @@ def _worker_fanout(rank, world, port, q):
             snd = GroupedSender(Xv, Yv, groups=2, bucket_limit=32 << 10)
             link = transport.PeerLink(rank, world, dev, [2, 3], [])
             for step in range(3):
+                pending = []
                 for g, p in enumerate(snd.parts):
                     p.ctx.sync_extract_batched(p.old_ptrs, p.new_ptrs, p.I, p.V, p.counts)
                     link.fence(g)
+                    if deferred:
+                        p.compress_pack_async()
+                        link.mark_ready(g)
+                        pending.append(g)
+                        if len(pending) > 1:
+                            h = pending.pop(0)
+                            link.send(snd.parts[h].buckets, snd.parts[h].pack_result(), tag=h,
+                                      marked=not snd.parts[h].redone)
+                        continue
                     blist = p.compress_pack()
                     link.send(p.buckets, blist, tag=g)
+                for h in pending:
+                    link.send(snd.parts[h].buckets, snd.parts[h].pack_result(), tag=h,
+                              marked=not snd.parts[h].redone)
                 snd.commit(mode="swap")
                 X, Y = Y, X
             for g in range(2):
@@ -161,15 +176,17 @@ def _worker_fanout(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_peer_fanout_world4():
-    """Send-only / receive-only PeerLink roles: 2 sharded Trainers fan out to 2 full replicas (3 syncs)."""
+@pytest.mark.parametrize("deferred", [False, True])
+def test_peer_fanout_world4(deferred):
+    """Send-only / receive-only PeerLink roles: 2 sharded Trainers fan out to 2 full replicas (3 syncs); with
+    deferred manifests (enqueue-only compress + pack) as well."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker_fanout, args=(r, 4, port, q)) for r in range(4)]
+    ps = [ctx.Process(target=_worker_fanout, args=(r, 4, port, q, deferred)) for r in range(4)]
     for p in ps:
         p.start()
     for p in ps:
