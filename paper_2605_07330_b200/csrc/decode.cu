@@ -19,6 +19,9 @@
 // decode launch variants (CTAs per SM, prefetch depth) for dense / sparse calls; dev overrides for A/B builds.
 // Dense (decode-bound): 4 CTAs / 3-deep beat 3 / 4-deep by 13% at rho = 10% (BF16 and FP8; 4 / 2-deep -9%,
 // 4 / 4-deep spills); sparse (scatter-bound): 2 CTAs at 124 registers / 8-deep, more CTAs lose 1-3% (round 2)
+#ifndef SS_DEC_FAST
+#define SS_DEC_FAST 1
+#endif
 #ifndef SS_DEC_DMINB
 #define SS_DEC_DMINB 4
 #endif
@@ -423,6 +426,71 @@ __global__ void __launch_bounds__(256, kMinB) k_decode(DecodeBatch bb, u32 n_ten
     u32 ptr = 0;
     u32 carry = (r.mode == 0 || esc) ? base : 0u;
     bool range_bad = false, word_bad = false;
+#if SS_DEC_FAST
+    if (kApply && kMinB <= 2 && cm == 1 && r.mode == 0 && !esc && !e8) {   // sparse variant only (r4e)
+      // the common record kind (rANS hi chunk, DELTA16 indices, 16-bit values, apply) without the per-step
+      // mode branches of the general loop below: same steps, same checks. A chunk is one warp's dependent
+      // chain, so in a small sync (fewer chunks than warps) its instruction count is the launch's latency
+      // (small syncs): 4B in 24 groups 6.68 -> 5.20 ms of decode, 30B at rho = 1% +-0; the dense
+      // (decode-bound, 64-register) variant keeps the general loop (+3.5% with this one).
+      u32 nlb2[kPF], ndd2[kPF];
+#pragma unroll
+      for (int i = 0; i < kPF; ++i) {
+        const u32 qq = (u32)i * 32 + lane;
+        nlb2[i] = qq < nk ? (u32)lo[qq] : 0u;
+        ndd2[i] = qq < nk ? (u32)D[qq] : 0u;
+      }
+      for (u32 g0 = 0; g0 < G; g0 += kPF) {
+        u32 lb[kPF], dd[kPF];
+#pragma unroll
+        for (int i = 0; i < kPF; ++i) {
+          lb[i] = nlb2[i];
+          dd[i] = ndd2[i];
+        }
+        if (g0 + kPF < G) {
+#pragma unroll
+          for (int i = 0; i < kPF; ++i) {
+            const u32 qq = (g0 + kPF + (u32)i) * 32 + lane;
+            nlb2[i] = qq < nk ? (u32)lo[qq] : 0u;
+            ndd2[i] = qq < nk ? (u32)D[qq] : 0u;
+          }
+        }
+        if (lane < 8 && ptr + 64 * (lane + 1) < nwords)  // warm L1 with the next words
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(words + ptr + 64 * (lane + 1)));
+#pragma unroll
+        for (int i = 0; i < kPF; ++i) {
+          const u32 gs = g0 + i;
+          if (gs >= G) break;
+          const u32 qq = gs * 32 + lane;
+          const bool act = qq < nk;
+          u32 sym = 0;
+          if (act) {
+            const u32 slot = x & (kM - 1);
+            sym = dm.slot2sym[slot];
+            x = (u32)dm.freq[sym] * (x >> 12) + slot - dm.cum[sym];
+          }
+          const bool need = act && x < kLow;
+          const u32 nm = __ballot_sync(0xffffffffu, need);
+          if (need) {
+            const u32 pos = ptr + __popc(nm >> lane >> 1);
+            if (pos < nwords) x = (x << 16) | words[pos];
+            else word_bad = true;
+          }
+          ptr += __popc(nm);
+          const u32 idx = carry + warp_incl_scan(dd[i]);
+          carry = __shfl_sync(0xffffffffu, idx, 31);
+          if (act) {
+            if (idx < lim) W[idx] = (u16)((sym << 8) | lb[i]);
+            else range_bad = true;
+          }
+        }
+      }
+      const bool endbad = word_bad || x != kLow || ptr != nwords;
+      if (__any_sync(0xffffffffu, endbad) && lane == 0) latch(status, SYNC_ERR_CORRUPT);
+      if (__any_sync(0xffffffffu, range_bad) && lane == 0) latch(status, SYNC_ERR_INDEX_RANGE);
+      continue;
+    }
+#endif
     // software pipeline: the lo bytes and the index words (DELTA16 delta or
     // ABS32 index) of the next 8 steps are loaded while the current 8 decode
     u32 nlb[kPF], ndd[kPF];
