@@ -17,16 +17,17 @@
 #include "kernels.h"
 
 // decode launch variants (CTAs per SM, prefetch depth) for dense / sparse calls; dev overrides for A/B builds.
-// Dense (decode-bound): 4 CTAs / 3-deep beat 3 / 4-deep by 13% at rho = 10% (BF16 and FP8; 4 / 2-deep -9%,
-// 4 / 4-deep spills); sparse (scatter-bound): 2 CTAs at 124 registers / 8-deep, more CTAs lose 1-3% (round 2)
+// Dense (decode-bound): with the general loop, 4 CTAs / 3-deep beat 3 / 4-deep by 13% at rho = 10% (BF16 and
+// FP8); with the specialised loop of the common record kind, 3 CTAs / 4-deep (80 registers, no spill) is best
+// (4 / 3-deep spills: +3.5%); sparse (scatter-bound): 2 CTAs / 8-deep, more CTAs lose 1-3% (round 2)
 #ifndef SS_DEC_FAST
 #define SS_DEC_FAST 1
 #endif
 #ifndef SS_DEC_DMINB
-#define SS_DEC_DMINB 4
+#define SS_DEC_DMINB 3
 #endif
 #ifndef SS_DEC_DPF
-#define SS_DEC_DPF 3
+#define SS_DEC_DPF 4
 #endif
 #ifndef SS_DEC_SMINB
 #define SS_DEC_SMINB 1
@@ -427,12 +428,12 @@ __global__ void __launch_bounds__(256, kMinB) k_decode(DecodeBatch bb, u32 n_ten
     u32 carry = (r.mode == 0 || esc) ? base : 0u;
     bool range_bad = false, word_bad = false;
 #if SS_DEC_FAST
-    if (kApply && kMinB <= 2 && cm == 1 && r.mode == 0 && !esc && !e8) {   // sparse variant only (r4e)
+    if (kApply && cm == 1 && r.mode == 0 && !esc && !e8) {
       // the common record kind (rANS hi chunk, DELTA16 indices, 16-bit values, apply) without the per-step
       // mode branches of the general loop below: same steps, same checks. A chunk is one warp's dependent
       // chain, so in a small sync (fewer chunks than warps) its instruction count is the launch's latency
-      // (small syncs): 4B in 24 groups 6.68 -> 5.20 ms of decode, 30B at rho = 1% +-0; the dense
-      // (decode-bound, 64-register) variant keeps the general loop (+3.5% with this one).
+      // (small syncs): 4B in 24 groups 6.68 -> 5.20 ms of decode, 30B at rho = 1% +-0, and the dense
+      // variant at 3 CTAs / 4-deep with it beats 4 CTAs / 3-deep without it by 1-4% (rho = 10% / 5%).
       u32 nlb2[kPF], ndd2[kPF];
 #pragma unroll
       for (int i = 0; i < kPF; ++i) {
@@ -648,9 +649,11 @@ void launch_decode(const u8* const* buckets, const u64* bytes, u32 n_buckets, u3
       bb.bytes[i] = bytes[b0 + i];
     }
     const u32* bad = crc_bad ? crc_bad + b0 : nullptr;
-    // dense syncs are decode-bound: the 4-CTA / 3-deep variant keeps more chunks in flight; sparse ones are
+    // dense syncs are decode-bound: the 3-CTA / 4-deep variant keeps more chunks in flight; sparse ones are
     // scatter-bound and keep the 8-deep load pipeline
-    if (dense)
+    if (dense && dtype == SYNC_DTYPE_FP8)   // no specialised loop for 8-bit values: the general loop's best
+      run_decode<4, 3>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad, dtype, grid, s);
+    else if (dense)
       run_decode<SS_DEC_DMINB, SS_DEC_DPF>(bb, n_tensors, numel, weights, views, I_out, V_out, out_cap, status, bad,
                                            dtype, grid, s);
     else
@@ -671,7 +674,9 @@ void launch_decode_table(const u64* t_hdr, const u64* t_off, const u64* t_size, 
     bb.t_base = base;
     bb.t_b0 = b0;
     bb.t_stride = stride;
-    if (dense)
+    if (dense && dtype == SYNC_DTYPE_FP8)
+      run_decode<4, 3>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status, nullptr, dtype, grid, s);
+    else if (dense)
       run_decode<SS_DEC_DMINB, SS_DEC_DPF>(bb, n_tensors, numel, weights, nullptr, nullptr, nullptr, 0, status,
                                            nullptr, dtype, grid, s);
     else
